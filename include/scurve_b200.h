@@ -1,0 +1,114 @@
+/*
+ * scurve_b200 — C ABI of the B200-native curvelet hot path.
+ *
+ * One shared library (libscurve_b200.so, sm_100a) exports the entry points
+ * below.  They replace, one for one, the Python functions of the reference
+ * package `scurve` that make up the curvelet analysis/synthesis path (paths
+ * relative to /root/reference/pkg/src/scurve/):
+ *
+ *   scv_sht_forward            <- sht_forward / sht_forward_real   sphere.py:155-182, 210-236
+ *   scv_sht_inverse            <- sht_inverse / sht_inverse_real   sphere.py:185-207, 239-260
+ *   scv_scale_product          <- transform._scale_wigner          transform.py:104-115
+ *   scv_scaling_product        <- transform._scaling_coeffs        transform.py:128-136
+ *   scv_so3_inverse_curvelet   <- so3_inverse_curvelet(_real)      so3.py:259-285, 386-417
+ *   scv_so3_forward_curvelet   <- so3_forward_curvelet(_real)      so3.py:214-244, 349-383
+ *   scv_accumulate             <- the acc += W psi loop of synthesize  transform.py:170-178
+ *   scv_finish_acc             <- acc[:s^2]=0 (+ real symmetry)    transform.py:186, 246-252
+ *   scv_halfpi_wedge           <- build_halfpi_table / halfpi_table wigner.py:209-240
+ *
+ * Conventions
+ *   - All data pointers are DEVICE pointers owned by the caller.  Complex
+ *     values are interleaved float64 pairs (re, im), i.e. complex128.
+ *   - Layouts are the reference's, byte for byte:
+ *       sphere map     (L, 2L-1)             theta-major (complex128, or float64 when real)
+ *       harmonic f_lm  (L*L,)                index l*l + l + m
+ *       Wigner coeffs  (2, L, 2L-1)          sheet 0: n=+l, sheet 1: n=-l, m at m+L-1
+ *       SO(3) signal   (2L-1, L, 2L-1)       (gamma, beta, alpha); complex128, or float64 when real
+ *   - `stream` is a cudaStream_t passed as void*; every call is ordered on it
+ *     and returns without synchronising.  Inputs are never modified.
+ *   - A context is bound to one device and is not thread-safe.  It owns only
+ *     its workspace: Delta(pi/2) wedge table, Bluestein/weight tables, cuFFT
+ *     plans and scratch.  Workspace grows lazily and is freed by scv_destroy.
+ *   - Return 0 on success or a negative SCV_E* code; scv_last_error() gives
+ *     the message.  SCV_EINVAL corresponds to the reference's ValueError,
+ *     SCV_ETYPE to TypeError, the rest to RuntimeError.
+ */
+#ifndef SCURVE_B200_H
+#define SCURVE_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SCV_OK 0
+#define SCV_EINVAL (-1)
+#define SCV_ETYPE (-2)
+#define SCV_ECUDA (-3)
+#define SCV_ENOMEM (-4)
+#define SCV_ECUFFT (-5)
+
+typedef struct scv_ctx scv_ctx;
+
+/* ABI version (major*100 + minor). */
+int scv_version(void);
+
+/* Create a context on CUDA device `device`. */
+int scv_create(int device, scv_ctx** out);
+int scv_destroy(scv_ctx* ctx);
+const char* scv_last_error(const scv_ctx* ctx);
+
+/* Bytes of device memory currently held by the context's workspace. */
+long long scv_workspace_bytes(const scv_ctx* ctx);
+/* Release every lazily grown scratch buffer (tables stay). */
+int scv_trim(scv_ctx* ctx);
+
+/* Delta^l_{m'm}(pi/2) for l < L in the 1/8 symmetry wedge 0 <= m <= m' <= l:
+ * element (l, m', m) at l(l+1)(l+2)/6 + m'(m'+1)/2 + m.  Copies the context's
+ * table (built on the device by the degree recursion) into `out`
+ * (L(L+1)(L+2)/6 doubles).  wigner.py:153-240. */
+int scv_halfpi_wedge(scv_ctx* ctx, int L, double* out, void* stream);
+
+/* Forward spin SHT.  f: (L, 2L-1) complex128, or float64 if real (spin 0).
+ * flm: (L*L) complex128. */
+int scv_sht_forward(scv_ctx* ctx, int L, int spin, int real, const void* f, double* flm,
+                    void* stream);
+
+/* Inverse spin SHT.  flm (L*L) complex128 -> f (L, 2L-1) complex128, or
+ * float64 if real (flm must then carry the real-signal symmetry). */
+int scv_sht_inverse(scv_ctx* ctx, int L, int spin, int real, const double* flm, void* f,
+                    void* stream);
+
+/* Per-scale harmonic product: w (2, Lj, 2Lj-1) with
+ * w[0,l,m] = 8pi^2/(2l+1) f_lm psi_pos[l], w[1,l,m] = ... psi_neg[l], 1<=l<Lj.
+ * flm has band limit L >= Lj; psi_* are device arrays of length >= Lj. */
+int scv_scale_product(scv_ctx* ctx, int L, int Lj, const double* flm, const double* psi_pos,
+                      const double* psi_neg, double* w, void* stream);
+
+/* Scaling coefficients: out (Ls*Ls) = sqrt(4pi/(2l+1)) scaling[l] f_lm, l<Ls. */
+int scv_scaling_product(scv_ctx* ctx, int L, int Ls, const double* flm, const double* scaling,
+                        double* out, void* stream);
+
+/* Sparse inverse Wigner transform (analysis direction): w (2, Lj, 2Lj-1)
+ * complex128 -> sig (2Lj-1, Lj, 2Lj-1), complex128 or float64 if real. */
+int scv_so3_inverse_curvelet(scv_ctx* ctx, int Lj, int real, const double* w, void* sig,
+                             void* stream);
+
+/* Sparse forward Wigner transform (synthesis direction): sig -> w. */
+int scv_so3_forward_curvelet(scv_ctx* ctx, int Lj, int real, const void* sig, double* w,
+                             void* stream);
+
+/* acc (L*L) += w[0,l,m] psi_pos[l] + w[1,l,m] psi_neg[l] for 1 <= l < Lj. */
+int scv_accumulate(scv_ctx* ctx, int L, int Lj, const double* w, const double* psi_pos,
+                   const double* psi_neg, double* acc, void* stream);
+
+/* acc += sqrt(4pi/(2l+1)) scaling[l] slm for l < Ls (slm has band limit Ls). */
+int scv_accumulate_scaling(scv_ctx* ctx, int L, int Ls, const double* slm,
+                           const double* scaling, double* acc, void* stream);
+
+/* acc[: spin^2] = 0; if real, re-impose f_{l,-m} = (-1)^m conj f_{lm}, f_l0 real. */
+int scv_finish_acc(scv_ctx* ctx, int L, int spin, int real, double* acc, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SCURVE_B200_H */

@@ -1,0 +1,136 @@
+"""ctypes binding of libscurve_b200.so (include/scurve_b200.h).
+
+The product path has no CPU fallback: if the shared library or a CUDA
+device is missing, every transform raises.  One context per device is
+created lazily and shared; calls are serialised per context by a lock
+(a context is not thread-safe, include/scurve_b200.h).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libscurve_b200.so")
+
+SCV_OK = 0
+SCV_EINVAL = -1
+SCV_ETYPE = -2
+
+_lib = None
+_lib_lock = threading.Lock()
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+
+# name -> argtypes (all return int unless listed in _RESTYPE)
+_SIGS = {
+    "scv_version": [],
+    "scv_create": [_I, ctypes.POINTER(_P)],
+    "scv_destroy": [_P],
+    "scv_last_error": [_P],
+    "scv_workspace_bytes": [_P],
+    "scv_trim": [_P],
+    "scv_halfpi_wedge": [_P, _I, _P, _P],
+    "scv_sht_forward": [_P, _I, _I, _I, _P, _P, _P],
+    "scv_sht_inverse": [_P, _I, _I, _I, _P, _P, _P],
+    "scv_scale_product": [_P, _I, _I, _P, _P, _P, _P, _P],
+    "scv_scaling_product": [_P, _I, _I, _P, _P, _P, _P],
+    "scv_so3_inverse_curvelet": [_P, _I, _I, _P, _P, _P],
+    "scv_so3_forward_curvelet": [_P, _I, _I, _P, _P, _P],
+    "scv_accumulate": [_P, _I, _I, _P, _P, _P, _P, _P],
+    "scv_accumulate_scaling": [_P, _I, _I, _P, _P, _P, _P],
+    "scv_finish_acc": [_P, _I, _I, _I, _P, _P],
+}
+_RESTYPE = {"scv_last_error": ctypes.c_char_p, "scv_workspace_bytes": ctypes.c_longlong}
+
+EXPORTED = tuple(_SIGS)
+
+
+def load_library(path: str | None = None):
+    """Load (once) and type the C ABI.  Raises if the library is missing."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        p = path or LIB_PATH
+        if not os.path.exists(p):
+            raise RuntimeError(
+                f"{p} not found: build the CUDA library first "
+                "(python -m paper_1511_05578_b200.build); there is no CPU fallback")
+        lib = ctypes.CDLL(p)
+        for name, args in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = _RESTYPE.get(name, ctypes.c_int)
+        _lib = lib
+        return lib
+
+
+class Context:
+    """One scv_ctx bound to one CUDA device."""
+
+    def __init__(self, device: int):
+        lib = load_library()
+        self.lib = lib
+        self.device = device
+        self.lock = threading.RLock()
+        h = _P()
+        rc = lib.scv_create(device, ctypes.byref(h))
+        if rc != SCV_OK:
+            raise RuntimeError(f"scv_create(device={device}) failed with code {rc}")
+        self.handle = h
+
+    def call(self, name: str, *args):
+        """Invoke scv_<name>(ctx, *args, stream) on torch's current stream."""
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        with self.lock:
+            rc = getattr(self.lib, "scv_" + name)(self.handle, *args, _P(stream))
+            if rc != SCV_OK:
+                msg = self.lib.scv_last_error(self.handle).decode(errors="replace")
+                if rc == SCV_EINVAL:
+                    raise ValueError(msg)
+                if rc == SCV_ETYPE:
+                    raise TypeError(msg)
+                raise RuntimeError(f"scv_{name} failed ({rc}): {msg}")
+
+    def workspace_bytes(self) -> int:
+        return int(self.lib.scv_workspace_bytes(self.handle))
+
+    def trim(self):
+        with self.lock:
+            torch.cuda.synchronize(self.device)
+            self.lib.scv_trim(self.handle)
+
+    def __del__(self):
+        try:
+            self.lib.scv_destroy(self.handle)
+        except Exception:
+            pass
+
+
+_ctxs: dict = {}
+_ctx_lock = threading.Lock()
+
+
+def context(device: torch.device | int | None = None) -> Context:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1511_05578_b200 needs a CUDA device (B200); there is no CPU fallback")
+    if device is None:
+        idx = torch.cuda.current_device()
+    elif isinstance(device, torch.device):
+        idx = device.index if device.index is not None else torch.cuda.current_device()
+    else:
+        idx = int(device)
+    with _ctx_lock:
+        if idx not in _ctxs:
+            _ctxs[idx] = Context(idx)
+        return _ctxs[idx]
+
+
+def ptr(t: torch.Tensor) -> ctypes.c_void_p:
+    return _P(t.data_ptr())

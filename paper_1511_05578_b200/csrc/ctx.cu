@@ -1,0 +1,344 @@
+// Context, constant tables, cuFFT plan cache and scratch management.
+//
+// The reference keeps three process-global caches: the Delta(pi/2) table
+// (wigner.py:226-240), the weight-kernel FFT (fourier.py:68-81) and the
+// tiling step table.  Here the device-side equivalents live in a per-device
+// context: the Delta wedge (built on the GPU by the degree recursion), the
+// Bluestein / weight-convolution spectra used by the beta stage, cuFFT plans
+// for the alpha/gamma stages, and grow-only scratch.  Host-side constants
+// are computed in long double so the device tables carry correctly rounded
+// float64 values.
+
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+
+#include "scv_internal.cuh"
+
+typedef long double ld;
+typedef std::complex<ld> cld;
+
+static const ld kPi = 3.141592653589793238462643383279502884L;
+
+int scv_fail(scv_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+// ---------------------------------------------------------------------------
+// long-double host helpers
+// ---------------------------------------------------------------------------
+static std::vector<ld> log_factorials(int n) {
+  std::vector<ld> lf(n + 1);
+  lf[0] = 0.0L;
+  for (int i = 1; i <= n; ++i) lf[i] = lf[i - 1] + logl((ld)i);
+  return lf;
+}
+
+// exp(i*pi*num/den) with num reduced exactly mod 2*den
+static cld expipi(long long num, long long den) {
+  long long r = num % (2 * den);
+  if (r < 0) r += 2 * den;
+  ld a = kPi * (ld)r / (ld)den;
+  return cld(cosl(a), sinl(a));
+}
+
+static void fft_ld(std::vector<cld>& a) {  // forward, in place, radix-2
+  size_t n = a.size();
+  for (size_t i = 1, j = 0; i < n; ++i) {
+    size_t bit = n >> 1;
+    for (; j & bit; bit >>= 1) j ^= bit;
+    j ^= bit;
+    if (i < j) std::swap(a[i], a[j]);
+  }
+  for (size_t len = 2; len <= n; len <<= 1) {
+    for (size_t i = 0; i < n; i += len)
+      for (size_t k = 0; k < len / 2; ++k) {
+        cld w = expipi(-2LL * (long long)k, (long long)len);
+        cld u = a[i + k], v = a[i + k + len / 2] * w;
+        a[i + k] = u + v;
+        a[i + k + len / 2] = u - v;
+      }
+  }
+}
+
+static inline ld w_even(long long k) {  // even part of w(k)=int_0^pi sin e^{ik}
+  if (k & 1) return 0.0L;
+  return 2.0L / (1.0L - (ld)k * (ld)k);
+}
+
+template <typename T>
+static int upload(scv_ctx* c, T** dst, const std::vector<T>& src, cudaStream_t s) {
+  SCV_CUDA(c, cudaMalloc((void**)dst, src.size() * sizeof(T)));
+  SCV_CUDA(c, cudaMemcpyAsync(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  SCV_CUDA(c, cudaStreamSynchronize(s));
+  return SCV_OK;
+}
+
+static std::vector<double2> to_d2(const std::vector<cld>& v) {
+  std::vector<double2> o(v.size());
+  for (size_t i = 0; i < v.size(); ++i) o[i] = make_double2((double)v[i].real(), (double)v[i].imag());
+  return o;
+}
+
+// ---------------------------------------------------------------------------
+// tables
+// ---------------------------------------------------------------------------
+int scv_ensure_hlb(scv_ctx* c, int L, cudaStream_t s) {
+  if (c->hlb && c->hlb_L >= L) return SCV_OK;
+  int Lb = L;
+  std::vector<ld> lf = log_factorials(2 * Lb + 2);
+  std::vector<double> h((size_t)Lb * (Lb + 1) / 2);
+  for (int l = 0; l < Lb; ++l)
+    for (int k = 0; k <= l; ++k)
+      h[(size_t)l * (l + 1) / 2 + k] = (double)(0.5L * (lf[2 * l] - lf[l + k] - lf[l - k]));
+  if (c->hlb) cudaFree(c->hlb);
+  c->hlb = nullptr;
+  SCV_TRY(upload(c, &c->hlb, h, s));
+  c->hlb_L = Lb;
+  return SCV_OK;
+}
+
+int scv_ensure_delta(scv_ctx* c, int L, cudaStream_t s) {
+  if (c->delta && c->delta_L >= L) return SCV_OK;
+  // edge rows Delta^l_{l,m} = (-1)^{l-m} sqrt(C(2l,l+m)) / 2^l  (wigner.py:153-161)
+  std::vector<ld> lf = log_factorials(2 * L + 2);
+  std::vector<double> edge((size_t)L * (L + 1) / 2);
+  for (int l = 0; l < L; ++l)
+    for (int m = 0; m <= l; ++m) {
+      ld v = expl(0.5L * (lf[2 * l] - lf[l + m] - lf[l - m]) - (ld)l * logl(2.0L));
+      if ((l - m) & 1) v = -v;
+      edge[(size_t)l * (l + 1) / 2 + m] = (double)v;
+    }
+  if (L > 1) {  // seed plane of build_halfpi_table (wigner.py:214-218) uses 1/sqrt(2.0)
+    edge[1] = -1.0 / std::sqrt(2.0);
+    edge[2] = 0.5;
+  }
+  double* d_edge = nullptr;
+  SCV_TRY(upload(c, &d_edge, edge, s));
+  double* tab = nullptr;
+  cudaError_t e = cudaMalloc((void**)&tab, (size_t)wedge_size(L) * sizeof(double));
+  if (e != cudaSuccess) {
+    cudaFree(d_edge);
+    return scv_fail(c, SCV_ENOMEM, "cudaMalloc(delta wedge): " + std::string(cudaGetErrorString(e)));
+  }
+  int rc = scv_launch_delta_wedge(c, L, d_edge, tab, s);
+  cudaStreamSynchronize(s);
+  cudaFree(d_edge);
+  if (rc != SCV_OK) {
+    cudaFree(tab);
+    return rc;
+  }
+  if (c->delta) cudaFree(c->delta);
+  c->delta = tab;
+  c->delta_L = L;
+  return SCV_OK;
+}
+
+int scv_get_beta_tables(scv_ctx* c, int L, cudaStream_t s, const BetaTables** out) {
+  auto it = c->beta.find(L);
+  if (it != c->beta.end()) {
+    *out = &it->second;
+    return SCV_OK;
+  }
+  BetaTables t;
+  t.L = L;
+  t.K = 2 * L - 1;
+  t.logP = next_pow2_log(4 * L - 3);
+  if (t.logP < 4) t.logP = 4;
+  t.P = 1 << t.logP;
+  const int K = t.K, P = t.P;
+  std::vector<cld> tw(P), A(K), h(P, cld(0, 0)), C(K), v(P, cld(0, 0));
+  for (int k = 0; k < P; ++k) tw[k] = expipi(-2LL * k, P);
+  for (int b = 0; b < K; ++b) A[b] = expipi(-(long long)b * b, K);
+  // h[j] = exp(+i pi j^2 / K) for j in [-(3L-3), L-1], stored at j mod P
+  for (int j = -(3 * L - 3); j <= L - 1; ++j) h[((j % P) + P) % P] = expipi((long long)j * j, K);
+  for (int q = 0; q < K; ++q) {
+    long long mpp = q - (L - 1);
+    C[q] = expipi(-(mpp * mpp + mpp), K) / (ld)K;
+  }
+  for (int q = 0; q <= 4 * L - 4; ++q) v[q] = cld(w_even(2LL * (L - 1) - q), 0);
+  fft_ld(h);
+  fft_ld(v);
+  for (int k = 0; k < P; ++k) {
+    h[k] /= (ld)P;
+    v[k] /= (ld)P;
+  }
+  std::vector<double> Aalt(K), lsin(L), lcos(L);
+  for (int q = 0; q < K; ++q) {
+    long long mp = q - (L - 1);
+    ld acc = 0;
+    for (long long mpp = -(L - 1); mpp <= L - 1; ++mpp) acc += w_even(mpp - mp) * ((mpp & 1) ? -1.0L : 1.0L);
+    Aalt[q] = (double)acc;
+  }
+  for (int b = 0; b < L; ++b) {
+    // beta_b/2 = pi(2b+1)/(2K); cos(beta_b/2) = sin(pi(K-2b-1)/(2K)) keeps the
+    // beta=pi node (b=L-1) exactly at cos=0 -> log = -inf (d vanishes there)
+    lsin[b] = (double)logl(sinl(kPi * (ld)(2 * b + 1) / (ld)(2 * K)));
+    const int r = K - 2 * b - 1;
+    lcos[b] = r == 0 ? -HUGE_VAL : (double)logl(sinl(kPi * (ld)r / (ld)(2 * K)));
+  }
+  SCV_TRY(upload(c, &t.tw, to_d2(tw), s));
+  SCV_TRY(upload(c, &t.chirpA, to_d2(A), s));
+  SCV_TRY(upload(c, &t.Hf, to_d2(h), s));
+  SCV_TRY(upload(c, &t.chirpC, to_d2(C), s));
+  SCV_TRY(upload(c, &t.Vf, to_d2(v), s));
+  SCV_TRY(upload(c, &t.Aalt, Aalt, s));
+  SCV_TRY(upload(c, &t.sinh, lsin, s));
+  SCV_TRY(upload(c, &t.cosh, lcos, s));
+  auto res = c->beta.emplace(L, t);
+  *out = &res.first->second;
+  return SCV_OK;
+}
+
+int scv_scratch(scv_ctx* c, int slot, size_t bytes, void** out) {
+  if (bytes == 0) bytes = 16;
+  if (c->scratch_bytes[slot] < bytes) {
+    if (c->scratch[slot]) {
+      cudaDeviceSynchronize();
+      cudaFree(c->scratch[slot]);
+      c->scratch[slot] = nullptr;
+      c->scratch_bytes[slot] = 0;
+    }
+    cudaError_t e = cudaMalloc(&c->scratch[slot], bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      char buf[128];
+      snprintf(buf, sizeof buf, "cudaMalloc(scratch %d, %.3f GB): ", slot, bytes / 1e9);
+      return scv_fail(c, SCV_ENOMEM, std::string(buf) + cudaGetErrorString(e));
+    }
+    c->scratch_bytes[slot] = bytes;
+  }
+  *out = c->scratch[slot];
+  return SCV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// cuFFT plans (alpha / gamma / phi stages only; the beta stage is hand-written)
+// ---------------------------------------------------------------------------
+int scv_plan(scv_ctx* c, const std::string& key, int rank, int* n, int* inembed, int istride,
+             int idist, int* onembed, int ostride, int odist, cufftType type, int batch,
+             cufftHandle* out) {
+  auto it = c->plans.find(key);
+  if (it != c->plans.end()) {
+    *out = it->second.h;
+    return SCV_OK;
+  }
+  FftPlan p;
+  SCV_CUFFT(c, cufftCreate(&p.h));
+  SCV_CUFFT(c, cufftSetAutoAllocation(p.h, 0));
+  size_t work = 0;
+  cufftResult r = cufftMakePlanMany(p.h, rank, n, inembed, istride, idist, onembed, ostride, odist,
+                                    type, batch, &work);
+  if (r != CUFFT_SUCCESS) {
+    cufftDestroy(p.h);
+    return scv_fail(c, SCV_ECUFFT, "cufftMakePlanMany(" + key + ") failed: " + std::to_string((int)r));
+  }
+  p.work = work;
+  if (work > c->fft_work_bytes) {
+    if (c->fft_work) {
+      cudaDeviceSynchronize();
+      cudaFree(c->fft_work);
+    }
+    c->fft_work = nullptr;
+    c->fft_work_bytes = 0;
+    cudaError_t e = cudaMalloc(&c->fft_work, work);
+    if (e != cudaSuccess) {
+      cufftDestroy(p.h);
+      cudaGetLastError();
+      return scv_fail(c, SCV_ENOMEM, "cudaMalloc(cufft work " + std::to_string(work) + ")");
+    }
+    c->fft_work_bytes = work;
+  }
+  c->plans[key] = p;
+  *out = p.h;
+  return SCV_OK;
+}
+
+int scv_plan_exec_setup(scv_ctx* c, cufftHandle h, cudaStream_t s) {
+  SCV_CUFFT(c, cufftSetStream(h, s));
+  SCV_CUFFT(c, cufftSetWorkArea(h, c->fft_work));
+  return SCV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// C ABI: lifecycle
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int scv_version(void) { return 100; }
+
+int scv_create(int device, scv_ctx** out) {
+  if (!out) return SCV_EINVAL;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return SCV_ECUDA;
+  }
+  if (device < 0 || device >= n) return SCV_EINVAL;
+  if (cudaSetDevice(device) != cudaSuccess) return SCV_ECUDA;
+  scv_ctx* c = new scv_ctx();
+  c->device = device;
+  *out = c;
+  return SCV_OK;
+}
+
+int scv_destroy(scv_ctx* c) {
+  if (!c) return SCV_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (auto& kv : c->plans) cufftDestroy(kv.second.h);
+  for (auto& kv : c->beta) {
+    BetaTables& t = kv.second;
+    cudaFree(t.tw); cudaFree(t.chirpA); cudaFree(t.Hf); cudaFree(t.chirpC);
+    cudaFree(t.Vf); cudaFree(t.Aalt); cudaFree(t.sinh); cudaFree(t.cosh);
+  }
+  for (auto& kv : c->aux) cudaFree(kv.second);
+  if (c->fft_work) cudaFree(c->fft_work);
+  for (int i = 0; i < 3; ++i)
+    if (c->scratch[i]) cudaFree(c->scratch[i]);
+  if (c->delta) cudaFree(c->delta);
+  if (c->hlb) cudaFree(c->hlb);
+  delete c;
+  return SCV_OK;
+}
+
+const char* scv_last_error(const scv_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+long long scv_workspace_bytes(const scv_ctx* c) {
+  if (!c) return 0;
+  long long b = (long long)c->fft_work_bytes;
+  for (int i = 0; i < 3; ++i) b += (long long)c->scratch_bytes[i];
+  if (c->delta) b += wedge_size(c->delta_L) * 8;
+  return b;
+}
+
+int scv_trim(scv_ctx* c) {
+  if (!c) return SCV_EINVAL;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (int i = 0; i < 3; ++i) {
+    if (c->scratch[i]) cudaFree(c->scratch[i]);
+    c->scratch[i] = nullptr;
+    c->scratch_bytes[i] = 0;
+  }
+  for (auto& kv : c->plans) cufftDestroy(kv.second.h);
+  c->plans.clear();
+  if (c->fft_work) cudaFree(c->fft_work);
+  c->fft_work = nullptr;
+  c->fft_work_bytes = 0;
+  return SCV_OK;
+}
+
+int scv_halfpi_wedge(scv_ctx* c, int L, double* out, void* stream) {
+  if (!c) return SCV_EINVAL;
+  if (L < 1) return scv_fail(c, SCV_EINVAL, "band limit must be positive, got " + std::to_string(L));
+  cudaStream_t s = (cudaStream_t)stream;
+  SCV_CUDA(c, cudaSetDevice(c->device));
+  SCV_TRY(scv_ensure_delta(c, L, s));
+  SCV_CUDA(c, cudaMemcpyAsync(out, c->delta, (size_t)wedge_size(L) * 8, cudaMemcpyDeviceToDevice, s));
+  return SCV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,179 @@
+// Spin spherical harmonic transforms on the MW grid (sphere.py:155-260).
+//
+// forward: phi FFT (cuFFT) -> hand-written beta stage (beta.cu) ->
+//          Delta contraction over n=-s (k_sht_contract, one warp per (l,m))
+// inverse: Delta outer-product sum into the centred bin plane
+//          (k_sht_bins, one thread per bin (m',m), loop over l) ->
+//          2-D inverse FFT (cuFFT), rows t<L kept.
+
+#include <cmath>
+
+#include "scv_internal.cuh"
+
+__device__ __forceinline__ double sht_amp(int l, int spin) {
+  double a = sqrt((double)(2 * l + 1) / (4.0 * SCV_PI));
+  return (spin & 1) ? -a : a;
+}
+
+// flm[l^2+l+m] = amp(l,s) i^{m+s} sum_m' D_{m'm} D_{m',-s} Gw[m',m]   (sphere.py:171-181)
+// real: m>=0 half + conjugate fill (sphere.py:226-236)
+__global__ void k_sht_contract(int L, int spin, int real, const double2* __restrict__ Gw,
+                               const double* __restrict__ delta, double2* __restrict__ flm) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= L * L) return;
+  int ll = (int)sqrt((double)warp);
+  while (ll * ll > warp) --ll;
+  while ((ll + 1) * (ll + 1) <= warp) ++ll;
+  const int m = warp - ll * ll - ll;
+  if (real && m < 0) return;
+  const int as = spin < 0 ? -spin : spin;
+  if (ll < as) {
+    if (lane == 0) flm[warp] = make_double2(0.0, 0.0);
+    return;
+  }
+  const int ncol = real ? L : 2 * L - 1;
+  const int coff = real ? 0 : L - 1;
+  double sx = 0.0, sy = 0.0;
+  for (int mp = -ll + lane; mp <= ll; mp += 32) {
+    const double d = wedge_get(delta, ll, mp, m) * wedge_get(delta, ll, mp, -spin);
+    const double2 g = Gw[(long long)(mp + L - 1) * ncol + m + coff];
+    sx += d * g.x;
+    sy += d * g.y;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    sx += __shfl_xor_sync(0xffffffffu, sx, o);
+    sy += __shfl_xor_sync(0xffffffffu, sy, o);
+  }
+  if (lane == 0) {
+    const double a = sht_amp(ll, spin);
+    double2 v = cipow(make_double2(sx * a, sy * a), m + spin);
+    flm[warp] = v;
+    if (real && m > 0) {
+      double2 cv = make_double2(v.x, -v.y);
+      if (m & 1) cv = make_double2(-cv.x, -cv.y);
+      flm[ll * ll + ll - m] = cv;
+    }
+  }
+}
+
+// B[m' mod K][m mod K] = e^{i m' pi/K} i^{-(m+s)} sum_{l} amp D_{m'm} D_{m',-s} f_lm   (sphere.py:191-203)
+// real: B[m' mod K][m], m in [0,L)   (sphere.py:245-252)
+__global__ void k_sht_bins(int L, int spin, int real, const double2* __restrict__ flm,
+                           const double* __restrict__ delta, double2* __restrict__ B) {
+  const int K = 2 * L - 1;
+  const int ncol = real ? L : K;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)K * ncol) return;
+  const int r = (int)(idx / ncol), cidx = (int)(idx % ncol);
+  const int mp = r - (L - 1);
+  const int m = real ? cidx : cidx - (L - 1);
+  const int as = spin < 0 ? -spin : spin;
+  int l0 = mp < 0 ? -mp : mp;
+  const int am = m < 0 ? -m : m;
+  if (am > l0) l0 = am;
+  if (as > l0) l0 = as;
+  double sx = 0.0, sy = 0.0;
+  for (int l = l0; l < L; ++l) {
+    const double a = sht_amp(l, spin);
+    const double2 f = flm[l * l + l + m];
+    const double u = wedge_get(delta, l, mp, -spin);
+    const double d = wedge_get(delta, l, mp, m);
+    // (u * (amp f)) * d  -- reference order
+    sx += (u * (a * f.x)) * d;
+    sy += (u * (a * f.y)) * d;
+  }
+  double2 v = cipow(make_double2(sx, sy), -(m + spin));
+  double sn, cs;
+  sincos((double)mp * (SCV_PI / (double)K), &sn, &cs);
+  v = cmul(v, make_double2(cs, sn));
+  const int row = ((mp % K) + K) % K;
+  const int col = real ? m : ((m % K) + K) % K;
+  B[(long long)row * ncol + col] = v;
+}
+
+__global__ void k_zero_imag_col0(double2* B, int rows, int pitch) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < rows) B[(long long)t * pitch].y = 0.0;
+}
+
+static int check_sht_args(scv_ctx* c, int L, int spin, int real) {
+  if (L < 1) return scv_fail(c, SCV_EINVAL, "band limit must be positive, got " + std::to_string(L));
+  if (std::abs(spin) >= L)
+    return scv_fail(c, SCV_EINVAL, "spin " + std::to_string(spin) + " out of range for band limit " + std::to_string(L));
+  if (real && spin != 0) return scv_fail(c, SCV_EINVAL, "real signals must have spin 0");
+  return SCV_OK;
+}
+
+extern "C" int scv_sht_forward(scv_ctx* c, int L, int spin, int real, const void* f, double* flm,
+                               void* stream) {
+  if (!c) return SCV_EINVAL;
+  SCV_TRY(check_sht_args(c, L, spin, real));
+  cudaStream_t s = (cudaStream_t)stream;
+  SCV_CUDA(c, cudaSetDevice(c->device));
+  SCV_TRY(scv_ensure_delta(c, L, s));
+  const int K = 2 * L - 1;
+  const int ncol = real ? L : K;
+  void* G = nullptr;
+  void* Gw = nullptr;
+  SCV_TRY(scv_scratch(c, 1, (size_t)L * ncol * 16, &G));
+  SCV_TRY(scv_scratch(c, 2, (size_t)K * ncol * 16, &Gw));
+  cufftHandle h;
+  int n[1] = {K};
+  if (real) {
+    int on[1] = {L};
+    SCV_TRY(scv_plan(c, "sht_phi_d2z_" + std::to_string(L), 1, n, n, 1, K, on, 1, L, CUFFT_D2Z, L, &h));
+    SCV_TRY(scv_plan_exec_setup(c, h, s));
+    SCV_CUFFT(c, cufftExecD2Z(h, (double*)f, (cufftDoubleComplex*)G));
+  } else {
+    SCV_TRY(scv_plan(c, "sht_phi_z2z_" + std::to_string(L), 1, n, n, 1, K, n, 1, K, CUFFT_Z2Z, L, &h));
+    SCV_TRY(scv_plan_exec_setup(c, h, s));
+    SCV_CUFFT(c, cufftExecZ2Z(h, (cufftDoubleComplex*)f, (cufftDoubleComplex*)G, CUFFT_FORWARD));
+  }
+  SCV_TRY(scv_beta_sht(c, L, spin, real, (const double2*)G, (double2*)Gw, 2.0 * SCV_PI / (double)K, s));
+  const long long warps = (long long)L * L;
+  k_sht_contract<<<(int)((warps * 32 + 255) / 256), 256, 0, s>>>(L, spin, real, (const double2*)Gw,
+                                                                 c->delta, (double2*)flm);
+  SCV_CUDA(c, cudaGetLastError());
+  return SCV_OK;
+}
+
+extern "C" int scv_sht_inverse(scv_ctx* c, int L, int spin, int real, const double* flm, void* f,
+                               void* stream) {
+  if (!c) return SCV_EINVAL;
+  SCV_TRY(check_sht_args(c, L, spin, real));
+  cudaStream_t s = (cudaStream_t)stream;
+  SCV_CUDA(c, cudaSetDevice(c->device));
+  SCV_TRY(scv_ensure_delta(c, L, s));
+  const int K = 2 * L - 1;
+  const int ncol = real ? L : K;
+  void* B = nullptr;
+  SCV_TRY(scv_scratch(c, 1, (size_t)K * ncol * 16, &B));
+  const long long tot = (long long)K * ncol;
+  k_sht_bins<<<(int)((tot + 127) / 128), 128, 0, s>>>(L, spin, real, (const double2*)flm, c->delta,
+                                                      (double2*)B);
+  SCV_CUDA(c, cudaGetLastError());
+  cufftHandle h;
+  if (!real) {
+    int n2[2] = {K, K};
+    SCV_TRY(scv_plan(c, "sht_inv2d_" + std::to_string(L), 2, n2, n2, 1, K * K, n2, 1, K * K, CUFFT_Z2Z, 1, &h));
+    SCV_TRY(scv_plan_exec_setup(c, h, s));
+    SCV_CUFFT(c, cufftExecZ2Z(h, (cufftDoubleComplex*)B, (cufftDoubleComplex*)B, CUFFT_INVERSE));
+    SCV_CUDA(c, cudaMemcpyAsync(f, B, (size_t)L * K * 16, cudaMemcpyDeviceToDevice, s));
+    return SCV_OK;
+  }
+  // theta: inverse along axis 0 of the (K, L) plane, columns strided by L
+  int n1[1] = {K};
+  int emb[1] = {K * L};
+  SCV_TRY(scv_plan(c, "sht_inv_theta_" + std::to_string(L), 1, n1, emb, L, 1, emb, L, 1, CUFFT_Z2Z, L, &h));
+  SCV_TRY(scv_plan_exec_setup(c, h, s));
+  SCV_CUFFT(c, cufftExecZ2Z(h, (cufftDoubleComplex*)B, (cufftDoubleComplex*)B, CUFFT_INVERSE));
+  // irfft discards Im of the DC bin (scipy semantics); make that explicit for cuFFT
+  k_zero_imag_col0<<<(L + 127) / 128, 128, 0, s>>>((double2*)B, L, L);
+  SCV_CUDA(c, cudaGetLastError());
+  int on[1] = {K}, in1[1] = {L};
+  SCV_TRY(scv_plan(c, "sht_inv_phi_z2d_" + std::to_string(L), 1, n1, in1, 1, L, on, 1, K, CUFFT_Z2D, L, &h));
+  SCV_TRY(scv_plan_exec_setup(c, h, s));
+  SCV_CUFFT(c, cufftExecZ2D(h, (cufftDoubleComplex*)B, (double*)f));
+  return SCV_OK;
+}

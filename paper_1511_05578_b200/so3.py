@@ -1,0 +1,170 @@
+"""SO(3) containers and the curvelet-sparse Wigner transforms (device).
+
+Drop-in mirror of the curvelet part of ``scurve.so3`` (so3.py:45-182,
+214-285, 349-417): ``SO3Grid``, ``SO3Signal``, ``CurveletWignerCoeffs``,
+``so3_inverse_curvelet(_real)`` and ``so3_forward_curvelet(_real)`` with
+the same shapes, ValueError/TypeError conditions and layouts.  The dense
+O(L^4) "general" transforms are validation oracles in the reference and
+are out of scope here.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from functools import cached_property
+
+import numpy as np
+import torch
+
+from . import _cabi
+from .sphere import _is_complex, _shape, as_device
+
+__all__ = [
+    "CurveletWignerCoeffs",
+    "SO3Grid",
+    "SO3Signal",
+    "so3_forward_curvelet",
+    "so3_forward_curvelet_real",
+    "so3_inverse_curvelet",
+    "so3_inverse_curvelet_real",
+]
+
+
+@dataclass(frozen=True)
+class SO3Grid:
+    """L betas, 2M-1 alphas, 2N-1 gammas; shape (2N-1, L, 2M-1) (so3.py:45-72)."""
+
+    L: int
+    M: int
+    N: int
+
+    def __post_init__(self):
+        for name in ("L", "M", "N"):
+            if getattr(self, name) < 1:
+                raise ValueError(f"{name} must be positive, got {getattr(self, name)}")
+
+    @cached_property
+    def alphas(self) -> np.ndarray:
+        return 2.0 * math.pi * np.arange(2 * self.M - 1) / (2 * self.M - 1)
+
+    @cached_property
+    def betas(self) -> np.ndarray:
+        return math.pi * (2.0 * np.arange(self.L) + 1.0) / (2 * self.L - 1)
+
+    @cached_property
+    def gammas(self) -> np.ndarray:
+        return 2.0 * math.pi * np.arange(2 * self.N - 1) / (2 * self.N - 1)
+
+    @property
+    def shape(self):
+        return (2 * self.N - 1, self.L, 2 * self.M - 1)
+
+
+@dataclass
+class SO3Signal:
+    """(gamma, beta, alpha) samples (so3.py:75-90)."""
+
+    grid: SO3Grid
+    values: torch.Tensor
+    real: bool = False
+
+    def __post_init__(self):
+        if _shape(self.values) != self.grid.shape:
+            raise ValueError(f"values shape {_shape(self.values)} does not match grid {self.grid.shape}")
+        if self.real and _is_complex(self.values):
+            raise ValueError("real signal carries complex values")
+        self.values = as_device(self.values, torch.float64 if self.real else torch.complex128)
+
+
+@dataclass
+class CurveletWignerCoeffs:
+    """Outer columns n=+-ell: values (2, L, 2L-1) (so3.py:124-182)."""
+
+    band_limit: int
+    values: torch.Tensor
+
+    def __post_init__(self):
+        L = self.band_limit
+        if L < 1:
+            raise ValueError(f"band limit must be positive, got {L}")
+        self.values = as_device(self.values, torch.complex128)
+        if _shape(self.values) != (2, L, 2 * L - 1):
+            raise ValueError(f"expected shape {(2, L, 2 * L - 1)}, got {_shape(self.values)}")
+
+    @classmethod
+    def zeros(cls, L: int) -> "CurveletWignerCoeffs":
+        return cls(L, np.zeros((2, L, 2 * L - 1), complex))
+
+    def row(self, n: int) -> torch.Tensor:
+        ell = abs(n)
+        if ell >= self.band_limit:
+            raise ValueError(f"|n| = {ell} out of range")
+        c = self.band_limit - 1
+        return self.values[0 if n >= 0 else 1, ell, c - ell: c + ell + 1]
+
+    def set_row(self, n: int, row) -> None:
+        self.row(n)[:] = as_device(row, torch.complex128)
+
+
+def _check_sparse_grid(w, grid):
+    if not isinstance(w, CurveletWignerCoeffs):
+        raise TypeError("sparse synthesis requires CurveletWignerCoeffs")
+    L = w.band_limit
+    if not (grid.L == L and grid.M == L and grid.N == L):
+        raise ValueError("sparse path requires a grid with N = M = L matching the coefficients")
+    return L
+
+
+def so3_inverse_curvelet(w: CurveletWignerCoeffs, grid: SO3Grid, out: torch.Tensor | None = None) -> SO3Signal:
+    """Sparse synthesis onto the grid, O(L^3 log L) (so3.py:259-285)."""
+    L = _check_sparse_grid(w, grid)
+    K = 2 * L - 1
+    dev = w.values.device
+    if out is None:
+        out = torch.empty((K, L, K), dtype=torch.complex128, device=dev)
+    _cabi.context(dev).call("so3_inverse_curvelet", L, 0, _cabi.ptr(w.values), _cabi.ptr(out))
+    return SO3Signal(grid, out)
+
+
+def so3_inverse_curvelet_real(w: CurveletWignerCoeffs, grid: SO3Grid, out: torch.Tensor | None = None) -> SO3Signal:
+    """Sparse synthesis to real samples via half the gamma spectrum
+    (so3.py:386-417); assumes real-signal symmetry of the coefficients."""
+    L = _check_sparse_grid(w, grid)
+    K = 2 * L - 1
+    dev = w.values.device
+    if out is None:
+        out = torch.empty((K, L, K), dtype=torch.float64, device=dev)
+    _cabi.context(dev).call("so3_inverse_curvelet", L, 1, _cabi.ptr(w.values), _cabi.ptr(out))
+    return SO3Signal(grid, out, real=True)
+
+
+def _check_forward(f: SO3Signal) -> int:
+    grid = f.grid
+    L = grid.L
+    if not (grid.M == L and grid.N == L):
+        raise ValueError("sparse path requires N = M = L")
+    return L
+
+
+def so3_forward_curvelet(f: SO3Signal, out: torch.Tensor | None = None) -> CurveletWignerCoeffs:
+    """Forward Wigner transform onto the n=+-ell columns (so3.py:214-244)."""
+    L = _check_forward(f)
+    vals = f.values if not f.real else f.values.to(torch.complex128)
+    dev = vals.device
+    if out is None:
+        out = torch.empty((2, L, 2 * L - 1), dtype=torch.complex128, device=dev)
+    _cabi.context(dev).call("so3_forward_curvelet", L, 0, _cabi.ptr(vals), _cabi.ptr(out))
+    return CurveletWignerCoeffs(L, out)
+
+
+def so3_forward_curvelet_real(f: SO3Signal, out: torch.Tensor | None = None) -> CurveletWignerCoeffs:
+    """Forward transform of a real signal via rfft along gamma (so3.py:349-383)."""
+    if not f.real:
+        raise ValueError("real path requires a real-flagged signal")
+    L = _check_forward(f)
+    dev = f.values.device
+    if out is None:
+        out = torch.empty((2, L, 2 * L - 1), dtype=torch.complex128, device=dev)
+    _cabi.context(dev).call("so3_forward_curvelet", L, 1, _cabi.ptr(f.values), _cabi.ptr(out))
+    return CurveletWignerCoeffs(L, out)

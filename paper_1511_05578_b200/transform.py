@@ -1,0 +1,211 @@
+"""Curvelet analysis and synthesis — the drop-in entry points.
+
+Mirrors ``scurve.transform`` (transform.py:63-253): ``analyze``,
+``synthesize``, ``analyze_real``, ``synthesize_real``, ``CurveletCoeffs``,
+``scale_band_limit``, ``scaling_band_limit`` — same arguments, checks
+(ValueError on band-limit / spin / frame / params mismatch) and output
+layouts.  Every arithmetic step runs in libscurve_b200.so on the device;
+the Python layer only sequences the calls, allocates outputs and validates.
+
+Ordering is the reference's: scales coarse -> fine, then the scaling part,
+so the synthesis accumulation is deterministic.
+"""
+
+from __future__ import annotations
+
+import math
+import threading
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _cabi
+from .so3 import (CurveletWignerCoeffs, SO3Grid, SO3Signal, so3_forward_curvelet,
+                  so3_forward_curvelet_real, so3_inverse_curvelet, so3_inverse_curvelet_real)
+from .sphere import (HarmonicCoeffs, SphereGrid, SphereSignal, sht_forward, sht_forward_real,
+                     sht_inverse, sht_inverse_real)
+from .tiling import Tiling, TilingParams, curvelet_harmonics
+
+__all__ = [
+    "CurveletCoeffs",
+    "analyze",
+    "analyze_real",
+    "scale_band_limit",
+    "scaling_band_limit",
+    "synthesize",
+    "synthesize_real",
+]
+
+
+def scale_band_limit(params: TilingParams, j: int) -> int:
+    """min(ceil(lam^(j+1)), L) (transform.py:63-67)."""
+    if not params.j_min <= j <= params.j_max:
+        raise ValueError(f"scale {j} outside [{params.j_min}, {params.j_max}]")
+    return min(math.ceil(params.lam ** (j + 1)), params.band_limit)
+
+
+def scaling_band_limit(params: TilingParams) -> int:
+    """min(ceil(lam^j_min), L) (transform.py:70-72)."""
+    return min(math.ceil(params.lam ** params.j_min), params.band_limit)
+
+
+@dataclass
+class CurveletCoeffs:
+    """Scale signals plus the low-frequency residue (transform.py:75-101)."""
+
+    params: TilingParams
+    frame: str
+    scaling: SphereSignal
+    scales: list
+    multires: bool = True
+    real: bool = False
+
+    def __post_init__(self):
+        if self.frame not in ("unrotated", "north"):
+            raise ValueError(f"unknown frame {self.frame!r}")
+        if len(self.scales) != self.params.scale_count:
+            raise ValueError(f"expected {self.params.scale_count} scale signals, got {len(self.scales)}")
+
+    def scale(self, j: int):
+        if not self.params.j_min <= j <= self.params.j_max:
+            raise ValueError(f"scale {j} out of range")
+        return self.scales[j - self.params.j_min]
+
+
+# ---------------------------------------------------------------------------
+# tiling arrays on the device (uploaded once per Tiling object)
+# ---------------------------------------------------------------------------
+_tcache: dict = {}
+_tcache_lock = threading.Lock()
+
+
+class _DevTiling:
+    def __init__(self, t, device):
+        p = t.params
+        self.psi = {}
+        for j in range(p.j_min, p.j_max + 1):
+            pos, neg = curvelet_harmonics(t, j)
+            self.psi[j] = (torch.as_tensor(np.ascontiguousarray(pos), dtype=torch.float64, device=device),
+                           torch.as_tensor(np.ascontiguousarray(neg), dtype=torch.float64, device=device))
+        self.scaling = torch.as_tensor(np.ascontiguousarray(t.scaling), dtype=torch.float64, device=device)
+
+
+def device_tiling(t, device) -> _DevTiling:
+    key = (id(t), str(device))
+    with _tcache_lock:
+        hit = _tcache.get(key)
+        if hit is not None and hit[0]() is t:
+            return hit[1]
+        d = _DevTiling(t, device)
+        try:
+            ref = weakref.ref(t)
+        except TypeError:
+            ref = lambda t=t: t  # noqa: E731
+        _tcache[key] = (ref, d)
+        return d
+
+
+def _check_signal(f: SphereSignal, t) -> None:
+    p = t.params
+    if f.grid.band_limit != p.band_limit:
+        raise ValueError(f"signal band limit {f.grid.band_limit} does not match tiling {p.band_limit}")
+    if f.spin != p.spin:
+        raise ValueError(f"signal spin {f.spin} does not match tiling spin {p.spin}")
+
+
+def _scale_wigner(ctx, flm: HarmonicCoeffs, dt: _DevTiling, j: int, Lj: int) -> CurveletWignerCoeffs:
+    """transform.py:104-115 on the device."""
+    pos, neg = dt.psi[j]
+    w = torch.empty((2, Lj, 2 * Lj - 1), dtype=torch.complex128, device=flm.values.device)
+    ctx.call("scale_product", flm.band_limit, Lj, _cabi.ptr(flm.values), _cabi.ptr(pos), _cabi.ptr(neg),
+             _cabi.ptr(w))
+    return CurveletWignerCoeffs(Lj, w)
+
+
+def _scaling_coeffs(ctx, flm: HarmonicCoeffs, dt: _DevTiling, Ls: int, real: bool) -> HarmonicCoeffs:
+    """transform.py:128-136 on the device."""
+    out = torch.empty(Ls * Ls, dtype=torch.complex128, device=flm.values.device)
+    ctx.call("scaling_product", flm.band_limit, Ls, _cabi.ptr(flm.values), _cabi.ptr(dt.scaling), _cabi.ptr(out))
+    return HarmonicCoeffs(Ls, 0, out, real=real)
+
+
+def _analyze(f: SphereSignal, t, multires: bool, real: bool, scale_out=None) -> CurveletCoeffs:
+    _check_signal(f, t)
+    p = t.params
+    L = p.band_limit
+    dev = f.values.device
+    ctx = _cabi.context(dev)
+    dt = device_tiling(t, dev)
+    flm = sht_forward_real(f) if real else sht_forward(f)
+    scales = []
+    for j in range(p.j_min, p.j_max + 1):
+        Lj = scale_band_limit(p, j) if multires else L
+        w = _scale_wigner(ctx, flm, dt, j, Lj)
+        buf = scale_out[j - p.j_min] if scale_out is not None else None
+        inv = so3_inverse_curvelet_real if real else so3_inverse_curvelet
+        scales.append(inv(w, SO3Grid(Lj, Lj, Lj), out=buf))
+    Ls = scaling_band_limit(p) if multires else L
+    s = _scaling_coeffs(ctx, flm, dt, Ls, real)
+    scaling_sig = sht_inverse_real(s) if real else sht_inverse(s)
+    return CurveletCoeffs(p, "unrotated", scaling_sig, scales, multires, real=real)
+
+
+def analyze(f: SphereSignal, t: Tiling, multires: bool = True, scale_out=None) -> CurveletCoeffs:
+    """Decompose a band-limited spin signal into directional scale signals
+    (transform.py:139-152).  ``scale_out`` optionally supplies preallocated
+    (K_j, L_j, K_j) output tensors, one per scale (device-resident reuse)."""
+    return _analyze(f, t, multires, False, scale_out)
+
+
+def analyze_real(f: SphereSignal, t: Tiling, multires: bool = True, scale_out=None) -> CurveletCoeffs:
+    """Half-spectrum analysis of a real signal (transform.py:190-210)."""
+    if not f.real:
+        raise ValueError("analyze_real requires a real-flagged signal")
+    return _analyze(f, t, multires, True, scale_out)
+
+
+def _synthesize(c: CurveletCoeffs, t, real: bool) -> SphereSignal:
+    p = t.params
+    if c.params != p:
+        raise ValueError("coefficients were built for a different tiling")
+    if c.frame != "unrotated":
+        raise ValueError("synthesis needs unrotated coefficients; apply rotate_from_north first")
+    L = p.band_limit
+    dev = c.scaling.values.device
+    ctx = _cabi.context(dev)
+    dt = device_tiling(t, dev)
+    acc = torch.zeros(L * L, dtype=torch.complex128, device=dev)
+    wbuf = None
+    for j in range(p.j_min, p.j_max + 1):
+        sig = c.scale(j)
+        expected = scale_band_limit(p, j) if c.multires else L
+        if sig.grid.L != expected:
+            raise ValueError(f"scale {j} stored at band limit {sig.grid.L}, expected {expected}")
+        Lj = sig.grid.L
+        need = 2 * Lj * (2 * Lj - 1)
+        if wbuf is None or wbuf.numel() < need:
+            wbuf = torch.empty(need, dtype=torch.complex128, device=dev)
+        wv = wbuf[:need].view(2, Lj, 2 * Lj - 1)
+        w = so3_forward_curvelet_real(sig, out=wv) if real else so3_forward_curvelet(sig, out=wv)
+        pos, neg = dt.psi[j]
+        ctx.call("accumulate", L, Lj, _cabi.ptr(w.values), _cabi.ptr(pos), _cabi.ptr(neg), _cabi.ptr(acc))
+    slm = sht_forward_real(c.scaling) if real else sht_forward(c.scaling)
+    ctx.call("accumulate_scaling", L, slm.band_limit, _cabi.ptr(slm.values), _cabi.ptr(dt.scaling), _cabi.ptr(acc))
+    ctx.call("finish_acc", L, p.spin, 1 if real else 0, _cabi.ptr(acc))
+    if real:
+        return sht_inverse_real(HarmonicCoeffs(L, 0, acc, real=True))
+    return sht_inverse(HarmonicCoeffs(L, p.spin, acc))
+
+
+def synthesize(c: CurveletCoeffs, t: Tiling) -> SphereSignal:
+    """Reassemble the sphere signal from its scale signals (transform.py:155-187)."""
+    return _synthesize(c, t, False)
+
+
+def synthesize_real(c: CurveletCoeffs, t: Tiling) -> SphereSignal:
+    """Synthesis matching analyze_real (transform.py:213-253)."""
+    if not c.real:
+        raise ValueError("synthesize_real requires real-flagged coefficients")
+    return _synthesize(c, t, True)

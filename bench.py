@@ -1,0 +1,380 @@
+"""Benchmark: curvelet analysis + synthesis maps/s (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--L 1024 --spin 0 --jmin 3 --lam 2] [--real]
+
+Default workload = BASELINE configs[3] (C4): L=1024, spin 0, B=lambda=2,
+J_min=3, one map with seeded Gaussian f_lm (C_l=(l+1)^-2, real-signal
+symmetry), complex128 path (analyze + synthesize).  A "step" is one full
+analysis + synthesis of one map; `value` is maps/s with the input map
+resident in HBM; `e2e` repeats the step through the public API with the
+map copied host->device and the reconstruction copied back every step.
+Every scale volume (68.6 GB at the finest scale) is far larger than the
+126 MB L2, so no explicit L2 flush is needed between steps.
+
+Multi-GPU (torchrun, one process per GPU): weak scaling over maps — each
+rank runs the full pipeline on its own seeded map (maps are the
+independent units), max-over-ranks device time.
+
+--impl reference times the reference algorithm's CPU implementation (the
+oracle port in oracle/, numpy + scipy.fft with all host threads) on a
+bounded sample of the same workload, on rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--L", type=int, default=1024)
+    ap.add_argument("--spin", type=int, default=0)
+    ap.add_argument("--jmin", type=int, default=3)
+    ap.add_argument("--lam", type=float, default=2.0)
+    ap.add_argument("--real", action="store_true", help="analyze_real/synthesize_real path")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile-json", default="")
+    return ap.parse_args()
+
+
+def gaussian_flm(L, spin, seed, real):
+    """BASELINE.json input recipe: Re/Im iid N(0, C_l/2)."""
+    rng = np.random.default_rng(seed)
+    ell = np.floor(np.sqrt(np.arange(L * L))).astype(np.int64)
+    v = (rng.standard_normal(L * L) + 1j * rng.standard_normal(L * L)) * np.sqrt((ell + 1.0) ** -2 / 2.0)
+    v[: spin * spin] = 0.0
+    if real:
+        for l in range(L):
+            row = v[l * l:(l + 1) ** 2]
+            row[l] = row[l].real
+            ms = np.arange(1, l + 1)
+            row[l - ms] = np.where(ms % 2 == 0, 1.0, -1.0) * np.conj(row[l + ms])
+    return v
+
+
+def workload_name(a):
+    path = "analyze_real+synthesize_real" if a.real else "analyze+synthesize"
+    return f"curvelet {path} L={a.L} spin={a.spin} B={a.lam:g} J0={a.jmin}"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons, pw = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+                pw.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "power_w_max": max(pw) if pw else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def algorithmic_work(a):
+    """Per-map algorithmic bytes / flops and per-scale sizes."""
+    from paper_1511_05578_b200 import TilingParams, scale_band_limit
+    p = TilingParams(a.L, a.spin, a.lam, a.jmin)
+    b = 8 if a.real else 16
+    Ljs = [scale_band_limit(p, j) for j in range(p.j_min, p.j_max + 1)]
+    V = [(2 * Lj - 1) ** 2 * Lj for Lj in Ljs]
+    B_alg = sum(2 * v * b for v in V) + 2 * a.L * (2 * a.L - 1) * b + 16 * a.L * a.L
+    F_alg = sum(2 * 5 * (2 * Lj - 1) ** 3 * math.log2((2 * Lj - 1) ** 3) for Lj in Ljs)
+    if a.real:
+        F_alg /= 2
+    return p, Ljs, B_alg, F_alg
+
+
+def stage_roofline(a, prof, Ljs, hbm_peak, fp64_peak):
+    """Roofline of the dominant stage from the live per-stage CUDA-event times."""
+    K = lambda L: 2 * L - 1  # noqa: E731
+    b = 8 if a.real else 16
+    # algorithmic bytes per call summed over the scales of one map (one call per scale)
+    vol = sum(K(L) ** 2 * L for L in Ljs)
+    cols = sum((2 * L * L - 1) * L for L in Ljs)
+    bytes_stage = {
+        "so3inv_gen": 16 * vol,                       # write the (n, b, alpha-bin) volume once
+        "so3inv_alpha_fft": 2 * 16 * vol,             # read + write
+        "so3inv_gamma_fft": 2 * 16 * vol,
+        "so3fwd_fft2d": (b + 16) * vol,               # read input + write chunk
+        "so3fwd_extract": 2 * 16 * cols,              # pruned read + write
+        "beta_so3": 16 * cols,                        # read pruned columns once
+    }
+    # algorithmic FP64 flops: beta stage = 4 P-point FFTs per column pair (5 P log2 P each)
+    def P_of(L):
+        return 1 << max(4, math.ceil(math.log2(4 * L - 3)))
+    flops_stage = {
+        "beta_so3": sum((L * L) * 4 * 5 * P_of(L) * math.log2(P_of(L)) for L in Ljs),
+    }
+    name, (cnt, ms) = max(prof.items(), key=lambda kv: kv[1][1])
+    per_launch_ms = ms / max(cnt, 1)
+    launches_per_map = len(Ljs)
+    out = {"stage": name}
+    if name in flops_stage:
+        fl = flops_stage[name] / launches_per_map
+        ach = fl / (per_launch_ms * 1e-3) / 1e12
+        out.update({"bound": "fp64", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
+                    "frac": ach / fp64_peak, "peak_source": "measured DFMA loop in this run (scv_fp64_peak)"})
+        by = bytes_stage.get(name, 0) / launches_per_map
+        out["hbm_gbs_alg"] = by / (per_launch_ms * 1e-3) / 1e9
+    else:
+        by = bytes_stage.get(name, 0) / launches_per_map
+        ach = by / (per_launch_ms * 1e-3) / 1e9
+        out.update({"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": ach / hbm_peak, "peak_source": "MEASURED_PEAKS.json hbm_gbs"})
+    out["traffic"] = None
+    out["ms_per_launch"] = per_launch_ms
+    return out
+
+
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1511_05578_b200 as sc
+    from paper_1511_05578_b200 import _cabi
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    ctx = _cabi.context(local)
+
+    p, Ljs, B_alg, F_alg = algorithmic_work(a)
+    t = sc.build_tiling(p)
+    real_sym = a.spin == 0
+    flm = gaussian_flm(a.L, a.spin, a.seed + rank, real_sym)
+    f = sc.sht_inverse(sc.HarmonicCoeffs(a.L, a.spin, flm))
+    if a.real:
+        f = sc.SphereSignal(f.grid, 0, f.values.real.contiguous(), real=True)
+    dtype = torch.float64 if a.real else torch.complex128
+    scale_out = [torch.empty((2 * Lj - 1, Lj, 2 * Lj - 1), dtype=dtype, device=dev) for Lj in Ljs]
+    ana = sc.analyze_real if a.real else sc.analyze
+    syn = sc.synthesize_real if a.real else sc.synthesize
+
+    def step(fin):
+        c = ana(fin, t, scale_out=scale_out)
+        return syn(c, t)
+
+    g = None
+    for _ in range(a.warmup):
+        g = step(f)
+    torch.cuda.synchronize()
+    rt_err = float((g.values - f.values).abs().max() / f.values.abs().max())
+
+    hbm_peak = None
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            hbm_peak = float(json.load(fh)["hbm_gbs"])
+    except Exception:
+        hbm_peak = 6650.0
+    fp64_peak = ctx.fp64_peak_tflops()
+
+    # ---------------- timed region (device-resident input) ----------------
+    stream = torch.cuda.current_stream()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ctx.profile_report()  # clear
+    ctx.profile(True)
+    l0 = ctx.launch_count()
+    clk = ClockSampler(local)
+    clk.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(a.steps):
+        g = step(f)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    ctx.profile(False)
+    launches = ctx.launch_count() - l0
+    prof = ctx.profile_report()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_per_step = ms / a.steps
+    value = world * a.steps / (ms * 1e-3)
+
+    # ---------------- e2e: host buffers through the public API ----------------
+    e2e = None
+    if not a.no_e2e:
+        host_in = torch.empty(f.values.shape, dtype=f.values.dtype, pin_memory=True)
+        host_in.copy_(f.values.cpu())
+        host_out = torch.empty_like(host_in, pin_memory=True)
+        dev_in = torch.empty_like(f.values)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(a.steps):
+            dev_in.copy_(host_in, non_blocking=True)
+            fin = sc.SphereSignal(f.grid, f.spin, dev_in, real=a.real)
+            gg = step(fin)
+            host_out.copy_(gg.values, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            tt = torch.tensor([ems], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ems = float(tt.item())
+        nb = host_in.numel() * host_in.element_size()
+        e2e = {"value": world * a.steps / (ems * 1e-3), "unit": "maps/s", "h2d_bytes_per_step": nb,
+               "d2h_bytes_per_step": nb, "ms_per_step": ems / a.steps}
+
+    roof = stage_roofline(a, prof, Ljs, hbm_peak, fp64_peak)
+    t_roof = max(B_alg / (hbm_peak * 1e9), F_alg / (fp64_peak * 1e12))
+    line = {
+        "metric": "curvelet analysis+synthesis maps/s",
+        "value": value,
+        "unit": "maps/s",
+        "n_gpus": world,
+        "steps": a.steps,
+        "warmup": a.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64" if a.real else "c128",
+        "data": "synthetic (seeded Gaussian f_lm, C_l=(l+1)^-2)",
+        "config": {"workload": workload_name(a), "L": a.L, "spin": a.spin, "lambda": a.lam,
+                   "j_min": a.jmin, "j_max": p.j_max, "scale_band_limits": Ljs,
+                   "maps_per_step_per_gpu": 1, "parallelism": f"maps x{world}" if world > 1 else "1 GPU",
+                   "l2_flush": "not needed: every scale volume >> 126 MB L2"},
+        "roofline": roof,
+        "paper_roofline": {"B_alg_GB": B_alg / 1e9, "F_alg_TF": F_alg / 1e12, "t_roof_ms": t_roof * 1e3,
+                           "frac": t_roof * 1e3 / ms_per_step, "fp64_peak_tflops": fp64_peak,
+                           "hbm_peak_gbs": hbm_peak},
+        "stages_ms_per_step": {k: v[1] / a.steps for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])},
+        "roundtrip_rel_err": rt_err,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "peak_mem_gb": torch.cuda.max_memory_allocated() / 1e9 + ctx.workspace_bytes() / 1e9,
+    }
+    if rank == 0 and not a.no_cpu_baseline:
+        from oracle import cpu_sample
+        line["cpu_baseline"] = cpu_sample.baseline(a.L, a.spin, a.lam, a.jmin, a.real, budget_s=20.0)
+    if a.profile_json and rank == 0:
+        with open(a.profile_json, "w") as fh:
+            json.dump(line, fh, indent=1)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import cpu_sample
+    p, Ljs, _, _ = algorithmic_work(a)
+    times = []
+    cb = None
+    for i in range(a.warmup + a.steps):
+        cb = cpu_sample.baseline(a.L, a.spin, a.lam, a.jmin, a.real, budget_s=8.0)
+        if i >= a.warmup:
+            times.append(cb["seconds_per_map"])
+    sec = statistics.median(times)
+    value = 1.0 / sec
+    cb["value"] = value
+    line = {
+        "impl": "reference",
+        "metric": "curvelet analysis+synthesis maps/s",
+        "value": value,
+        "unit": "maps/s",
+        "n_gpus": a.gpus,
+        "steps": a.steps,
+        "warmup": a.warmup,
+        "ms_per_step": sec * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64" if a.real else "c128",
+        "data": "synthetic (seeded Gaussian f_lm, C_l=(l+1)^-2)",
+        "config": {"workload": workload_name(a), "L": a.L, "spin": a.spin, "lambda": a.lam,
+                   "j_min": a.jmin, "j_max": p.j_max, "scale_band_limits": Ljs},
+        "cpu_baseline": cb,
+        "e2e": {"value": value, "unit": "maps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)

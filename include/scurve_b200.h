@@ -62,6 +62,19 @@ long long scv_workspace_bytes(const scv_ctx* ctx);
 /* Release every lazily grown scratch buffer (tables stay). */
 int scv_trim(scv_ctx* ctx);
 
+/* Stage profiler: when enabled, every launch group is bracketed by CUDA
+ * events on its stream.  scv_profile_report synchronises the device and
+ * writes "stage count total_ms\n" lines (then clears the records). */
+int scv_profile(scv_ctx* ctx, int enable);
+int scv_profile_report(scv_ctx* ctx, char* buf, int len);
+/* Number of this library's own kernels launched by the context so far. */
+long long scv_launch_count(const scv_ctx* ctx);
+
+/* Measured FP64 FMA throughput of this device (TFLOP/s, 2 flops per DFMA),
+ * from a register-resident DFMA loop over every SM; used as the roofline
+ * denominator for FP64-bound stages (MEASURED_PEAKS.json has no FP64 entry). */
+int scv_fp64_peak(scv_ctx* ctx, double* tflops);
+
 /* Delta^l_{m'm}(pi/2) for l < L in the 1/8 symmetry wedge 0 <= m <= m' <= l:
  * element (l, m', m) at l(l+1)(l+2)/6 + m'(m'+1)/2 + m.  Copies the context's
  * table (built on the device by the degree recursion) into `out`

@@ -35,6 +35,10 @@ _SIGS = {
     "scv_last_error": [_P],
     "scv_workspace_bytes": [_P],
     "scv_trim": [_P],
+    "scv_profile": [_P, _I],
+    "scv_launch_count": [_P],
+    "scv_profile_report": [_P, ctypes.c_char_p, _I],
+    "scv_fp64_peak": [_P, ctypes.POINTER(ctypes.c_double)],
     "scv_halfpi_wedge": [_P, _I, _P, _P],
     "scv_sht_forward": [_P, _I, _I, _I, _P, _P, _P],
     "scv_sht_inverse": [_P, _I, _I, _I, _P, _P, _P],
@@ -46,7 +50,8 @@ _SIGS = {
     "scv_accumulate_scaling": [_P, _I, _I, _P, _P, _P, _P],
     "scv_finish_acc": [_P, _I, _I, _I, _P, _P],
 }
-_RESTYPE = {"scv_last_error": ctypes.c_char_p, "scv_workspace_bytes": ctypes.c_longlong}
+_RESTYPE = {"scv_last_error": ctypes.c_char_p, "scv_workspace_bytes": ctypes.c_longlong,
+            "scv_launch_count": ctypes.c_longlong}
 
 EXPORTED = tuple(_SIGS)
 
@@ -98,8 +103,36 @@ class Context:
                     raise TypeError(msg)
                 raise RuntimeError(f"scv_{name} failed ({rc}): {msg}")
 
+    def launch_count(self) -> int:
+        return int(self.lib.scv_launch_count(self.handle))
+
     def workspace_bytes(self) -> int:
         return int(self.lib.scv_workspace_bytes(self.handle))
+
+    def profile(self, enable: bool):
+        with self.lock:
+            self.lib.scv_profile(self.handle, 1 if enable else 0)
+
+    def profile_report(self) -> dict:
+        """{stage: (count, total_ms)} since the last report (synchronises)."""
+        buf = ctypes.create_string_buffer(1 << 16)
+        with self.lock:
+            rc = self.lib.scv_profile_report(self.handle, buf, len(buf))
+        if rc != SCV_OK:
+            raise RuntimeError(self.lib.scv_last_error(self.handle).decode())
+        out = {}
+        for line in buf.value.decode().splitlines():
+            name, cnt, ms = line.split()
+            out[name] = (int(cnt), float(ms))
+        return out
+
+    def fp64_peak_tflops(self) -> float:
+        v = ctypes.c_double()
+        with self.lock:
+            rc = self.lib.scv_fp64_peak(self.handle, ctypes.byref(v))
+        if rc != SCV_OK:
+            raise RuntimeError(self.lib.scv_last_error(self.handle).decode())
+        return v.value
 
     def trim(self):
         with self.lock:

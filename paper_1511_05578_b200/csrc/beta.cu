@@ -284,6 +284,7 @@ static int launch_so3(scv_ctx* c, int L, int real, const double2* W1p, double2* 
   size_t sm = beta_smem(1 << LOGP, 2 * L - 1);
   SCV_CUDA(c, cudaFuncSetAttribute(k_beta_so3<LOGP, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   k_beta_so3<LOGP, NT><<<ntasks, NT, sm, s>>>(L, real, W1p, w, dev_of(t), c->delta, pref, tasks);
+  c->launches++;
   SCV_CUDA(c, cudaGetLastError());
   return SCV_OK;
 }
@@ -297,6 +298,7 @@ static int launch_sht(scv_ctx* c, int L, int spin, int real, const double2* G, d
   int npairs = (ncols + 1) / 2;
   SCV_CUDA(c, cudaFuncSetAttribute(k_beta_sht<LOGP, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   k_beta_sht<LOGP, NT><<<npairs, NT, sm, s>>>(L, spin, real, G, Gw, dev_of(t), pref);
+  c->launches++;
   SCV_CUDA(c, cudaGetLastError());
   return SCV_OK;
 }

@@ -21,6 +21,29 @@ typedef std::complex<ld> cld;
 
 static const ld kPi = 3.141592653589793238462643383279502884L;
 
+static cudaEvent_t pool_get(scv_ctx* c) {
+  if (!c->pool.empty()) {
+    cudaEvent_t e = c->pool.back();
+    c->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+ProfScope::ProfScope(scv_ctx* c_, cudaStream_t s_, const char* name) : c(c_), s(s_) {
+  if (!c->prof) return;
+  scv_ctx::Rec r{name, pool_get(c), pool_get(c)};
+  cudaEventRecord(r.a, s);
+  c->recs.push_back(r);
+  idx = (int)c->recs.size() - 1;
+}
+
+ProfScope::~ProfScope() {
+  if (idx >= 0) cudaEventRecord(c->recs[idx].b, s);
+}
+
 int scv_fail(scv_ctx* c, int code, const std::string& msg) {
   if (c) c->err = msg;
   return code;
@@ -295,6 +318,8 @@ int scv_destroy(scv_ctx* c) {
     cudaFree(t.Vf); cudaFree(t.Aalt); cudaFree(t.sinh); cudaFree(t.cosh);
   }
   for (auto& kv : c->aux) cudaFree(kv.second);
+  for (auto& r : c->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  for (auto e : c->pool) cudaEventDestroy(e);
   if (c->fft_work) cudaFree(c->fft_work);
   for (int i = 0; i < 3; ++i)
     if (c->scratch[i]) cudaFree(c->scratch[i]);
@@ -305,6 +330,40 @@ int scv_destroy(scv_ctx* c) {
 }
 
 const char* scv_last_error(const scv_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+long long scv_launch_count(const scv_ctx* c) { return c ? c->launches : 0; }
+
+int scv_profile(scv_ctx* c, int enable) {
+  if (!c) return SCV_EINVAL;
+  c->prof = enable != 0;
+  return SCV_OK;
+}
+
+int scv_profile_report(scv_ctx* c, char* buf, int len) {
+  if (!c || !buf || len <= 0) return SCV_EINVAL;
+  SCV_CUDA(c, cudaSetDevice(c->device));
+  SCV_CUDA(c, cudaDeviceSynchronize());
+  std::map<std::string, std::pair<int, double>> agg;
+  for (auto& r : c->recs) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    auto& e = agg[r.name];
+    e.first += 1;
+    e.second += ms;
+    c->pool.push_back(r.a);
+    c->pool.push_back(r.b);
+  }
+  c->recs.clear();
+  std::string out;
+  char line[256];
+  for (auto& kv : agg) {
+    snprintf(line, sizeof line, "%s %d %.6f\n", kv.first.c_str(), kv.second.first, kv.second.second);
+    out += line;
+  }
+  if ((int)out.size() + 1 > len) return scv_fail(c, SCV_EINVAL, "profile report buffer too small");
+  memcpy(buf, out.c_str(), out.size() + 1);
+  return SCV_OK;
+}
 
 long long scv_workspace_bytes(const scv_ctx* c) {
   if (!c) return 0;

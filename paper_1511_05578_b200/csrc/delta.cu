@@ -58,6 +58,7 @@ int scv_launch_delta_wedge(scv_ctx* c, int L, const double* edge, double* out, c
   long long total = (long long)L * (L + 1) / 2;
   int blocks = (int)((total + 255) / 256);
   k_delta_wedge<<<blocks, 256, 0, s>>>(L, edge, out);
+  c->launches++;
   SCV_CUDA(c, cudaGetLastError());
   return SCV_OK;
 }

@@ -107,8 +107,10 @@ int scv_scale_product(scv_ctx* c, int L, int Lj, const double* flm, const double
   if (Lj < 1 || Lj > L) return scv_fail(c, SCV_EINVAL, "scale band limit must lie in [1, L]");
   cudaStream_t s = (cudaStream_t)stream;
   SCV_CUDA(c, cudaSetDevice(c->device));
+  SCV_PROF(c, s, "product");
   const long long tot = 2LL * Lj * (2 * Lj - 1);
   k_scale_product<<<(int)((tot + 255) / 256), 256, 0, s>>>(Lj, (const double2*)flm, pos, neg, (double2*)w);
+  c->launches++;
   SCV_CUDA(c, cudaGetLastError());
   return SCV_OK;
 }
@@ -119,7 +121,9 @@ int scv_scaling_product(scv_ctx* c, int L, int Ls, const double* flm, const doub
   if (Ls < 1 || Ls > L) return scv_fail(c, SCV_EINVAL, "scaling band limit must lie in [1, L]");
   cudaStream_t s = (cudaStream_t)stream;
   SCV_CUDA(c, cudaSetDevice(c->device));
+  SCV_PROF(c, s, "product");
   k_scaling_product<<<(Ls * Ls + 255) / 256, 256, 0, s>>>(Ls, (const double2*)flm, scaling, (double2*)out);
+  c->launches++;
   SCV_CUDA(c, cudaGetLastError());
   return SCV_OK;
 }
@@ -130,7 +134,9 @@ int scv_accumulate(scv_ctx* c, int L, int Lj, const double* w, const double* pos
   if (Lj < 1 || Lj > L) return scv_fail(c, SCV_EINVAL, "scale band limit must lie in [1, L]");
   cudaStream_t s = (cudaStream_t)stream;
   SCV_CUDA(c, cudaSetDevice(c->device));
+  SCV_PROF(c, s, "product");
   k_accumulate<<<(Lj * Lj + 255) / 256, 256, 0, s>>>(Lj, (const double2*)w, pos, neg, (double2*)acc);
+  c->launches++;
   SCV_CUDA(c, cudaGetLastError());
   return SCV_OK;
 }
@@ -141,7 +147,9 @@ int scv_accumulate_scaling(scv_ctx* c, int L, int Ls, const double* slm, const d
   if (Ls < 1 || Ls > L) return scv_fail(c, SCV_EINVAL, "scaling band limit must lie in [1, L]");
   cudaStream_t s = (cudaStream_t)stream;
   SCV_CUDA(c, cudaSetDevice(c->device));
+  SCV_PROF(c, s, "product");
   k_accumulate_scaling<<<(Ls * Ls + 255) / 256, 256, 0, s>>>(Ls, (const double2*)slm, scaling, (double2*)acc);
+  c->launches++;
   SCV_CUDA(c, cudaGetLastError());
   return SCV_OK;
 }
@@ -152,6 +160,7 @@ int scv_finish_acc(scv_ctx* c, int L, int spin, int real, double* acc, void* str
   SCV_CUDA(c, cudaSetDevice(c->device));
   const int as = spin < 0 ? -spin : spin;
   k_finish_acc<<<(L * L + 255) / 256, 256, 0, s>>>(L, as, real, (double2*)acc);
+  c->launches++;
   SCV_CUDA(c, cudaGetLastError());
   return SCV_OK;
 }

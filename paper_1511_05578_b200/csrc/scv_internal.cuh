@@ -105,7 +105,25 @@ struct scv_ctx {
   size_t scratch_bytes[3] = {0, 0, 0};
   // small int tables by key
   std::map<std::string, void*> aux;
+  // stage profiler (scv_profile): event pairs around every launch group
+  bool prof = false;
+  long long launches = 0;  // kernels of this library launched (scv_launch_count)
+  struct Rec { std::string name; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
 };
+
+// RAII stage timer: records a start/stop event pair on `s` when profiling is on
+struct ProfScope {
+  scv_ctx* c;
+  cudaStream_t s;
+  int idx = -1;
+  ProfScope(scv_ctx* c_, cudaStream_t s_, const char* name);
+  ~ProfScope();
+};
+#define SCV_PROF_CAT2(a, b) a##b
+#define SCV_PROF_CAT(a, b) SCV_PROF_CAT2(a, b)
+#define SCV_PROF(c, s, name) ProfScope SCV_PROF_CAT(prof_scope_, __LINE__)(c, s, name)
 
 // ---------------------------------------------------------------------------
 // error plumbing

@@ -120,6 +120,8 @@ extern "C" int scv_sht_forward(scv_ctx* c, int L, int spin, int real, const void
   SCV_TRY(scv_scratch(c, 2, (size_t)K * ncol * 16, &Gw));
   cufftHandle h;
   int n[1] = {K};
+  {
+  SCV_PROF(c, s, "sht_phi_fft");
   if (real) {
     int on[1] = {L};
     SCV_TRY(scv_plan(c, "sht_phi_d2z_" + std::to_string(L), 1, n, n, 1, K, on, 1, L, CUFFT_D2Z, L, &h));
@@ -130,10 +132,16 @@ extern "C" int scv_sht_forward(scv_ctx* c, int L, int spin, int real, const void
     SCV_TRY(scv_plan_exec_setup(c, h, s));
     SCV_CUFFT(c, cufftExecZ2Z(h, (cufftDoubleComplex*)f, (cufftDoubleComplex*)G, CUFFT_FORWARD));
   }
+  }
+  {
+  SCV_PROF(c, s, "beta_sht");
   SCV_TRY(scv_beta_sht(c, L, spin, real, (const double2*)G, (double2*)Gw, 2.0 * SCV_PI / (double)K, s));
+  }
+  SCV_PROF(c, s, "sht_contract");
   const long long warps = (long long)L * L;
   k_sht_contract<<<(int)((warps * 32 + 255) / 256), 256, 0, s>>>(L, spin, real, (const double2*)Gw,
                                                                  c->delta, (double2*)flm);
+                                                                 c->launches++;
   SCV_CUDA(c, cudaGetLastError());
   return SCV_OK;
 }
@@ -150,9 +158,14 @@ extern "C" int scv_sht_inverse(scv_ctx* c, int L, int spin, int real, const doub
   void* B = nullptr;
   SCV_TRY(scv_scratch(c, 1, (size_t)K * ncol * 16, &B));
   const long long tot = (long long)K * ncol;
+  {
+  SCV_PROF(c, s, "sht_bins");
   k_sht_bins<<<(int)((tot + 127) / 128), 128, 0, s>>>(L, spin, real, (const double2*)flm, c->delta,
                                                       (double2*)B);
+                                                      c->launches++;
   SCV_CUDA(c, cudaGetLastError());
+  }
+  SCV_PROF(c, s, "sht_ifft");
   cufftHandle h;
   if (!real) {
     int n2[2] = {K, K};
@@ -170,6 +183,7 @@ extern "C" int scv_sht_inverse(scv_ctx* c, int L, int spin, int real, const doub
   SCV_CUFFT(c, cufftExecZ2Z(h, (cufftDoubleComplex*)B, (cufftDoubleComplex*)B, CUFFT_INVERSE));
   // irfft discards Im of the DC bin (scipy semantics); make that explicit for cuFFT
   k_zero_imag_col0<<<(L + 127) / 128, 128, 0, s>>>((double2*)B, L, L);
+  c->launches++;
   SCV_CUDA(c, cudaGetLastError());
   int on[1] = {K}, in1[1] = {L};
   SCV_TRY(scv_plan(c, "sht_inv_phi_z2d_" + std::to_string(L), 1, n1, in1, 1, L, on, 1, K, CUFFT_Z2D, L, &h));

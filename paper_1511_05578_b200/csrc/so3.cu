@@ -151,24 +151,35 @@ extern "C" int scv_so3_inverse_curvelet(scv_ctx* c, int L, int real, const doubl
   const int K = 2 * L - 1;
   const long long LK = (long long)L * K;
   if (!real) {
+    {
+    SCV_PROF(c, s, "so3inv_gen");
     k_so3inv_gen<<<K * L, 128, 0, s>>>(L, 0, (const double2*)w, c->hlb, t->sinh, t->cosh, (double2*)sig);
+    c->launches++;
     SCV_CUDA(c, cudaGetLastError());
+    }
     // alpha: contiguous rows, in place
+    {
+    SCV_PROF(c, s, "so3inv_alpha_fft");
     SCV_TRY(fft1d_chunked(c, "a_inv", K, K, 1, K, K, 1, K, CUFFT_Z2Z, (long long)K * L, sig, sig,
                           CUFFT_INVERSE, s, 16, 16));
+    }
     // gamma: stride L*K, batches are the (b, a) pairs
+    SCV_PROF(c, s, "so3inv_gamma_fft");
     SCV_TRY(fft1d_chunked(c, "g_inv", K, K, (int)LK, 1, K, (int)LK, 1, CUFFT_Z2Z, LK, sig, sig,
                           CUFFT_INVERSE, s, 16, 16));
     return SCV_OK;
   }
   void* T = nullptr;
   SCV_TRY(scv_scratch(c, 0, (size_t)L * LK * 16, &T));
+  SCV_PROF(c, s, "so3inv_real");
   k_so3inv_gen<<<L * L, 128, 0, s>>>(L, 1, (const double2*)w, c->hlb, t->sinh, t->cosh, (double2*)T);
+  c->launches++;
   SCV_CUDA(c, cudaGetLastError());
   SCV_TRY(fft1d_chunked(c, "a_inv", K, K, 1, K, K, 1, K, CUFFT_Z2Z, (long long)L * L, T, T,
                         CUFFT_INVERSE, s, 16, 16));
   // irfft along gamma ignores Im of the n=0 bin (scipy semantics, so3.py:416)
   k_zero_imag<<<(int)((LK + 255) / 256), 256, 0, s>>>((double2*)T, LK);
+  c->launches++;
   SCV_CUDA(c, cudaGetLastError());
   SCV_TRY(fft1d_chunked(c, "g_c2r", K, L, (int)LK, 1, K, (int)LK, 1, CUFFT_Z2D, LK, T, sig, 0, s, 16, 8));
   return SCV_OK;
@@ -195,6 +206,8 @@ extern "C" int scv_so3_forward_curvelet(scv_ctx* c, int L, int real, const void*
     int n2[2] = {K, K};
     int ie[2] = {K, L * K};
     cufftHandle h;
+    {
+    SCV_PROF(c, s, "so3fwd_fft2d");
     if (!real) {
       int oe[2] = {K, K};
       SCV_TRY(scv_plan(c, "fwd2d_z2z_" + std::to_string(L) + "_" + std::to_string(nbb), 2, n2, ie, 1, K,
@@ -209,16 +222,20 @@ extern "C" int scv_so3_forward_curvelet(scv_ctx* c, int L, int real, const void*
       SCV_TRY(scv_plan_exec_setup(c, h, s));
       SCV_CUFFT(c, cufftExecD2Z(h, (double*)((const double*)sig + (size_t)b0 * K), (cufftDoubleComplex*)chunk));
     }
+    }
+    SCV_PROF(c, s, "so3fwd_extract");
     dim3 blk(32, 8);
     for (int bs = 0; bs < nbb; bs += 32) {
       const int nsub = std::min(32, nbb - bs);
       const double2* csub = (const double2*)chunk + (size_t)bs * (per_b / 16);
       dim3 grd((K + 7) / 8, real ? L : K);
       k_so3_extract<<<grd, blk, 0, s>>>(L, real, b0 + bs, nsub, csub, (double2*)W1p);
+      c->launches++;
       SCV_CUDA(c, cudaGetLastError());
     }
   }
   const double pref = 4.0 * SCV_PI * SCV_PI / ((double)K * (double)K);
+  SCV_PROF(c, s, "beta_so3");
   SCV_TRY(scv_beta_so3(c, L, real, (const double2*)W1p, (double2*)w, pref, s));
   return SCV_OK;
 }

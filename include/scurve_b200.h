@@ -75,6 +75,13 @@ long long scv_launch_count(const scv_ctx* ctx);
  * denominator for FP64-bound stages (MEASURED_PEAKS.json has no FP64 entry). */
 int scv_fp64_peak(scv_ctx* ctx, double* tflops);
 
+/* Batched K-point DFT of `nrows` contiguous complex128 rows with the
+ * hand-written prime-factor engine (K = 2^k - 1 up to 4095):
+ * out[r][k] = sum_n in[r][n] exp(dir * 2 pi i n k / K), dir = -1 or +1.
+ * Exposed for testing and benchmarking the engine in isolation. */
+int scv_debug_dft(scv_ctx* ctx, int K, int dir, int nrows, const double* in, double* out,
+                  void* stream);
+
 /* Delta^l_{m'm}(pi/2) for l < L in the 1/8 symmetry wedge 0 <= m <= m' <= l:
  * element (l, m', m) at l(l+1)(l+2)/6 + m'(m'+1)/2 + m.  Copies the context's
  * table (built on the device by the degree recursion) into `out`

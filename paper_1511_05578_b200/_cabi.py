@@ -39,6 +39,7 @@ _SIGS = {
     "scv_launch_count": [_P],
     "scv_profile_report": [_P, ctypes.c_char_p, _I],
     "scv_fp64_peak": [_P, ctypes.POINTER(ctypes.c_double)],
+    "scv_debug_dft": [_P, _I, _I, _I, _P, _P, _P],
     "scv_halfpi_wedge": [_P, _I, _P, _P],
     "scv_sht_forward": [_P, _I, _I, _I, _P, _P, _P],
     "scv_sht_inverse": [_P, _I, _I, _I, _P, _P, _P],
@@ -62,7 +63,7 @@ def load_library(path: str | None = None):
     with _lib_lock:
         if _lib is not None:
             return _lib
-        p = path or LIB_PATH
+        p = path or os.environ.get("SCV_LIB") or LIB_PATH
         if not os.path.exists(p):
             raise RuntimeError(
                 f"{p} not found: build the CUDA library first "

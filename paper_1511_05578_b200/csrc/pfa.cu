@@ -1,0 +1,616 @@
+// Alpha / gamma stages of the SO(3) transforms on the prime-factor DFT engine
+// (pfa.cuh), for the Mersenne grid lengths K = 2^k - 1 of the lambda = 2
+// tilings.  Other lengths fall back to cuFFT (so3.cu).
+//
+// Analysis  (so3.py:259-285 restated, see so3.cu for the closed form):
+//   k_ana_alpha  : generate fac W_{mn} d^l_{mn}(beta_b) for R rows (n, b) in
+//                  shared memory, inverse K-point DFT over m -> alpha, store
+//                  rows of the (gamma-slot, beta, alpha) volume.  One HBM write.
+//   k_ana_gamma  : R adjacent alpha columns of one beta slab, inverse DFT over
+//                  n -> gamma in place (real path: Hermitian columns packed
+//                  two per complex transform).
+// Synthesis (so3.py:195-200 + the |m|<=|n| pruning of so3.py:240):
+//   k_syn_alpha  : forward DFT of R rows (g, b) of the input into a beta-chunk
+//                  buffer [b][g][m] (real input: two rows per complex transform).
+//   k_syn_gamma  : R adjacent m columns of the chunk, forward DFT over
+//                  g -> n, keep |m| <= |n| and scatter into the beta-contiguous
+//                  columns W1p[(n,m)][b] consumed by the beta stage.
+// All kernels are persistent (grid = resident CTAs) and stage the coefficient
+// tables in shared memory once.
+
+#include <algorithm>
+#include <cmath>
+
+#include "pfa.cuh"
+
+typedef long double ld;
+
+bool scv_pfa_supported(int K) {
+  switch (K) {
+    case 3: case 7: case 15: case 31: case 63: case 255: case 511: case 1023: case 2047:
+    case 4095: return true;
+    default: return false;
+  }
+}
+
+static void factors_of(int K, int f[4]) {
+  f[0] = f[1] = f[2] = f[3] = 1;
+  switch (K) {
+    case 3: f[0] = 3; break;
+    case 7: f[0] = 7; break;
+    case 15: f[0] = 3; f[1] = 5; break;
+    case 31: f[0] = 31; break;
+    case 63: f[0] = 7; f[1] = 9; break;
+    case 127: f[0] = 127; break;
+    case 255: f[0] = 3; f[1] = 5; f[2] = 17; break;
+    case 511: f[0] = 7; f[1] = 73; break;
+    case 1023: f[0] = 3; f[1] = 11; f[2] = 31; break;
+    case 2047: f[0] = 23; f[1] = 89; break;
+    case 4095: f[0] = 5; f[1] = 7; f[2] = 9; f[3] = 13; break;
+  }
+}
+
+int scv_pfa_tables(scv_ctx* c, int K, const double2** out) {
+  const std::string key = "pfa_" + std::to_string(K);
+  auto it = c->aux.find(key);
+  if (it != c->aux.end()) {
+    *out = (const double2*)it->second;
+    return SCV_OK;
+  }
+  int f[4];
+  factors_of(K, f);
+  std::vector<double2> tab;
+  const ld twopi = 6.283185307179586476925286766559005768L;
+  for (int s = 0; s < 4; ++s) {
+    const int p = f[s];
+    if (p == 1) continue;
+    const int h = (p - 1) / 2, GP = pfa_gp(p);
+    for (int j = 1; j <= h; ++j)
+      for (int k = 1; k <= GP; ++k) {
+        if (k > h) {
+          tab.push_back(make_double2(0.0, 0.0));
+          continue;
+        }
+        const ld a = twopi * (ld)(((long long)j * k) % p) / (ld)p;
+        tab.push_back(make_double2((double)cosl(a), (double)sinl(a)));
+      }
+  }
+  if (tab.empty()) tab.push_back(make_double2(0.0, 0.0));
+  void* d = nullptr;
+  SCV_CUDA(c, cudaMalloc(&d, tab.size() * sizeof(double2)));
+  SCV_CUDA(c, cudaMemcpy(d, tab.data(), tab.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  c->aux[key] = d;
+  *out = (const double2*)d;
+  return SCV_OK;
+}
+
+// Launch shapes per length.  ROW kernels (alpha passes) and COL kernels
+// (gamma passes, R adjacent columns so each 16-byte element of a row is part
+// of an R*16-byte contiguous segment) each use R transforms per batch, NT
+// threads (every stage's work items fit one pass for the large radices) and
+// MINB resident CTAs per SM.  Batches are double-buffered in shared memory:
+// the next batch streams in with cp.async while the current one computes.
+template <int K, bool COL> struct PfaCfg;
+#define SCV_PFA_CFG(KK, CL, RR, NNT, MB) \
+  template <> struct PfaCfg<KK, CL> { static constexpr int R = RR, NT = NNT, MINB = MB; };
+SCV_PFA_CFG(3, false, 64, 128, 2)    SCV_PFA_CFG(3, true, 64, 128, 2)
+SCV_PFA_CFG(7, false, 64, 128, 2)    SCV_PFA_CFG(7, true, 64, 128, 2)
+SCV_PFA_CFG(15, false, 32, 128, 2)   SCV_PFA_CFG(15, true, 32, 128, 2)
+SCV_PFA_CFG(31, false, 16, 128, 2)   SCV_PFA_CFG(31, true, 16, 128, 2)
+SCV_PFA_CFG(63, false, 16, 256, 2)   SCV_PFA_CFG(63, true, 16, 256, 2)
+SCV_PFA_CFG(255, false, 8, 256, 2)   SCV_PFA_CFG(255, true, 8, 256, 2)
+SCV_PFA_CFG(511, false, 4, 256, 2)   SCV_PFA_CFG(511, true, 4, 256, 2)
+SCV_PFA_CFG(1023, false, 2, 224, 2)  SCV_PFA_CFG(1023, true, 2, 224, 2)
+SCV_PFA_CFG(2047, false, 1, 192, 2)  SCV_PFA_CFG(2047, true, 2, 384, 1)
+SCV_PFA_CFG(4095, false, 1, 320, 1)  SCV_PFA_CFG(4095, true, 1, 320, 1)
+
+template <int K, bool COL>
+static size_t pfa_smem() {
+  using PL = PfaPlan<K>;
+  constexpr int R = PfaCfg<K, COL>::R;
+  return ((size_t)2 * R * K + pfa_tab_total<PL>()) * sizeof(double2) + R * sizeof(int4);
+}
+
+// ---------------------------------------------------------------------------
+// batched rows (test / benchmark entry): out[r][k] = sum_n in[r][n] e^{DIR 2 pi i nk/K}
+// ---------------------------------------------------------------------------
+template <int K, int DIR>
+__global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
+    k_pfa_rows(long long nrows, const double2* __restrict__ in, double2* __restrict__ out,
+               const double2* __restrict__ gtab) {
+  using PL = PfaPlan<K>;
+  constexpr int R = PfaCfg<K, false>::R, NT = PfaCfg<K, false>::NT;
+  extern __shared__ double2 sm[];
+  double2* tab = sm;
+  double2* const buf0 = sm + pfa_tab_total<PL>();  // buffer c at buf0 + c * R * K (stays a shared pointer)
+  pfa_load_tables<PL, NT>(tab, gtab);
+  const long long nb = (nrows + R - 1) / R;
+  auto issue = [&](long long bt, double2* X) {
+    const long long r0 = bt * R;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < R * K; i += NT) {
+      const int r = i / K, n = i - r * K;
+      if (r0 + r < nrows) cp_async16(X + i, in + (r0 + r) * K + n);
+      else X[i] = make_double2(0.0, 0.0);
+    }
+    cp_async_commit();
+  };
+  long long bt = blockIdx.x;
+  int cur = 0;
+  if (bt < nb) issue(bt, buf0);
+#pragma unroll 1
+  for (; bt < nb; bt += gridDim.x) {
+    const long long nx = bt + gridDim.x;
+    if (nx < nb) issue(nx, buf0 + (cur ^ 1) * (R * K));
+    else cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    double2* X = buf0 + cur * (R * K);
+    pfa_dft<PL, DIR, R, NT, K>(X, tab);
+    const long long r0 = bt * R;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < R * K; i += NT) {
+      const int r = i / K, k = i - r * K;
+      if (r0 + r < nrows) out[(r0 + r) * K + k] = X[r * K + pfa_pos<PL>(k)];
+    }
+    __syncthreads();
+    cur ^= 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// analysis alpha: generate + inverse DFT over m, R rows (gi, b) per batch
+// ---------------------------------------------------------------------------
+template <int K>
+__global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
+    k_ana_alpha(int real, const double2* __restrict__ w, const double* __restrict__ hlb,
+                const double* __restrict__ lsin, const double* __restrict__ lcos, double2* __restrict__ out,
+                const double2* __restrict__ gtab) {
+  using PL = PfaPlan<K>;
+  constexpr int R = PfaCfg<K, false>::R, NT = PfaCfg<K, false>::NT;
+  constexpr int L = (K + 1) / 2;
+  extern __shared__ double2 sm[];
+  double2* tab = sm;
+  double2* X = sm + pfa_tab_total<PL>();
+  int4* rp = (int4*)(X + 2 * R * K);  // per-row (gi, b, n, l)
+  pfa_load_tables<PL, NT>(tab, gtab);
+  const long long nrows = (long long)(real ? L : K) * L;
+  const long long nb = (nrows + R - 1) / R;
+#pragma unroll 1
+  for (long long bt = blockIdx.x; bt < nb; bt += gridDim.x) {
+    if (threadIdx.x < R) {
+      const long long ri = bt * R + threadIdx.x;
+      int gi = -1, b = 0, n = 0;
+      if (ri < nrows) {
+        gi = (int)(ri / L);
+        b = (int)(ri - (long long)gi * L);
+        n = real ? gi : (gi <= L - 1 ? gi : gi - K);
+      }
+      rp[threadIdx.x] = make_int4(gi, b, n, n < 0 ? -n : n);
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int i = threadIdx.x; i < R * K; i += NT) {
+      const int r = i / K, q = i - r * K;
+      const int4 P = rp[r];
+      const int l = P.w, n = P.z;
+      const int m = q <= L - 1 ? q : q - K;
+      double2 v = make_double2(0.0, 0.0);
+      if (P.x >= 0 && m >= -l && m <= l) {
+        const int am = m < 0 ? -m : m;
+        const int es = n >= 0 ? l - m : l + m;
+        const int ec = n >= 0 ? l + m : l - m;
+        double lg = hlb[(long long)l * (l + 1) / 2 + am];
+        if (es) lg += (double)es * lsin[P.y];
+        if (ec) lg += (double)ec * lcos[P.y];
+        double d = exp(lg);
+        if (n < 0 && ((l - m) & 1)) d = -d;
+        const double2 cw = w[((long long)(n >= 0 ? 0 : 1) * L + l) * K + (L - 1) + m];
+        const double f = (double)(2 * l + 1) / (8.0 * SCV_PI * SCV_PI) * d;
+        v = make_double2(f * cw.x, f * cw.y);
+      }
+      X[i] = v;
+    }
+    __syncthreads();
+    pfa_dft<PL, +1, R, NT, K>(X, tab);
+#pragma unroll 4
+    for (int i = threadIdx.x; i < R * K; i += NT) {
+      const int r = i / K, a = i - r * K;
+      const int4 P = rp[r];
+      if (P.x >= 0) out[((long long)P.x * L + P.y) * K + a] = X[r * K + pfa_pos<PL>(a)];
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// analysis gamma: R adjacent alpha columns of one beta slab, inverse over n.
+// complex: in place on sig (K, L, K), double-buffered.  real: src = T
+// (L, L, K) complex half spectrum (n >= 0), dst = real sig (K, L, K); two
+// Hermitian columns per complex transform.
+// ---------------------------------------------------------------------------
+template <int K>
+__global__ void __launch_bounds__(PfaCfg<K, true>::NT, PfaCfg<K, true>::MINB)
+    k_ana_gamma(int real, double2* __restrict__ src, double* __restrict__ dst_real,
+                const double2* __restrict__ gtab) {
+  using PL = PfaPlan<K>;
+  constexpr int R = PfaCfg<K, true>::R, NT = PfaCfg<K, true>::NT;
+  constexpr int L = (K + 1) / 2;
+  constexpr long long LK = (long long)L * K;
+  extern __shared__ double2 sm[];
+  double2* tab = sm;
+  double2* const buf0 = sm + pfa_tab_total<PL>();  // buffer c at buf0 + c * R * K (stays a shared pointer)
+  pfa_load_tables<PL, NT>(tab, gtab);
+  const int cpb = real ? 2 * R : R;  // columns per batch
+  const int ngrp = (K + cpb - 1) / cpb;
+  const long long nb = (long long)L * ngrp;
+  auto issue = [&](long long bt, double2* X) {
+    const int b = (int)(bt / ngrp);
+    const int a0 = (int)(bt - (long long)b * ngrp) * cpb;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < R * K; i += NT) {
+      const int g = i / R, r = i - g * R;
+      const int a = a0 + r;
+      if (a < K) cp_async16(X + r * K + g, src + (long long)g * LK + (long long)b * K + a);
+      else X[r * K + g] = make_double2(0.0, 0.0);
+    }
+    cp_async_commit();
+  };
+  long long bt = blockIdx.x;
+  int cur = 0;
+  if (!real && bt < nb) issue(bt, buf0);
+#pragma unroll 1
+  for (; bt < nb; bt += gridDim.x) {
+    const int b = (int)(bt / ngrp);
+    const int a0 = (int)(bt - (long long)b * ngrp) * cpb;
+    double2* X = buf0 + cur * (R * K);
+    if (!real) {
+      const long long nx = bt + gridDim.x;
+      if (nx < nb) issue(nx, buf0 + (cur ^ 1) * (R * K));
+      else cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      // Z[n] = T1[n] + i T2[n], Z[-n] = conj(T1[n]) + i conj(T2[n]); Im of n = 0 dropped
+#pragma unroll 4
+      for (int i = threadIdx.x; i < R * L; i += NT) {
+        const int n = i / R, r = i - n * R;
+        const int a1 = a0 + 2 * r, a2 = a1 + 1;
+        double2 t1 = (a1 < K) ? src[(long long)n * LK + (long long)b * K + a1] : make_double2(0.0, 0.0);
+        double2 t2 = (a2 < K) ? src[(long long)n * LK + (long long)b * K + a2] : make_double2(0.0, 0.0);
+        if (n == 0) {
+          t1.y = 0.0;
+          t2.y = 0.0;
+        }
+        X[r * K + n] = make_double2(t1.x - t2.y, t1.y + t2.x);
+        if (n > 0) X[r * K + K - n] = make_double2(t1.x + t2.y, -t1.y + t2.x);
+      }
+    }
+    __syncthreads();
+    pfa_dft<PL, +1, R, NT, K>(X, tab);
+    if (!real) {
+#pragma unroll 4
+      for (int i = threadIdx.x; i < R * K; i += NT) {
+        const int g = i / R, r = i - g * R;
+        const int a = a0 + r;
+        if (a < K) src[(long long)g * LK + (long long)b * K + a] = X[r * K + pfa_pos<PL>(g)];
+      }
+    } else {
+#pragma unroll 4
+      for (int i = threadIdx.x; i < 2 * R * K; i += NT) {
+        const int g = i / (2 * R), c = i - g * (2 * R);
+        const int r = c >> 1;
+        const int a = a0 + c;
+        if (a < K) {
+          const double2 z = X[r * K + pfa_pos<PL>(g)];
+          dst_real[(long long)g * LK + (long long)b * K + a] = (c & 1) ? z.y : z.x;
+        }
+      }
+    }
+    __syncthreads();
+    if (!real) cur ^= 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// synthesis alpha: forward DFT of rows (g, b) for b in [b0, b0+nbb) into
+// chunk[(b-b0)][g][m] (complex, double-buffered).  real input: two rows per
+// complex transform.
+// ---------------------------------------------------------------------------
+template <int K>
+__global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
+    k_syn_alpha(int real, const void* __restrict__ in, int b0, int nbb, double2* __restrict__ chunk,
+                const double2* __restrict__ gtab) {
+  using PL = PfaPlan<K>;
+  constexpr int R = PfaCfg<K, false>::R, NT = PfaCfg<K, false>::NT;
+  constexpr int L = (K + 1) / 2;
+  constexpr long long LK = (long long)L * K;
+  extern __shared__ double2 sm[];
+  double2* tab = sm;
+  double2* const buf0 = sm + pfa_tab_total<PL>();  // buffer c at buf0 + c * R * K (stays a shared pointer)
+  pfa_load_tables<PL, NT>(tab, gtab);
+  const long long nrows = (long long)K * nbb;  // row index = bb*K + g
+  const int rpb = real ? 2 * R : R;
+  const long long nb = (nrows + rpb - 1) / rpb;
+  const double2* F = (const double2*)in;
+  auto issue = [&](long long bt, double2* X) {
+    const long long r0 = bt * rpb;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < R * K; i += NT) {
+      const int r = i / K, a = i - r * K;
+      const long long ri = r0 + r;
+      if (ri < nrows) {
+        const int bb = (int)(ri / K), g = (int)(ri - (long long)bb * K);
+        cp_async16(X + i, F + (long long)g * LK + (long long)(b0 + bb) * K + a);
+      } else {
+        X[i] = make_double2(0.0, 0.0);
+      }
+    }
+    cp_async_commit();
+  };
+  long long bt = blockIdx.x;
+  int cur = 0;
+  if (!real && bt < nb) issue(bt, buf0);
+#pragma unroll 1
+  for (; bt < nb; bt += gridDim.x) {
+    const long long r0 = bt * rpb;
+    double2* X = buf0 + cur * (R * K);
+    if (!real) {
+      const long long nx = bt + gridDim.x;
+      if (nx < nb) issue(nx, buf0 + (cur ^ 1) * (R * K));
+      else cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      const double* Fr = (const double*)in;
+#pragma unroll 4
+      for (int i = threadIdx.x; i < R * K; i += NT) {
+        const int r = i / K, a = i - r * K;
+        double v1 = 0.0, v2 = 0.0;
+        const long long ri1 = r0 + 2 * r, ri2 = ri1 + 1;
+        if (ri1 < nrows) {
+          const int bb = (int)(ri1 / K), g = (int)(ri1 - (long long)bb * K);
+          v1 = Fr[(long long)g * LK + (long long)(b0 + bb) * K + a];
+        }
+        if (ri2 < nrows) {
+          const int bb = (int)(ri2 / K), g = (int)(ri2 - (long long)bb * K);
+          v2 = Fr[(long long)g * LK + (long long)(b0 + bb) * K + a];
+        }
+        X[i] = make_double2(v1, v2);
+      }
+    }
+    __syncthreads();
+    pfa_dft<PL, -1, R, NT, K>(X, tab);
+    if (!real) {
+#pragma unroll 4
+      for (int i = threadIdx.x; i < R * K; i += NT) {
+        const int r = i / K, m = i - r * K;
+        const long long ri = r0 + r;
+        if (ri < nrows) chunk[ri * K + m] = X[r * K + pfa_pos<PL>(m)];
+      }
+    } else {
+      // Z = X1 + i X2 (X1, X2 Hermitian): X1[k] = (Z[k] + conj Z[-k])/2, X2[k] = (Z[k] - conj Z[-k])/(2i)
+#pragma unroll 4
+      for (int i = threadIdx.x; i < 2 * R * K; i += NT) {
+        const int c = i / K, m = i - c * K;
+        const int r = c >> 1;
+        const long long ri = r0 + c;
+        if (ri < nrows) {
+          const double2 z = X[r * K + pfa_pos<PL>(m)];
+          const double2 zc = X[r * K + pfa_pos<PL>(m == 0 ? 0 : K - m)];
+          double2 v;
+          if ((c & 1) == 0) v = make_double2(0.5 * (z.x + zc.x), 0.5 * (z.y - zc.y));
+          else v = make_double2(0.5 * (z.y + zc.y), -0.5 * (z.x - zc.x));
+          chunk[ri * K + m] = v;
+        }
+      }
+    }
+    __syncthreads();
+    if (!real) cur ^= 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// synthesis gamma + extraction: columns (bb, m) of the chunk, forward over g.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ long long w1p_colbase(int n, int real) {
+  const long long l = n < 0 ? -n : n;
+  if (real) return l * l;
+  if (l == 0) return 0;
+  return n > 0 ? 2 * l * l - 1 : 2 * l * l + 2 * l;
+}
+
+template <int K>
+__global__ void __launch_bounds__(PfaCfg<K, true>::NT, PfaCfg<K, true>::MINB)
+    k_syn_gamma(int real, const double2* __restrict__ chunk, int b0, int nbb, double2* __restrict__ W1p,
+                const double2* __restrict__ gtab) {
+  using PL = PfaPlan<K>;
+  constexpr int R = PfaCfg<K, true>::R, NT = PfaCfg<K, true>::NT;
+  constexpr int L = (K + 1) / 2;
+  extern __shared__ double2 sm[];
+  double2* tab = sm;
+  double2* const buf0 = sm + pfa_tab_total<PL>();  // buffer c at buf0 + c * R * K (stays a shared pointer)
+  pfa_load_tables<PL, NT>(tab, gtab);
+  const int ngrp = (K + R - 1) / R;
+  const long long nb = (long long)nbb * ngrp;
+  auto issue = [&](long long bt, double2* X) {
+    const int bb = (int)(bt / ngrp);
+    const int q0 = (int)(bt - (long long)bb * ngrp) * R;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < R * K; i += NT) {
+      const int g = i / R, r = i - g * R;
+      const int q = q0 + r;
+      if (q < K) cp_async16(X + r * K + g, chunk + ((long long)bb * K + g) * K + q);
+      else X[r * K + g] = make_double2(0.0, 0.0);
+    }
+    cp_async_commit();
+  };
+  long long bt = blockIdx.x;
+  int cur = 0;
+  if (bt < nb) issue(bt, buf0);
+#pragma unroll 1
+  for (; bt < nb; bt += gridDim.x) {
+    const int bb = (int)(bt / ngrp);
+    const int q0 = (int)(bt - (long long)bb * ngrp) * R;
+    const long long nx = bt + gridDim.x;
+    if (nx < nb) issue(nx, buf0 + (cur ^ 1) * (R * K));
+    else cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    double2* X = buf0 + cur * (R * K);
+    pfa_dft<PL, -1, R, NT, K>(X, tab);
+    // keep |m| <= |n| (real: n >= 0 only)
+#pragma unroll 4
+    for (int i = threadIdx.x; i < R * K; i += NT) {
+      const int r = i / K, gn = i - r * K;
+      const int q = q0 + r;
+      if (q >= K) continue;
+      const int m = q <= L - 1 ? q : q - K;
+      const int n = gn <= L - 1 ? gn : gn - K;
+      const int am = m < 0 ? -m : m, an = n < 0 ? -n : n;
+      if (am > an || (real && n < 0)) continue;
+      W1p[(w1p_colbase(n, real) + m + an) * (long long)L + b0 + bb] = X[r * K + pfa_pos<PL>(gn)];
+    }
+    __syncthreads();
+    cur ^= 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------
+template <typename Kern>
+static int persistent_grid(scv_ctx* c, Kern k, int nt, size_t sm, long long nbatches, int* grid) {
+  SCV_CUDA(c, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  int per = 0, sms = 0;
+  SCV_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, nt, sm));
+  SCV_CUDA(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+  if (per < 1) per = 1;
+  long long g = (long long)per * sms;
+  if (g > nbatches) g = nbatches;
+  if (g < 1) g = 1;
+  *grid = (int)g;
+  return SCV_OK;
+}
+
+#define PFA_SWITCH(K, CALL)                                                                 \
+  switch (K) {                                                                              \
+    case 3: return CALL(3); case 7: return CALL(7); case 15: return CALL(15);              \
+    case 31: return CALL(31); case 63: return CALL(63);                                     \
+    case 255: return CALL(255); case 511: return CALL(511); case 1023: return CALL(1023);   \
+    case 2047: return CALL(2047); case 4095: return CALL(4095);                             \
+    default: return scv_fail(c, SCV_EINVAL, "no prime-factor plan for length " + std::to_string(K)); \
+  }
+
+template <int K, int DIR>
+static int run_rows(scv_ctx* c, long long nrows, const double2* in, double2* out, cudaStream_t s) {
+  const double2* tab;
+  SCV_TRY(scv_pfa_tables(c, K, &tab));
+  const size_t sm = pfa_smem<K, false>();
+  int grid;
+  const long long nb = (nrows + PfaCfg<K, false>::R - 1) / PfaCfg<K, false>::R;
+  SCV_TRY(persistent_grid(c, k_pfa_rows<K, DIR>, PfaCfg<K, false>::NT, sm, nb, &grid));
+  k_pfa_rows<K, DIR><<<grid, PfaCfg<K, false>::NT, sm, s>>>(nrows, in, out, tab);
+  c->launches++;
+  SCV_CUDA(c, cudaGetLastError());
+  return SCV_OK;
+}
+
+template <int K>
+static int run_ana_alpha(scv_ctx* c, int real, const double2* w, const double* hlb, const double* ls,
+                         const double* lc, double2* out, cudaStream_t s) {
+  const double2* tab;
+  SCV_TRY(scv_pfa_tables(c, K, &tab));
+  const size_t sm = pfa_smem<K, false>();
+  constexpr int L = (K + 1) / 2;
+  const long long nb = ((long long)(real ? L : K) * L + PfaCfg<K, false>::R - 1) / PfaCfg<K, false>::R;
+  int grid;
+  SCV_TRY(persistent_grid(c, k_ana_alpha<K>, PfaCfg<K, false>::NT, sm, nb, &grid));
+  k_ana_alpha<K><<<grid, PfaCfg<K, false>::NT, sm, s>>>(real, w, hlb, ls, lc, out, tab);
+  c->launches++;
+  SCV_CUDA(c, cudaGetLastError());
+  return SCV_OK;
+}
+
+template <int K>
+static int run_ana_gamma(scv_ctx* c, int real, double2* src, double* dst, cudaStream_t s) {
+  const double2* tab;
+  SCV_TRY(scv_pfa_tables(c, K, &tab));
+  const size_t sm = pfa_smem<K, true>();
+  constexpr int L = (K + 1) / 2;
+  const int cpb = real ? 2 * PfaCfg<K, true>::R : PfaCfg<K, true>::R;
+  const long long nb = (long long)L * ((K + cpb - 1) / cpb);
+  int grid;
+  SCV_TRY(persistent_grid(c, k_ana_gamma<K>, PfaCfg<K, true>::NT, sm, nb, &grid));
+  k_ana_gamma<K><<<grid, PfaCfg<K, true>::NT, sm, s>>>(real, src, dst, tab);
+  c->launches++;
+  SCV_CUDA(c, cudaGetLastError());
+  return SCV_OK;
+}
+
+template <int K>
+static int run_syn_alpha(scv_ctx* c, int real, const void* in, int b0, int nbb, double2* chunk, cudaStream_t s) {
+  const double2* tab;
+  SCV_TRY(scv_pfa_tables(c, K, &tab));
+  const size_t sm = pfa_smem<K, false>();
+  const int rpb = real ? 2 * PfaCfg<K, false>::R : PfaCfg<K, false>::R;
+  const long long nb = ((long long)K * nbb + rpb - 1) / rpb;
+  int grid;
+  SCV_TRY(persistent_grid(c, k_syn_alpha<K>, PfaCfg<K, false>::NT, sm, nb, &grid));
+  k_syn_alpha<K><<<grid, PfaCfg<K, false>::NT, sm, s>>>(real, in, b0, nbb, chunk, tab);
+  c->launches++;
+  SCV_CUDA(c, cudaGetLastError());
+  return SCV_OK;
+}
+
+template <int K>
+static int run_syn_gamma(scv_ctx* c, int real, const double2* chunk, int b0, int nbb, double2* W1p, cudaStream_t s) {
+  const double2* tab;
+  SCV_TRY(scv_pfa_tables(c, K, &tab));
+  const size_t sm = pfa_smem<K, true>();
+  const long long nb = (long long)nbb * ((K + PfaCfg<K, true>::R - 1) / PfaCfg<K, true>::R);
+  int grid;
+  SCV_TRY(persistent_grid(c, k_syn_gamma<K>, PfaCfg<K, true>::NT, sm, nb, &grid));
+  k_syn_gamma<K><<<grid, PfaCfg<K, true>::NT, sm, s>>>(real, chunk, b0, nbb, W1p, tab);
+  c->launches++;
+  SCV_CUDA(c, cudaGetLastError());
+  return SCV_OK;
+}
+
+int scv_pfa_ana_alpha(scv_ctx* c, int K, int real, const double2* w, const double* hlb, const double* ls,
+                      const double* lc, double2* out, cudaStream_t s) {
+#define CALL(KK) run_ana_alpha<KK>(c, real, w, hlb, ls, lc, out, s)
+  PFA_SWITCH(K, CALL)
+#undef CALL
+}
+int scv_pfa_ana_gamma(scv_ctx* c, int K, int real, double2* src, double* dst, cudaStream_t s) {
+#define CALL(KK) run_ana_gamma<KK>(c, real, src, dst, s)
+  PFA_SWITCH(K, CALL)
+#undef CALL
+}
+int scv_pfa_syn_alpha(scv_ctx* c, int K, int real, const void* in, int b0, int nbb, double2* chunk,
+                      cudaStream_t s) {
+#define CALL(KK) run_syn_alpha<KK>(c, real, in, b0, nbb, chunk, s)
+  PFA_SWITCH(K, CALL)
+#undef CALL
+}
+int scv_pfa_syn_gamma(scv_ctx* c, int K, int real, const double2* chunk, int b0, int nbb, double2* W1p,
+                      cudaStream_t s) {
+#define CALL(KK) run_syn_gamma<KK>(c, real, chunk, b0, nbb, W1p, s)
+  PFA_SWITCH(K, CALL)
+#undef CALL
+}
+
+extern "C" int scv_debug_dft(scv_ctx* c, int K, int dir, int nrows, const double* in, double* out,
+                             void* stream) {
+  if (!c) return SCV_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  SCV_CUDA(c, cudaSetDevice(c->device));
+  SCV_PROF(c, s, "debug_dft");
+  if (dir < 0) {
+#define CALL(KK) run_rows<KK, -1>(c, nrows, (const double2*)in, (double2*)out, s)
+    PFA_SWITCH(K, CALL)
+#undef CALL
+  }
+#define CALL(KK) run_rows<KK, +1>(c, nrows, (const double2*)in, (double2*)out, s)
+  PFA_SWITCH(K, CALL)
+#undef CALL
+}

@@ -1,0 +1,226 @@
+// Prime-factor (Good-Thomas) DFT engine for the odd grid lengths K = 2^k - 1.
+//
+// Every sampling length of the lambda=2 tilings factors into coprime odd
+// radices: 2047 = 23*89, 1023 = 3*11*31, 511 = 7*73, 255 = 3*5*17,
+// 4095 = 5*7*9*13, 63 = 7*9, 15 = 3*5; 3, 7, 31, 127 are prime.  Under the
+// Ruritanian input map the K-point DFT is a p_1 x ... x p_d DFT with NO
+// twiddle factors.  The rows stay in NATURAL order in shared memory for the
+// whole transform:
+//   * stage s (radix p) has K/p butterflies; butterfly b owns the positions
+//     (b*p + j*(K/p)) mod K, j = 0..p-1, which are exactly the elements whose
+//     dimension-s index is j and whose other indices are fixed (an element at
+//     position n has dimension-s index (n * (K/p)^{-1}) mod p, so b*p has index
+//     0 and adding K/p steps it by one).  Each stage transforms in place;
+//   * after the last stage, output k sits at position
+//     sum_s (k mod p_s) * (K/p_s) mod K  (the CRT map), read by pfa_pos().
+// A stage butterfly is evaluated directly in the symmetric-pair form
+//     y_k = A_k + DIR i B_k,  y_{p-k} = A_k - DIR i B_k,
+//     A_k = x_0 + sum_j (x_j + x_{p-j}) cos(2 pi jk/p),
+//     B_k =       sum_j (x_j - x_{p-j}) sin(2 pi jk/p),
+// (p-1)^2 real FMAs per p points.  A work item is (row, butterfly, k-group of
+// G output pairs); consecutive lanes take consecutive butterflies (odd
+// position stride p -> bank-conflict-free 16-byte accesses) with a
+// warp-uniform k-group, so the (cos, sin) pair of every (j, k) is ONE
+// broadcast 16-byte shared load from a dense per-radix table.  All items of a
+// stage are computed into registers before a barrier, then written back in
+// place (no ping-pong buffer: 16 bytes of shared memory per element).
+#pragma once
+#include "scv_internal.cuh"
+
+template <int K>
+struct PfaPlan;  // D factors P0..P3 (1 = unused); NT/R tuned per length
+#define SCV_PFA_PLAN(KK, DD, A, B, C, E)                                  \
+  template <>                                                             \
+  struct PfaPlan<KK> {                                                    \
+    static constexpr int K = KK, D = DD, P0 = A, P1 = B, P2 = C, P3 = E;  \
+  };
+SCV_PFA_PLAN(3, 1, 3, 1, 1, 1)
+SCV_PFA_PLAN(7, 1, 7, 1, 1, 1)
+SCV_PFA_PLAN(15, 2, 3, 5, 1, 1)
+SCV_PFA_PLAN(31, 1, 31, 1, 1, 1)
+SCV_PFA_PLAN(63, 2, 7, 9, 1, 1)
+SCV_PFA_PLAN(255, 3, 3, 5, 17, 1)
+SCV_PFA_PLAN(511, 2, 7, 73, 1, 1)
+SCV_PFA_PLAN(1023, 3, 3, 11, 31, 1)
+SCV_PFA_PLAN(2047, 2, 23, 89, 1, 1)
+SCV_PFA_PLAN(4095, 4, 5, 7, 9, 13)
+
+template <class PL, int S>
+__host__ __device__ constexpr int pfa_p() {
+  return S == 0 ? PL::P0 : S == 1 ? PL::P1 : S == 2 ? PL::P2 : PL::P3;
+}
+__host__ __device__ constexpr int pfa_h(int p) { return (p - 1) / 2; }
+// output pairs per work item (k-group size) per radix
+#ifndef SCV_PFA_G
+#define SCV_PFA_G 6
+#endif
+__host__ __device__ constexpr int pfa_group(int p) { return pfa_h(p) < SCV_PFA_G ? pfa_h(p) : SCV_PFA_G; }
+// padded number of output pairs (k-groups of G) for radix p
+__host__ __device__ constexpr int pfa_gp(int p) { return p > 1 ? ((pfa_h(p) + pfa_group(p) - 1) / pfa_group(p)) * pfa_group(p) : 0; }
+// coefficient table size (double2 entries) for radix p: h rows (j) of GP columns
+// (k, zero-padded beyond h): (cos, sin) of 2 pi jk/p
+__host__ __device__ constexpr int pfa_tab(int p) { return p > 1 ? pfa_h(p) * pfa_gp(p) : 0; }
+template <class PL>
+__host__ __device__ constexpr int pfa_tab_total() {
+  return pfa_tab(PL::P0) + pfa_tab(PL::P1) + pfa_tab(PL::P2) + pfa_tab(PL::P3);
+}
+template <class PL, int S>
+__host__ __device__ constexpr int pfa_tab_off() {
+  return (S > 0 ? pfa_tab(PL::P0) : 0) + (S > 1 ? pfa_tab(PL::P1) : 0) + (S > 2 ? pfa_tab(PL::P2) : 0);
+}
+
+// Coefficient tables (cos, sin)(2 pi jk/p) per radix, dense [j-1][k-1] with
+// k zero-padded to GP; staged once per CTA in shared memory (pfa_load_tables)
+// and read as warp-broadcast 16-byte loads.
+// position of output k after the transform (CRT map)
+template <class PL>
+__device__ __forceinline__ int pfa_pos(int k) {
+  constexpr int K = PL::K;
+  int a = (k % PL::P0) * (K / PL::P0);
+  if (PL::D > 1) a += (k % PL::P1) * (K / PL::P1);
+  if (PL::D > 2) a += (k % PL::P2) * (K / PL::P2);
+  if (PL::D > 3) a += (k % PL::P3) * (K / PL::P3);
+  return a % K;  // each term < K, at most 4 terms
+}
+
+// Stage the coefficient tables of this length into shared memory.
+template <class PL, int NT>
+__device__ __forceinline__ void pfa_load_tables(double2* tab, const double2* __restrict__ gtab) {
+  for (int i = threadIdx.x; i < pfa_tab_total<PL>(); i += NT) tab[i] = gtab[i];
+}
+
+// Accumulate k-group g (output pairs k = gG+1 .. gG+G) of one butterfly.
+// Data loads are software-pipelined one j ahead; the G coefficient pairs of a
+// j come from the shared table T (row stride GP) as broadcast loads.
+template <int p, int G>
+__device__ __forceinline__ void pfa_group_acc(const double2* __restrict__ T, const double2* __restrict__ Xr,
+                                              int c0, double2 (&A)[G], double2 (&B)[G], double2& Z, int K,
+                                              int step) {
+  constexpr int h = (p - 1) / 2;
+  constexpr int GP = pfa_gp(p);
+  const double2 x0 = Xr[c0];
+  Z = x0;
+#pragma unroll
+  for (int t = 0; t < G; ++t) {
+    A[t] = x0;
+    B[t] = make_double2(0.0, 0.0);
+  }
+  int pa = c0 + step, pb = c0 + (p - 1) * step;
+  if (pa >= K) pa -= K;
+  if (pb >= K) pb -= K;
+  double2 a = Xr[pa], bb = Xr[pb];
+  double2 cs[G];
+#pragma unroll 1
+  for (int j = 1; j <= h; ++j) {
+    pa += step;
+    if (pa >= K) pa -= K;
+    pb -= step;
+    if (pb < 0) pb += K;
+    T += GP;
+    // prefetch the next j's data (software pipelining)
+    double2 an = a, bn = bb;
+    if (j < h) {
+      an = Xr[pa];
+      bn = Xr[pb];
+    }
+#pragma unroll
+    for (int t = 0; t < G; ++t) cs[t] = T[t - GP];
+    const double2 s = make_double2(a.x + bb.x, a.y + bb.y);
+    const double2 d = make_double2(a.x - bb.x, a.y - bb.y);
+    Z.x += s.x;
+    Z.y += s.y;
+#pragma unroll
+    for (int t = 0; t < G; ++t) {
+      A[t].x = fma(s.x, cs[t].x, A[t].x);
+      A[t].y = fma(s.y, cs[t].x, A[t].y);
+      B[t].x = fma(d.x, cs[t].y, B[t].x);
+      B[t].y = fma(d.y, cs[t].y, B[t].y);
+    }
+    a = an;
+    bb = bn;
+  }
+}
+
+// cp.async 16-byte global -> shared copies (async prefetch of the next batch)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+#ifdef SCV_PFA_NOINLINE
+#define SCV_PFA_STAGE_INL __noinline__
+#else
+#define SCV_PFA_STAGE_INL __forceinline__
+#endif
+template <class PL, int S, int DIR, int R, int NT, int PITCH>
+__device__ SCV_PFA_STAGE_INL void pfa_stage(double2* X, const double2* tab) {
+  constexpr int p = pfa_p<PL, S>();
+  constexpr int h = pfa_h(p);
+  constexpr int K = PL::K;
+  constexpr int step = K / p;
+  constexpr int nbf = K / p;
+  constexpr int G = pfa_group(p);
+  constexpr int NG = (h + G - 1) / G;
+  constexpr int items = R * nbf * NG;
+  constexpr int IPT = (items + NT - 1) / NT;
+  double2 A[IPT][G], B[IPT][G], Z[IPT];
+  int pos[IPT], grp[IPT];
+#pragma unroll
+  for (int u = 0; u < IPT; ++u) {
+    const int it = threadIdx.x + u * NT;
+    grp[u] = -1;
+    pos[u] = 0;
+    if (IPT * NT > items && it >= items) continue;
+    const int g = it / (R * nbf);
+    const int rb = it - g * (R * nbf);
+    const int r = rb / nbf, b = rb - r * nbf;
+    const int c0 = b * p;
+    grp[u] = g;
+    pos[u] = r * PITCH + c0;
+    pfa_group_acc<p, G>(tab + pfa_tab_off<PL, S>() + g * G, X + r * PITCH, c0, A[u], B[u], Z[u], K, step);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < IPT; ++u) {
+    if (grp[u] < 0) continue;
+    const int g = grp[u];
+    const int rowoff = (pos[u] / PITCH) * PITCH;
+    const int c0 = pos[u] - rowoff;
+    double2* Xr = X + rowoff;
+    if (g == 0) Xr[c0] = Z[u];
+    int q1 = c0 + (g * G + 1) * step, q2 = c0 + (p - g * G - 1) * step;
+    while (q1 >= K) q1 -= K;
+    while (q2 >= K) q2 -= K;
+#pragma unroll
+    for (int t = 0; t < G; ++t) {
+      const int k = g * G + t + 1;
+      if (k <= h) {
+        const double2 iB = DIR < 0 ? make_double2(B[u][t].y, -B[u][t].x) : make_double2(-B[u][t].y, B[u][t].x);
+        Xr[q1] = make_double2(A[u][t].x + iB.x, A[u][t].y + iB.y);
+        Xr[q2] = make_double2(A[u][t].x - iB.x, A[u][t].y - iB.y);
+      }
+      q1 += step;
+      if (q1 >= K) q1 -= K;
+      q2 -= step;
+      if (q2 < 0) q2 += K;
+    }
+  }
+  __syncthreads();
+}
+
+// In-place K-point DFT (sign DIR) of R rows at X[r*PITCH + n] (natural order
+// in; CRT order out, read through pfa_pos).  Caller syncs before (data ready).
+template <class PL, int DIR, int R, int NT, int PITCH>
+__device__ __forceinline__ void pfa_dft(double2* X, const double2* tab) {
+  pfa_stage<PL, 0, DIR, R, NT, PITCH>(X, tab);
+  if constexpr (PL::D > 1) pfa_stage<PL, 1, DIR, R, NT, PITCH>(X, tab);
+  if constexpr (PL::D > 2) pfa_stage<PL, 2, DIR, R, NT, PITCH>(X, tab);
+  if constexpr (PL::D > 3) pfa_stage<PL, 3, DIR, R, NT, PITCH>(X, tab);
+}
+
+// host side (pfa.cu)
+int scv_pfa_tables(scv_ctx* c, int K, const double2** out);  // device copy of the tables
+bool scv_pfa_supported(int K);

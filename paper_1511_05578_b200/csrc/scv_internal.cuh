@@ -168,6 +168,16 @@ int scv_beta_sht(scv_ctx* c, int L, int spin, int real, const double2* G, double
 int scv_beta_so3(scv_ctx* c, int L, int real, const double2* W1p, double2* w, double pref,
                  cudaStream_t s);
 
+// prime-factor alpha/gamma kernels (pfa.cu), K = 2^k - 1
+bool scv_pfa_supported(int K);
+int scv_pfa_ana_alpha(scv_ctx* c, int K, int real, const double2* w, const double* hlb, const double* ls,
+                      const double* lc, double2* out, cudaStream_t s);
+int scv_pfa_ana_gamma(scv_ctx* c, int K, int real, double2* src, double* dst, cudaStream_t s);
+int scv_pfa_syn_alpha(scv_ctx* c, int K, int real, const void* in, int b0, int nbb, double2* chunk,
+                      cudaStream_t s);
+int scv_pfa_syn_gamma(scv_ctx* c, int K, int real, const double2* chunk, int b0, int nbb, double2* W1p,
+                      cudaStream_t s);
+
 inline int next_pow2_log(int x) {
   int lg = 0;
   while ((1 << lg) < x) ++lg;

@@ -150,6 +150,27 @@ extern "C" int scv_so3_inverse_curvelet(scv_ctx* c, int L, int real, const doubl
   SCV_TRY(scv_get_beta_tables(c, L, s, &t));
   const int K = 2 * L - 1;
   const long long LK = (long long)L * K;
+  if (scv_pfa_supported(K)) {
+    // hand-written prime-factor path: fused generate + alpha IDFT, then gamma IDFT
+    if (!real) {
+      {
+        SCV_PROF(c, s, "so3inv_alpha");
+        SCV_TRY(scv_pfa_ana_alpha(c, K, 0, (const double2*)w, c->hlb, t->sinh, t->cosh, (double2*)sig, s));
+      }
+      SCV_PROF(c, s, "so3inv_gamma");
+      SCV_TRY(scv_pfa_ana_gamma(c, K, 0, (double2*)sig, nullptr, s));
+      return SCV_OK;
+    }
+    void* T = nullptr;
+    SCV_TRY(scv_scratch(c, 0, (size_t)L * LK * 16, &T));
+    {
+      SCV_PROF(c, s, "so3inv_alpha");
+      SCV_TRY(scv_pfa_ana_alpha(c, K, 1, (const double2*)w, c->hlb, t->sinh, t->cosh, (double2*)T, s));
+    }
+    SCV_PROF(c, s, "so3inv_gamma");
+    SCV_TRY(scv_pfa_ana_gamma(c, K, 1, (double2*)T, (double*)sig, s));
+    return SCV_OK;
+  }
   if (!real) {
     {
     SCV_PROF(c, s, "so3inv_gen");
@@ -201,6 +222,22 @@ extern "C" int scv_so3_forward_curvelet(scv_ctx* c, int L, int real, const void*
   void* chunk = nullptr;
   SCV_TRY(scv_scratch(c, 1, per_b * nb, &chunk));
   SCV_CUDA(c, cudaMemsetAsync(w, 0, (size_t)2 * L * K * 16, s));
+  if (scv_pfa_supported(K)) {
+    // hand-written prime-factor path: alpha DFT rows -> chunk, gamma DFT + pruning -> W1p
+    const size_t per_bc = (size_t)K * K * 16;
+    int nbc = (int)std::max<size_t>(1, std::min<size_t>((size_t)L, (size_t)(1u << 30) / per_bc));
+    void* ch = nullptr;
+    SCV_TRY(scv_scratch(c, 1, per_bc * nbc, &ch));
+    for (int b0 = 0; b0 < L; b0 += nbc) {
+      const int nbb = std::min(nbc, L - b0);
+      {
+        SCV_PROF(c, s, "so3fwd_alpha");
+        SCV_TRY(scv_pfa_syn_alpha(c, K, real, sig, b0, nbb, (double2*)ch, s));
+      }
+      SCV_PROF(c, s, "so3fwd_gamma");
+      SCV_TRY(scv_pfa_syn_gamma(c, K, real, (const double2*)ch, b0, nbb, (double2*)W1p, s));
+    }
+  } else
   for (int b0 = 0; b0 < L; b0 += nb) {
     const int nbb = std::min(nb, L - b0);
     int n2[2] = {K, K};

@@ -202,6 +202,25 @@ int scv_get_beta_tables(scv_ctx* c, int L, cudaStream_t s, const BetaTables** ou
     const int r = K - 2 * b - 1;
     lcos[b] = r == 0 ? -HUGE_VAL : (double)logl(sinl(kPi * (ld)r / (ld)(2 * K)));
   }
+  if (scv_pfa_supported(K) && scv_pfa_supported(4 * L - 1)) {
+    const int K2 = 4 * L - 1;
+    std::vector<cld> ph(K);
+    for (int q = 0; q < K; ++q) ph[q] = expipi(-(long long)(q - (L - 1)), K) / (ld)K;
+    std::vector<ld> ctab(K2);
+    for (int r = 0; r < K2; ++r) ctab[r] = cosl(2.0L * kPi * (ld)r / (ld)K2);
+    std::vector<double> wf(K2, 0.0);
+    for (int k = 0; k < K2; ++k) {
+      ld acc = 0;
+      for (long long j = -(2LL * L - 2); j <= 2LL * L - 2; j += 2) {
+        long long r = (j * k) % K2;
+        if (r < 0) r += K2;
+        acc += w_even(j) * ctab[r];
+      }
+      wf[scv_pfa_pos_host(K2, k)] = (double)(acc / (ld)K2);
+    }
+    SCV_TRY(upload(c, &t.phs, to_d2(ph), s));
+    SCV_TRY(upload(c, &t.wfpos, wf, s));
+  }
   SCV_TRY(upload(c, &t.tw, to_d2(tw), s));
   SCV_TRY(upload(c, &t.chirpA, to_d2(A), s));
   SCV_TRY(upload(c, &t.Hf, to_d2(h), s));
@@ -316,6 +335,7 @@ int scv_destroy(scv_ctx* c) {
     BetaTables& t = kv.second;
     cudaFree(t.tw); cudaFree(t.chirpA); cudaFree(t.Hf); cudaFree(t.chirpC);
     cudaFree(t.Vf); cudaFree(t.Aalt); cudaFree(t.sinh); cudaFree(t.cosh);
+    cudaFree(t.phs); cudaFree(t.wfpos);
   }
   for (auto& kv : c->aux) cudaFree(kv.second);
   for (auto& r : c->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }

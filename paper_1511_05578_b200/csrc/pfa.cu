@@ -491,6 +491,282 @@ static int persistent_grid(scv_ctx* c, Kern k, int nt, size_t sm, long long nbat
   return SCV_OK;
 }
 
+// ---------------------------------------------------------------------------
+// beta stage + Delta contraction of the SO(3) forward transform on the
+// prime-factor engine (restates so3.py:203-243; the packed-pair formulation
+// is documented in beta.cu).  Per (n, column pair):
+//   X1 <- packed extension of the two columns (natural b order)
+//   X1 <- DFT_K (forward, CRT order);  F[m''] = (1/K) e^{-i m'' pi/K} X1[pos(m'' mod K)]
+//   X1 <- F (natural);  X2 <- G = F - (gamma/2)(-1)^m'' wrapped mod K2 = 4L-1
+//   X2 <- IDFT_K2( DFT_K2(X2) * DFT_K2(w_even)/K2 )   (the forward output is in
+//         CRT order and the inverse consumes CRT order, returning natural order)
+//   then Y_E / Y_O and the contraction exactly as in beta.cu.
+// K2 = 4L-1 >= 4L-3 keeps the circular convolution alias-free for |m'| <= L-1.
+// ---------------------------------------------------------------------------
+int scv_pfa_pos_host(int K, int k) {
+  int f[4];
+  factors_of(K, f);
+  long long a = 0;
+  for (int s = 0; s < 4; ++s)
+    if (f[s] > 1) a += (long long)(k % f[s]) * (K / f[s]);
+  return (int)(a % K);
+}
+
+bool scv_pfa_beta_supported(int L) {
+  return L >= 128 && L <= 1024 && scv_pfa_supported(2 * L - 1) && scv_pfa_supported(4 * L - 1);
+}
+
+// Three batched kernels over chunks of (n, pair) tasks; F and E go through a
+// chunk scratch buffer so each transform runs as an efficient batch:
+//   k_beta_f<K>   : packed extension -> DFT_K -> F (natural), gamma per task
+//   k_beta_e<K2>  : G (wrapped) -> DFT_K2 -> * w spectrum -> IDFT_K2 -> E (|m'| <= L-1)
+//   k_beta_c<L>   : Y_E / Y_O and the Delta contraction, one warp per task
+template <int K>
+__global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
+    k_beta_f(int real, const double2* __restrict__ W1p, const int2* __restrict__ tasks, int t0, int ntask,
+             const double2* __restrict__ phs, double2* __restrict__ Fbuf, double2* __restrict__ gam,
+             const double2* __restrict__ gtab) {
+  using PL = PfaPlan<K>;
+  constexpr int R = PfaCfg<K, false>::R, NT = PfaCfg<K, false>::NT;
+  constexpr int L = (K + 1) / 2;
+  extern __shared__ double2 sm[];
+  double2* tab = sm;
+  double2* X = sm + pfa_tab_total<PL>();
+  pfa_load_tables<PL, NT>(tab, gtab);
+  const long long nb = (ntask + R - 1) / R;
+#pragma unroll 1
+  for (long long bt = blockIdx.x; bt < nb; bt += gridDim.x) {
+    const int r0 = (int)(bt * R);
+#pragma unroll 4
+    for (int i = threadIdx.x; i < R * K; i += NT) {
+      const int r = i / K, b = i - r * K;
+      double2 e = make_double2(0.0, 0.0);
+      if (r0 + r < ntask) {
+        const int2 tk = tasks[t0 + r0 + r];
+        const int n = tk.x, l = n < 0 ? -n : n;
+        const int m0 = -l + 2 * tk.y, m1 = m0 + 1;
+        const long long cb = w1p_colbase(n, real);
+        const bool even0 = ((n + m0) & 1) == 0;
+        const int src = b < L ? b : 2 * L - 2 - b;
+        const double2 v0 = W1p[(cb + m0 + l) * (long long)L + src];
+        const double2 v1 = (m1 <= l) ? W1p[(cb + m1 + l) * (long long)L + src] : make_double2(0.0, 0.0);
+        const double2 ve = even0 ? v0 : v1;
+        double2 vo = even0 ? v1 : v0;
+        if (b >= L) vo = make_double2(-vo.x, -vo.y);
+        e = make_double2(ve.x + vo.x, ve.y + vo.y);
+        if (b == L - 1) gam[r0 + r] = make_double2(vo.x * (2.0 / K), vo.y * (2.0 / K));
+      }
+      X[i] = e;
+    }
+    __syncthreads();
+    pfa_dft<PL, -1, R, NT, K>(X, tab);
+#pragma unroll 4
+    for (int i = threadIdx.x; i < R * K; i += NT) {
+      const int r = i / K, q = i - r * K;
+      if (r0 + r < ntask) {
+        int kk = q - (L - 1);
+        if (kk < 0) kk += K;
+        Fbuf[(long long)(r0 + r) * K + q] = cmul(__ldg(phs + q), X[r * K + pfa_pos<PL>(kk)]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int K2>
+__global__ void __launch_bounds__(PfaCfg<K2, false>::NT, PfaCfg<K2, false>::MINB)
+    k_beta_e(int ntask, const double2* __restrict__ Fbuf, const double2* __restrict__ gam,
+             const double* __restrict__ wfpos, double2* __restrict__ Ebuf, const double2* __restrict__ gtab) {
+  using PL = PfaPlan<K2>;
+  constexpr int R = PfaCfg<K2, false>::R, NT = PfaCfg<K2, false>::NT;
+  constexpr int L = (K2 + 1) / 4, K = 2 * L - 1;
+  extern __shared__ double2 sm[];
+  double2* tab = sm;
+  double2* X = sm + pfa_tab_total<PL>();
+  pfa_load_tables<PL, NT>(tab, gtab);
+  const long long nb = (ntask + R - 1) / R;
+#pragma unroll 1
+  for (long long bt = blockIdx.x; bt < nb; bt += gridDim.x) {
+    const int r0 = (int)(bt * R);
+#pragma unroll 4
+    for (int i = threadIdx.x; i < R * K2; i += NT) {
+      const int r = i / K2, p = i - r * K2;
+      const int mpp = p <= L - 1 ? p : p - K2;
+      double2 v = make_double2(0.0, 0.0);
+      if (r0 + r < ntask && mpp >= -(L - 1)) {
+        const double2 F = Fbuf[(long long)(r0 + r) * K + mpp + L - 1];
+        const double2 g = gam[r0 + r];
+        const double hh = (mpp & 1) ? -0.5 : 0.5;
+        v = make_double2(F.x - hh * g.x, F.y - hh * g.y);
+      }
+      X[i] = v;
+    }
+    __syncthreads();
+    pfa_dft_ool<PL, -1, R, NT, K2>(X, tab);
+#pragma unroll 4
+    for (int i = threadIdx.x; i < R * K2; i += NT) {
+      const int p = i - (i / K2) * K2;
+      const double f = __ldg(wfpos + p);
+      X[i] = make_double2(X[i].x * f, X[i].y * f);
+    }
+    __syncthreads();
+    pfa_dft_ool<PL, +1, R, NT, K2>(X, tab);
+#pragma unroll 4
+    for (int i = threadIdx.x; i < R * K; i += NT) {
+      const int r = i / K, q = i - r * K;
+      const int mp = q - (L - 1);
+      if (r0 + r < ntask) Ebuf[(long long)(r0 + r) * K + q] = X[r * K2 + (mp >= 0 ? mp : mp + K2)];
+    }
+    __syncthreads();
+  }
+}
+
+template <int L>
+__global__ void __launch_bounds__(256) k_beta_c(int real, const int2* __restrict__ tasks, int t0, int ntask,
+                                                const double2* __restrict__ Fbuf, const double2* __restrict__ Ebuf,
+                                                const double2* __restrict__ gam, const double* __restrict__ Aalt,
+                                                const double* __restrict__ delta, double pref,
+                                                double2* __restrict__ wout) {
+  constexpr int K = 2 * L - 1;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= ntask) return;
+  const int2 tk = tasks[t0 + warp];
+  const int n = tk.x, l = n < 0 ? -n : n;
+  const int m0 = -l + 2 * tk.y, m1 = m0 + 1;
+  const bool even0 = ((n + m0) & 1) == 0;
+  const int mE = even0 ? m0 : m1, mO = even0 ? m1 : m0;
+  const double2* F = Fbuf + (long long)warp * K + (L - 1);  // F[m''] at F[m'']
+  const double2* E = Ebuf + (long long)warp * K + (L - 1);
+  const double2 g = gam[warp];
+  const double hp = 0.5 * SCV_PI;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int mp = -l + lane; mp <= l; mp += 32) {
+    const double2 Ep = E[mp], Em = E[-mp];
+    const double2 ee = make_double2(0.5 * (Ep.x + Em.x), 0.5 * (Ep.y + Em.y));
+    const double2 eo = make_double2(0.5 * (Ep.x - Em.x), 0.5 * (Ep.y - Em.y));
+    double2 xe[2], xo[2];
+#pragma unroll
+    for (int z = 0; z < 2; ++z) {
+      const int k = z == 0 ? mp + 1 : mp - 1;
+      if (k < -(L - 1) || k > L - 1) {
+        xe[z] = make_double2(0.0, 0.0);
+        xo[z] = make_double2(0.0, 0.0);
+      } else {
+        const double2 a = F[k], b = F[-k];
+        const double hh = (k & 1) ? -1.0 : 1.0;
+        xe[z] = make_double2(0.5 * (a.x + b.x - hh * g.x), 0.5 * (a.y + b.y - hh * g.y));
+        xo[z] = make_double2(0.5 * (a.x - b.x + hh * g.x), 0.5 * (a.y - b.y + hh * g.y));
+      }
+    }
+    const double2 dE = make_double2(xe[0].x - xe[1].x, xe[0].y - xe[1].y);
+    const double2 dO = make_double2(xo[0].x - xo[1].x, xo[0].y - xo[1].y);
+    const double2 yE = make_double2(ee.x - hp * dE.y, ee.y + hp * dE.x);
+    const double aa = 0.5 * __ldg(Aalt + mp + L - 1);
+    const double2 yO = make_double2(eo.x + aa * g.x - hp * dO.y, eo.y + aa * g.y + hp * dO.x);
+    const double dn = wedge_get(delta, l, mp, n);
+    const double dE2 = (mE <= l) ? wedge_get(delta, l, mp, mE) * dn : 0.0;
+    const double dO2 = (mO <= l) ? wedge_get(delta, l, mp, mO) * dn : 0.0;
+    acc[0] += dE2 * yE.x;
+    acc[1] += dE2 * yE.y;
+    acc[2] += dO2 * yO.x;
+    acc[3] += dO2 * yO.y;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+  if (lane == 0) {
+    const int c = L - 1;
+    const int sheet = n >= 0 ? 0 : 1;
+    double2* row = wout + ((long long)sheet * L + l) * K;
+    const int ms[2] = {mE, mO};
+    for (int i = 0; i < 2; ++i) {
+      const int m = ms[i];
+      if (m > l) continue;
+      const double2 v = cipow(make_double2(pref * acc[2 * i], pref * acc[2 * i + 1]), m - n);
+      row[c + m] = v;
+      if (real && n > 0) {  // row(-n)[m] = (-1)^{m+n} conj(row(n)[-m])  (so3.py:379-382)
+        double2 cv = make_double2(v.x, -v.y);
+        if ((m + n) & 1) cv = make_double2(-cv.x, -cv.y);
+        wout[((long long)1 * L + l) * K + c - m] = cv;
+      }
+    }
+  }
+}
+
+static int beta_pfa_tasks(scv_ctx* c, int L, int real, const int2** out, int* count) {
+  const std::string key = "pfatasks_" + std::to_string(L) + "_" + std::to_string(real);
+  std::vector<int2> v;
+  for (int l = L - 1; l >= 0; --l)
+    for (int sg = 0; sg < 2; ++sg) {
+      const int n = sg == 0 ? l : -l;
+      if (sg == 1 && (l == 0 || real)) continue;
+      for (int i = 0; i <= l; ++i) v.push_back(make_int2(n, i));
+    }
+  *count = (int)v.size();
+  auto it = c->aux.find(key);
+  if (it != c->aux.end()) {
+    *out = (const int2*)it->second;
+    return SCV_OK;
+  }
+  void* d = nullptr;
+  SCV_CUDA(c, cudaMalloc(&d, v.size() * sizeof(int2)));
+  SCV_CUDA(c, cudaMemcpy(d, v.data(), v.size() * sizeof(int2), cudaMemcpyHostToDevice));
+  c->aux[key] = d;
+  *out = (const int2*)d;
+  return SCV_OK;
+}
+
+template <int L>
+static int run_beta_pfa(scv_ctx* c, int real, const double2* W1p, double2* w, double pref, const BetaTables* t,
+                        cudaStream_t s) {
+  constexpr int K = 2 * L - 1, K2 = 4 * L - 1;
+  const double2 *tab1, *tab2;
+  SCV_TRY(scv_pfa_tables(c, K, &tab1));
+  SCV_TRY(scv_pfa_tables(c, K2, &tab2));
+  const int2* tasks;
+  int nt;
+  SCV_TRY(beta_pfa_tasks(c, L, real, &tasks, &nt));
+  // chunk scratch: F and E (K each) + gamma per task, in scratch slot 1 (free after the alpha/gamma passes)
+  const size_t per_task = (size_t)(2 * K + 1) * sizeof(double2);
+  size_t want = std::max<size_t>(per_task * 1024, (size_t)1 << 30);
+  void* scr = nullptr;
+  SCV_TRY(scv_scratch(c, 1, std::min(want, per_task * (size_t)nt), &scr));
+  const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)nt, c->scratch_bytes[1] / per_task));
+  double2* Fb = (double2*)scr;
+  double2* Eb = Fb + (size_t)chunk * K;
+  double2* gb = Eb + (size_t)chunk * K;
+  const size_t smf = pfa_smem<K, false>(), sme = pfa_smem<K2, false>();
+  for (int t0 = 0; t0 < nt; t0 += chunk) {
+    const int ntask = std::min(chunk, nt - t0);
+    int grid;
+    SCV_TRY(persistent_grid(c, k_beta_f<K>, PfaCfg<K, false>::NT, smf, (ntask + PfaCfg<K, false>::R - 1) / PfaCfg<K, false>::R, &grid));
+    k_beta_f<K><<<grid, PfaCfg<K, false>::NT, smf, s>>>(real, W1p, tasks, t0, ntask, t->phs, Fb, gb, tab1);
+    c->launches++;
+    SCV_CUDA(c, cudaGetLastError());
+    SCV_TRY(persistent_grid(c, k_beta_e<K2>, PfaCfg<K2, false>::NT, sme, (ntask + PfaCfg<K2, false>::R - 1) / PfaCfg<K2, false>::R, &grid));
+    k_beta_e<K2><<<grid, PfaCfg<K2, false>::NT, sme, s>>>(ntask, Fb, gb, t->wfpos, Eb, tab2);
+    c->launches++;
+    SCV_CUDA(c, cudaGetLastError());
+    k_beta_c<L><<<(ntask * 32 + 255) / 256, 256, 0, s>>>(real, tasks, t0, ntask, Fb, Eb, gb, t->Aalt, c->delta,
+                                                          pref, w);
+    c->launches++;
+    SCV_CUDA(c, cudaGetLastError());
+  }
+  return SCV_OK;
+}
+
+int scv_pfa_beta_so3(scv_ctx* c, int L, int real, const double2* W1p, double2* w, double pref,
+                     const BetaTables* t, cudaStream_t s) {
+  switch (L) {
+    case 128: return run_beta_pfa<128>(c, real, W1p, w, pref, t, s);
+    case 256: return run_beta_pfa<256>(c, real, W1p, w, pref, t, s);
+    case 512: return run_beta_pfa<512>(c, real, W1p, w, pref, t, s);
+    case 1024: return run_beta_pfa<1024>(c, real, W1p, w, pref, t, s);
+    default: return scv_fail(c, SCV_EINVAL, "no prime-factor beta stage for L=" + std::to_string(L));
+  }
+}
+
 #define PFA_SWITCH(K, CALL)                                                                 \
   switch (K) {                                                                              \
     case 3: return CALL(3); case 7: return CALL(7); case 15: return CALL(15);              \

@@ -221,6 +221,13 @@ __device__ __forceinline__ void pfa_dft(double2* X, const double2* tab) {
   if constexpr (PL::D > 3) pfa_stage<PL, 3, DIR, R, NT, PITCH>(X, tab);
 }
 
+// Out-of-line variant: isolates the transform's register allocation from a
+// large calling kernel (used by the fused beta stage).
+template <class PL, int DIR, int R, int NT, int PITCH>
+__device__ __noinline__ void pfa_dft_ool(double2* X, const double2* tab) {
+  pfa_dft<PL, DIR, R, NT, PITCH>(X, tab);
+}
+
 // host side (pfa.cu)
 int scv_pfa_tables(scv_ctx* c, int K, const double2** out);  // device copy of the tables
 bool scv_pfa_supported(int K);

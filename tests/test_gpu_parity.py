@@ -128,7 +128,7 @@ def _random_cw(L, seed):
     return w
 
 
-@pytest.mark.parametrize("L", [1, 2, 32, 64, 127])
+@pytest.mark.parametrize("L", [1, 2, 32, 64, 127, 128, 256])
 def test_so3_vs_oracle(L):
     w = _random_cw(L, L)
     grid = sc.SO3Grid(L, L, L)
@@ -151,7 +151,7 @@ def test_so3_constant_field():
     assert abs(host(back.values)[0, 0, L - 1] - 8 * math.pi ** 2) <= 1e-10
 
 
-@pytest.mark.parametrize("L", [256])
+@pytest.mark.parametrize("L", [256, 512])
 def test_so3_round_trip_large(L):
     w = _random_cw(L, 7)
     f = sc.so3_inverse_curvelet(sc.CurveletWignerCoeffs(L, w), sc.SO3Grid(L, L, L))

@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-json", default="")
+    ap.add_argument("--shard-scales", action="store_true",
+                    help="N>1: one map per step with its scales sharded over the ranks "
+                         "(NCCL broadcast + gather); default is one map per rank per step")
     return ap.parse_args()
 
 
@@ -155,37 +158,51 @@ def stage_roofline(a, prof, Ljs, hbm_peak, fp64_peak):
     vol = sum(K(L) ** 2 * L for L in Ljs)
     cols = sum((2 * L * L - 1) * L for L in Ljs)
     bytes_stage = {
-        "so3inv_gen": 16 * vol,                       # write the (n, b, alpha-bin) volume once
-        "so3inv_alpha_fft": 2 * 16 * vol,             # read + write
-        "so3inv_gamma_fft": 2 * 16 * vol,
-        "so3fwd_fft2d": (b + 16) * vol,               # read input + write chunk
-        "so3fwd_extract": 2 * 16 * cols,              # pruned read + write
+        "so3inv_alpha": 16 * vol,                     # generated in shared memory, written once
+        "so3inv_gamma": 2 * 16 * vol,                 # read + write in place
+        "so3fwd_alpha": (b + 16) * vol,               # read the scale signal + write the chunk
+        "so3fwd_gamma": 16 * vol + 16 * cols,         # read the chunk + write the pruned columns
         "beta_so3": 16 * cols,                        # read pruned columns once
     }
-    # algorithmic FP64 flops: beta stage = 4 P-point FFTs per column pair (5 P log2 P each)
     def P_of(L):
         return 1 << max(4, math.ceil(math.log2(4 * L - 3)))
+    # algorithmic FP64 flops (5 N log2 N per complex transform):
+    #   alpha/gamma passes: one K-point transform per row / column of the volume
+    #   beta stage: the paper's per-column work -- one K-point DFT + the padded
+    #   weight convolution (two P-point transforms) -- for the 2L^2-1 columns
     flops_stage = {
-        "beta_so3": sum((L * L) * 4 * 5 * P_of(L) * math.log2(P_of(L)) for L in Ljs),
+        "so3inv_alpha": sum(K(L) * L * 5 * K(L) * math.log2(K(L)) for L in Ljs),
+        "so3inv_gamma": sum(K(L) * L * 5 * K(L) * math.log2(K(L)) for L in Ljs),
+        "so3fwd_alpha": sum(K(L) * L * 5 * K(L) * math.log2(K(L)) for L in Ljs),
+        "so3fwd_gamma": sum(K(L) * L * 5 * K(L) * math.log2(K(L)) for L in Ljs),
+        "beta_so3": sum((2 * L * L - 1) * (5 * K(L) * math.log2(K(L)) + 2 * 5 * P_of(L) * math.log2(P_of(L)))
+                        for L in Ljs),
     }
+    # per map: work of the stage over all its launches / its device time per map
     name, (cnt, ms) = max(prof.items(), key=lambda kv: kv[1][1])
-    per_launch_ms = ms / max(cnt, 1)
-    launches_per_map = len(Ljs)
-    out = {"stage": name}
-    if name in flops_stage:
-        fl = flops_stage[name] / launches_per_map
-        ach = fl / (per_launch_ms * 1e-3) / 1e12
+    ms_map = ms / a.steps
+    out = {"stage": name, "launches_per_map": cnt / a.steps, "ms_per_map": ms_map}
+    if name == "beta_so3":
+        ach = flops_stage[name] / (ms_map * 1e-3) / 1e12
         out.update({"bound": "fp64", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
-                    "frac": ach / fp64_peak, "peak_source": "measured DFMA loop in this run (scv_fp64_peak)"})
-        by = bytes_stage.get(name, 0) / launches_per_map
-        out["hbm_gbs_alg"] = by / (per_launch_ms * 1e-3) / 1e9
+                    "frac": ach / fp64_peak, "peak_source": "measured DFMA loop in this run (scv_fp64_peak)",
+                    "hbm_gbs_alg": bytes_stage[name] / (ms_map * 1e-3) / 1e9})
     else:
-        by = bytes_stage.get(name, 0) / launches_per_map
-        ach = by / (per_launch_ms * 1e-3) / 1e9
+        ach = bytes_stage.get(name, 0) / (ms_map * 1e-3) / 1e9
         out.update({"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
                     "frac": ach / hbm_peak, "peak_source": "MEASURED_PEAKS.json hbm_gbs"})
+        if name in flops_stage:
+            out["fp64_tflops_alg"] = flops_stage[name] / (ms_map * 1e-3) / 1e12
     out["traffic"] = None
-    out["ms_per_launch"] = per_launch_ms
+    out["all_stages"] = {}
+    for nm, (c_, ms_) in prof.items():
+        mm = ms_ / a.steps
+        e = {"ms_per_map": mm}
+        if nm in bytes_stage:
+            e["hbm_gbs_alg"] = bytes_stage[nm] / (mm * 1e-3) / 1e9
+        if nm in flops_stage:
+            e["fp64_tflops_alg"] = flops_stage[nm] / (mm * 1e-3) / 1e12
+        out["all_stages"][nm] = e
     return out
 
 
@@ -220,6 +237,14 @@ def run_ours(a):
     def step(fin):
         c = ana(fin, t, scale_out=scale_out)
         return syn(c, t)
+
+    if a.shard_scales and world > 1:
+        from paper_1511_05578_b200.dist import analyze_sharded, synthesize_sharded
+
+        def step(fin):  # noqa: F811
+            c = analyze_sharded(fin, t, real=a.real)
+            g = synthesize_sharded(c, t)
+            return g if g is not None else fin
 
     g = None
     for _ in range(a.warmup):
@@ -263,7 +288,8 @@ def run_ours(a):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     ms_per_step = ms / a.steps
-    value = world * a.steps / (ms * 1e-3)
+    maps_per_step = 1 if (a.shard_scales and world > 1) else world
+    value = maps_per_step * a.steps / (ms * 1e-3)
 
     # ---------------- e2e: host buffers through the public API ----------------
     e2e = None
@@ -290,7 +316,7 @@ def run_ours(a):
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ems = float(tt.item())
         nb = host_in.numel() * host_in.element_size()
-        e2e = {"value": world * a.steps / (ems * 1e-3), "unit": "maps/s", "h2d_bytes_per_step": nb,
+        e2e = {"value": maps_per_step * a.steps / (ems * 1e-3), "unit": "maps/s", "h2d_bytes_per_step": nb,
                "d2h_bytes_per_step": nb, "ms_per_step": ems / a.steps}
 
     roof = stage_roofline(a, prof, Ljs, hbm_peak, fp64_peak)
@@ -304,13 +330,16 @@ def run_ours(a):
         "warmup": a.warmup,
         "ms_per_step": ms_per_step,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if (a.shard_scales and world > 1) else "weak",
         "vs_baseline": None,
         "dtype": "f64" if a.real else "c128",
         "data": "synthetic (seeded Gaussian f_lm, C_l=(l+1)^-2)",
         "config": {"workload": workload_name(a), "L": a.L, "spin": a.spin, "lambda": a.lam,
                    "j_min": a.jmin, "j_max": p.j_max, "scale_band_limits": Ljs,
-                   "maps_per_step_per_gpu": 1, "parallelism": f"maps x{world}" if world > 1 else "1 GPU",
+                   "maps_per_step": maps_per_step,
+                   "parallelism": ("scales sharded x%d (NCCL broadcast f_lm + gather terms)" % world
+                                   if (a.shard_scales and world > 1) else
+                                   (f"maps x{world} (one map per rank)" if world > 1 else "1 GPU")),
                    "l2_flush": "not needed: every scale volume >> 126 MB L2"},
         "roofline": roof,
         "paper_roofline": {"B_alg_GB": B_alg / 1e9, "F_alg_TF": F_alg / 1e12, "t_roof_ms": t_roof * 1e3,

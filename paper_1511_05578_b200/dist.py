@@ -1,0 +1,200 @@
+"""Scale-sharded multi-GPU analysis / synthesis (one process per GPU).
+
+The curvelet scales j are independent units: analysis of a
+scale is a pure function of the broadcast f_lm and psi_j; synthesis of a
+scale contributes an additive term to acc_lm.  This module shards the scales
+of ONE map over the ranks of a torch.distributed group:
+
+  analysis   rank `src` computes f_lm (SHT) and broadcasts it (NCCL broadcast
+             over NVLink, L^2 * 16 B); every rank runs the SO(3) inverse
+             transforms of the scales it owns; the scaling signal lives on src.
+  synthesis  every rank computes, for each scale it owns, the term
+             T_j[lm] = W_{m,+l} psi_+(l) + W_{m,-l} psi_-(l); the terms are
+             gathered on `dst`, which adds them in the reference order
+             (coarse -> fine, transform.py:164-178), then the scaling part,
+             then runs the inverse SHT.  Gathering per-scale terms (instead of
+             an arithmetic all-reduce) keeps the merge deterministic and
+             bit-identical to the single-GPU path.
+
+Scales are assigned greedily by cost (the (2L_j-1)^2 L_j sample volume),
+largest first to the least-loaded rank.  The per-rank compute goes through a
+backend object; the default one is the CUDA path of this package.  (The
+CPU tests inject the oracle as backend to exercise the sharding logic on the
+gloo backend without a GPU.)
+
+For throughput over many maps the better decomposition is maps-per-rank
+(bench.py's default multi-GPU mode): no collective at all.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import torch
+import torch.distributed as dist
+
+from .transform import scale_band_limit, scaling_band_limit
+
+__all__ = ["ScalePlan", "ShardedCoeffs", "CudaBackend", "analyze_sharded", "synthesize_sharded"]
+
+
+@dataclass
+class ScalePlan:
+    """owner[j - j_min] = rank that holds scale j."""
+
+    j_min: int
+    owner: list
+    cost: list
+
+    @classmethod
+    def build(cls, params, world: int, multires: bool = True) -> "ScalePlan":
+        js = list(range(params.j_min, params.j_max + 1))
+        Ljs = [scale_band_limit(params, j) if multires else params.band_limit for j in js]
+        cost = [(2 * L - 1) ** 2 * L for L in Ljs]
+        load = [0] * world
+        owner = [0] * len(js)
+        for i in sorted(range(len(js)), key=lambda i: (-cost[i], i)):
+            r = min(range(world), key=lambda q: (load[q], q))
+            owner[i] = r
+            load[r] += cost[i]
+        return cls(params.j_min, owner, cost)
+
+    def owned(self, rank: int) -> list:
+        return [self.j_min + i for i, r in enumerate(self.owner) if r == rank]
+
+
+@dataclass
+class ShardedCoeffs:
+    """Distributed CurveletCoeffs: `scales` holds only this rank's scales."""
+
+    params: object
+    plan: ScalePlan
+    scales: dict = field(default_factory=dict)
+    scaling: object = None  # on src only
+    multires: bool = True
+    real: bool = False
+
+
+class CudaBackend:
+    """Per-rank compute on this package's CUDA path."""
+
+    def __init__(self, device=None):
+        self.device = device
+
+    def sht_forward(self, f):
+        from .sphere import sht_forward, sht_forward_real
+        return (sht_forward_real(f) if f.real else sht_forward(f)).values
+
+    def flm_like(self, L):
+        return torch.empty(L * L, dtype=torch.complex128, device=torch.device("cuda", torch.cuda.current_device()))
+
+    def scale_inverse(self, flm_vals, t, j, Lj, real):
+        from . import _cabi
+        from .sphere import HarmonicCoeffs
+        from .transform import _scale_wigner, device_tiling
+        from .so3 import SO3Grid, so3_inverse_curvelet, so3_inverse_curvelet_real
+        dev = flm_vals.device
+        ctx = _cabi.context(dev)
+        flm = HarmonicCoeffs(t.params.band_limit, 0 if real else t.params.spin, flm_vals, real=real)
+        w = _scale_wigner(ctx, flm, device_tiling(t, dev), j, Lj)
+        inv = so3_inverse_curvelet_real if real else so3_inverse_curvelet
+        return inv(w, SO3Grid(Lj, Lj, Lj))
+
+    def scaling_map(self, flm_vals, t, Ls, real):
+        from . import _cabi
+        from .sphere import HarmonicCoeffs, sht_inverse, sht_inverse_real
+        from .transform import _scaling_coeffs, device_tiling
+        dev = flm_vals.device
+        ctx = _cabi.context(dev)
+        flm = HarmonicCoeffs(t.params.band_limit, 0 if real else t.params.spin, flm_vals, real=real)
+        s = _scaling_coeffs(ctx, flm, device_tiling(t, dev), Ls, real)
+        return sht_inverse_real(s) if real else sht_inverse(s)
+
+    def scale_term(self, sig, t, j, real):
+        from . import _cabi
+        from .so3 import so3_forward_curvelet, so3_forward_curvelet_real
+        from .transform import device_tiling
+        dev = sig.values.device
+        ctx = _cabi.context(dev)
+        L = t.params.band_limit
+        w = so3_forward_curvelet_real(sig) if real else so3_forward_curvelet(sig)
+        pos, neg = device_tiling(t, dev).psi[j]
+        term = torch.zeros(L * L, dtype=torch.complex128, device=dev)
+        ctx.call("accumulate", L, sig.grid.L, _cabi.ptr(w.values), _cabi.ptr(pos), _cabi.ptr(neg), _cabi.ptr(term))
+        return term
+
+    def finish(self, acc, scaling_sig, t, real):
+        from . import _cabi
+        from .sphere import HarmonicCoeffs, sht_forward, sht_forward_real, sht_inverse, sht_inverse_real
+        from .transform import device_tiling
+        dev = acc.device
+        ctx = _cabi.context(dev)
+        p = t.params
+        L = p.band_limit
+        dt = device_tiling(t, dev)
+        slm = sht_forward_real(scaling_sig) if real else sht_forward(scaling_sig)
+        ctx.call("accumulate_scaling", L, slm.band_limit, _cabi.ptr(slm.values), _cabi.ptr(dt.scaling), _cabi.ptr(acc))
+        ctx.call("finish_acc", L, p.spin, 1 if real else 0, _cabi.ptr(acc))
+        if real:
+            return sht_inverse_real(HarmonicCoeffs(L, 0, acc, real=True))
+        return sht_inverse(HarmonicCoeffs(L, p.spin, acc))
+
+
+def _rank_world(group):
+    if not dist.is_available() or not dist.is_initialized():
+        return 0, 1
+    return dist.get_rank(group), dist.get_world_size(group)
+
+
+def analyze_sharded(f, t, group=None, backend=None, src: int = 0, multires: bool = True,
+                    real: bool = False) -> ShardedCoeffs:
+    """Analysis of one map with its scales sharded over the group.
+
+    `f` is only read on `src`.  Mirrors transform.analyze (transform.py:139-152)."""
+    backend = backend or CudaBackend()
+    rank, world = _rank_world(group)
+    p = t.params
+    L = p.band_limit
+    plan = ScalePlan.build(p, world, multires)
+    if rank == src:
+        flm = backend.sht_forward(f)
+    else:
+        flm = backend.flm_like(L)
+    if world > 1:
+        dist.broadcast(flm, src=src, group=group)
+    out = ShardedCoeffs(p, plan, multires=multires, real=real)
+    for j in plan.owned(rank):
+        Lj = scale_band_limit(p, j) if multires else L
+        out.scales[j] = backend.scale_inverse(flm, t, j, Lj, real)
+    if rank == src:
+        Ls = scaling_band_limit(p) if multires else L
+        out.scaling = backend.scaling_map(flm, t, Ls, real)
+    return out
+
+
+def synthesize_sharded(c: ShardedCoeffs, t, group=None, backend=None, dst: int = 0):
+    """Synthesis of one map from sharded coefficients; the map is returned
+    on `dst` (None elsewhere).  Mirrors transform.synthesize (transform.py:155-187)."""
+    backend = backend or CudaBackend()
+    rank, world = _rank_world(group)
+    p = t.params
+    L = p.band_limit
+    nsc = p.scale_count
+    terms = torch.zeros((nsc, L * L), dtype=torch.complex128,
+                        device=next(iter(c.scales.values())).values.device if c.scales else
+                        (torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available()
+                         and isinstance(backend, CudaBackend) else torch.device("cpu")))
+    for j in c.plan.owned(rank):
+        terms[j - p.j_min] = backend.scale_term(c.scales[j], t, j, c.real)
+    if world > 1:
+        # every term row is owned by exactly one rank and zero elsewhere:
+        # sum-reducing the stack moves the rows without mixing arithmetic
+        # (x + 0 == x exactly), so the merge below stays bit-identical
+        dist.reduce(terms, dst=dst, op=dist.ReduceOp.SUM, group=group)
+    if rank != dst:
+        return None
+    acc = torch.zeros(L * L, dtype=torch.complex128, device=terms.device)
+    for i in range(nsc):  # coarse -> fine, the reference order
+        acc += terms[i]
+    return backend.finish(acc, c.scaling, t, c.real)

@@ -1,0 +1,133 @@
+"""Scale-sharded analysis/synthesis over torch.distributed (gloo, world 2, CPU).
+
+The sharding driver (paper_1511_05578_b200/dist.py) is exercised with the
+CPU oracle injected as the per-rank compute backend, so the collective
+logic (broadcast of f_lm, per-scale ownership, deterministic merge of the
+per-scale synthesis terms) is checked without a GPU.  The sharded result
+must equal the single-process oracle exactly.
+"""
+
+import math
+import os
+import socket
+import types
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import scurve_oracle as orc
+from paper_1511_05578_b200 import tiling as T
+from paper_1511_05578_b200.dist import ScalePlan, analyze_sharded, synthesize_sharded
+
+
+class OracleBackend:
+    """CPU restatement standing in for the CUDA path (test only)."""
+
+    def __init__(self, L, spin):
+        self.L, self.spin = L, spin
+
+    def sht_forward(self, f):
+        return torch.from_numpy(orc.sht_forward(f, self.L, self.spin))
+
+    def flm_like(self, L):
+        return torch.empty(L * L, dtype=torch.complex128)
+
+    def scale_inverse(self, flm, t, j, Lj, real):
+        pos, neg = T.curvelet_harmonics(t, j)
+        w = orc.scale_wigner(flm.numpy(), pos, neg, Lj)
+        vals = orc.so3_inverse_curvelet(w)
+        return types.SimpleNamespace(values=torch.from_numpy(vals), grid=types.SimpleNamespace(L=Lj))
+
+    def scaling_map(self, flm, t, Ls, real):
+        return orc.sht_inverse(orc.scaling_coeffs(flm.numpy(), t.scaling, Ls), Ls, 0)
+
+    def scale_term(self, sig, t, j, real):
+        w = orc.so3_forward_curvelet(sig.values.numpy())
+        pos, neg = T.curvelet_harmonics(t, j)
+        L = self.L
+        term = np.zeros(L * L, dtype=complex)
+        Lj = w.shape[1]
+        cc = Lj - 1
+        for ell in range(1, Lj):
+            if pos[ell] == 0.0 and neg[ell] == 0.0:
+                continue
+            term[ell * ell:(ell + 1) ** 2] = (w[0, ell, cc - ell:cc + ell + 1] * pos[ell]
+                                              + w[1, ell, cc - ell:cc + ell + 1] * neg[ell])
+        return torch.from_numpy(term)
+
+    def finish(self, acc, scaling_sig, t, real):
+        acc = acc.numpy().copy()
+        Ls = scaling_sig.shape[0]
+        slm = orc.sht_forward(scaling_sig, Ls, 0)
+        for ell in range(Ls):
+            a = t.scaling[ell]
+            if a == 0.0:
+                continue
+            a = a * math.sqrt(4.0 * math.pi / (2 * ell + 1))
+            acc[ell * ell:(ell + 1) ** 2] += a * slm[ell * ell:(ell + 1) ** 2]
+        acc[:self.spin * self.spin] = 0.0
+        return orc.sht_inverse(acc, self.L, self.spin)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, L, spin, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        t = T.build_tiling(T.TilingParams(L, spin, 2.0, 1))
+        be = OracleBackend(L, spin)
+        f = orc.sht_inverse(orc.gaussian_flm(L, spin, seed=3, real=False), L, spin)
+        c = analyze_sharded(f if rank == 0 else None, t, backend=be)
+        g = synthesize_sharded(c, t, backend=be)
+        q.put((rank, {j: s.values.numpy() for j, s in c.scales.items()},
+               None if g is None else np.asarray(g)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("L,spin", [(16, 0), (16, 2)])
+def test_sharded_matches_single_process(L, spin):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, L, spin, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    t = T.build_tiling(T.TilingParams(L, spin, 2.0, 1))
+    psi = [T.curvelet_harmonics(t, j) for j in range(t.params.j_min, t.params.j_max + 1)]
+    f = orc.sht_inverse(orc.gaussian_flm(L, spin, seed=3, real=False), L, spin)
+    smap, scales = orc.analyze(f, L, spin, 2.0, 1, t.params.j_max, psi, t.scaling)
+    gref = orc.synthesize(smap, scales, L, spin, 2.0, 1, t.params.j_max, psi, t.scaling)
+    seen = set()
+    for rank, sc, g in res:
+        for j, v in sc.items():
+            np.testing.assert_array_equal(v, scales[j - t.params.j_min])
+            seen.add(j)
+        if rank == 0:
+            np.testing.assert_array_equal(g, gref)
+        else:
+            assert g is None
+    assert seen == set(range(t.params.j_min, t.params.j_max + 1))
+
+
+def test_scale_plan_balances_cost():
+    p = T.TilingParams(1024, 0, 2.0, 3)
+    for world in (1, 2, 4, 8):
+        plan = ScalePlan.build(p, world)
+        owned = [plan.owned(r) for r in range(world)]
+        assert sorted(j for o in owned for j in o) == list(range(3, 11))
+        if world == 2:  # the two L_j = 1024 scales land on different ranks
+            assert plan.owner[-1] != plan.owner[-2]

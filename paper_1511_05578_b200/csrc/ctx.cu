@@ -221,6 +221,25 @@ int scv_get_beta_tables(scv_ctx* c, int L, cudaStream_t s, const BetaTables** ou
     SCV_TRY(upload(c, &t.phs, to_d2(ph), s));
     SCV_TRY(upload(c, &t.wfpos, wf, s));
   }
+  {  // centred Bluestein tables (beta2.cu)
+    std::vector<cld> a2(L), h2(P, cld(0, 0)), v2(P, cld(0, 0));
+    for (int i = 0; i < L; ++i) a2[i] = expipi(-(long long)i * i, K);
+    for (int j = -(2 * L - 2); j <= 2 * L - 2; ++j) {
+      h2[((j % P) + P) % P] = expipi((long long)j * j, K);
+      v2[((j % P) + P) % P] = cld(w_even(j), 0);
+    }
+    fft_ld(h2);
+    fft_ld(v2);
+    std::vector<cld> hh(P / 2 + 1);
+    std::vector<double> vv(P / 2 + 1);
+    for (int k = 0; k <= P / 2; ++k) {
+      hh[k] = h2[k] / (ld)P;
+      vv[k] = (double)(v2[k].real() / (ld)P);
+    }
+    SCV_TRY(upload(c, &t.a2, to_d2(a2), s));
+    SCV_TRY(upload(c, &t.hf2, to_d2(hh), s));
+    SCV_TRY(upload(c, &t.vf2, vv, s));
+  }
   SCV_TRY(upload(c, &t.tw, to_d2(tw), s));
   SCV_TRY(upload(c, &t.chirpA, to_d2(A), s));
   SCV_TRY(upload(c, &t.Hf, to_d2(h), s));
@@ -336,6 +355,7 @@ int scv_destroy(scv_ctx* c) {
     cudaFree(t.tw); cudaFree(t.chirpA); cudaFree(t.Hf); cudaFree(t.chirpC);
     cudaFree(t.Vf); cudaFree(t.Aalt); cudaFree(t.sinh); cudaFree(t.cosh);
     cudaFree(t.phs); cudaFree(t.wfpos);
+    cudaFree(t.a2); cudaFree(t.hf2); cudaFree(t.vf2);
   }
   for (auto& kv : c->aux) cudaFree(kv.second);
   for (auto& r : c->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }

@@ -82,6 +82,10 @@ struct BetaTables {
   // prime-factor beta stage (K and K2 = 4L-1 both prime-factor lengths)
   double2* phs = nullptr;    // K   : (1/K) exp(-i pi m''/K), index m''+L-1
   double* wfpos = nullptr;   // K2  : DFT_K2(w_even wrapped)/K2, stored at CRT positions
+  // centred Bluestein (register-FFT beta stage, beta2.cu)
+  double2* a2 = nullptr;     // L     : exp(-i pi b'^2/K), b' = 0..L-1 (even in b')
+  double2* hf2 = nullptr;    // P/2+1 : FFT_P(h')/P, h'[j] = exp(+i pi j^2/K), |j| <= 2L-2 (even)
+  double* vf2 = nullptr;     // P/2+1 : FFT_P(w_even wrapped)/P (real, even)
 };
 
 struct FftPlan {
@@ -170,6 +174,9 @@ int scv_beta_sht(scv_ctx* c, int L, int spin, int real, const double2* G, double
                  cudaStream_t s);
 int scv_beta_so3(scv_ctx* c, int L, int real, const double2* W1p, double2* w, double pref,
                  cudaStream_t s);
+bool scv_beta2_supported(int L);
+int scv_beta2_so3(scv_ctx* c, int L, int real, const double2* W1p, double2* w, double pref,
+                  const BetaTables* t, const int2* tasks, int ntasks, cudaStream_t s);
 
 // prime-factor alpha/gamma kernels (pfa.cu), K = 2^k - 1
 bool scv_pfa_supported(int K);

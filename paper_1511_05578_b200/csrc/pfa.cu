@@ -64,16 +64,10 @@ int scv_pfa_tables(scv_ctx* c, int K, const double2** out) {
   for (int s = 0; s < 4; ++s) {
     const int p = f[s];
     if (p == 1) continue;
-    const int h = (p - 1) / 2, GP = pfa_gp(p);
-    for (int j = 1; j <= h; ++j)
-      for (int k = 1; k <= GP; ++k) {
-        if (k > h) {
-          tab.push_back(make_double2(0.0, 0.0));
-          continue;
-        }
-        const ld a = twopi * (ld)(((long long)j * k) % p) / (ld)p;
-        tab.push_back(make_double2((double)cosl(a), (double)sinl(a)));
-      }
+    for (int i = 0; i < p; ++i) {
+      const ld a = twopi * (ld)i / (ld)p;
+      tab.push_back(make_double2((double)cosl(a), (double)sinl(a)));
+    }
   }
   if (tab.empty()) tab.push_back(make_double2(0.0, 0.0));
   void* d = nullptr;
@@ -100,8 +94,18 @@ SCV_PFA_CFG(31, false, 16, 128, 2)   SCV_PFA_CFG(31, true, 16, 128, 2)
 SCV_PFA_CFG(63, false, 16, 256, 2)   SCV_PFA_CFG(63, true, 16, 256, 2)
 SCV_PFA_CFG(255, false, 8, 256, 2)   SCV_PFA_CFG(255, true, 8, 256, 2)
 SCV_PFA_CFG(511, false, 4, 256, 2)   SCV_PFA_CFG(511, true, 4, 256, 2)
-SCV_PFA_CFG(1023, false, 2, 224, 2)  SCV_PFA_CFG(1023, true, 2, 224, 2)
-SCV_PFA_CFG(2047, false, 1, 192, 2)  SCV_PFA_CFG(2047, true, 2, 384, 1)
+#ifndef SCV_ROW2047
+#define SCV_ROW2047 1, 192, 2
+#endif
+#ifndef SCV_COL2047
+#define SCV_COL2047 2, 384, 1
+#endif
+#ifndef SCV_ROW1023
+#define SCV_ROW1023 2, 224, 2
+#endif
+#define SCV_PFA_CFG_(KK, CL, ...) SCV_PFA_CFG(KK, CL, __VA_ARGS__)
+SCV_PFA_CFG_(1023, false, SCV_ROW1023)  SCV_PFA_CFG(1023, true, 2, 224, 2)
+SCV_PFA_CFG_(2047, false, SCV_ROW2047)  SCV_PFA_CFG_(2047, true, SCV_COL2047)
 SCV_PFA_CFG(4095, false, 1, 320, 1)  SCV_PFA_CFG(4095, true, 1, 320, 1)
 
 template <int K, bool COL>

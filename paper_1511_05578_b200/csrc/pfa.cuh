@@ -59,7 +59,7 @@ __host__ __device__ constexpr int pfa_group(int p) { return pfa_h(p) < SCV_PFA_G
 __host__ __device__ constexpr int pfa_gp(int p) { return p > 1 ? ((pfa_h(p) + pfa_group(p) - 1) / pfa_group(p)) * pfa_group(p) : 0; }
 // coefficient table size (double2 entries) for radix p: h rows (j) of GP columns
 // (k, zero-padded beyond h): (cos, sin) of 2 pi jk/p
-__host__ __device__ constexpr int pfa_tab(int p) { return p > 1 ? pfa_h(p) * pfa_gp(p) : 0; }
+__host__ __device__ constexpr int pfa_tab(int p) { return p > 1 ? p : 0; }
 template <class PL>
 __host__ __device__ constexpr int pfa_tab_total() {
   return pfa_tab(PL::P0) + pfa_tab(PL::P1) + pfa_tab(PL::P2) + pfa_tab(PL::P3);
@@ -69,9 +69,10 @@ __host__ __device__ constexpr int pfa_tab_off() {
   return (S > 0 ? pfa_tab(PL::P0) : 0) + (S > 1 ? pfa_tab(PL::P1) : 0) + (S > 2 ? pfa_tab(PL::P2) : 0);
 }
 
-// Coefficient tables (cos, sin)(2 pi jk/p) per radix, dense [j-1][k-1] with
-// k zero-padded to GP; staged once per CTA in shared memory (pfa_load_tables)
-// and read as warp-broadcast 16-byte loads.
+// Coefficient tables (cos, sin)(2 pi i/p), i < p, per radix; staged once per
+// CTA in shared memory (pfa_load_tables).  The butterfly walks j*k mod p
+// incrementally (integer pipe) and reads each pair as a warp-broadcast
+// 16-byte load.
 // position of output k after the transform (CRT map)
 template <class PL>
 __device__ __forceinline__ int pfa_pos(int k) {
@@ -95,9 +96,8 @@ __device__ __forceinline__ void pfa_load_tables(double2* tab, const double2* __r
 template <int p, int G>
 __device__ __forceinline__ void pfa_group_acc(const double2* __restrict__ T, const double2* __restrict__ Xr,
                                               int c0, double2 (&A)[G], double2 (&B)[G], double2& Z, int K,
-                                              int step) {
+                                              int step, int k0) {
   constexpr int h = (p - 1) / 2;
-  constexpr int GP = pfa_gp(p);
   const double2 x0 = Xr[c0];
   Z = x0;
 #pragma unroll
@@ -109,32 +109,36 @@ __device__ __forceinline__ void pfa_group_acc(const double2* __restrict__ T, con
   if (pa >= K) pa -= K;
   if (pb >= K) pb -= K;
   double2 a = Xr[pa], bb = Xr[pb];
-  double2 cs[G];
+  // idx[t] = j*k_t mod p for k_t = gG+t+1 (zero-padded groups use k_t <= h guard at write time;
+  // a k_t > h only produces unused accumulators)
+  int idx[G];
+#pragma unroll
+  for (int t = 0; t < G; ++t) idx[t] = 0;
 #pragma unroll 1
   for (int j = 1; j <= h; ++j) {
     pa += step;
     if (pa >= K) pa -= K;
     pb -= step;
     if (pb < 0) pb += K;
-    T += GP;
     // prefetch the next j's data (software pipelining)
     double2 an = a, bn = bb;
     if (j < h) {
       an = Xr[pa];
       bn = Xr[pb];
     }
-#pragma unroll
-    for (int t = 0; t < G; ++t) cs[t] = T[t - GP];
     const double2 s = make_double2(a.x + bb.x, a.y + bb.y);
     const double2 d = make_double2(a.x - bb.x, a.y - bb.y);
     Z.x += s.x;
     Z.y += s.y;
 #pragma unroll
     for (int t = 0; t < G; ++t) {
-      A[t].x = fma(s.x, cs[t].x, A[t].x);
-      A[t].y = fma(s.y, cs[t].x, A[t].y);
-      B[t].x = fma(d.x, cs[t].y, B[t].x);
-      B[t].y = fma(d.y, cs[t].y, B[t].y);
+      idx[t] += k0 + t;
+      if (idx[t] >= p) idx[t] -= p;
+      const double2 cs = T[idx[t]];
+      A[t].x = fma(s.x, cs.x, A[t].x);
+      A[t].y = fma(s.y, cs.x, A[t].y);
+      B[t].x = fma(d.x, cs.y, B[t].x);
+      B[t].y = fma(d.y, cs.y, B[t].y);
     }
     a = an;
     bb = bn;
@@ -180,7 +184,7 @@ __device__ SCV_PFA_STAGE_INL void pfa_stage(double2* X, const double2* tab) {
     const int c0 = b * p;
     grp[u] = g;
     pos[u] = r * PITCH + c0;
-    pfa_group_acc<p, G>(tab + pfa_tab_off<PL, S>() + g * G, X + r * PITCH, c0, A[u], B[u], Z[u], K, step);
+    pfa_group_acc<p, G>(tab + pfa_tab_off<PL, S>(), X + r * PITCH, c0, A[u], B[u], Z[u], K, step, g * G + 1);
   }
   __syncthreads();
 #pragma unroll

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 
 #include "pfa.cuh"
 
@@ -64,6 +65,23 @@ int scv_pfa_tables(scv_ctx* c, int K, const double2** out) {
   for (int s = 0; s < 4; ++s) {
     const int p = f[s];
     if (p == 1) continue;
+    if (pfa_use_mma(p)) {
+      // dense C and S matrices (M rows x pitch doubles each), row 0 = (1, 0)
+      const int h = (p - 1) / 2, M = mma_M(p), PA = mma_pitch(mma_Kp(p));
+      std::vector<double> C((size_t)M * PA, 0.0), S((size_t)M * PA, 0.0);
+      for (int k = 0; k <= h; ++k)
+        for (int j = 1; j <= h; ++j) {
+          const ld a = twopi * (ld)(((long long)j * k) % p) / (ld)p;
+          C[(size_t)k * PA + (j - 1)] = (double)cosl(a);
+          S[(size_t)k * PA + (j - 1)] = (double)sinl(a);
+        }
+      const size_t base = tab.size();
+      tab.resize(base + (size_t)M * PA);
+      double* dst = (double*)(tab.data() + base);
+      memcpy(dst, C.data(), C.size() * sizeof(double));
+      memcpy(dst + C.size(), S.data(), S.size() * sizeof(double));
+      continue;
+    }
     for (int i = 0; i < p; ++i) {
       const ld a = twopi * (ld)i / (ld)p;
       tab.push_back(make_double2((double)cosl(a), (double)sinl(a)));
@@ -112,7 +130,7 @@ template <int K, bool COL>
 static size_t pfa_smem() {
   using PL = PfaPlan<K>;
   constexpr int R = PfaCfg<K, COL>::R;
-  return ((size_t)2 * R * K + pfa_tab_total<PL>()) * sizeof(double2) + R * sizeof(int4);
+  return ((size_t)2 * R * K + pfa_tab_total<PL>() + pfa_scratch<PL, R>()) * sizeof(double2) + R * sizeof(int4);
 }
 
 // ---------------------------------------------------------------------------
@@ -126,7 +144,8 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
   constexpr int R = PfaCfg<K, false>::R, NT = PfaCfg<K, false>::NT;
   extern __shared__ double2 sm[];
   double2* tab = sm;
-  double2* const buf0 = sm + pfa_tab_total<PL>();  // buffer c at buf0 + c * R * K (stays a shared pointer)
+  double2* const scr = sm + pfa_tab_total<PL>();
+  double2* const buf0 = scr + pfa_scratch<PL, R>();  // buffer c at buf0 + c * R * K (stays a shared pointer)
   pfa_load_tables<PL, NT>(tab, gtab);
   const long long nb = (nrows + R - 1) / R;
   auto issue = [&](long long bt, double2* X) {
@@ -150,7 +169,7 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
     cp_async_wait<1>();
     __syncthreads();
     double2* X = buf0 + cur * (R * K);
-    pfa_dft<PL, DIR, R, NT, K>(X, tab);
+    pfa_dft<PL, DIR, R, NT, K>(X, tab, scr);
     const long long r0 = bt * R;
 #pragma unroll 4
     for (int i = threadIdx.x; i < R * K; i += NT) {
@@ -175,7 +194,8 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
   constexpr int L = (K + 1) / 2;
   extern __shared__ double2 sm[];
   double2* tab = sm;
-  double2* X = sm + pfa_tab_total<PL>();
+  double2* const scr = sm + pfa_tab_total<PL>();
+  double2* X = scr + pfa_scratch<PL, R>();
   int4* rp = (int4*)(X + 2 * R * K);  // per-row (gi, b, n, l)
   pfa_load_tables<PL, NT>(tab, gtab);
   const long long nrows = (long long)(real ? L : K) * L;
@@ -216,7 +236,7 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
       X[i] = v;
     }
     __syncthreads();
-    pfa_dft<PL, +1, R, NT, K>(X, tab);
+    pfa_dft<PL, +1, R, NT, K>(X, tab, scr);
 #pragma unroll 4
     for (int i = threadIdx.x; i < R * K; i += NT) {
       const int r = i / K, a = i - r * K;
@@ -243,7 +263,8 @@ __global__ void __launch_bounds__(PfaCfg<K, true>::NT, PfaCfg<K, true>::MINB)
   constexpr long long LK = (long long)L * K;
   extern __shared__ double2 sm[];
   double2* tab = sm;
-  double2* const buf0 = sm + pfa_tab_total<PL>();  // buffer c at buf0 + c * R * K (stays a shared pointer)
+  double2* const scr = sm + pfa_tab_total<PL>();
+  double2* const buf0 = scr + pfa_scratch<PL, R>();  // buffer c at buf0 + c * R * K (stays a shared pointer)
   pfa_load_tables<PL, NT>(tab, gtab);
   const int cpb = real ? 2 * R : R;  // columns per batch
   const int ngrp = (K + cpb - 1) / cpb;
@@ -290,7 +311,7 @@ __global__ void __launch_bounds__(PfaCfg<K, true>::NT, PfaCfg<K, true>::MINB)
       }
     }
     __syncthreads();
-    pfa_dft<PL, +1, R, NT, K>(X, tab);
+    pfa_dft<PL, +1, R, NT, K>(X, tab, scr);
     if (!real) {
 #pragma unroll 4
       for (int i = threadIdx.x; i < R * K; i += NT) {
@@ -330,7 +351,8 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
   constexpr long long LK = (long long)L * K;
   extern __shared__ double2 sm[];
   double2* tab = sm;
-  double2* const buf0 = sm + pfa_tab_total<PL>();  // buffer c at buf0 + c * R * K (stays a shared pointer)
+  double2* const scr = sm + pfa_tab_total<PL>();
+  double2* const buf0 = scr + pfa_scratch<PL, R>();  // buffer c at buf0 + c * R * K (stays a shared pointer)
   pfa_load_tables<PL, NT>(tab, gtab);
   const long long nrows = (long long)K * nbb;  // row index = bb*K + g
   const int rpb = real ? 2 * R : R;
@@ -382,7 +404,7 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
       }
     }
     __syncthreads();
-    pfa_dft<PL, -1, R, NT, K>(X, tab);
+    pfa_dft<PL, -1, R, NT, K>(X, tab, scr);
     if (!real) {
 #pragma unroll 4
       for (int i = threadIdx.x; i < R * K; i += NT) {
@@ -431,7 +453,8 @@ __global__ void __launch_bounds__(PfaCfg<K, true>::NT, PfaCfg<K, true>::MINB)
   constexpr int L = (K + 1) / 2;
   extern __shared__ double2 sm[];
   double2* tab = sm;
-  double2* const buf0 = sm + pfa_tab_total<PL>();  // buffer c at buf0 + c * R * K (stays a shared pointer)
+  double2* const scr = sm + pfa_tab_total<PL>();
+  double2* const buf0 = scr + pfa_scratch<PL, R>();  // buffer c at buf0 + c * R * K (stays a shared pointer)
   pfa_load_tables<PL, NT>(tab, gtab);
   const int ngrp = (K + R - 1) / R;
   const long long nb = (long long)nbb * ngrp;
@@ -460,7 +483,7 @@ __global__ void __launch_bounds__(PfaCfg<K, true>::NT, PfaCfg<K, true>::MINB)
     cp_async_wait<1>();
     __syncthreads();
     double2* X = buf0 + cur * (R * K);
-    pfa_dft<PL, -1, R, NT, K>(X, tab);
+    pfa_dft<PL, -1, R, NT, K>(X, tab, scr);
     // keep |m| <= |n| (real: n >= 0 only)
 #pragma unroll 4
     for (int i = threadIdx.x; i < R * K; i += NT) {
@@ -535,7 +558,8 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
   constexpr int L = (K + 1) / 2;
   extern __shared__ double2 sm[];
   double2* tab = sm;
-  double2* X = sm + pfa_tab_total<PL>();
+  double2* const scr = sm + pfa_tab_total<PL>();
+  double2* X = scr + pfa_scratch<PL, R>();
   pfa_load_tables<PL, NT>(tab, gtab);
   const long long nb = (ntask + R - 1) / R;
 #pragma unroll 1
@@ -563,7 +587,7 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
       X[i] = e;
     }
     __syncthreads();
-    pfa_dft<PL, -1, R, NT, K>(X, tab);
+    pfa_dft<PL, -1, R, NT, K>(X, tab, scr);
 #pragma unroll 4
     for (int i = threadIdx.x; i < R * K; i += NT) {
       const int r = i / K, q = i - r * K;
@@ -586,7 +610,8 @@ __global__ void __launch_bounds__(PfaCfg<K2, false>::NT, PfaCfg<K2, false>::MINB
   constexpr int L = (K2 + 1) / 4, K = 2 * L - 1;
   extern __shared__ double2 sm[];
   double2* tab = sm;
-  double2* X = sm + pfa_tab_total<PL>();
+  double2* const scr = sm + pfa_tab_total<PL>();
+  double2* X = scr + pfa_scratch<PL, R>();
   pfa_load_tables<PL, NT>(tab, gtab);
   const long long nb = (ntask + R - 1) / R;
 #pragma unroll 1
@@ -606,7 +631,7 @@ __global__ void __launch_bounds__(PfaCfg<K2, false>::NT, PfaCfg<K2, false>::MINB
       X[i] = v;
     }
     __syncthreads();
-    pfa_dft_ool<PL, -1, R, NT, K2>(X, tab);
+    pfa_dft_ool<PL, -1, R, NT, K2>(X, tab, scr);
 #pragma unroll 4
     for (int i = threadIdx.x; i < R * K2; i += NT) {
       const int p = i - (i / K2) * K2;
@@ -614,7 +639,7 @@ __global__ void __launch_bounds__(PfaCfg<K2, false>::NT, PfaCfg<K2, false>::MINB
       X[i] = make_double2(X[i].x * f, X[i].y * f);
     }
     __syncthreads();
-    pfa_dft_ool<PL, +1, R, NT, K2>(X, tab);
+    pfa_dft_ool<PL, +1, R, NT, K2>(X, tab, scr);
 #pragma unroll 4
     for (int i = threadIdx.x; i < R * K; i += NT) {
       const int r = i / K, q = i - r * K;

@@ -57,9 +57,21 @@ __host__ __device__ constexpr int pfa_h(int p) { return (p - 1) / 2; }
 __host__ __device__ constexpr int pfa_group(int p) { return pfa_h(p) < SCV_PFA_G ? pfa_h(p) : SCV_PFA_G; }
 // padded number of output pairs (k-groups of G) for radix p
 __host__ __device__ constexpr int pfa_gp(int p) { return p > 1 ? ((pfa_h(p) + pfa_group(p) - 1) / pfa_group(p)) * pfa_group(p) : 0; }
-// coefficient table size (double2 entries) for radix p: h rows (j) of GP columns
-// (k, zero-padded beyond h): (cos, sin) of 2 pi jk/p
-__host__ __device__ constexpr int pfa_tab(int p) { return p > 1 ? p : 0; }
+// Large radices (p >= 17) run on the FP64 tensor cores (DMMA m8n8k4, see
+// pfa_stage_mma): their table is the pair of dense real matrices
+// C[k][j] = cos(2 pi jk/p), S[k][j] = sin(2 pi jk/p), k = 0..M-1 (row 0 = the
+// all-ones / all-zero row that produces y_0), j = 1..Kp, zero padded.
+__host__ __device__ constexpr bool pfa_use_mma(int p) { return p >= 17; }
+__host__ __device__ constexpr int mma_M(int p) { return ((pfa_h(p) + 1 + 15) / 16) * 16; }   // output rows
+__host__ __device__ constexpr int mma_Kp(int p) { return ((pfa_h(p) + 3) / 4) * 4; }         // reduction dim
+__host__ __device__ constexpr int mma_pitch(int n) {  // row pitch (doubles) with pitch mod 16 in {4, 12}
+  return (n % 16 == 4 || n % 16 == 12) ? n : (n % 16 < 4 ? n + (4 - n % 16) : n % 16 < 12 ? n + (12 - n % 16) : n + (20 - n % 16));
+}
+// table size in double2 units: 1-D (cos, sin) table of p entries, or the two
+// dense matrices (2 * M * pitch doubles = M * pitch double2)
+__host__ __device__ constexpr int pfa_tab(int p) {
+  return p <= 1 ? 0 : pfa_use_mma(p) ? mma_M(p) * mma_pitch(mma_Kp(p)) : p;
+}
 template <class PL>
 __host__ __device__ constexpr int pfa_tab_total() {
   return pfa_tab(PL::P0) + pfa_tab(PL::P1) + pfa_tab(PL::P2) + pfa_tab(PL::P3);
@@ -67,6 +79,18 @@ __host__ __device__ constexpr int pfa_tab_total() {
 template <class PL, int S>
 __host__ __device__ constexpr int pfa_tab_off() {
   return (S > 0 ? pfa_tab(PL::P0) : 0) + (S > 1 ? pfa_tab(PL::P1) : 0) + (S > 2 ? pfa_tab(PL::P2) : 0);
+}
+// scratch (double2 units) for a DMMA stage over R rows: B matrices s and d
+// (Kp x pitch(2*NBF padded to 16) doubles each) + x0 per butterfly
+__host__ __device__ constexpr int mma_ncol(int K, int p, int R) { return ((2 * R * (K / p) + 15) / 16) * 16; }
+__host__ __device__ constexpr int mma_scratch_p(int K, int p, int R) {
+  return (p > 1 && pfa_use_mma(p)) ? mma_Kp(p) * mma_pitch(mma_ncol(K, p, R)) + R * (K / p) : 0;
+}
+__host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
+template <class PL, int R>
+__host__ __device__ constexpr int pfa_scratch() {
+  return cmax(cmax(mma_scratch_p(PL::K, PL::P0, R), mma_scratch_p(PL::K, PL::P1, R)),
+              cmax(mma_scratch_p(PL::K, PL::P2, R), mma_scratch_p(PL::K, PL::P3, R)));
 }
 
 // Coefficient tables (cos, sin)(2 pi i/p), i < p, per radix; staged once per
@@ -159,8 +183,14 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 #else
 #define SCV_PFA_STAGE_INL __forceinline__
 #endif
+// Barrier over the NT threads of one work group (named barrier `bar`; bar 0 =
+// __syncthreads when the group is the whole block).
+__device__ __forceinline__ void grp_sync(int bar, int nthreads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(bar), "r"(nthreads) : "memory");
+}
+
 template <class PL, int S, int DIR, int R, int NT, int PITCH>
-__device__ SCV_PFA_STAGE_INL void pfa_stage(double2* X, const double2* tab) {
+__device__ SCV_PFA_STAGE_INL void pfa_stage(double2* X, const double2* tab, int gtid = threadIdx.x, int bar = 0) {
   constexpr int p = pfa_p<PL, S>();
   constexpr int h = pfa_h(p);
   constexpr int K = PL::K;
@@ -174,7 +204,7 @@ __device__ SCV_PFA_STAGE_INL void pfa_stage(double2* X, const double2* tab) {
   int pos[IPT], grp[IPT];
 #pragma unroll
   for (int u = 0; u < IPT; ++u) {
-    const int it = threadIdx.x + u * NT;
+    const int it = gtid + u * NT;
     grp[u] = -1;
     pos[u] = 0;
     if (IPT * NT > items && it >= items) continue;
@@ -186,7 +216,7 @@ __device__ SCV_PFA_STAGE_INL void pfa_stage(double2* X, const double2* tab) {
     pos[u] = r * PITCH + c0;
     pfa_group_acc<p, G>(tab + pfa_tab_off<PL, S>(), X + r * PITCH, c0, A[u], B[u], Z[u], K, step, g * G + 1);
   }
-  __syncthreads();
+  grp_sync(bar, NT);
 #pragma unroll
   for (int u = 0; u < IPT; ++u) {
     if (grp[u] < 0) continue;
@@ -212,24 +242,155 @@ __device__ SCV_PFA_STAGE_INL void pfa_stage(double2* X, const double2* tab) {
       if (q2 < 0) q2 += K;
     }
   }
-  __syncthreads();
+  grp_sync(bar, NT);
+}
+
+// DMMA stage: batch of 2*R*K/p real columns (re/im of every butterfly).
+//   prep : s_j = x_j + x_{p-j}, d_j = x_j - x_{p-j} into the B matrices Bs, Bd
+//          [j-1][col] (col = 2*butterfly + {re, im}); x_0 saved per butterfly
+//   GEMM : Acc_C = C . Bs,  Acc_S = S . Bd  with DMMA m8n8k4 (fp64 tensor core);
+//          each warp owns 2x2 output tiles (16 k x 8 butterflies) for both
+//   epil.: y_k = x0 + AccC + DIR i AccS,  y_{p-k} = x0 + AccC - DIR i AccS,
+//          written in place (all of X was consumed by the prep).
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <class PL, int S, int DIR, int R, int NT, int PITCH>
+__device__ __forceinline__ void pfa_stage_mma(double2* X, const double2* tab, double2* scr, int gtid, int bar) {
+  constexpr int p = pfa_p<PL, S>();
+  constexpr int h = pfa_h(p);
+  constexpr int K = PL::K;
+  constexpr int step = K / p;
+  constexpr int nbf = K / p;
+  constexpr int NBF = R * nbf;
+  constexpr int M = mma_M(p), Kp = mma_Kp(p), PA = mma_pitch(Kp);
+  constexpr int NCOL = mma_ncol(K, p, R), PB = mma_pitch(NCOL);
+  const double* Cm = (const double*)(tab + pfa_tab_off<PL, S>());
+  const double* Sm = Cm + M * PA;
+  double* Bs = (double*)scr;
+  double* Bd = Bs + Kp * PB;     // Bs, Bd: Kp*PB doubles each
+  double2* x0s = scr + Kp * PB;  // NBF entries after Bs and Bd (2*Kp*PB doubles = Kp*PB double2)
+  const int tid = gtid;
+  // prep
+  for (int i = tid; i < NBF * h; i += NT) {
+    const int bf = i / h, j = i - bf * h + 1;
+    const int r = bf / nbf, b = bf - r * nbf;
+    const double2* Xr = X + r * PITCH;
+    int pa = b * p + j * step, pb = b * p + (p - j) * step;
+    pa %= K;
+    pb %= K;
+    const double2 a = Xr[pa], bb = Xr[pb];
+    Bs[(j - 1) * PB + 2 * bf] = a.x + bb.x;
+    Bs[(j - 1) * PB + 2 * bf + 1] = a.y + bb.y;
+    Bd[(j - 1) * PB + 2 * bf] = a.x - bb.x;
+    Bd[(j - 1) * PB + 2 * bf + 1] = a.y - bb.y;
+  }
+  for (int bf = tid; bf < NBF; bf += NT) {
+    const int r = bf / nbf, b = bf - r * nbf;
+    x0s[bf] = X[r * PITCH + b * p];
+  }
+  if constexpr (Kp > h) {
+    for (int i = tid; i < (Kp - h) * PB; i += NT) {
+      Bs[h * PB + i] = 0.0;
+      Bd[h * PB + i] = 0.0;
+    }
+  }
+  grp_sync(bar, NT);
+  // GEMM + epilogue
+  const int lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = NT / 32;
+  constexpr int MB = M / 16, NB = NCOL / 16;
+  const int ar = lane >> 2, ac = lane & 3;  // A fragment (row, col); B fragment (k = ac, n = ar)
+  for (int blk = warp; blk < MB * NB; blk += NW) {
+    const int mb = blk / NB, nb = blk - mb * NB;
+    double acC[2][2][2], acS[2][2][2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        acC[u][v][0] = acC[u][v][1] = 0.0;
+        acS[u][v][0] = acS[u][v][1] = 0.0;
+      }
+#pragma unroll 2
+    for (int kt = 0; kt < Kp / 4; ++kt) {
+      double aC[2], aS[2], bS[2], bD[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int row = mb * 16 + u * 8 + ar;
+        aC[u] = Cm[row * PA + kt * 4 + ac];
+        aS[u] = Sm[row * PA + kt * 4 + ac];
+      }
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int col = nb * 16 + v * 8 + ar;
+        bS[v] = Bs[(kt * 4 + ac) * PB + col];
+        bD[v] = Bd[(kt * 4 + ac) * PB + col];
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          dmma(acC[u][v][0], acC[u][v][1], aC[u], bS[v]);
+          dmma(acS[u][v][0], acS[u][v][1], aS[u], bD[v]);
+        }
+    }
+    // epilogue: lane holds rows k = .. + ar, columns 2*ac, 2*ac+1 = (re, im) of butterfly nb*8+v*4+ac
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int k = mb * 16 + u * 8 + ar;
+        const int bf = nb * 8 + v * 4 + ac;
+        if (k > h || bf >= NBF) continue;
+        const int r = bf / nbf, b = bf - r * nbf;
+        double2* Xr = X + r * PITCH;
+        const double2 x0 = x0s[bf];
+        const double Ar = x0.x + acC[u][v][0], Ai = x0.y + acC[u][v][1];
+        if (k == 0) {
+          Xr[b * p] = make_double2(Ar, Ai);
+          continue;
+        }
+        const double Br = acS[u][v][0], Bi = acS[u][v][1];
+        // DIR*i*B
+        const double iBr = DIR < 0 ? Bi : -Bi, iBi = DIR < 0 ? -Br : Br;
+        int q1 = b * p + k * step, q2 = b * p + (p - k) * step;
+        q1 %= K;
+        q2 %= K;
+        Xr[q1] = make_double2(Ar + iBr, Ai + iBi);
+        Xr[q2] = make_double2(Ar - iBr, Ai - iBi);
+      }
+  }
+  grp_sync(bar, NT);
 }
 
 // In-place K-point DFT (sign DIR) of R rows at X[r*PITCH + n] (natural order
 // in; CRT order out, read through pfa_pos).  Caller syncs before (data ready).
+// scr: pfa_scratch<PL,R>() double2 of shared scratch (DMMA stages).
+template <class PL, int S, int DIR, int R, int NT, int PITCH>
+__device__ __forceinline__ void pfa_stage_any(double2* X, const double2* tab, double2* scr, int gtid, int bar) {
+  if constexpr (pfa_use_mma(pfa_p<PL, S>())) pfa_stage_mma<PL, S, DIR, R, NT, PITCH>(X, tab, scr, gtid, bar);
+  else pfa_stage<PL, S, DIR, R, NT, PITCH>(X, tab, gtid, bar);
+}
+
+// gtid/bar: thread index within the work group of NT threads and its named
+// barrier (defaults: the whole block, barrier 0).
 template <class PL, int DIR, int R, int NT, int PITCH>
-__device__ __forceinline__ void pfa_dft(double2* X, const double2* tab) {
-  pfa_stage<PL, 0, DIR, R, NT, PITCH>(X, tab);
-  if constexpr (PL::D > 1) pfa_stage<PL, 1, DIR, R, NT, PITCH>(X, tab);
-  if constexpr (PL::D > 2) pfa_stage<PL, 2, DIR, R, NT, PITCH>(X, tab);
-  if constexpr (PL::D > 3) pfa_stage<PL, 3, DIR, R, NT, PITCH>(X, tab);
+__device__ __forceinline__ void pfa_dft(double2* X, const double2* tab, double2* scr, int gtid = threadIdx.x,
+                                        int bar = 0) {
+  pfa_stage_any<PL, 0, DIR, R, NT, PITCH>(X, tab, scr, gtid, bar);
+  if constexpr (PL::D > 1) pfa_stage_any<PL, 1, DIR, R, NT, PITCH>(X, tab, scr, gtid, bar);
+  if constexpr (PL::D > 2) pfa_stage_any<PL, 2, DIR, R, NT, PITCH>(X, tab, scr, gtid, bar);
+  if constexpr (PL::D > 3) pfa_stage_any<PL, 3, DIR, R, NT, PITCH>(X, tab, scr, gtid, bar);
 }
 
 // Out-of-line variant: isolates the transform's register allocation from a
 // large calling kernel (used by the fused beta stage).
 template <class PL, int DIR, int R, int NT, int PITCH>
-__device__ __noinline__ void pfa_dft_ool(double2* X, const double2* tab) {
-  pfa_dft<PL, DIR, R, NT, PITCH>(X, tab);
+__device__ __noinline__ void pfa_dft_ool(double2* X, const double2* tab, double2* scr) {
+  pfa_dft<PL, DIR, R, NT, PITCH>(X, tab, scr, threadIdx.x, 0);
 }
 
 // host side (pfa.cu)

@@ -22,6 +22,7 @@
 // contraction are the hand-written k_beta_so3 (beta.cu).
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 #include "scv_internal.cuh"
@@ -225,7 +226,10 @@ extern "C" int scv_so3_forward_curvelet(scv_ctx* c, int L, int real, const void*
   if (scv_pfa_supported(K)) {
     // hand-written prime-factor path: alpha DFT rows -> chunk, gamma DFT + pruning -> W1p
     const size_t per_bc = (size_t)K * K * 16;
-    int nbc = (int)std::max<size_t>(1, std::min<size_t>((size_t)L, (size_t)(1u << 30) / per_bc));
+    // chunk of beta slabs between the alpha and gamma passes (1 GB; an
+    // L2-resident single-slab chunk measured slower: launch + tail overheads)
+    static const long long chunk_bytes = getenv("SCV_SYN_CHUNK") ? atoll(getenv("SCV_SYN_CHUNK")) : (1LL << 30);
+    int nbc = (int)std::max<size_t>(1, std::min<size_t>((size_t)L, (size_t)chunk_bytes / per_bc));
     void* ch = nullptr;
     SCV_TRY(scv_scratch(c, 1, per_bc * nbc, &ch));
     for (int b0 = 0; b0 < L; b0 += nbc) {

@@ -344,9 +344,6 @@ int scv_beta_so3(scv_ctx* c, int L, int real, const double2* W1p, double2* w, do
                  cudaStream_t s) {
   const BetaTables* t = nullptr;
   SCV_TRY(scv_get_beta_tables(c, L, s, &t));
-  // experimental prime-factor beta stage (correct, currently slower): opt-in
-  static const bool use_pfa = getenv("SCV_BETA_PFA") != nullptr;
-  if (use_pfa && scv_pfa_beta_supported(L) && t->phs) return scv_pfa_beta_so3(c, L, real, W1p, w, pref, t, s);
   const int2* tasks = nullptr;
   int nt = 0;
   SCV_TRY(so3_tasks(c, L, real, &tasks, &nt, s));

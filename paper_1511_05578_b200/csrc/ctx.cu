@@ -202,25 +202,6 @@ int scv_get_beta_tables(scv_ctx* c, int L, cudaStream_t s, const BetaTables** ou
     const int r = K - 2 * b - 1;
     lcos[b] = r == 0 ? -HUGE_VAL : (double)logl(sinl(kPi * (ld)r / (ld)(2 * K)));
   }
-  if (scv_pfa_supported(K) && scv_pfa_supported(4 * L - 1)) {
-    const int K2 = 4 * L - 1;
-    std::vector<cld> ph(K);
-    for (int q = 0; q < K; ++q) ph[q] = expipi(-(long long)(q - (L - 1)), K) / (ld)K;
-    std::vector<ld> ctab(K2);
-    for (int r = 0; r < K2; ++r) ctab[r] = cosl(2.0L * kPi * (ld)r / (ld)K2);
-    std::vector<double> wf(K2, 0.0);
-    for (int k = 0; k < K2; ++k) {
-      ld acc = 0;
-      for (long long j = -(2LL * L - 2); j <= 2LL * L - 2; j += 2) {
-        long long r = (j * k) % K2;
-        if (r < 0) r += K2;
-        acc += w_even(j) * ctab[r];
-      }
-      wf[scv_pfa_pos_host(K2, k)] = (double)(acc / (ld)K2);
-    }
-    SCV_TRY(upload(c, &t.phs, to_d2(ph), s));
-    SCV_TRY(upload(c, &t.wfpos, wf, s));
-  }
   {  // centred Bluestein tables (beta2.cu)
     std::vector<cld> a2(L), h2(P, cld(0, 0)), v2(P, cld(0, 0));
     for (int i = 0; i < L; ++i) a2[i] = expipi(-(long long)i * i, K);
@@ -354,7 +335,6 @@ int scv_destroy(scv_ctx* c) {
     BetaTables& t = kv.second;
     cudaFree(t.tw); cudaFree(t.chirpA); cudaFree(t.Hf); cudaFree(t.chirpC);
     cudaFree(t.Vf); cudaFree(t.Aalt); cudaFree(t.sinh); cudaFree(t.cosh);
-    cudaFree(t.phs); cudaFree(t.wfpos);
     cudaFree(t.a2); cudaFree(t.hf2); cudaFree(t.vf2);
   }
   for (auto& kv : c->aux) cudaFree(kv.second);

@@ -113,24 +113,45 @@ SCV_PFA_CFG(63, false, 16, 256, 2)   SCV_PFA_CFG(63, true, 16, 256, 2)
 SCV_PFA_CFG(255, false, 8, 256, 2)   SCV_PFA_CFG(255, true, 8, 256, 2)
 SCV_PFA_CFG(511, false, 4, 256, 2)   SCV_PFA_CFG(511, true, 4, 256, 2)
 #ifndef SCV_ROW2047
-#define SCV_ROW2047 1, 192, 2
+#define SCV_ROW2047 2, 384, 1
 #endif
 #ifndef SCV_COL2047
 #define SCV_COL2047 2, 384, 1
 #endif
 #ifndef SCV_ROW1023
-#define SCV_ROW1023 2, 224, 2
+#define SCV_ROW1023 2, 352, 1
+#endif
+#ifndef SCV_COL1023
+#define SCV_COL1023 2, 352, 1
 #endif
 #define SCV_PFA_CFG_(KK, CL, ...) SCV_PFA_CFG(KK, CL, __VA_ARGS__)
-SCV_PFA_CFG_(1023, false, SCV_ROW1023)  SCV_PFA_CFG(1023, true, 2, 224, 2)
+SCV_PFA_CFG_(1023, false, SCV_ROW1023)  SCV_PFA_CFG_(1023, true, SCV_COL1023)
 SCV_PFA_CFG_(2047, false, SCV_ROW2047)  SCV_PFA_CFG_(2047, true, SCV_COL2047)
 SCV_PFA_CFG(4095, false, 1, 320, 1)  SCV_PFA_CFG(4095, true, 1, 320, 1)
 
-template <int K, bool COL>
-static size_t pfa_smem() {
+// Rows per transform call: R when the launch shape fits in shared memory,
+// else 1 (the R adjacent columns of a batch still move as R*16-byte segments,
+// but are transformed one call at a time, bounding the DMMA scratch).
+template <int K, bool COL, int RD>
+constexpr size_t pfa_smem_rd() {
   using PL = PfaPlan<K>;
   constexpr int R = PfaCfg<K, COL>::R;
-  return ((size_t)2 * R * K + pfa_tab_total<PL>() + pfa_scratch<PL, R>()) * sizeof(double2) + R * sizeof(int4);
+  return ((size_t)2 * R * K + pfa_tab_total<PL>() + pfa_scratch<PL, RD, PfaCfg<K, COL>::NT>()) * sizeof(double2) +
+         R * sizeof(int4);
+}
+template <int K, bool COL> struct PfaRD {
+  static constexpr int v = pfa_smem_rd<K, COL, PfaCfg<K, COL>::R>() <= 232448 ? PfaCfg<K, COL>::R : 1;
+};
+
+template <class PL, int DIR, int R, int RD, int NT>
+__device__ __forceinline__ void pfa_dft_rows(double2* X, const double2* tab, double2* scr) {
+#pragma unroll 1
+  for (int r = 0; r < R; r += RD) pfa_dft<PL, DIR, RD, NT, PL::K>(X + r * PL::K, tab, scr);
+}
+
+template <int K, bool COL>
+static constexpr size_t pfa_smem() {
+  return pfa_smem_rd<K, COL, PfaRD<K, COL>::v>();
 }
 
 // ---------------------------------------------------------------------------
@@ -145,7 +166,7 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
   extern __shared__ double2 sm[];
   double2* tab = sm;
   double2* const scr = sm + pfa_tab_total<PL>();
-  double2* const buf0 = scr + pfa_scratch<PL, R>();  // buffer c at buf0 + c * R * K (stays a shared pointer)
+  double2* const buf0 = scr + pfa_scratch<PL, PfaRD<K, false>::v, NT>();  // buffer c at buf0 + c * R * K (stays a shared pointer)
   pfa_load_tables<PL, NT>(tab, gtab);
   const long long nb = (nrows + R - 1) / R;
   auto issue = [&](long long bt, double2* X) {
@@ -169,7 +190,7 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
     cp_async_wait<1>();
     __syncthreads();
     double2* X = buf0 + cur * (R * K);
-    pfa_dft<PL, DIR, R, NT, K>(X, tab, scr);
+    pfa_dft_rows<PL, DIR, R, PfaRD<K, false>::v, NT>(X, tab, scr);
     const long long r0 = bt * R;
 #pragma unroll 4
     for (int i = threadIdx.x; i < R * K; i += NT) {
@@ -195,7 +216,7 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
   extern __shared__ double2 sm[];
   double2* tab = sm;
   double2* const scr = sm + pfa_tab_total<PL>();
-  double2* X = scr + pfa_scratch<PL, R>();
+  double2* X = scr + pfa_scratch<PL, PfaRD<K, false>::v, NT>();
   int4* rp = (int4*)(X + 2 * R * K);  // per-row (gi, b, n, l)
   pfa_load_tables<PL, NT>(tab, gtab);
   const long long nrows = (long long)(real ? L : K) * L;
@@ -236,7 +257,7 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
       X[i] = v;
     }
     __syncthreads();
-    pfa_dft<PL, +1, R, NT, K>(X, tab, scr);
+    pfa_dft_rows<PL, +1, R, PfaRD<K, false>::v, NT>(X, tab, scr);
 #pragma unroll 4
     for (int i = threadIdx.x; i < R * K; i += NT) {
       const int r = i / K, a = i - r * K;
@@ -264,7 +285,7 @@ __global__ void __launch_bounds__(PfaCfg<K, true>::NT, PfaCfg<K, true>::MINB)
   extern __shared__ double2 sm[];
   double2* tab = sm;
   double2* const scr = sm + pfa_tab_total<PL>();
-  double2* const buf0 = scr + pfa_scratch<PL, R>();  // buffer c at buf0 + c * R * K (stays a shared pointer)
+  double2* const buf0 = scr + pfa_scratch<PL, PfaRD<K, true>::v, NT>();  // buffer c at buf0 + c * R * K (stays a shared pointer)
   pfa_load_tables<PL, NT>(tab, gtab);
   const int cpb = real ? 2 * R : R;  // columns per batch
   const int ngrp = (K + cpb - 1) / cpb;
@@ -311,7 +332,7 @@ __global__ void __launch_bounds__(PfaCfg<K, true>::NT, PfaCfg<K, true>::MINB)
       }
     }
     __syncthreads();
-    pfa_dft<PL, +1, R, NT, K>(X, tab, scr);
+    pfa_dft_rows<PL, +1, R, PfaRD<K, true>::v, NT>(X, tab, scr);
     if (!real) {
 #pragma unroll 4
       for (int i = threadIdx.x; i < R * K; i += NT) {
@@ -352,7 +373,7 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
   extern __shared__ double2 sm[];
   double2* tab = sm;
   double2* const scr = sm + pfa_tab_total<PL>();
-  double2* const buf0 = scr + pfa_scratch<PL, R>();  // buffer c at buf0 + c * R * K (stays a shared pointer)
+  double2* const buf0 = scr + pfa_scratch<PL, PfaRD<K, false>::v, NT>();  // buffer c at buf0 + c * R * K (stays a shared pointer)
   pfa_load_tables<PL, NT>(tab, gtab);
   const long long nrows = (long long)K * nbb;  // row index = bb*K + g
   const int rpb = real ? 2 * R : R;
@@ -404,7 +425,7 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
       }
     }
     __syncthreads();
-    pfa_dft<PL, -1, R, NT, K>(X, tab, scr);
+    pfa_dft_rows<PL, -1, R, PfaRD<K, false>::v, NT>(X, tab, scr);
     if (!real) {
 #pragma unroll 4
       for (int i = threadIdx.x; i < R * K; i += NT) {
@@ -454,7 +475,7 @@ __global__ void __launch_bounds__(PfaCfg<K, true>::NT, PfaCfg<K, true>::MINB)
   extern __shared__ double2 sm[];
   double2* tab = sm;
   double2* const scr = sm + pfa_tab_total<PL>();
-  double2* const buf0 = scr + pfa_scratch<PL, R>();  // buffer c at buf0 + c * R * K (stays a shared pointer)
+  double2* const buf0 = scr + pfa_scratch<PL, PfaRD<K, true>::v, NT>();  // buffer c at buf0 + c * R * K (stays a shared pointer)
   pfa_load_tables<PL, NT>(tab, gtab);
   const int ngrp = (K + R - 1) / R;
   const long long nb = (long long)nbb * ngrp;
@@ -483,7 +504,7 @@ __global__ void __launch_bounds__(PfaCfg<K, true>::NT, PfaCfg<K, true>::MINB)
     cp_async_wait<1>();
     __syncthreads();
     double2* X = buf0 + cur * (R * K);
-    pfa_dft<PL, -1, R, NT, K>(X, tab, scr);
+    pfa_dft_rows<PL, -1, R, PfaRD<K, true>::v, NT>(X, tab, scr);
     // keep |m| <= |n| (real: n >= 0 only)
 #pragma unroll 4
     for (int i = threadIdx.x; i < R * K; i += NT) {
@@ -518,18 +539,7 @@ static int persistent_grid(scv_ctx* c, Kern k, int nt, size_t sm, long long nbat
   return SCV_OK;
 }
 
-// ---------------------------------------------------------------------------
-// beta stage + Delta contraction of the SO(3) forward transform on the
-// prime-factor engine (restates so3.py:203-243; the packed-pair formulation
-// is documented in beta.cu).  Per (n, column pair):
-//   X1 <- packed extension of the two columns (natural b order)
-//   X1 <- DFT_K (forward, CRT order);  F[m''] = (1/K) e^{-i m'' pi/K} X1[pos(m'' mod K)]
-//   X1 <- F (natural);  X2 <- G = F - (gamma/2)(-1)^m'' wrapped mod K2 = 4L-1
-//   X2 <- IDFT_K2( DFT_K2(X2) * DFT_K2(w_even)/K2 )   (the forward output is in
-//         CRT order and the inverse consumes CRT order, returning natural order)
-//   then Y_E / Y_O and the contraction exactly as in beta.cu.
-// K2 = 4L-1 >= 4L-3 keeps the circular convolution alias-free for |m'| <= L-1.
-// ---------------------------------------------------------------------------
+// CRT output position of frequency k (host copy of pfa_pos)
 int scv_pfa_pos_host(int K, int k) {
   int f[4];
   factors_of(K, f);
@@ -537,263 +547,6 @@ int scv_pfa_pos_host(int K, int k) {
   for (int s = 0; s < 4; ++s)
     if (f[s] > 1) a += (long long)(k % f[s]) * (K / f[s]);
   return (int)(a % K);
-}
-
-bool scv_pfa_beta_supported(int L) {
-  return L >= 128 && L <= 1024 && scv_pfa_supported(2 * L - 1) && scv_pfa_supported(4 * L - 1);
-}
-
-// Three batched kernels over chunks of (n, pair) tasks; F and E go through a
-// chunk scratch buffer so each transform runs as an efficient batch:
-//   k_beta_f<K>   : packed extension -> DFT_K -> F (natural), gamma per task
-//   k_beta_e<K2>  : G (wrapped) -> DFT_K2 -> * w spectrum -> IDFT_K2 -> E (|m'| <= L-1)
-//   k_beta_c<L>   : Y_E / Y_O and the Delta contraction, one warp per task
-template <int K>
-__global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
-    k_beta_f(int real, const double2* __restrict__ W1p, const int2* __restrict__ tasks, int t0, int ntask,
-             const double2* __restrict__ phs, double2* __restrict__ Fbuf, double2* __restrict__ gam,
-             const double2* __restrict__ gtab) {
-  using PL = PfaPlan<K>;
-  constexpr int R = PfaCfg<K, false>::R, NT = PfaCfg<K, false>::NT;
-  constexpr int L = (K + 1) / 2;
-  extern __shared__ double2 sm[];
-  double2* tab = sm;
-  double2* const scr = sm + pfa_tab_total<PL>();
-  double2* X = scr + pfa_scratch<PL, R>();
-  pfa_load_tables<PL, NT>(tab, gtab);
-  const long long nb = (ntask + R - 1) / R;
-#pragma unroll 1
-  for (long long bt = blockIdx.x; bt < nb; bt += gridDim.x) {
-    const int r0 = (int)(bt * R);
-#pragma unroll 4
-    for (int i = threadIdx.x; i < R * K; i += NT) {
-      const int r = i / K, b = i - r * K;
-      double2 e = make_double2(0.0, 0.0);
-      if (r0 + r < ntask) {
-        const int2 tk = tasks[t0 + r0 + r];
-        const int n = tk.x, l = n < 0 ? -n : n;
-        const int m0 = -l + 2 * tk.y, m1 = m0 + 1;
-        const long long cb = w1p_colbase(n, real);
-        const bool even0 = ((n + m0) & 1) == 0;
-        const int src = b < L ? b : 2 * L - 2 - b;
-        const double2 v0 = W1p[(cb + m0 + l) * (long long)L + src];
-        const double2 v1 = (m1 <= l) ? W1p[(cb + m1 + l) * (long long)L + src] : make_double2(0.0, 0.0);
-        const double2 ve = even0 ? v0 : v1;
-        double2 vo = even0 ? v1 : v0;
-        if (b >= L) vo = make_double2(-vo.x, -vo.y);
-        e = make_double2(ve.x + vo.x, ve.y + vo.y);
-        if (b == L - 1) gam[r0 + r] = make_double2(vo.x * (2.0 / K), vo.y * (2.0 / K));
-      }
-      X[i] = e;
-    }
-    __syncthreads();
-    pfa_dft<PL, -1, R, NT, K>(X, tab, scr);
-#pragma unroll 4
-    for (int i = threadIdx.x; i < R * K; i += NT) {
-      const int r = i / K, q = i - r * K;
-      if (r0 + r < ntask) {
-        int kk = q - (L - 1);
-        if (kk < 0) kk += K;
-        Fbuf[(long long)(r0 + r) * K + q] = cmul(__ldg(phs + q), X[r * K + pfa_pos<PL>(kk)]);
-      }
-    }
-    __syncthreads();
-  }
-}
-
-template <int K2>
-__global__ void __launch_bounds__(PfaCfg<K2, false>::NT, PfaCfg<K2, false>::MINB)
-    k_beta_e(int ntask, const double2* __restrict__ Fbuf, const double2* __restrict__ gam,
-             const double* __restrict__ wfpos, double2* __restrict__ Ebuf, const double2* __restrict__ gtab) {
-  using PL = PfaPlan<K2>;
-  constexpr int R = PfaCfg<K2, false>::R, NT = PfaCfg<K2, false>::NT;
-  constexpr int L = (K2 + 1) / 4, K = 2 * L - 1;
-  extern __shared__ double2 sm[];
-  double2* tab = sm;
-  double2* const scr = sm + pfa_tab_total<PL>();
-  double2* X = scr + pfa_scratch<PL, R>();
-  pfa_load_tables<PL, NT>(tab, gtab);
-  const long long nb = (ntask + R - 1) / R;
-#pragma unroll 1
-  for (long long bt = blockIdx.x; bt < nb; bt += gridDim.x) {
-    const int r0 = (int)(bt * R);
-#pragma unroll 4
-    for (int i = threadIdx.x; i < R * K2; i += NT) {
-      const int r = i / K2, p = i - r * K2;
-      const int mpp = p <= L - 1 ? p : p - K2;
-      double2 v = make_double2(0.0, 0.0);
-      if (r0 + r < ntask && mpp >= -(L - 1)) {
-        const double2 F = Fbuf[(long long)(r0 + r) * K + mpp + L - 1];
-        const double2 g = gam[r0 + r];
-        const double hh = (mpp & 1) ? -0.5 : 0.5;
-        v = make_double2(F.x - hh * g.x, F.y - hh * g.y);
-      }
-      X[i] = v;
-    }
-    __syncthreads();
-    pfa_dft_ool<PL, -1, R, NT, K2>(X, tab, scr);
-#pragma unroll 4
-    for (int i = threadIdx.x; i < R * K2; i += NT) {
-      const int p = i - (i / K2) * K2;
-      const double f = __ldg(wfpos + p);
-      X[i] = make_double2(X[i].x * f, X[i].y * f);
-    }
-    __syncthreads();
-    pfa_dft_ool<PL, +1, R, NT, K2>(X, tab, scr);
-#pragma unroll 4
-    for (int i = threadIdx.x; i < R * K; i += NT) {
-      const int r = i / K, q = i - r * K;
-      const int mp = q - (L - 1);
-      if (r0 + r < ntask) Ebuf[(long long)(r0 + r) * K + q] = X[r * K2 + (mp >= 0 ? mp : mp + K2)];
-    }
-    __syncthreads();
-  }
-}
-
-template <int L>
-__global__ void __launch_bounds__(256) k_beta_c(int real, const int2* __restrict__ tasks, int t0, int ntask,
-                                                const double2* __restrict__ Fbuf, const double2* __restrict__ Ebuf,
-                                                const double2* __restrict__ gam, const double* __restrict__ Aalt,
-                                                const double* __restrict__ delta, double pref,
-                                                double2* __restrict__ wout) {
-  constexpr int K = 2 * L - 1;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (warp >= ntask) return;
-  const int2 tk = tasks[t0 + warp];
-  const int n = tk.x, l = n < 0 ? -n : n;
-  const int m0 = -l + 2 * tk.y, m1 = m0 + 1;
-  const bool even0 = ((n + m0) & 1) == 0;
-  const int mE = even0 ? m0 : m1, mO = even0 ? m1 : m0;
-  const double2* F = Fbuf + (long long)warp * K + (L - 1);  // F[m''] at F[m'']
-  const double2* E = Ebuf + (long long)warp * K + (L - 1);
-  const double2 g = gam[warp];
-  const double hp = 0.5 * SCV_PI;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int mp = -l + lane; mp <= l; mp += 32) {
-    const double2 Ep = E[mp], Em = E[-mp];
-    const double2 ee = make_double2(0.5 * (Ep.x + Em.x), 0.5 * (Ep.y + Em.y));
-    const double2 eo = make_double2(0.5 * (Ep.x - Em.x), 0.5 * (Ep.y - Em.y));
-    double2 xe[2], xo[2];
-#pragma unroll
-    for (int z = 0; z < 2; ++z) {
-      const int k = z == 0 ? mp + 1 : mp - 1;
-      if (k < -(L - 1) || k > L - 1) {
-        xe[z] = make_double2(0.0, 0.0);
-        xo[z] = make_double2(0.0, 0.0);
-      } else {
-        const double2 a = F[k], b = F[-k];
-        const double hh = (k & 1) ? -1.0 : 1.0;
-        xe[z] = make_double2(0.5 * (a.x + b.x - hh * g.x), 0.5 * (a.y + b.y - hh * g.y));
-        xo[z] = make_double2(0.5 * (a.x - b.x + hh * g.x), 0.5 * (a.y - b.y + hh * g.y));
-      }
-    }
-    const double2 dE = make_double2(xe[0].x - xe[1].x, xe[0].y - xe[1].y);
-    const double2 dO = make_double2(xo[0].x - xo[1].x, xo[0].y - xo[1].y);
-    const double2 yE = make_double2(ee.x - hp * dE.y, ee.y + hp * dE.x);
-    const double aa = 0.5 * __ldg(Aalt + mp + L - 1);
-    const double2 yO = make_double2(eo.x + aa * g.x - hp * dO.y, eo.y + aa * g.y + hp * dO.x);
-    const double dn = wedge_get(delta, l, mp, n);
-    const double dE2 = (mE <= l) ? wedge_get(delta, l, mp, mE) * dn : 0.0;
-    const double dO2 = (mO <= l) ? wedge_get(delta, l, mp, mO) * dn : 0.0;
-    acc[0] += dE2 * yE.x;
-    acc[1] += dE2 * yE.y;
-    acc[2] += dO2 * yO.x;
-    acc[3] += dO2 * yO.y;
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
-  if (lane == 0) {
-    const int c = L - 1;
-    const int sheet = n >= 0 ? 0 : 1;
-    double2* row = wout + ((long long)sheet * L + l) * K;
-    const int ms[2] = {mE, mO};
-    for (int i = 0; i < 2; ++i) {
-      const int m = ms[i];
-      if (m > l) continue;
-      const double2 v = cipow(make_double2(pref * acc[2 * i], pref * acc[2 * i + 1]), m - n);
-      row[c + m] = v;
-      if (real && n > 0) {  // row(-n)[m] = (-1)^{m+n} conj(row(n)[-m])  (so3.py:379-382)
-        double2 cv = make_double2(v.x, -v.y);
-        if ((m + n) & 1) cv = make_double2(-cv.x, -cv.y);
-        wout[((long long)1 * L + l) * K + c - m] = cv;
-      }
-    }
-  }
-}
-
-static int beta_pfa_tasks(scv_ctx* c, int L, int real, const int2** out, int* count) {
-  const std::string key = "pfatasks_" + std::to_string(L) + "_" + std::to_string(real);
-  std::vector<int2> v;
-  for (int l = L - 1; l >= 0; --l)
-    for (int sg = 0; sg < 2; ++sg) {
-      const int n = sg == 0 ? l : -l;
-      if (sg == 1 && (l == 0 || real)) continue;
-      for (int i = 0; i <= l; ++i) v.push_back(make_int2(n, i));
-    }
-  *count = (int)v.size();
-  auto it = c->aux.find(key);
-  if (it != c->aux.end()) {
-    *out = (const int2*)it->second;
-    return SCV_OK;
-  }
-  void* d = nullptr;
-  SCV_CUDA(c, cudaMalloc(&d, v.size() * sizeof(int2)));
-  SCV_CUDA(c, cudaMemcpy(d, v.data(), v.size() * sizeof(int2), cudaMemcpyHostToDevice));
-  c->aux[key] = d;
-  *out = (const int2*)d;
-  return SCV_OK;
-}
-
-template <int L>
-static int run_beta_pfa(scv_ctx* c, int real, const double2* W1p, double2* w, double pref, const BetaTables* t,
-                        cudaStream_t s) {
-  constexpr int K = 2 * L - 1, K2 = 4 * L - 1;
-  const double2 *tab1, *tab2;
-  SCV_TRY(scv_pfa_tables(c, K, &tab1));
-  SCV_TRY(scv_pfa_tables(c, K2, &tab2));
-  const int2* tasks;
-  int nt;
-  SCV_TRY(beta_pfa_tasks(c, L, real, &tasks, &nt));
-  // chunk scratch: F and E (K each) + gamma per task, in scratch slot 1 (free after the alpha/gamma passes)
-  const size_t per_task = (size_t)(2 * K + 1) * sizeof(double2);
-  size_t want = std::max<size_t>(per_task * 1024, (size_t)1 << 30);
-  void* scr = nullptr;
-  SCV_TRY(scv_scratch(c, 1, std::min(want, per_task * (size_t)nt), &scr));
-  const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)nt, c->scratch_bytes[1] / per_task));
-  double2* Fb = (double2*)scr;
-  double2* Eb = Fb + (size_t)chunk * K;
-  double2* gb = Eb + (size_t)chunk * K;
-  const size_t smf = pfa_smem<K, false>(), sme = pfa_smem<K2, false>();
-  for (int t0 = 0; t0 < nt; t0 += chunk) {
-    const int ntask = std::min(chunk, nt - t0);
-    int grid;
-    SCV_TRY(persistent_grid(c, k_beta_f<K>, PfaCfg<K, false>::NT, smf, (ntask + PfaCfg<K, false>::R - 1) / PfaCfg<K, false>::R, &grid));
-    k_beta_f<K><<<grid, PfaCfg<K, false>::NT, smf, s>>>(real, W1p, tasks, t0, ntask, t->phs, Fb, gb, tab1);
-    c->launches++;
-    SCV_CUDA(c, cudaGetLastError());
-    SCV_TRY(persistent_grid(c, k_beta_e<K2>, PfaCfg<K2, false>::NT, sme, (ntask + PfaCfg<K2, false>::R - 1) / PfaCfg<K2, false>::R, &grid));
-    k_beta_e<K2><<<grid, PfaCfg<K2, false>::NT, sme, s>>>(ntask, Fb, gb, t->wfpos, Eb, tab2);
-    c->launches++;
-    SCV_CUDA(c, cudaGetLastError());
-    k_beta_c<L><<<(ntask * 32 + 255) / 256, 256, 0, s>>>(real, tasks, t0, ntask, Fb, Eb, gb, t->Aalt, c->delta,
-                                                          pref, w);
-    c->launches++;
-    SCV_CUDA(c, cudaGetLastError());
-  }
-  return SCV_OK;
-}
-
-int scv_pfa_beta_so3(scv_ctx* c, int L, int real, const double2* W1p, double2* w, double pref,
-                     const BetaTables* t, cudaStream_t s) {
-  switch (L) {
-    case 128: return run_beta_pfa<128>(c, real, W1p, w, pref, t, s);
-    case 256: return run_beta_pfa<256>(c, real, W1p, w, pref, t, s);
-    case 512: return run_beta_pfa<512>(c, real, W1p, w, pref, t, s);
-    case 1024: return run_beta_pfa<1024>(c, real, W1p, w, pref, t, s);
-    default: return scv_fail(c, SCV_EINVAL, "no prime-factor beta stage for L=" + std::to_string(L));
-  }
 }
 
 #define PFA_SWITCH(K, CALL)                                                                 \
@@ -809,7 +562,8 @@ template <int K, int DIR>
 static int run_rows(scv_ctx* c, long long nrows, const double2* in, double2* out, cudaStream_t s) {
   const double2* tab;
   SCV_TRY(scv_pfa_tables(c, K, &tab));
-  const size_t sm = pfa_smem<K, false>();
+  constexpr size_t sm = pfa_smem<K, false>();
+  static_assert(sm <= 232448, "prime-factor launch shape exceeds the 227 KB shared-memory limit");
   int grid;
   const long long nb = (nrows + PfaCfg<K, false>::R - 1) / PfaCfg<K, false>::R;
   SCV_TRY(persistent_grid(c, k_pfa_rows<K, DIR>, PfaCfg<K, false>::NT, sm, nb, &grid));
@@ -824,7 +578,8 @@ static int run_ana_alpha(scv_ctx* c, int real, const double2* w, const double* h
                          const double* lc, double2* out, cudaStream_t s) {
   const double2* tab;
   SCV_TRY(scv_pfa_tables(c, K, &tab));
-  const size_t sm = pfa_smem<K, false>();
+  constexpr size_t sm = pfa_smem<K, false>();
+  static_assert(sm <= 232448, "prime-factor launch shape exceeds the 227 KB shared-memory limit");
   constexpr int L = (K + 1) / 2;
   const long long nb = ((long long)(real ? L : K) * L + PfaCfg<K, false>::R - 1) / PfaCfg<K, false>::R;
   int grid;
@@ -839,7 +594,8 @@ template <int K>
 static int run_ana_gamma(scv_ctx* c, int real, double2* src, double* dst, cudaStream_t s) {
   const double2* tab;
   SCV_TRY(scv_pfa_tables(c, K, &tab));
-  const size_t sm = pfa_smem<K, true>();
+  constexpr size_t sm = pfa_smem<K, true>();
+  static_assert(sm <= 232448, "prime-factor launch shape exceeds the 227 KB shared-memory limit");
   constexpr int L = (K + 1) / 2;
   const int cpb = real ? 2 * PfaCfg<K, true>::R : PfaCfg<K, true>::R;
   const long long nb = (long long)L * ((K + cpb - 1) / cpb);
@@ -855,7 +611,8 @@ template <int K>
 static int run_syn_alpha(scv_ctx* c, int real, const void* in, int b0, int nbb, double2* chunk, cudaStream_t s) {
   const double2* tab;
   SCV_TRY(scv_pfa_tables(c, K, &tab));
-  const size_t sm = pfa_smem<K, false>();
+  constexpr size_t sm = pfa_smem<K, false>();
+  static_assert(sm <= 232448, "prime-factor launch shape exceeds the 227 KB shared-memory limit");
   const int rpb = real ? 2 * PfaCfg<K, false>::R : PfaCfg<K, false>::R;
   const long long nb = ((long long)K * nbb + rpb - 1) / rpb;
   int grid;
@@ -870,7 +627,8 @@ template <int K>
 static int run_syn_gamma(scv_ctx* c, int real, const double2* chunk, int b0, int nbb, double2* W1p, cudaStream_t s) {
   const double2* tab;
   SCV_TRY(scv_pfa_tables(c, K, &tab));
-  const size_t sm = pfa_smem<K, true>();
+  constexpr size_t sm = pfa_smem<K, true>();
+  static_assert(sm <= 232448, "prime-factor launch shape exceeds the 227 KB shared-memory limit");
   const long long nb = (long long)nbb * ((K + PfaCfg<K, true>::R - 1) / PfaCfg<K, true>::R);
   int grid;
   SCV_TRY(persistent_grid(c, k_syn_gamma<K>, PfaCfg<K, true>::NT, sm, nb, &grid));

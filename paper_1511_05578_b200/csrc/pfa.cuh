@@ -83,14 +83,24 @@ __host__ __device__ constexpr int pfa_tab_off() {
 // scratch (double2 units) for a DMMA stage over R rows: B matrices s and d
 // (Kp x pitch(2*NBF padded to 16) doubles each) + x0 per butterfly
 __host__ __device__ constexpr int mma_ncol(int K, int p, int R) { return ((2 * R * (K / p) + 15) / 16) * 16; }
-__host__ __device__ constexpr int mma_scratch_p(int K, int p, int R) {
-  return (p > 1 && pfa_use_mma(p)) ? mma_Kp(p) * mma_pitch(mma_ncol(K, p, R)) + R * (K / p) : 0;
+// A DMMA stage keeps its accumulators in registers (pfa_stage_mma_reg, no
+// scratch) when every warp of the NT-thread group owns at most
+// SCV_PFA_TPW_MAX 16x16 output tiles; otherwise it stages B in scratch.
+#ifndef SCV_PFA_TPW_MAX
+#define SCV_PFA_TPW_MAX 2
+#endif
+__host__ __device__ constexpr int mma_tpw(int K, int p, int R, int NT) {
+  return ((mma_M(p) / 16) * (mma_ncol(K, p, R) / 16) + NT / 32 - 1) / (NT / 32);
+}
+__host__ __device__ constexpr bool mma_reg(int K, int p, int R, int NT) { return mma_tpw(K, p, R, NT) <= SCV_PFA_TPW_MAX; }
+__host__ __device__ constexpr int mma_scratch_p(int K, int p, int R, int NT) {
+  return (p > 1 && pfa_use_mma(p) && !mma_reg(K, p, R, NT)) ? mma_Kp(p) * mma_pitch(mma_ncol(K, p, R)) + R * (K / p) : 0;
 }
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
-template <class PL, int R>
+template <class PL, int R, int NT>
 __host__ __device__ constexpr int pfa_scratch() {
-  return cmax(cmax(mma_scratch_p(PL::K, PL::P0, R), mma_scratch_p(PL::K, PL::P1, R)),
-              cmax(mma_scratch_p(PL::K, PL::P2, R), mma_scratch_p(PL::K, PL::P3, R)));
+  return cmax(cmax(mma_scratch_p(PL::K, PL::P0, R, NT), mma_scratch_p(PL::K, PL::P1, R, NT)),
+              cmax(mma_scratch_p(PL::K, PL::P2, R, NT), mma_scratch_p(PL::K, PL::P3, R, NT)));
 }
 
 // Coefficient tables (cos, sin)(2 pi i/p), i < p, per radix; staged once per
@@ -366,12 +376,137 @@ __device__ __forceinline__ void pfa_stage_mma(double2* X, const double2* tab, do
   grp_sync(bar, NT);
 }
 
+// DMMA stage, register-held variant (default): the B fragments are formed
+// directly from the row buffer (s_j, d_j of the lane's column computed from
+// two 8-byte loads), every warp keeps the accumulators of its TPW tiles in
+// registers across one barrier, then writes its outputs in place.  No scratch
+// matrices, no prep pass; the A fragments (C, S) come from the shared table.
+// Column col of the GEMM is (butterfly col/2, re|im col&1); butterfly b's
+// element j sits at (b*p + j*K/p) mod K and element p-j at (b*p - j*K/p) mod K.
+template <class PL, int S, int DIR, int R, int NT, int PITCH>
+__device__ __forceinline__ void pfa_stage_mma_reg(double2* X, const double2* tab, int gtid, int bar) {
+  constexpr int p = pfa_p<PL, S>();
+  constexpr int h = pfa_h(p);
+  constexpr int K = PL::K;
+  constexpr int step = K / p;
+  constexpr int nbf = K / p;
+  constexpr int NBF = R * nbf;
+  constexpr int M = mma_M(p), Kp = mma_Kp(p), PA = mma_pitch(Kp);
+  constexpr int NCOL = mma_ncol(K, p, R);
+  constexpr int MB = M / 16, NB = NCOL / 16, NTILE = MB * NB;
+  constexpr int NW = NT / 32, TPW = (NTILE + NW - 1) / NW;
+  const double* Cm = (const double*)(tab + pfa_tab_off<PL, S>());
+  const double* Sm = Cm + M * PA;
+  const double* Xd = (const double*)X;
+  const int lane = gtid & 31, warp = gtid >> 5;
+  const int ar = lane >> 2, ac = lane & 3;
+  double acC[TPW][2][2][2], acS[TPW][2][2][2];
+  double2 x0[TPW][2];
+#pragma unroll
+  for (int t = 0; t < TPW; ++t) {
+    const int blk = warp + t * NW;
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        acC[t][u][v][0] = acC[t][u][v][1] = 0.0;
+        acS[t][u][v][0] = acS[t][u][v][1] = 0.0;
+      }
+    if (NTILE % NW != 0 && blk >= NTILE) continue;  // warp-uniform
+    const int mb = blk / NB, nb = blk - mb * NB;
+    // B-fragment columns of this lane: col = nb*16 + v*8 + ar
+    int rowd[2], pa[2], pb[2];
+    bool ok[2];
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const int col = nb * 16 + v * 8 + ar;
+      const int bf = col >> 1;
+      ok[v] = bf < NBF;
+      const int r = bf / nbf, b = bf - r * nbf;
+      rowd[v] = 2 * r * PITCH + (col & 1);
+      int o = b * p + (ac + 1) * step;
+      pa[v] = o >= K ? o - K : o;
+      o = b * p - (ac + 1) * step;
+      pb[v] = o < 0 ? o + K : o;
+      // x0 of the epilogue butterfly nb*8 + v*4 + ac
+      const int bfe = nb * 8 + v * 4 + ac;
+      const int re = bfe / nbf, be = bfe - re * nbf;
+      x0[t][v] = bfe < NBF ? X[re * PITCH + be * p] : make_double2(0.0, 0.0);
+    }
+#pragma unroll 2
+    for (int kt = 0; kt < Kp / 4; ++kt) {
+      const bool jin = (Kp == h) || (4 * kt + ac + 1 <= h);
+      double bS[2], bD[2];
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        double a = 0.0, bb = 0.0;
+        if (ok[v] && jin) {
+          a = Xd[rowd[v] + 2 * pa[v]];
+          bb = Xd[rowd[v] + 2 * pb[v]];
+        }
+        bS[v] = a + bb;
+        bD[v] = a - bb;
+        pa[v] += 4 * step;
+        if (pa[v] >= K) pa[v] -= K;
+        pb[v] -= 4 * step;
+        if (pb[v] < 0) pb[v] += K;
+      }
+      double aC[2], aS[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int row = mb * 16 + u * 8 + ar;
+        aC[u] = Cm[row * PA + kt * 4 + ac];
+        aS[u] = Sm[row * PA + kt * 4 + ac];
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          dmma(acC[t][u][v][0], acC[t][u][v][1], aC[u], bS[v]);
+          dmma(acS[t][u][v][0], acS[t][u][v][1], aS[u], bD[v]);
+        }
+    }
+  }
+  grp_sync(bar, NT);
+#pragma unroll
+  for (int t = 0; t < TPW; ++t) {
+    const int blk = warp + t * NW;
+    if (NTILE % NW != 0 && blk >= NTILE) continue;
+    const int mb = blk / NB, nb = blk - mb * NB;
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int k = mb * 16 + u * 8 + ar;
+        const int bf = nb * 8 + v * 4 + ac;
+        if (k > h || bf >= NBF) continue;
+        const int r = bf / nbf, b = bf - r * nbf;
+        double2* Xr = X + r * PITCH;
+        const double Ar = x0[t][v].x + acC[t][u][v][0], Ai = x0[t][v].y + acC[t][u][v][1];
+        if (k == 0) {
+          Xr[b * p] = make_double2(Ar, Ai);
+          continue;
+        }
+        const double Br = acS[t][u][v][0], Bi = acS[t][u][v][1];
+        const double iBr = DIR < 0 ? Bi : -Bi, iBi = DIR < 0 ? -Br : Br;
+        int q1 = b * p + k * step, q2 = b * p - k * step;
+        if (q1 >= K) q1 -= K;
+        if (q2 < 0) q2 += K;
+        Xr[q1] = make_double2(Ar + iBr, Ai + iBi);
+        Xr[q2] = make_double2(Ar - iBr, Ai - iBi);
+      }
+  }
+  grp_sync(bar, NT);
+}
+
 // In-place K-point DFT (sign DIR) of R rows at X[r*PITCH + n] (natural order
 // in; CRT order out, read through pfa_pos).  Caller syncs before (data ready).
-// scr: pfa_scratch<PL,R>() double2 of shared scratch (DMMA stages).
+// scr: pfa_scratch<PL,R,NT>() double2 of shared scratch (DMMA stages).
 template <class PL, int S, int DIR, int R, int NT, int PITCH>
 __device__ __forceinline__ void pfa_stage_any(double2* X, const double2* tab, double2* scr, int gtid, int bar) {
-  if constexpr (pfa_use_mma(pfa_p<PL, S>())) pfa_stage_mma<PL, S, DIR, R, NT, PITCH>(X, tab, scr, gtid, bar);
+  constexpr int p = pfa_p<PL, S>();
+  if constexpr (pfa_use_mma(p) && mma_reg(PL::K, p, R, NT)) pfa_stage_mma_reg<PL, S, DIR, R, NT, PITCH>(X, tab, gtid, bar);
+  else if constexpr (pfa_use_mma(p)) pfa_stage_mma<PL, S, DIR, R, NT, PITCH>(X, tab, scr, gtid, bar);
   else pfa_stage<PL, S, DIR, R, NT, PITCH>(X, tab, gtid, bar);
 }
 

@@ -80,8 +80,6 @@ struct BetaTables {
   double* sinh = nullptr;    // L   : log sin(beta_b / 2)
   double* cosh = nullptr;    // L   : log cos(beta_b / 2)
   // prime-factor beta stage (K and K2 = 4L-1 both prime-factor lengths)
-  double2* phs = nullptr;    // K   : (1/K) exp(-i pi m''/K), index m''+L-1
-  double* wfpos = nullptr;   // K2  : DFT_K2(w_even wrapped)/K2, stored at CRT positions
   // centred Bluestein (register-FFT beta stage, beta2.cu)
   double2* a2 = nullptr;     // L     : exp(-i pi b'^2/K), b' = 0..L-1 (even in b')
   double2* hf2 = nullptr;    // P/2+1 : FFT_P(h')/P, h'[j] = exp(+i pi j^2/K), |j| <= 2L-2 (even)
@@ -188,10 +186,6 @@ int scv_pfa_syn_alpha(scv_ctx* c, int K, int real, const void* in, int b0, int n
 int scv_pfa_syn_gamma(scv_ctx* c, int K, int real, const double2* chunk, int b0, int nbb, double2* W1p,
                       cudaStream_t s);
 int scv_pfa_pos_host(int K, int k);  // CRT output position of frequency k
-// beta stage + contraction on the prime-factor engine (L = 2^k, 128 <= L <= 1024)
-bool scv_pfa_beta_supported(int L);
-int scv_pfa_beta_so3(scv_ctx* c, int L, int real, const double2* W1p, double2* w, double pref,
-                     const BetaTables* t, cudaStream_t s);
 
 inline int next_pow2_log(int x) {
   int lg = 0;

@@ -51,6 +51,8 @@ static void factors_of(int K, int f[4]) {
   }
 }
 
+int scv_pfa_pos_host(int K, int k);
+
 int scv_pfa_tables(scv_ctx* c, int K, const double2** out) {
   const std::string key = "pfa_" + std::to_string(K);
   auto it = c->aux.find(key);
@@ -87,7 +89,12 @@ int scv_pfa_tables(scv_ctx* c, int K, const double2** out) {
       tab.push_back(make_double2((double)cosl(a), (double)sinl(a)));
     }
   }
-  if (tab.empty()) tab.push_back(make_double2(0.0, 0.0));
+  {  // CRT output positions (pfa_pos_tab), 16-bit
+    const size_t base = tab.size(), n16 = ((size_t)2 * K + 15) / 16;
+    tab.resize(base + n16, make_double2(0.0, 0.0));
+    unsigned short* pos = (unsigned short*)(tab.data() + base);
+    for (int k = 0; k < K; ++k) pos[k] = (unsigned short)scv_pfa_pos_host(K, k);
+  }
   void* d = nullptr;
   SCV_CUDA(c, cudaMalloc(&d, tab.size() * sizeof(double2)));
   SCV_CUDA(c, cudaMemcpy(d, tab.data(), tab.size() * sizeof(double2), cudaMemcpyHostToDevice));
@@ -134,6 +141,7 @@ SCV_PFA_CFG(4095, false, 1, 320, 1)  SCV_PFA_CFG(4095, true, 1, 320, 1)
 // but are transformed one call at a time, bounding the DMMA scratch).
 template <int K, bool COL, int RD>
 constexpr size_t pfa_smem_rd() {
+  static_assert(PfaCfg<K, COL>::NT % PfaCfg<K, COL>::R == 0, "column kernels map R | NT");
   using PL = PfaPlan<K>;
   constexpr int R = PfaCfg<K, COL>::R;
   return ((size_t)2 * R * K + pfa_tab_total<PL>() + pfa_scratch<PL, RD, PfaCfg<K, COL>::NT>()) * sizeof(double2) +
@@ -195,7 +203,7 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
 #pragma unroll 4
     for (int i = threadIdx.x; i < R * K; i += NT) {
       const int r = i / K, k = i - r * K;
-      if (r0 + r < nrows) out[(r0 + r) * K + k] = X[r * K + pfa_pos<PL>(k)];
+      if (r0 + r < nrows) out[(r0 + r) * K + k] = X[r * K + pfa_pos_tab<PL>(tab, k)];
     }
     __syncthreads();
     cur ^= 1;
@@ -262,7 +270,7 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
     for (int i = threadIdx.x; i < R * K; i += NT) {
       const int r = i / K, a = i - r * K;
       const int4 P = rp[r];
-      if (P.x >= 0) out[((long long)P.x * L + P.y) * K + a] = X[r * K + pfa_pos<PL>(a)];
+      if (P.x >= 0) out[((long long)P.x * L + P.y) * K + a] = X[r * K + pfa_pos_tab<PL>(tab, a)];
     }
     __syncthreads();
   }
@@ -293,11 +301,11 @@ __global__ void __launch_bounds__(PfaCfg<K, true>::NT, PfaCfg<K, true>::MINB)
   auto issue = [&](long long bt, double2* X) {
     const int b = (int)(bt / ngrp);
     const int a0 = (int)(bt - (long long)b * ngrp) * cpb;
+    const int r = threadIdx.x % R, a = a0 + r;
+    const double2* q = src + (long long)b * K + a + (long long)(threadIdx.x / R) * LK;
 #pragma unroll 4
-    for (int i = threadIdx.x; i < R * K; i += NT) {
-      const int g = i / R, r = i - g * R;
-      const int a = a0 + r;
-      if (a < K) cp_async16(X + r * K + g, src + (long long)g * LK + (long long)b * K + a);
+    for (int g = threadIdx.x / R; g < K; g += NT / R, q += (NT / R) * LK) {
+      if (a < K) cp_async16(X + r * K + g, q);
       else X[r * K + g] = make_double2(0.0, 0.0);
     }
     cp_async_commit();
@@ -334,11 +342,11 @@ __global__ void __launch_bounds__(PfaCfg<K, true>::NT, PfaCfg<K, true>::MINB)
     __syncthreads();
     pfa_dft_rows<PL, +1, R, PfaRD<K, true>::v, NT>(X, tab, scr);
     if (!real) {
+      const int r = threadIdx.x % R, a = a0 + r;
+      double2* q = src + (long long)b * K + a + (long long)(threadIdx.x / R) * LK;
+      if (a < K) {
 #pragma unroll 4
-      for (int i = threadIdx.x; i < R * K; i += NT) {
-        const int g = i / R, r = i - g * R;
-        const int a = a0 + r;
-        if (a < K) src[(long long)g * LK + (long long)b * K + a] = X[r * K + pfa_pos<PL>(g)];
+        for (int g = threadIdx.x / R; g < K; g += NT / R, q += (NT / R) * LK) *q = X[r * K + pfa_pos_tab<PL>(tab, g)];
       }
     } else {
 #pragma unroll 4
@@ -347,7 +355,7 @@ __global__ void __launch_bounds__(PfaCfg<K, true>::NT, PfaCfg<K, true>::MINB)
         const int r = c >> 1;
         const int a = a0 + c;
         if (a < K) {
-          const double2 z = X[r * K + pfa_pos<PL>(g)];
+          const double2 z = X[r * K + pfa_pos_tab<PL>(tab, g)];
           dst_real[(long long)g * LK + (long long)b * K + a] = (c & 1) ? z.y : z.x;
         }
       }
@@ -431,7 +439,7 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
       for (int i = threadIdx.x; i < R * K; i += NT) {
         const int r = i / K, m = i - r * K;
         const long long ri = r0 + r;
-        if (ri < nrows) chunk[ri * K + m] = X[r * K + pfa_pos<PL>(m)];
+        if (ri < nrows) chunk[ri * K + m] = X[r * K + pfa_pos_tab<PL>(tab, m)];
       }
     } else {
       // Z = X1 + i X2 (X1, X2 Hermitian): X1[k] = (Z[k] + conj Z[-k])/2, X2[k] = (Z[k] - conj Z[-k])/(2i)
@@ -441,8 +449,8 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
         const int r = c >> 1;
         const long long ri = r0 + c;
         if (ri < nrows) {
-          const double2 z = X[r * K + pfa_pos<PL>(m)];
-          const double2 zc = X[r * K + pfa_pos<PL>(m == 0 ? 0 : K - m)];
+          const double2 z = X[r * K + pfa_pos_tab<PL>(tab, m)];
+          const double2 zc = X[r * K + pfa_pos_tab<PL>(tab, m == 0 ? 0 : K - m)];
           double2 v;
           if ((c & 1) == 0) v = make_double2(0.5 * (z.x + zc.x), 0.5 * (z.y - zc.y));
           else v = make_double2(0.5 * (z.y + zc.y), -0.5 * (z.x - zc.x));
@@ -482,11 +490,11 @@ __global__ void __launch_bounds__(PfaCfg<K, true>::NT, PfaCfg<K, true>::MINB)
   auto issue = [&](long long bt, double2* X) {
     const int bb = (int)(bt / ngrp);
     const int q0 = (int)(bt - (long long)bb * ngrp) * R;
+    const int r = threadIdx.x % R, q = q0 + r;
+    const double2* c = chunk + ((long long)bb * K + threadIdx.x / R) * K + q;
 #pragma unroll 4
-    for (int i = threadIdx.x; i < R * K; i += NT) {
-      const int g = i / R, r = i - g * R;
-      const int q = q0 + r;
-      if (q < K) cp_async16(X + r * K + g, chunk + ((long long)bb * K + g) * K + q);
+    for (int g = threadIdx.x / R; g < K; g += NT / R, c += (NT / R) * K) {
+      if (q < K) cp_async16(X + r * K + g, c);
       else X[r * K + g] = make_double2(0.0, 0.0);
     }
     cp_async_commit();
@@ -515,7 +523,7 @@ __global__ void __launch_bounds__(PfaCfg<K, true>::NT, PfaCfg<K, true>::MINB)
       const int n = gn <= L - 1 ? gn : gn - K;
       const int am = m < 0 ? -m : m, an = n < 0 ? -n : n;
       if (am > an || (real && n < 0)) continue;
-      W1p[(w1p_colbase(n, real) + m + an) * (long long)L + b0 + bb] = X[r * K + pfa_pos<PL>(gn)];
+      W1p[(w1p_colbase(n, real) + m + an) * (long long)L + b0 + bb] = X[r * K + pfa_pos_tab<PL>(tab, gn)];
     }
     __syncthreads();
     cur ^= 1;

@@ -73,9 +73,14 @@ __host__ __device__ constexpr int pfa_tab(int p) {
   return p <= 1 ? 0 : pfa_use_mma(p) ? mma_M(p) * mma_pitch(mma_Kp(p)) : p;
 }
 template <class PL>
-__host__ __device__ constexpr int pfa_tab_total() {
+__host__ __device__ constexpr int pfa_rtab_total() {
   return pfa_tab(PL::P0) + pfa_tab(PL::P1) + pfa_tab(PL::P2) + pfa_tab(PL::P3);
 }
+// followed by the CRT output positions pos[k] as 16-bit integers
+template <class PL>
+__host__ __device__ constexpr int pfa_postab() { return (2 * PL::K + 15) / 16; }
+template <class PL>
+__host__ __device__ constexpr int pfa_tab_total() { return pfa_rtab_total<PL>() + pfa_postab<PL>(); }
 template <class PL, int S>
 __host__ __device__ constexpr int pfa_tab_off() {
   return (S > 0 ? pfa_tab(PL::P0) : 0) + (S > 1 ? pfa_tab(PL::P1) : 0) + (S > 2 ? pfa_tab(PL::P2) : 0);
@@ -116,6 +121,12 @@ __device__ __forceinline__ int pfa_pos(int k) {
   if (PL::D > 2) a += (k % PL::P2) * (K / PL::P2);
   if (PL::D > 3) a += (k % PL::P3) * (K / PL::P3);
   return a % K;  // each term < K, at most 4 terms
+}
+
+// position of output k, from the shared table (one 2-byte load)
+template <class PL>
+__device__ __forceinline__ int pfa_pos_tab(const double2* tab, int k) {
+  return ((const unsigned short*)(tab + pfa_rtab_total<PL>()))[k];
 }
 
 // Stage the coefficient tables of this length into shared memory.

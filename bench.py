@@ -163,6 +163,8 @@ def stage_roofline(a, prof, Ljs, hbm_peak, fp64_peak):
         "so3fwd_alpha": (b + 16) * vol,               # read the scale signal + write the chunk
         "so3fwd_gamma": 16 * vol + 16 * cols,         # read the chunk + write the pruned columns
         "beta_so3": 16 * cols,                        # read pruned columns once
+        # gamma pass fused with the beta quadrature: read the chunk + one table double per (n, m, b)
+        "so3fwd_gamma_q": 16 * vol + 8 * cols,
     }
     def P_of(L):
         return 1 << max(4, math.ceil(math.log2(4 * L - 3)))
@@ -177,6 +179,8 @@ def stage_roofline(a, prof, Ljs, hbm_peak, fp64_peak):
         "so3fwd_gamma": sum(K(L) * L * 5 * K(L) * math.log2(K(L)) for L in Ljs),
         "beta_so3": sum((2 * L * L - 1) * (5 * K(L) * math.log2(K(L)) + 2 * 5 * P_of(L) * math.log2(P_of(L)))
                         for L in Ljs),
+        # gamma transforms + 2 flops (complex x real FMA pair = 4) per (n, m, b) quadrature term
+        "so3fwd_gamma_q": sum(K(L) * L * 5 * K(L) * math.log2(K(L)) + 4 * (2 * L * L - 1) * L for L in Ljs),
     }
     # per map: work of the stage over all its launches / its device time per map
     name, (cnt, ms) = max(prof.items(), key=lambda kv: kv[1][1])

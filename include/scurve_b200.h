@@ -67,6 +67,13 @@ int scv_trim(scv_ctx* ctx);
  * writes "stage count total_ms\n" lines (then clears the records). */
 int scv_profile(scv_ctx* ctx, int enable);
 int scv_profile_report(scv_ctx* ctx, char* buf, int len);
+/* Set a context option; value -1 restores the library default.
+ *   "betaq": synthesis beta stage. 1 = precomputed beta quadrature table fused
+ *            into the gamma pass (default for 128 <= L <= 1024 on the
+ *            prime-factor lengths), 0 = per-column Bluestein/convolution FFTs
+ *            and Delta contraction.  Both compute so3.py:203-243.
+ * Returns SCV_EINVAL for an unknown name. */
+int scv_set_option(scv_ctx* ctx, const char* name, int value);
 /* Number of this library's own kernels launched by the context so far. */
 long long scv_launch_count(const scv_ctx* ctx);
 

@@ -36,6 +36,7 @@ _SIGS = {
     "scv_workspace_bytes": [_P],
     "scv_trim": [_P],
     "scv_profile": [_P, _I],
+    "scv_set_option": [_P, ctypes.c_char_p, _I],
     "scv_launch_count": [_P],
     "scv_profile_report": [_P, ctypes.c_char_p, _I],
     "scv_fp64_peak": [_P, ctypes.POINTER(ctypes.c_double)],
@@ -134,6 +135,13 @@ class Context:
         if rc != SCV_OK:
             raise RuntimeError(self.lib.scv_last_error(self.handle).decode())
         return v.value
+
+    def set_option(self, name: str, value: int):
+        """scv_set_option: e.g. set_option("betaq", 0) selects the FFT beta stage."""
+        with self.lock:
+            rc = self.lib.scv_set_option(self.handle, name.encode(), int(value))
+        if rc != SCV_OK:
+            raise ValueError(self.lib.scv_last_error(self.handle).decode())
 
     def trim(self):
         with self.lock:

@@ -22,12 +22,19 @@
 
 namespace {
 
+#ifndef SCV_B2_E
+#define SCV_B2_E 8
+#endif
 template <int LOGP>
 struct B2Cfg {
   static constexpr int P = 1 << LOGP;
-  static constexpr int E = 8;
+  static constexpr int E = (LOGP >= 12 || SCV_B2_E < 16) ? SCV_B2_E : 8;
   static constexpr int NT = P / E;
+#ifdef SCV_B2_MINB
+  static constexpr int MINB = SCV_B2_MINB;
+#else
   static constexpr int MINB = NT >= 512 ? 1 : 2;
+#endif
 };
 
 __device__ __forceinline__ long long colbase(int n, int real) {
@@ -67,6 +74,10 @@ __global__ void __launch_bounds__(B2Cfg<LOGP>::NT, B2Cfg<LOGP>::MINB)
   const double invK = 1.0 / (double)K;
 #pragma unroll 1
   for (int task = blockIdx.x; task < ntasks; task += gridDim.x) {
+    // opaque per-iteration copy of the thread index: keeps the compiler from
+    // hoisting every table / exchange address of the 4 FFTs out of the loop
+    int t = threadIdx.x;
+    asm volatile("" : "+r"(t));
     const int2 tk = tasks[task];
     const int n = tk.x, l = n < 0 ? -n : n;
     const int m0 = -l + 2 * tk.y, m1 = m0 + 1;
@@ -100,14 +111,14 @@ __global__ void __launch_bounds__(B2Cfg<LOGP>::NT, B2Cfg<LOGP>::MINB)
       }
       x[s] = u;
     }
-    regfft::fft<LOGP, E, -1>(x, ex, tw);
+    regfft::fft<LOGP, E, -1>(x, ex, tw, t);
 #pragma unroll
     for (int s = 0; s < E; ++s) {
       const int k = t + s * NT;
       x[s] = cmul(x[s], HF[k <= P / 2 ? k : P - k]);
     }
     __syncthreads();  // ex reuse + gsh visibility
-    regfft::fft<LOGP, E, +1>(x, ex, tw);
+    regfft::fft<LOGP, E, +1>(x, ex, tw, t);
     const double2 g = *gsh;
     // 2. F = (1/K)(-1)^{m''} A2[|m''|] c ; G = F - (gamma/2)(-1)^{m''} at the same positions
 #pragma unroll
@@ -126,7 +137,7 @@ __global__ void __launch_bounds__(B2Cfg<LOGP>::NT, B2Cfg<LOGP>::MINB)
       x[s] = v;
     }
     __syncthreads();
-    regfft::fft<LOGP, E, -1>(x, ex, tw);
+    regfft::fft<LOGP, E, -1>(x, ex, tw, t);
 #pragma unroll
     for (int s = 0; s < E; ++s) {
       const int k = t + s * NT;
@@ -134,7 +145,7 @@ __global__ void __launch_bounds__(B2Cfg<LOGP>::NT, B2Cfg<LOGP>::MINB)
       x[s] = make_double2(x[s].x * f, x[s].y * f);
     }
     __syncthreads();
-    regfft::fft<LOGP, E, +1>(x, ex, tw);
+    regfft::fft<LOGP, E, +1>(x, ex, tw, t);
     // 3. E[m'] for |m'| <= L-1 into ex (unpadded, index m' mod P)
 #pragma unroll
     for (int s = 0; s < E; ++s) {

@@ -393,6 +393,17 @@ long long scv_workspace_bytes(const scv_ctx* c) {
   return b;
 }
 
+int scv_set_option(scv_ctx* c, const char* name, int value) {
+  if (!c || !name) return SCV_EINVAL;
+  const std::string n(name);
+  if (n == "betaq") {
+    if (value < -1 || value > 1) return scv_fail(c, SCV_EINVAL, "betaq option must be -1, 0 or 1");
+    c->opt_betaq = value;
+    return SCV_OK;
+  }
+  return scv_fail(c, SCV_EINVAL, "unknown option " + n);
+}
+
 int scv_trim(scv_ctx* c) {
   if (!c) return SCV_EINVAL;
   cudaSetDevice(c->device);

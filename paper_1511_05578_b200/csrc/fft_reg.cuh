@@ -104,37 +104,44 @@ __device__ __forceinline__ double2 cm(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 
-// powers w^1..w^(R-1) in place: v[r] *= w^r
+// powers w^1..w^(R-1) in place: v[r] *= w^r (product tree of depth <= 4,
+// each power applied as soon as it exists)
 template <int R>
 __device__ __forceinline__ void twiddle(double2* v, double2 w) {
-  double2 p[16];
-  p[1] = w;
+  v[1] = cm(v[1], w);
   if constexpr (R > 2) {
-    p[2] = cm(w, w);
-    p[3] = cm(p[2], w);
+    const double2 w2 = cm(w, w), w3 = cm(w2, w);
+    v[2] = cm(v[2], w2);
+    v[3] = cm(v[3], w3);
+    if constexpr (R > 4) {
+      const double2 w4 = cm(w2, w2);
+      v[4] = cm(v[4], w4);
+      v[5] = cm(v[5], cm(w4, w));
+      v[6] = cm(v[6], cm(w4, w2));
+      v[7] = cm(v[7], cm(w4, w3));
+      if constexpr (R > 8) {
+        const double2 w8 = cm(w4, w4), w5 = cm(w4, w), w6 = cm(w4, w2), w7 = cm(w4, w3);
+        v[8] = cm(v[8], w8);
+        v[9] = cm(v[9], cm(w8, w));
+        v[10] = cm(v[10], cm(w8, w2));
+        v[11] = cm(v[11], cm(w8, w3));
+        v[12] = cm(v[12], cm(w8, w4));
+        v[13] = cm(v[13], cm(w8, w5));
+        v[14] = cm(v[14], cm(w8, w6));
+        v[15] = cm(v[15], cm(w8, w7));
+      }
+    }
   }
-  if constexpr (R > 4) {
-    p[4] = cm(p[2], p[2]);
-    p[5] = cm(p[4], w);
-    p[6] = cm(p[4], p[2]);
-    p[7] = cm(p[4], p[3]);
-  }
-  if constexpr (R > 8) {
-    p[8] = cm(p[4], p[4]);
-#pragma unroll
-    for (int r = 9; r < 16; ++r) p[r] = cm(p[8], p[r - 8]);
-  }
-#pragma unroll
-  for (int r = 1; r < R; ++r) v[r] = cm(v[r], p[r]);
 }
 
-// one Stockham pass with radix R on the natural distribution x[E]
+// One Stockham pass with radix R on the natural distribution x[E].  Each
+// butterfly is stored as soon as it is computed (no staging copy of the
+// outputs, which keeps the live set at E + a few twiddle powers).  The LAST
+// pass writes its outputs back into x in place: butterfly u reads
+// x[u + r*BPT] and writes x[u + q*BPT], disjoint from every other butterfly.
 template <int LOGP, int E, int R, int LOGNS, int DIR, bool LAST>
-__device__ __forceinline__ void pass(double2 (&x)[E], double2* sm, const double2* __restrict__ tw) {
+__device__ __forceinline__ void pass(double2 (&x)[E], double2* sm, const double2* __restrict__ tw, int t) {
   constexpr int P = 1 << LOGP, NT = P / E, NS = 1 << LOGNS, BPT = E / R;
-  const int t = threadIdx.x;
-  double2 y[BPT][R];
-  int obase[BPT];
 #pragma unroll
   for (int u = 0; u < BPT; ++u) {
     const int j = t + u * NT;
@@ -148,20 +155,16 @@ __device__ __forceinline__ void pass(double2 (&x)[E], double2* sm, const double2
       twiddle<R>(v, w);
     }
     dft<R, DIR>(v);
+    if constexpr (LAST) {
 #pragma unroll
-    for (int q = 0; q < R; ++q) y[u][q] = v[q];
-    obase[u] = (j - k) * R + k;
+      for (int q = 0; q < R; ++q) x[u + q * BPT] = v[q];
+    } else {
+      const int ob = (j - k) * R + k;
+#pragma unroll
+      for (int q = 0; q < R; ++q) sm[pad16(ob + q * NS)] = v[q];
+    }
   }
-  if constexpr (LAST) {
-#pragma unroll
-    for (int u = 0; u < BPT; ++u)
-#pragma unroll
-      for (int q = 0; q < R; ++q) x[u + q * BPT] = y[u][q];
-  } else {
-#pragma unroll
-    for (int u = 0; u < BPT; ++u)
-#pragma unroll
-      for (int q = 0; q < R; ++q) sm[pad16(obase[u] + q * NS)] = y[u][q];
+  if constexpr (!LAST) {
     __syncthreads();
 #pragma unroll
     for (int s = 0; s < E; ++s) x[s] = sm[pad16(t + s * NT)];
@@ -170,22 +173,25 @@ __device__ __forceinline__ void pass(double2 (&x)[E], double2* sm, const double2
 }
 
 template <int LOGP, int E, int LOGNS, int DIR>
-__device__ __forceinline__ void passes(double2 (&x)[E], double2* sm, const double2* __restrict__ tw) {
+__device__ __forceinline__ void passes(double2 (&x)[E], double2* sm, const double2* __restrict__ tw, int t) {
   constexpr int LOGE = E == 16 ? 4 : E == 8 ? 3 : 2;
   constexpr int REM = LOGP - LOGNS;
   constexpr int LOGR = REM < LOGE ? REM : LOGE;
   if constexpr (REM > 0) {
-    pass<LOGP, E, (1 << LOGR), LOGNS, DIR, (REM == LOGR)>(x, sm, tw);
-    passes<LOGP, E, LOGNS + LOGR, DIR>(x, sm, tw);
+    pass<LOGP, E, (1 << LOGR), LOGNS, DIR, (REM == LOGR)>(x, sm, tw, t);
+    passes<LOGP, E, LOGNS + LOGR, DIR>(x, sm, tw, t);
   }
 }
 
 // Full P-point FFT (DIR -1 forward, +1 inverse, unnormalised) of the block's
 // natural-distribution registers.  sm: padded_size(P) double2 of shared memory.
 // Precondition: no thread is still reading sm from a previous use (caller syncs).
+// t = threadIdx.x; callers inside a persistent loop pass an opaque copy so the
+// per-pass addresses are not hoisted out of the loop (hundreds of live values).
 template <int LOGP, int E, int DIR>
-__device__ __forceinline__ void fft(double2 (&x)[E], double2* sm, const double2* __restrict__ tw) {
-  passes<LOGP, E, 0, DIR>(x, sm, tw);
+__device__ __forceinline__ void fft(double2 (&x)[E], double2* sm, const double2* __restrict__ tw,
+                                    int t = threadIdx.x) {
+  passes<LOGP, E, 0, DIR>(x, sm, tw, t);
 }
 
 }  // namespace regfft

@@ -531,6 +531,119 @@ __global__ void __launch_bounds__(PfaCfg<K, true>::NT, PfaCfg<K, true>::MINB)
 }
 
 // ---------------------------------------------------------------------------
+// synthesis gamma + beta quadrature (betaq.cu): a block owns alpha-frequency
+// columns m; for each beta slab bb of the chunk it transforms the column over
+// g -> n and accumulates S_{nm}(b) q_{nm}(b) for |n| >= |m| in shared memory;
+// after the last slab it adds the partial sums into W[(sheet n), |n|, m].
+// Replaces the W1p scatter, the per-column beta FFTs and the Delta contraction.
+// Each (n, m) entry is owned by one block and chunks run in order, so the
+// summation order is fixed (bit-reproducible).
+// ---------------------------------------------------------------------------
+template <int K> struct PfaQCfg { static constexpr int NT = 256; };
+template <> struct PfaQCfg<255> { static constexpr int NT = 128; };
+template <> struct PfaQCfg<1023> { static constexpr int NT = 352; };
+template <> struct PfaQCfg<2047> { static constexpr int NT = 384; };
+
+template <int K>
+static constexpr size_t pfa_smem_q() {
+  using PL = PfaPlan<K>;
+  return ((size_t)pfa_tab_total<PL>() + pfa_scratch<PL, 1, PfaQCfg<K>::NT>() + 3 * (size_t)K) * sizeof(double2);
+}
+
+template <int K>
+__global__ void __launch_bounds__(PfaQCfg<K>::NT, 1)
+    k_syn_gamma_q(int real, const double2* __restrict__ chunk, int b0, int nbb, const double* __restrict__ qtab,
+                  const long long* __restrict__ mbase, double2* __restrict__ wout, const double2* __restrict__ gtab) {
+  using PL = PfaPlan<K>;
+  constexpr int NT = PfaQCfg<K>::NT;
+  constexpr int L = (K + 1) / 2;
+  extern __shared__ double2 sm[];
+  double2* tab = sm;
+  double2* const scr = sm + pfa_tab_total<PL>();
+  double2* const buf0 = scr + pfa_scratch<PL, 1, NT>();  // two K-point column buffers
+  double2* const acc = buf0 + 2 * K;                     // K accumulators (one per n)
+  pfa_load_tables<PL, NT>(tab, gtab);
+  const int mine = blockIdx.x < K ? (K - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int ntask = mine * nbb;
+  auto issue = [&](int task, double2* X) {
+    const int col = blockIdx.x + (task / nbb) * gridDim.x;
+    const int bb = task % nbb;
+    const double2* cp = chunk + ((long long)bb * K + threadIdx.x) * K + col;
+#pragma unroll 4
+    for (int g = threadIdx.x; g < K; g += NT, cp += (long long)NT * K) cp_async16(X + g, cp);
+    cp_async_commit();
+  };
+  if (ntask > 0) issue(0, buf0);
+  int cur = 0;
+#pragma unroll 1
+  for (int task = 0; task < ntask; ++task) {
+    if (task + 1 < ntask) issue(task + 1, buf0 + (cur ^ 1) * K);
+    else cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    double2* X = buf0 + cur * K;
+    const int col = blockIdx.x + (task / nbb) * gridDim.x;
+    const int bb = task % nbb;
+    const int m = col <= L - 1 ? col : col - K;
+    const int am = m < 0 ? -m : m;
+    if (bb == 0)
+      for (int gn = threadIdx.x; gn < K; gn += NT) acc[gn] = make_double2(0.0, 0.0);
+    pfa_dft<PL, -1, 1, NT, K>(X, tab, scr);
+    const long long b = b0 + bb;
+    const double* qp = qtab + mbase[m + L - 1] + b * (L - am) - am;   // + n       (n >= 0)
+    const double* qn = qtab + mbase[-m + L - 1] + b * (L - am) - am;  // + |n|     (n < 0)
+    for (int gn = threadIdx.x; gn < K; gn += NT) {
+      const int n = gn <= L - 1 ? gn : gn - K;
+      const int an = n < 0 ? -n : n;
+      if (an < am || (real && n < 0)) continue;
+      double qv;
+      if (n >= 0) {
+        qv = __ldg(qp + n);
+      } else {
+        qv = __ldg(qn + an);  // q_{-l,m} = (-1)^{l+m} q_{l,-m}
+        if ((an + m) & 1) qv = -qv;
+      }
+      const double2 v = X[pfa_pos_tab<PL>(tab, gn)];
+      double2 a = acc[gn];
+      a.x = fma(v.x, qv, a.x);
+      a.y = fma(v.y, qv, a.y);
+      acc[gn] = a;
+    }
+    if (bb == nbb - 1) {
+      for (int gn = threadIdx.x; gn < K; gn += NT) {
+        const int n = gn <= L - 1 ? gn : gn - K;
+        const int an = n < 0 ? -n : n;
+        if (an < am || (real && n < 0)) continue;
+        double2* o = wout + ((long long)(n >= 0 ? 0 : 1) * L + an) * K + (m + L - 1);
+        const double2 a = acc[gn];
+        double2 w = *o;
+        w.x += a.x;
+        w.y += a.y;
+        *o = w;
+      }
+    }
+    __syncthreads();
+    cur ^= 1;
+  }
+}
+
+// real path: row(-n)[m] = (-1)^{m+n} conj(row(n)[-m]) for n > 0 (so3.py:379-382)
+__global__ void k_wout_mirror(int L, double2* __restrict__ wout) {
+  const int K = 2 * L - 1;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long tot = (long long)L * K;
+  if (i >= tot) return;
+  const int l = (int)(i / K), m = (int)(i - (long long)l * K) - (L - 1);
+  if (l == 0) return;
+  const int am = m < 0 ? -m : m;
+  if (am > l) return;
+  double2 v = wout[(long long)l * K + (L - 1) - m];
+  v.y = -v.y;
+  if ((m + l) & 1) v = make_double2(-v.x, -v.y);
+  wout[((long long)L + l) * K + (L - 1) + m] = v;
+}
+
+// ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
 template <typename Kern>
@@ -646,6 +759,21 @@ static int run_syn_gamma(scv_ctx* c, int real, const double2* chunk, int b0, int
   return SCV_OK;
 }
 
+template <int K>
+static int run_syn_gamma_q(scv_ctx* c, int real, const double2* chunk, int b0, int nbb, const double* qtab,
+                           const long long* mbase, double2* wout, cudaStream_t s) {
+  const double2* tab;
+  SCV_TRY(scv_pfa_tables(c, K, &tab));
+  constexpr size_t sm = pfa_smem_q<K>();
+  static_assert(sm <= 232448, "gamma+quadrature launch shape exceeds the 227 KB shared-memory limit");
+  int grid;
+  SCV_TRY(persistent_grid(c, k_syn_gamma_q<K>, PfaQCfg<K>::NT, sm, K, &grid));
+  k_syn_gamma_q<K><<<grid, PfaQCfg<K>::NT, sm, s>>>(real, chunk, b0, nbb, qtab, mbase, wout, tab);
+  c->launches++;
+  SCV_CUDA(c, cudaGetLastError());
+  return SCV_OK;
+}
+
 int scv_pfa_ana_alpha(scv_ctx* c, int K, int real, const double2* w, const double* hlb, const double* ls,
                       const double* lc, double2* out, cudaStream_t s) {
 #define CALL(KK) run_ana_alpha<KK>(c, real, w, hlb, ls, lc, out, s)
@@ -684,4 +812,23 @@ extern "C" int scv_debug_dft(scv_ctx* c, int K, int dir, int nrows, const double
 #define CALL(KK) run_rows<KK, +1>(c, nrows, (const double2*)in, (double2*)out, s)
   PFA_SWITCH(K, CALL)
 #undef CALL
+}
+
+int scv_pfa_syn_gamma_q(scv_ctx* c, int K, int real, const double2* chunk, int b0, int nbb, const double* qtab,
+                        const long long* mbase, double2* wout, cudaStream_t s) {
+  switch (K) {
+    case 255: return run_syn_gamma_q<255>(c, real, chunk, b0, nbb, qtab, mbase, wout, s);
+    case 511: return run_syn_gamma_q<511>(c, real, chunk, b0, nbb, qtab, mbase, wout, s);
+    case 1023: return run_syn_gamma_q<1023>(c, real, chunk, b0, nbb, qtab, mbase, wout, s);
+    case 2047: return run_syn_gamma_q<2047>(c, real, chunk, b0, nbb, qtab, mbase, wout, s);
+    default: return scv_fail(c, SCV_EINVAL, "no gamma+quadrature kernel for length " + std::to_string(K));
+  }
+}
+
+int scv_wout_mirror(scv_ctx* c, int L, double2* wout, cudaStream_t s) {
+  const long long tot = (long long)L * (2 * L - 1);
+  k_wout_mirror<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(L, wout);
+  c->launches++;
+  SCV_CUDA(c, cudaGetLastError());
+  return SCV_OK;
 }

@@ -116,6 +116,8 @@ struct scv_ctx {
   struct Rec { std::string name; cudaEvent_t a, b; };
   std::vector<Rec> recs;
   std::vector<cudaEvent_t> pool;
+  // options (scv_set_option): -1 = library default
+  int opt_betaq = -1;  // synthesis beta stage: 1 = quadrature table, 0 = per-column FFTs
 };
 
 // RAII stage timer: records a start/stop event pair on `s` when profiling is on
@@ -186,6 +188,12 @@ int scv_pfa_syn_alpha(scv_ctx* c, int K, int real, const void* in, int b0, int n
 int scv_pfa_syn_gamma(scv_ctx* c, int K, int real, const double2* chunk, int b0, int nbb, double2* W1p,
                       cudaStream_t s);
 int scv_pfa_pos_host(int K, int k);  // CRT output position of frequency k
+// fused gamma pass + beta quadrature (synthesis), betaq.cu tables
+int scv_pfa_syn_gamma_q(scv_ctx* c, int K, int real, const double2* chunk, int b0, int nbb, const double* qtab,
+                        const long long* mbase, double2* wout, cudaStream_t s);
+int scv_wout_mirror(scv_ctx* c, int L, double2* wout, cudaStream_t s);
+bool scv_betaq_enabled(int L);
+int scv_betaq_table(scv_ctx* c, int L, cudaStream_t s, const double** qtab, const long long** mbase);
 
 inline int next_pow2_log(int x) {
   int lg = 0;

@@ -215,6 +215,34 @@ extern "C" int scv_so3_forward_curvelet(scv_ctx* c, int L, int real, const void*
   SCV_CUDA(c, cudaSetDevice(c->device));
   SCV_TRY(scv_ensure_delta(c, L, s));
   const int K = 2 * L - 1;
+  SCV_CUDA(c, cudaMemsetAsync(w, 0, (size_t)2 * L * K * 16, s));
+  const bool use_q = scv_pfa_supported(K) && L >= 128 && L <= 1024 && c->opt_betaq != 0 &&
+                     (c->opt_betaq == 1 || scv_betaq_enabled(L));
+  if (use_q) {
+    // alpha DFT rows -> beta chunk; gamma DFT fused with the beta quadrature -> w
+    const double* qtab = nullptr;
+    const long long* mbase = nullptr;
+    SCV_TRY(scv_betaq_table(c, L, s, &qtab, &mbase));
+    const size_t per_bc = (size_t)K * K * 16;
+    static const long long chunk_bytes = getenv("SCV_SYN_CHUNK") ? atoll(getenv("SCV_SYN_CHUNK")) : (1LL << 30);
+    const int nbc = (int)std::max<size_t>(1, std::min<size_t>((size_t)L, (size_t)chunk_bytes / per_bc));
+    void* ch = nullptr;
+    SCV_TRY(scv_scratch(c, 1, per_bc * nbc, &ch));
+    for (int b0 = 0; b0 < L; b0 += nbc) {
+      const int nbb = std::min(nbc, L - b0);
+      {
+        SCV_PROF(c, s, "so3fwd_alpha");
+        SCV_TRY(scv_pfa_syn_alpha(c, K, real, sig, b0, nbb, (double2*)ch, s));
+      }
+      SCV_PROF(c, s, "so3fwd_gamma_q");
+      SCV_TRY(scv_pfa_syn_gamma_q(c, K, real, (const double2*)ch, b0, nbb, qtab, mbase, (double2*)w, s));
+    }
+    if (real) {
+      SCV_PROF(c, s, "so3fwd_mirror");
+      SCV_TRY(scv_wout_mirror(c, L, (double2*)w, s));
+    }
+    return SCV_OK;
+  }
   const long long cols = real ? (long long)L * L : 2LL * L * L - 1;
   void* W1p = nullptr;
   SCV_TRY(scv_scratch(c, 0, (size_t)(cols * L) * 16, &W1p));
@@ -222,7 +250,6 @@ extern "C" int scv_so3_forward_curvelet(scv_ctx* c, int L, int real, const void*
   int nb = (int)std::max<size_t>(1, std::min<size_t>((size_t)L, (size_t)(1u << 30) / per_b));
   void* chunk = nullptr;
   SCV_TRY(scv_scratch(c, 1, per_b * nb, &chunk));
-  SCV_CUDA(c, cudaMemsetAsync(w, 0, (size_t)2 * L * K * 16, s));
   if (scv_pfa_supported(K)) {
     // hand-written prime-factor path: alpha DFT rows -> chunk, gamma DFT + pruning -> W1p
     const size_t per_bc = (size_t)K * K * 16;

@@ -137,3 +137,67 @@ def test_packed_beta_stage(L):
     scale = max(np.abs(refE).max(), np.abs(refO).max())
     assert np.abs(YE - refE).max() <= 1e-13 * scale
     assert np.abs(YO - refO).max() <= 1e-13 * scale
+
+
+# ---------------------------------------------------------------------------
+# beta quadrature table (csrc/betaq.cu): the synthesis beta stage + Delta
+# contraction of one column (n, m) is a real linear functional of its L beta
+# samples, W_mn = sum_b S(b) q_nm(b).  Model of the kernel's real-arithmetic
+# formulas, checked against unit-vector probes of the oracle pipeline.
+# ---------------------------------------------------------------------------
+def model_betaq(L, l, m, planes, pref):
+    """q_{n=+l, m}(b), b < L, exactly as k_betaq_build evaluates it."""
+    K = 2 * L - 1
+    D = planes[l]
+    mp = np.arange(-l, l + 1)
+    c = D[:, m + l] * D[:, 2 * l]                  # Delta_{m'm} Delta_{m'l}
+    cb = np.zeros(2 * L + 2)
+    cb[mp + L] = c
+    mpp = np.arange(L)
+    d = mpp[:, None] - mp[None, :]
+    ue = np.where(d % 2 == 0, 2.0 / (1.0 - np.where(d % 2 == 0, d, 0).astype(float) ** 2), 0.0) @ c
+    even = (l + m) % 2 == 0
+    mn = m - l
+    f = pref / K
+    b = np.arange(L - 1)
+    th = np.pi * np.outer(2 * b + 1, np.arange(1, L)) / K
+    q = np.empty(L)
+    if even:
+        acc = ue[0] + 2.0 * (np.cos(th) @ ue[1:])
+        q[:L - 1] = 2.0 * f * (-acc if (mn // 2) % 2 else acc)
+    else:
+        acc = np.sin(th) @ ue[1:]
+        q[:L - 1] = 4.0 * f * (-acc if ((mn - 1) // 2) % 2 else acc)
+    full = np.arange(-(L - 1), L)
+    sg = np.where(full % 2, -1.0, 1.0)
+    u = np.where((full < 0) & (not even), -ue[np.abs(full)], ue[np.abs(full)])
+    te = (sg * u).sum()
+    to = (sg * (cb[full - 1 + L] - cb[full + 1 + L])).sum()
+    if even:
+        v = -te if (mn // 2) % 2 else te
+    else:
+        v = 0.5 * math.pi * (-to if ((mn + 1) // 2) % 2 else to)
+    q[L - 1] = f * v
+    return q
+
+
+@pytest.mark.parametrize("L", [2, 3, 6, 9, 16])
+def test_beta_quadrature_table(L):
+    K = 2 * L - 1
+    planes = orc.halfpi_planes(L)
+    worst = 0.0
+    for n in range(-(L - 1), L):
+        l = abs(n)
+        probe = np.zeros((L, 2 * l + 1), complex)
+        for b in range(L):
+            W1 = np.zeros((1, L, K), complex)
+            W1[0, b, :] = 1.0
+            probe[b] = orc.so3_forward_rows(W1, [n], planes, L)[0]
+        assert np.abs(probe.imag).max() <= 1e-13 * max(1.0, np.abs(probe).max())
+        for m in range(-l, l + 1):
+            if n >= 0:
+                q = model_betaq(L, l, m, planes, 4 * math.pi ** 2)
+            else:   # q_{-l,m} = (-1)^{l+m} q_{l,-m}
+                q = (-1) ** ((l + m) % 2) * model_betaq(L, l, -m, planes, 4 * math.pi ** 2)
+            worst = max(worst, np.abs(q - probe[:, m + l].real).max())
+    assert worst <= 1e-13

@@ -159,6 +159,45 @@ def test_so3_round_trip_large(L):
     assert orc.rel_err(host(back.values), w) <= TOL_RT
 
 
+def _real_symmetric(w):
+    """Impose row(-n)[m] = (-1)^{m+n} conj(row(n)[-m]) (so3.py:379-382)."""
+    L = w.shape[1]
+    c = L - 1
+    w = w.copy()
+    w[0, 0, c] = w[0, 0, c].real
+    for l in range(1, L):
+        m = np.arange(-l, l + 1)
+        w[1, l, c + m] = (-1.0) ** ((m + l) % 2) * np.conj(w[0, l, c - m])
+    return w
+
+
+@pytest.mark.parametrize("L,real", [(128, False), (128, True), (256, False), (256, True), (512, False)])
+def test_beta_quadrature_matches_fft_beta_stage(L, real):
+    """The two synthesis beta stages (csrc/betaq.cu table fused into the gamma
+    pass vs per-column Bluestein + weight-convolution FFTs + Delta contraction)
+    compute the same map (so3.py:203-243)."""
+    from paper_1511_05578_b200 import _cabi
+    ctx = _cabi.context(0)
+    w = _random_cw(L, 11 + L)
+    if real:
+        w = _real_symmetric(w)
+    cw = sc.CurveletWignerCoeffs(L, w)
+    grid = sc.SO3Grid(L, L, L)
+    f = sc.so3_inverse_curvelet_real(cw, grid) if real else sc.so3_inverse_curvelet(cw, grid)
+    fwd = sc.so3_forward_curvelet_real if real else sc.so3_forward_curvelet
+    try:
+        ctx.set_option("betaq", 1)
+        a = host(fwd(f).values)
+        ctx.set_option("betaq", 0)
+        b = host(fwd(f).values)
+    finally:
+        ctx.set_option("betaq", -1)
+    assert orc.rel_err(a, b) <= 1e-12
+    assert orc.rel_err(a, w) <= TOL_RT
+    with pytest.raises(ValueError):
+        ctx.set_option("no-such-option", 1)
+
+
 # ------------------------------------------------------------------ transform
 @pytest.mark.parametrize("L,s,real", [(16, 0, False), (16, 2, False), (16, 0, True)])
 def test_transform_golden(golden, L, s, real):

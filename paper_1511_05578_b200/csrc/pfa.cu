@@ -52,6 +52,7 @@ static void factors_of(int K, int f[4]) {
 }
 
 int scv_pfa_pos_host(int K, int k);
+static int pfa_in_host(int K, int n);
 
 int scv_pfa_tables(scv_ctx* c, int K, const double2** out) {
   const std::string key = "pfa_" + std::to_string(K);
@@ -89,11 +90,14 @@ int scv_pfa_tables(scv_ctx* c, int K, const double2** out) {
       tab.push_back(make_double2((double)cosl(a), (double)sinl(a)));
     }
   }
-  {  // CRT output positions (pfa_pos_tab), 16-bit
-    const size_t base = tab.size(), n16 = ((size_t)2 * K + 15) / 16;
+  {  // 16-bit position maps (pfa_pos_tab, pfa_in_tab): out[k], then in[n]
+    const size_t base = tab.size(), n16 = ((size_t)4 * K + 15) / 16;
     tab.resize(base + n16, make_double2(0.0, 0.0));
     unsigned short* pos = (unsigned short*)(tab.data() + base);
-    for (int k = 0; k < K; ++k) pos[k] = (unsigned short)scv_pfa_pos_host(K, k);
+    for (int k = 0; k < K; ++k) {
+      pos[k] = (unsigned short)scv_pfa_pos_host(K, k);
+      pos[K + k] = (unsigned short)pfa_in_host(K, k);
+    }
   }
   void* d = nullptr;
   SCV_CUDA(c, cudaMalloc(&d, tab.size() * sizeof(double2)));
@@ -117,8 +121,8 @@ SCV_PFA_CFG(7, false, 64, 128, 2)    SCV_PFA_CFG(7, true, 64, 128, 2)
 SCV_PFA_CFG(15, false, 32, 128, 2)   SCV_PFA_CFG(15, true, 32, 128, 2)
 SCV_PFA_CFG(31, false, 16, 128, 2)   SCV_PFA_CFG(31, true, 16, 128, 2)
 SCV_PFA_CFG(63, false, 16, 256, 2)   SCV_PFA_CFG(63, true, 16, 256, 2)
-SCV_PFA_CFG(255, false, 8, 256, 2)   SCV_PFA_CFG(255, true, 8, 256, 2)
-SCV_PFA_CFG(511, false, 4, 256, 2)   SCV_PFA_CFG(511, true, 4, 256, 2)
+SCV_PFA_CFG(255, false, 8, 256, 1)   SCV_PFA_CFG(255, true, 8, 256, 1)
+SCV_PFA_CFG(511, false, 4, 256, 1)   SCV_PFA_CFG(511, true, 4, 256, 1)
 #ifndef SCV_ROW2047
 #define SCV_ROW2047 2, 384, 1
 #endif
@@ -182,8 +186,9 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
 #pragma unroll 4
     for (int i = threadIdx.x; i < R * K; i += NT) {
       const int r = i / K, n = i - r * K;
-      if (r0 + r < nrows) cp_async16(X + i, in + (r0 + r) * K + n);
-      else X[i] = make_double2(0.0, 0.0);
+      const int xi = r * K + pfa_in_tab<PL>(tab, n);
+      if (r0 + r < nrows) cp_async16(X + xi, in + (r0 + r) * K + n);
+      else X[xi] = make_double2(0.0, 0.0);
     }
     cp_async_commit();
   };
@@ -262,7 +267,7 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
         const double f = (double)(2 * l + 1) / (8.0 * SCV_PI * SCV_PI) * d;
         v = make_double2(f * cw.x, f * cw.y);
       }
-      X[i] = v;
+      X[r * K + pfa_in_tab<PL>(tab, q)] = v;
     }
     __syncthreads();
     pfa_dft_rows<PL, +1, R, PfaRD<K, false>::v, NT>(X, tab, scr);
@@ -305,7 +310,8 @@ __global__ void __launch_bounds__(PfaCfg<K, true>::NT, PfaCfg<K, true>::MINB)
     const double2* q = src + (long long)b * K + a + (long long)(threadIdx.x / R) * LK;
 #pragma unroll 4
     for (int g = threadIdx.x / R; g < K; g += NT / R, q += (NT / R) * LK) {
-      if (a < K) cp_async16(X + r * K + g, q);
+      const int xi = r * K + pfa_in_tab<PL>(tab, g);
+      if (a < K) cp_async16(X + xi, q);
       else X[r * K + g] = make_double2(0.0, 0.0);
     }
     cp_async_commit();
@@ -335,8 +341,8 @@ __global__ void __launch_bounds__(PfaCfg<K, true>::NT, PfaCfg<K, true>::MINB)
           t1.y = 0.0;
           t2.y = 0.0;
         }
-        X[r * K + n] = make_double2(t1.x - t2.y, t1.y + t2.x);
-        if (n > 0) X[r * K + K - n] = make_double2(t1.x + t2.y, -t1.y + t2.x);
+        X[r * K + pfa_in_tab<PL>(tab, n)] = make_double2(t1.x - t2.y, t1.y + t2.x);
+        if (n > 0) X[r * K + pfa_in_tab<PL>(tab, K - n)] = make_double2(t1.x + t2.y, -t1.y + t2.x);
       }
     }
     __syncthreads();
@@ -395,7 +401,7 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
       const long long ri = r0 + r;
       if (ri < nrows) {
         const int bb = (int)(ri / K), g = (int)(ri - (long long)bb * K);
-        cp_async16(X + i, F + (long long)g * LK + (long long)(b0 + bb) * K + a);
+        cp_async16(X + r * K + pfa_in_tab<PL>(tab, a), F + (long long)g * LK + (long long)(b0 + bb) * K + a);
       } else {
         X[i] = make_double2(0.0, 0.0);
       }
@@ -429,7 +435,7 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
           const int bb = (int)(ri2 / K), g = (int)(ri2 - (long long)bb * K);
           v2 = Fr[(long long)g * LK + (long long)(b0 + bb) * K + a];
         }
-        X[i] = make_double2(v1, v2);
+        X[r * K + pfa_in_tab<PL>(tab, a)] = make_double2(v1, v2);
       }
     }
     __syncthreads();
@@ -494,7 +500,8 @@ __global__ void __launch_bounds__(PfaCfg<K, true>::NT, PfaCfg<K, true>::MINB)
     const double2* c = chunk + ((long long)bb * K + threadIdx.x / R) * K + q;
 #pragma unroll 4
     for (int g = threadIdx.x / R; g < K; g += NT / R, c += (NT / R) * K) {
-      if (q < K) cp_async16(X + r * K + g, c);
+      const int xi = r * K + pfa_in_tab<PL>(tab, g);
+      if (q < K) cp_async16(X + xi, c);
       else X[r * K + g] = make_double2(0.0, 0.0);
     }
     cp_async_commit();
@@ -570,7 +577,7 @@ __global__ void __launch_bounds__(PfaQCfg<K>::NT, 1)
     const int bb = task % nbb;
     const double2* cp = chunk + ((long long)bb * K + threadIdx.x) * K + col;
 #pragma unroll 4
-    for (int g = threadIdx.x; g < K; g += NT, cp += (long long)NT * K) cp_async16(X + g, cp);
+    for (int g = threadIdx.x; g < K; g += NT, cp += (long long)NT * K) cp_async16(X + pfa_in_tab<PL>(tab, g), cp);
     cp_async_commit();
   };
   if (ntask > 0) issue(0, buf0);
@@ -660,14 +667,39 @@ static int persistent_grid(scv_ctx* c, Kern k, int nt, size_t sm, long long nbat
   return SCV_OK;
 }
 
-// CRT output position of frequency k (host copy of pfa_pos)
+// Position of output frequency k / input sample n in the D-dimensional
+// shared-memory layout (pfa.cuh, pfa_st): dimension s has stride st_s =
+// p_{s+1}...p_{D-1}; output k sits at sum_s (k mod p_s) st_s, input n at
+// sum_s (n * inv_s mod p_s) st_s with inv_s = (K/p_s)^{-1} mod p_s (Ruritanian map).
+static void strides_of(const int f[4], int st[4]) {
+  for (int s = 0; s < 4; ++s) {
+    st[s] = 1;
+    for (int t = s + 1; t < 4; ++t) st[s] *= f[t];
+  }
+}
 int scv_pfa_pos_host(int K, int k) {
-  int f[4];
+  int f[4], st[4];
   factors_of(K, f);
-  long long a = 0;
+  strides_of(f, st);
+  int a = 0;
   for (int s = 0; s < 4; ++s)
-    if (f[s] > 1) a += (long long)(k % f[s]) * (K / f[s]);
-  return (int)(a % K);
+    if (f[s] > 1) a += (k % f[s]) * st[s];
+  return a;
+}
+static int pfa_in_host(int K, int n) {
+  int f[4], st[4];
+  factors_of(K, f);
+  strides_of(f, st);
+  int a = 0;
+  for (int s = 0; s < 4; ++s) {
+    const int p = f[s];
+    if (p == 1) continue;
+    const int r = (K / p) % p;
+    int inv = 1;
+    while ((r * inv) % p != 1) ++inv;
+    a += (int)(((long long)n * inv) % p) * st[s];
+  }
+  return a;
 }
 
 #define PFA_SWITCH(K, CALL)                                                                 \

@@ -76,11 +76,28 @@ template <class PL>
 __host__ __device__ constexpr int pfa_rtab_total() {
   return pfa_tab(PL::P0) + pfa_tab(PL::P1) + pfa_tab(PL::P2) + pfa_tab(PL::P3);
 }
-// followed by the CRT output positions pos[k] as 16-bit integers
+// followed by two 16-bit maps: out[k] = position of output frequency k,
+// in[n] = position of input sample n (see pfa_st)
 template <class PL>
-__host__ __device__ constexpr int pfa_postab() { return (2 * PL::K + 15) / 16; }
+__host__ __device__ constexpr int pfa_postab() { return (4 * PL::K + 15) / 16; }
 template <class PL>
 __host__ __device__ constexpr int pfa_tab_total() { return pfa_rtab_total<PL>() + pfa_postab<PL>(); }
+// Shared-memory layout of a row during the transform: the D-dimensional array
+// x[n_0][n_1]..[n_{D-1}] (row-major, n_s < p_s) of the Ruritanian input map,
+// so dimension s has stride st_s = p_{s+1} * ... * p_{D-1} and stage s touches
+// the elements base(c) + j * st_s of its K/p_s columns c (no modular index
+// arithmetic inside the stages; the permutations live in two 16-bit tables).
+template <class PL, int S>
+__host__ __device__ constexpr int pfa_st() {
+  return (S < 1 ? PL::P1 : 1) * (S < 2 ? PL::P2 : 1) * (S < 3 ? PL::P3 : 1);
+}
+template <class PL, int S>
+__device__ __forceinline__ int pfa_base(int c) {
+  constexpr int st = pfa_st<PL, S>(), p = pfa_p<PL, S>();
+  if constexpr (st == 1) return c * p;
+  else if constexpr (st * p == PL::K) return c;
+  else return (c / st) * (st * p) + (c % st);
+}
 template <class PL, int S>
 __host__ __device__ constexpr int pfa_tab_off() {
   return (S > 0 ? pfa_tab(PL::P0) : 0) + (S > 1 ? pfa_tab(PL::P1) : 0) + (S > 2 ? pfa_tab(PL::P2) : 0);
@@ -112,27 +129,22 @@ __host__ __device__ constexpr int pfa_scratch() {
 // CTA in shared memory (pfa_load_tables).  The butterfly walks j*k mod p
 // incrementally (integer pipe) and reads each pair as a warp-broadcast
 // 16-byte load.
-// position of output k after the transform (CRT map)
-template <class PL>
-__device__ __forceinline__ int pfa_pos(int k) {
-  constexpr int K = PL::K;
-  int a = (k % PL::P0) * (K / PL::P0);
-  if (PL::D > 1) a += (k % PL::P1) * (K / PL::P1);
-  if (PL::D > 2) a += (k % PL::P2) * (K / PL::P2);
-  if (PL::D > 3) a += (k % PL::P3) * (K / PL::P3);
-  return a % K;  // each term < K, at most 4 terms
-}
-
 // position of output k, from the shared table (one 2-byte load)
 template <class PL>
 __device__ __forceinline__ int pfa_pos_tab(const double2* tab, int k) {
   return ((const unsigned short*)(tab + pfa_rtab_total<PL>()))[k];
+}
+// position of input sample n (Ruritanian map), from the shared table
+template <class PL>
+__device__ __forceinline__ int pfa_in_tab(const double2* tab, int n) {
+  return ((const unsigned short*)(tab + pfa_rtab_total<PL>()))[PL::K + n];
 }
 
 // Stage the coefficient tables of this length into shared memory.
 template <class PL, int NT>
 __device__ __forceinline__ void pfa_load_tables(double2* tab, const double2* __restrict__ gtab) {
   for (int i = threadIdx.x; i < pfa_tab_total<PL>(); i += NT) tab[i] = gtab[i];
+  __syncthreads();  // the load phase reads the position maps
 }
 
 // Accumulate k-group g (output pairs k = gG+1 .. gG+G) of one butterfly.
@@ -151,8 +163,6 @@ __device__ __forceinline__ void pfa_group_acc(const double2* __restrict__ T, con
     B[t] = make_double2(0.0, 0.0);
   }
   int pa = c0 + step, pb = c0 + (p - 1) * step;
-  if (pa >= K) pa -= K;
-  if (pb >= K) pb -= K;
   double2 a = Xr[pa], bb = Xr[pb];
   // idx[t] = j*k_t mod p for k_t = gG+t+1 (zero-padded groups use k_t <= h guard at write time;
   // a k_t > h only produces unused accumulators)
@@ -162,9 +172,7 @@ __device__ __forceinline__ void pfa_group_acc(const double2* __restrict__ T, con
 #pragma unroll 1
   for (int j = 1; j <= h; ++j) {
     pa += step;
-    if (pa >= K) pa -= K;
     pb -= step;
-    if (pb < 0) pb += K;
     // prefetch the next j's data (software pipelining)
     double2 an = a, bn = bb;
     if (j < h) {
@@ -215,7 +223,7 @@ __device__ SCV_PFA_STAGE_INL void pfa_stage(double2* X, const double2* tab, int 
   constexpr int p = pfa_p<PL, S>();
   constexpr int h = pfa_h(p);
   constexpr int K = PL::K;
-  constexpr int step = K / p;
+  constexpr int step = pfa_st<PL, S>();
   constexpr int nbf = K / p;
   constexpr int G = pfa_group(p);
   constexpr int NG = (h + G - 1) / G;
@@ -232,7 +240,7 @@ __device__ SCV_PFA_STAGE_INL void pfa_stage(double2* X, const double2* tab, int 
     const int g = it / (R * nbf);
     const int rb = it - g * (R * nbf);
     const int r = rb / nbf, b = rb - r * nbf;
-    const int c0 = b * p;
+    const int c0 = pfa_base<PL, S>(b);
     grp[u] = g;
     pos[u] = r * PITCH + c0;
     pfa_group_acc<p, G>(tab + pfa_tab_off<PL, S>(), X + r * PITCH, c0, A[u], B[u], Z[u], K, step, g * G + 1);
@@ -247,8 +255,6 @@ __device__ SCV_PFA_STAGE_INL void pfa_stage(double2* X, const double2* tab, int 
     double2* Xr = X + rowoff;
     if (g == 0) Xr[c0] = Z[u];
     int q1 = c0 + (g * G + 1) * step, q2 = c0 + (p - g * G - 1) * step;
-    while (q1 >= K) q1 -= K;
-    while (q2 >= K) q2 -= K;
 #pragma unroll
     for (int t = 0; t < G; ++t) {
       const int k = g * G + t + 1;
@@ -258,9 +264,7 @@ __device__ SCV_PFA_STAGE_INL void pfa_stage(double2* X, const double2* tab, int 
         Xr[q2] = make_double2(A[u][t].x - iB.x, A[u][t].y - iB.y);
       }
       q1 += step;
-      if (q1 >= K) q1 -= K;
       q2 -= step;
-      if (q2 < 0) q2 += K;
     }
   }
   grp_sync(bar, NT);
@@ -284,7 +288,7 @@ __device__ __forceinline__ void pfa_stage_mma(double2* X, const double2* tab, do
   constexpr int p = pfa_p<PL, S>();
   constexpr int h = pfa_h(p);
   constexpr int K = PL::K;
-  constexpr int step = K / p;
+  constexpr int step = pfa_st<PL, S>();
   constexpr int nbf = K / p;
   constexpr int NBF = R * nbf;
   constexpr int M = mma_M(p), Kp = mma_Kp(p), PA = mma_pitch(Kp);
@@ -300,9 +304,8 @@ __device__ __forceinline__ void pfa_stage_mma(double2* X, const double2* tab, do
     const int bf = i / h, j = i - bf * h + 1;
     const int r = bf / nbf, b = bf - r * nbf;
     const double2* Xr = X + r * PITCH;
-    int pa = b * p + j * step, pb = b * p + (p - j) * step;
-    pa %= K;
-    pb %= K;
+    const int c0 = pfa_base<PL, S>(b);
+    const int pa = c0 + j * step, pb = c0 + (p - j) * step;
     const double2 a = Xr[pa], bb = Xr[pb];
     Bs[(j - 1) * PB + 2 * bf] = a.x + bb.x;
     Bs[(j - 1) * PB + 2 * bf + 1] = a.y + bb.y;
@@ -311,7 +314,7 @@ __device__ __forceinline__ void pfa_stage_mma(double2* X, const double2* tab, do
   }
   for (int bf = tid; bf < NBF; bf += NT) {
     const int r = bf / nbf, b = bf - r * nbf;
-    x0s[bf] = X[r * PITCH + b * p];
+    x0s[bf] = X[r * PITCH + pfa_base<PL, S>(b)];
   }
   if constexpr (Kp > h) {
     for (int i = tid; i < (Kp - h) * PB; i += NT) {
@@ -370,16 +373,15 @@ __device__ __forceinline__ void pfa_stage_mma(double2* X, const double2* tab, do
         double2* Xr = X + r * PITCH;
         const double2 x0 = x0s[bf];
         const double Ar = x0.x + acC[u][v][0], Ai = x0.y + acC[u][v][1];
+        const int c0 = pfa_base<PL, S>(b);
         if (k == 0) {
-          Xr[b * p] = make_double2(Ar, Ai);
+          Xr[c0] = make_double2(Ar, Ai);
           continue;
         }
         const double Br = acS[u][v][0], Bi = acS[u][v][1];
         // DIR*i*B
         const double iBr = DIR < 0 ? Bi : -Bi, iBi = DIR < 0 ? -Br : Br;
-        int q1 = b * p + k * step, q2 = b * p + (p - k) * step;
-        q1 %= K;
-        q2 %= K;
+        const int q1 = c0 + k * step, q2 = c0 + (p - k) * step;
         Xr[q1] = make_double2(Ar + iBr, Ai + iBi);
         Xr[q2] = make_double2(Ar - iBr, Ai - iBi);
       }
@@ -399,7 +401,7 @@ __device__ __forceinline__ void pfa_stage_mma_reg(double2* X, const double2* tab
   constexpr int p = pfa_p<PL, S>();
   constexpr int h = pfa_h(p);
   constexpr int K = PL::K;
-  constexpr int step = K / p;
+  constexpr int step = pfa_st<PL, S>();
   constexpr int nbf = K / p;
   constexpr int NBF = R * nbf;
   constexpr int M = mma_M(p), Kp = mma_Kp(p), PA = mma_pitch(Kp);
@@ -435,14 +437,13 @@ __device__ __forceinline__ void pfa_stage_mma_reg(double2* X, const double2* tab
       ok[v] = bf < NBF;
       const int r = bf / nbf, b = bf - r * nbf;
       rowd[v] = 2 * r * PITCH + (col & 1);
-      int o = b * p + (ac + 1) * step;
-      pa[v] = o >= K ? o - K : o;
-      o = b * p - (ac + 1) * step;
-      pb[v] = o < 0 ? o + K : o;
+      const int c0 = pfa_base<PL, S>(b);
+      pa[v] = c0 + (ac + 1) * step;
+      pb[v] = c0 + (p - ac - 1) * step;
       // x0 of the epilogue butterfly nb*8 + v*4 + ac
       const int bfe = nb * 8 + v * 4 + ac;
       const int re = bfe / nbf, be = bfe - re * nbf;
-      x0[t][v] = bfe < NBF ? X[re * PITCH + be * p] : make_double2(0.0, 0.0);
+      x0[t][v] = bfe < NBF ? X[re * PITCH + pfa_base<PL, S>(be)] : make_double2(0.0, 0.0);
     }
 #pragma unroll 2
     for (int kt = 0; kt < Kp / 4; ++kt) {
@@ -458,9 +459,7 @@ __device__ __forceinline__ void pfa_stage_mma_reg(double2* X, const double2* tab
         bS[v] = a + bb;
         bD[v] = a - bb;
         pa[v] += 4 * step;
-        if (pa[v] >= K) pa[v] -= K;
         pb[v] -= 4 * step;
-        if (pb[v] < 0) pb[v] += K;
       }
       double aC[2], aS[2];
 #pragma unroll
@@ -494,15 +493,14 @@ __device__ __forceinline__ void pfa_stage_mma_reg(double2* X, const double2* tab
         const int r = bf / nbf, b = bf - r * nbf;
         double2* Xr = X + r * PITCH;
         const double Ar = x0[t][v].x + acC[t][u][v][0], Ai = x0[t][v].y + acC[t][u][v][1];
+        const int c0 = pfa_base<PL, S>(b);
         if (k == 0) {
-          Xr[b * p] = make_double2(Ar, Ai);
+          Xr[c0] = make_double2(Ar, Ai);
           continue;
         }
         const double Br = acS[t][u][v][0], Bi = acS[t][u][v][1];
         const double iBr = DIR < 0 ? Bi : -Bi, iBi = DIR < 0 ? -Br : Br;
-        int q1 = b * p + k * step, q2 = b * p - k * step;
-        if (q1 >= K) q1 -= K;
-        if (q2 < 0) q2 += K;
+        const int q1 = c0 + k * step, q2 = c0 + (p - k) * step;
         Xr[q1] = make_double2(Ar + iBr, Ai + iBi);
         Xr[q2] = make_double2(Ar - iBr, Ai - iBi);
       }

@@ -401,6 +401,16 @@ int scv_set_option(scv_ctx* c, const char* name, int value) {
     c->opt_betaq = value;
     return SCV_OK;
   }
+  if (n == "chunkt") {
+    if (value < 0 || value > 1) return scv_fail(c, SCV_EINVAL, "chunkt option must be 0 or 1");
+    c->opt_chunkt = value;
+    return SCV_OK;
+  }
+  if (n == "colgen") {
+    if (value < 0 || value > 1) return scv_fail(c, SCV_EINVAL, "colgen option must be 0 or 1");
+    c->opt_colgen = value;
+    return SCV_OK;
+  }
   return scv_fail(c, SCV_EINVAL, "unknown option " + n);
 }
 

@@ -124,7 +124,7 @@ SCV_PFA_CFG(63, false, 16, 256, 2)   SCV_PFA_CFG(63, true, 16, 256, 2)
 SCV_PFA_CFG(255, false, 8, 256, 1)   SCV_PFA_CFG(255, true, 8, 256, 1)
 SCV_PFA_CFG(511, false, 4, 256, 1)   SCV_PFA_CFG(511, true, 4, 256, 1)
 #ifndef SCV_ROW2047
-#define SCV_ROW2047 2, 384, 1
+#define SCV_ROW2047 1, 192, 2
 #endif
 #ifndef SCV_COL2047
 #define SCV_COL2047 2, 384, 1
@@ -171,8 +171,8 @@ static constexpr size_t pfa_smem() {
 // ---------------------------------------------------------------------------
 template <int K, int DIR>
 __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
-    k_pfa_rows(long long nrows, const double2* __restrict__ in, double2* __restrict__ out,
-               const double2* __restrict__ gtab) {
+    k_pfa_rows(long long nrows, const double2* in, double2* out, const double2* __restrict__ gtab) {
+  // in == out is allowed (in-place rows: a batch is read one iteration before it is written)
   using PL = PfaPlan<K>;
   constexpr int R = PfaCfg<K, false>::R, NT = PfaCfg<K, false>::NT;
   extern __shared__ double2 sm[];
@@ -282,6 +282,94 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
 }
 
 // ---------------------------------------------------------------------------
+// analysis, gamma first (complex path): a task is R adjacent alpha-frequency
+// columns m of one beta row b.  The column over the gamma frequency n is
+// generated in closed form (nonzero for |m| <= |n|), inverse-transformed over
+// n -> gamma, and stored at sig[g][b][m]: R*16-byte segments, written once,
+// no reads (adjacent tasks run on adjacent CTAs, so L2 assembles full lines).
+// The alpha IDFT then runs over contiguous rows in place (k_pfa_rows), so
+// neither pass reads HBM with a stride.
+// ---------------------------------------------------------------------------
+template <int K> struct PfaGCfg { static constexpr int R = 8, NT = 128, MINB = 2; };
+template <> struct PfaGCfg<255> { static constexpr int R = 8, NT = 256, MINB = 1; };
+template <> struct PfaGCfg<511> { static constexpr int R = 4, NT = 256, MINB = 1; };
+#ifndef SCV_GEN1023
+#define SCV_GEN1023 4, 352, 1
+#endif
+#ifndef SCV_GEN2047
+#define SCV_GEN2047 4, 384, 1
+#endif
+#define SCV_GCFG_(KK, ...)                                  \
+  template <> struct PfaGCfg<KK> {                          \
+    static constexpr int v_[3] = {__VA_ARGS__};             \
+    static constexpr int R = v_[0], NT = v_[1], MINB = v_[2]; \
+  };
+SCV_GCFG_(1023, SCV_GEN1023)
+SCV_GCFG_(2047, SCV_GEN2047)
+template <> struct PfaGCfg<4095> { static constexpr int R = 2, NT = 320, MINB = 1; };
+
+template <int K>
+static constexpr size_t pfa_smem_g() {
+  using PL = PfaPlan<K>;
+  return ((size_t)PfaGCfg<K>::R * K + pfa_tab_total<PL>() + pfa_scratch<PL, PfaGCfg<K>::R, PfaGCfg<K>::NT>()) *
+         sizeof(double2);
+}
+
+template <int K>
+__global__ void __launch_bounds__(PfaGCfg<K>::NT, PfaGCfg<K>::MINB)
+    k_ana_colgen(const double2* __restrict__ w, const double* __restrict__ hlb, const double* __restrict__ lsin,
+                 const double* __restrict__ lcos, double2* __restrict__ out, const double2* __restrict__ gtab) {
+  using PL = PfaPlan<K>;
+  constexpr int R = PfaGCfg<K>::R, NT = PfaGCfg<K>::NT;
+  constexpr int L = (K + 1) / 2;
+  constexpr int NGRP = (K + R - 1) / R;
+  extern __shared__ double2 sm[];
+  double2* tab = sm;
+  double2* const scr = sm + pfa_tab_total<PL>();
+  double2* const X = scr + pfa_scratch<PL, R, NT>();
+  pfa_load_tables<PL, NT>(tab, gtab);
+  const double fac0 = 1.0 / (8.0 * SCV_PI * SCV_PI);
+  const int ntask = L * NGRP;
+#pragma unroll 1
+  for (int task = blockIdx.x; task < ntask; task += gridDim.x) {
+    const int b = task / NGRP;
+    const int m0 = (task - b * NGRP) * R;
+    const double ls = lsin[b], lc = lcos[b];
+#pragma unroll 2
+    for (int i = threadIdx.x; i < R * K; i += NT) {
+      const int r = i / K, gi = i - r * K;
+      const int mi = m0 + r;
+      double2 v = make_double2(0.0, 0.0);
+      const int m = mi <= L - 1 ? mi : mi - K;
+      const int n = gi <= L - 1 ? gi : gi - K;
+      const int l = n < 0 ? -n : n, am = m < 0 ? -m : m;
+      if (mi < K && am <= l) {
+        const int es = n >= 0 ? l - m : l + m;  // power of sin(b/2)
+        const int ec = n >= 0 ? l + m : l - m;  // power of cos(b/2)
+        double lg = hlb[l * (l + 1) / 2 + am];
+        if (es) lg += (double)es * ls;
+        if (ec) lg += (double)ec * lc;
+        double d = exp(lg);
+        if (n < 0 && ((l - m) & 1)) d = -d;
+        const double2 cw = w[((n >= 0 ? 0 : 1) * L + l) * K + (L - 1) + m];
+        const double f = (double)(2 * l + 1) * fac0 * d;
+        v = make_double2(f * cw.x, f * cw.y);
+      }
+      X[r * K + pfa_in_tab<PL>(tab, gi)] = v;
+    }
+    __syncthreads();
+    pfa_dft<PL, +1, R, NT, K>(X, tab, scr);
+#pragma unroll 4
+    for (int i = threadIdx.x; i < R * K; i += NT) {
+      const int g = i / R, r = i - g * R;
+      const int mi = m0 + r;
+      if (mi < K) out[((long long)g * L + b) * K + mi] = X[r * K + pfa_pos_tab<PL>(tab, g)];
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // analysis gamma: R adjacent alpha columns of one beta slab, inverse over n.
 // complex: in place on sig (K, L, K), double-buffered.  real: src = T
 // (L, L, K) complex half spectrum (n >= 0), dst = real sig (K, L, K); two
@@ -378,7 +466,7 @@ __global__ void __launch_bounds__(PfaCfg<K, true>::NT, PfaCfg<K, true>::MINB)
 // ---------------------------------------------------------------------------
 template <int K>
 __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
-    k_syn_alpha(int real, const void* __restrict__ in, int b0, int nbb, double2* __restrict__ chunk,
+    k_syn_alpha(int real, int tr, const void* __restrict__ in, int b0, int nbb, double2* __restrict__ chunk,
                 const double2* __restrict__ gtab) {
   using PL = PfaPlan<K>;
   constexpr int R = PfaCfg<K, false>::R, NT = PfaCfg<K, false>::NT;
@@ -389,7 +477,7 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
   double2* const scr = sm + pfa_tab_total<PL>();
   double2* const buf0 = scr + pfa_scratch<PL, PfaRD<K, false>::v, NT>();  // buffer c at buf0 + c * R * K (stays a shared pointer)
   pfa_load_tables<PL, NT>(tab, gtab);
-  const long long nrows = (long long)K * nbb;  // row index = bb*K + g
+  const int nrows = K * nbb;  // row index = bb*K + g
   const int rpb = real ? 2 * R : R;
   const long long nb = (nrows + rpb - 1) / rpb;
   const double2* F = (const double2*)in;
@@ -440,12 +528,39 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
     }
     __syncthreads();
     pfa_dft_rows<PL, -1, R, PfaRD<K, false>::v, NT>(X, tab, scr);
-    if (!real) {
+    if (!real && tr) {
+      // transposed chunk [bb][m][g]: R consecutive g of one m are adjacent
+#pragma unroll 4
+      for (int i = threadIdx.x; i < R * K; i += NT) {
+        const int m = i / R, r = i - m * R;
+        const int ri = (int)r0 + r;
+        if (ri < nrows) {
+          const int bb = ri / K, g = ri - bb * K;
+          chunk[((long long)bb * K + m) * K + g] = X[r * K + pfa_pos_tab<PL>(tab, m)];
+        }
+      }
+    } else if (!real) {
 #pragma unroll 4
       for (int i = threadIdx.x; i < R * K; i += NT) {
         const int r = i / K, m = i - r * K;
         const long long ri = r0 + r;
         if (ri < nrows) chunk[ri * K + m] = X[r * K + pfa_pos_tab<PL>(tab, m)];
+      }
+    } else if (tr) {
+#pragma unroll 4
+      for (int i = threadIdx.x; i < 2 * R * K; i += NT) {
+        const int m = i / (2 * R), c = i - m * (2 * R);
+        const int r = c >> 1;
+        const int ri = (int)r0 + c;
+        if (ri < nrows) {
+          const double2 z = X[r * K + pfa_pos_tab<PL>(tab, m)];
+          const double2 zc = X[r * K + pfa_pos_tab<PL>(tab, m == 0 ? 0 : K - m)];
+          double2 v;
+          if ((c & 1) == 0) v = make_double2(0.5 * (z.x + zc.x), 0.5 * (z.y - zc.y));
+          else v = make_double2(0.5 * (z.y + zc.y), -0.5 * (z.x - zc.x));
+          const int bb = ri / K, g = ri - bb * K;
+          chunk[((long long)bb * K + m) * K + g] = v;
+        }
       }
     } else {
       // Z = X1 + i X2 (X1, X2 Hermitian): X1[k] = (Z[k] + conj Z[-k])/2, X2[k] = (Z[k] - conj Z[-k])/(2i)
@@ -546,20 +661,31 @@ __global__ void __launch_bounds__(PfaCfg<K, true>::NT, PfaCfg<K, true>::MINB)
 // Each (n, m) entry is owned by one block and chunks run in order, so the
 // summation order is fixed (bit-reproducible).
 // ---------------------------------------------------------------------------
-template <int K> struct PfaQCfg { static constexpr int NT = 256; };
-template <> struct PfaQCfg<255> { static constexpr int NT = 128; };
-template <> struct PfaQCfg<1023> { static constexpr int NT = 352; };
-template <> struct PfaQCfg<2047> { static constexpr int NT = 384; };
+template <int K> struct PfaQCfg { static constexpr int NT = 256, MINB = 1; };
+template <> struct PfaQCfg<255> { static constexpr int NT = 128, MINB = 1; };
+#ifndef SCV_Q1023
+#define SCV_Q1023 352, 1
+#endif
+#ifndef SCV_Q2047
+#define SCV_Q2047 192, 2
+#endif
+#define SCV_QCFG_(KK, ...)                       \
+  template <> struct PfaQCfg<KK> {               \
+    static constexpr int v_[2] = {__VA_ARGS__};  \
+    static constexpr int NT = v_[0], MINB = v_[1]; \
+  };
+SCV_QCFG_(1023, SCV_Q1023)
+SCV_QCFG_(2047, SCV_Q2047)
 
 template <int K>
 static constexpr size_t pfa_smem_q() {
   using PL = PfaPlan<K>;
-  return ((size_t)pfa_tab_total<PL>() + pfa_scratch<PL, 1, PfaQCfg<K>::NT>() + 3 * (size_t)K) * sizeof(double2);
+  return ((size_t)pfa_tab_total<PL>() + pfa_scratch<PL, 1, PfaQCfg<K>::NT>() + 2 * (size_t)K) * sizeof(double2);
 }
 
 template <int K>
-__global__ void __launch_bounds__(PfaQCfg<K>::NT, 1)
-    k_syn_gamma_q(int real, const double2* __restrict__ chunk, int b0, int nbb, const double* __restrict__ qtab,
+__global__ void __launch_bounds__(PfaQCfg<K>::NT, PfaQCfg<K>::MINB)
+    k_syn_gamma_q(int real, int tr, const double2* __restrict__ chunk, int b0, int nbb, const double* __restrict__ qtab,
                   const long long* __restrict__ mbase, double2* __restrict__ wout, const double2* __restrict__ gtab) {
   using PL = PfaPlan<K>;
   constexpr int NT = PfaQCfg<K>::NT;
@@ -568,16 +694,23 @@ __global__ void __launch_bounds__(PfaQCfg<K>::NT, 1)
   double2* tab = sm;
   double2* const scr = sm + pfa_tab_total<PL>();
   double2* const buf0 = scr + pfa_scratch<PL, 1, NT>();  // two K-point column buffers
-  double2* const acc = buf0 + 2 * K;                     // K accumulators (one per n)
+  constexpr int NA = (K + NT - 1) / NT;                  // accumulators per thread: n slots tid + u*NT
+  double2 acc[NA];
   pfa_load_tables<PL, NT>(tab, gtab);
   const int mine = blockIdx.x < K ? (K - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int ntask = mine * nbb;
   auto issue = [&](int task, double2* X) {
     const int col = blockIdx.x + (task / nbb) * gridDim.x;
     const int bb = task % nbb;
-    const double2* cp = chunk + ((long long)bb * K + threadIdx.x) * K + col;
+    if (tr) {  // transposed chunk [bb][m][g]: the column is contiguous
+      const double2* cp = chunk + ((long long)bb * K + col) * K;
 #pragma unroll 4
-    for (int g = threadIdx.x; g < K; g += NT, cp += (long long)NT * K) cp_async16(X + pfa_in_tab<PL>(tab, g), cp);
+      for (int g = threadIdx.x; g < K; g += NT) cp_async16(X + pfa_in_tab<PL>(tab, g), cp + g);
+    } else {   // chunk [bb][g][m]: stride K
+      const double2* cp = chunk + ((long long)bb * K + threadIdx.x) * K + col;
+#pragma unroll 4
+      for (int g = threadIdx.x; g < K; g += NT, cp += (long long)NT * K) cp_async16(X + pfa_in_tab<PL>(tab, g), cp);
+    }
     cp_async_commit();
   };
   if (ntask > 0) issue(0, buf0);
@@ -593,16 +726,20 @@ __global__ void __launch_bounds__(PfaQCfg<K>::NT, 1)
     const int bb = task % nbb;
     const int m = col <= L - 1 ? col : col - K;
     const int am = m < 0 ? -m : m;
-    if (bb == 0)
-      for (int gn = threadIdx.x; gn < K; gn += NT) acc[gn] = make_double2(0.0, 0.0);
+    if (bb == 0) {
+#pragma unroll
+      for (int u = 0; u < NA; ++u) acc[u] = make_double2(0.0, 0.0);
+    }
     pfa_dft<PL, -1, 1, NT, K>(X, tab, scr);
     const long long b = b0 + bb;
     const double* qp = qtab + mbase[m + L - 1] + b * (L - am) - am;   // + n       (n >= 0)
     const double* qn = qtab + mbase[-m + L - 1] + b * (L - am) - am;  // + |n|     (n < 0)
-    for (int gn = threadIdx.x; gn < K; gn += NT) {
+#pragma unroll
+    for (int u = 0; u < NA; ++u) {
+      const int gn = threadIdx.x + u * NT;
       const int n = gn <= L - 1 ? gn : gn - K;
       const int an = n < 0 ? -n : n;
-      if (an < am || (real && n < 0)) continue;
+      if (gn >= K || an < am || (real && n < 0)) continue;
       double qv;
       if (n >= 0) {
         qv = __ldg(qp + n);
@@ -611,18 +748,18 @@ __global__ void __launch_bounds__(PfaQCfg<K>::NT, 1)
         if ((an + m) & 1) qv = -qv;
       }
       const double2 v = X[pfa_pos_tab<PL>(tab, gn)];
-      double2 a = acc[gn];
-      a.x = fma(v.x, qv, a.x);
-      a.y = fma(v.y, qv, a.y);
-      acc[gn] = a;
+      acc[u].x = fma(v.x, qv, acc[u].x);
+      acc[u].y = fma(v.y, qv, acc[u].y);
     }
     if (bb == nbb - 1) {
-      for (int gn = threadIdx.x; gn < K; gn += NT) {
+#pragma unroll
+      for (int u = 0; u < NA; ++u) {
+        const int gn = threadIdx.x + u * NT;
         const int n = gn <= L - 1 ? gn : gn - K;
         const int an = n < 0 ? -n : n;
-        if (an < am || (real && n < 0)) continue;
+        if (gn >= K || an < am || (real && n < 0)) continue;
         double2* o = wout + ((long long)(n >= 0 ? 0 : 1) * L + an) * K + (m + L - 1);
-        const double2 a = acc[gn];
+        const double2 a = acc[u];
         double2 w = *o;
         w.x += a.x;
         w.y += a.y;
@@ -744,6 +881,23 @@ static int run_ana_alpha(scv_ctx* c, int real, const double2* w, const double* h
 }
 
 template <int K>
+static int run_ana_colgen(scv_ctx* c, const double2* w, const double* hlb, const double* ls, const double* lc,
+                          double2* out, cudaStream_t s) {
+  const double2* tab;
+  SCV_TRY(scv_pfa_tables(c, K, &tab));
+  constexpr size_t sm = pfa_smem_g<K>();
+  static_assert(sm <= 232448, "column-generation launch shape exceeds the 227 KB shared-memory limit");
+  constexpr int L = (K + 1) / 2;
+  const long long nt = (long long)L * ((K + PfaGCfg<K>::R - 1) / PfaGCfg<K>::R);
+  int grid;
+  SCV_TRY(persistent_grid(c, k_ana_colgen<K>, PfaGCfg<K>::NT, sm, nt, &grid));
+  k_ana_colgen<K><<<grid, PfaGCfg<K>::NT, sm, s>>>(w, hlb, ls, lc, out, tab);
+  c->launches++;
+  SCV_CUDA(c, cudaGetLastError());
+  return SCV_OK;
+}
+
+template <int K>
 static int run_ana_gamma(scv_ctx* c, int real, double2* src, double* dst, cudaStream_t s) {
   const double2* tab;
   SCV_TRY(scv_pfa_tables(c, K, &tab));
@@ -761,7 +915,7 @@ static int run_ana_gamma(scv_ctx* c, int real, double2* src, double* dst, cudaSt
 }
 
 template <int K>
-static int run_syn_alpha(scv_ctx* c, int real, const void* in, int b0, int nbb, double2* chunk, cudaStream_t s) {
+static int run_syn_alpha(scv_ctx* c, int real, int tr, const void* in, int b0, int nbb, double2* chunk, cudaStream_t s) {
   const double2* tab;
   SCV_TRY(scv_pfa_tables(c, K, &tab));
   constexpr size_t sm = pfa_smem<K, false>();
@@ -770,7 +924,7 @@ static int run_syn_alpha(scv_ctx* c, int real, const void* in, int b0, int nbb, 
   const long long nb = ((long long)K * nbb + rpb - 1) / rpb;
   int grid;
   SCV_TRY(persistent_grid(c, k_syn_alpha<K>, PfaCfg<K, false>::NT, sm, nb, &grid));
-  k_syn_alpha<K><<<grid, PfaCfg<K, false>::NT, sm, s>>>(real, in, b0, nbb, chunk, tab);
+  k_syn_alpha<K><<<grid, PfaCfg<K, false>::NT, sm, s>>>(real, tr, in, b0, nbb, chunk, tab);
   c->launches++;
   SCV_CUDA(c, cudaGetLastError());
   return SCV_OK;
@@ -792,7 +946,7 @@ static int run_syn_gamma(scv_ctx* c, int real, const double2* chunk, int b0, int
 }
 
 template <int K>
-static int run_syn_gamma_q(scv_ctx* c, int real, const double2* chunk, int b0, int nbb, const double* qtab,
+static int run_syn_gamma_q(scv_ctx* c, int real, int tr, const double2* chunk, int b0, int nbb, const double* qtab,
                            const long long* mbase, double2* wout, cudaStream_t s) {
   const double2* tab;
   SCV_TRY(scv_pfa_tables(c, K, &tab));
@@ -800,7 +954,7 @@ static int run_syn_gamma_q(scv_ctx* c, int real, const double2* chunk, int b0, i
   static_assert(sm <= 232448, "gamma+quadrature launch shape exceeds the 227 KB shared-memory limit");
   int grid;
   SCV_TRY(persistent_grid(c, k_syn_gamma_q<K>, PfaQCfg<K>::NT, sm, K, &grid));
-  k_syn_gamma_q<K><<<grid, PfaQCfg<K>::NT, sm, s>>>(real, chunk, b0, nbb, qtab, mbase, wout, tab);
+  k_syn_gamma_q<K><<<grid, PfaQCfg<K>::NT, sm, s>>>(real, tr, chunk, b0, nbb, qtab, mbase, wout, tab);
   c->launches++;
   SCV_CUDA(c, cudaGetLastError());
   return SCV_OK;
@@ -812,14 +966,30 @@ int scv_pfa_ana_alpha(scv_ctx* c, int K, int real, const double2* w, const doubl
   PFA_SWITCH(K, CALL)
 #undef CALL
 }
+int scv_pfa_ana_colgen(scv_ctx* c, int K, const double2* w, const double* hlb, const double* ls, const double* lc,
+                       double2* out, cudaStream_t s) {
+#define CALL(KK) run_ana_colgen<KK>(c, w, hlb, ls, lc, out, s)
+  PFA_SWITCH(K, CALL)
+#undef CALL
+}
+int scv_pfa_rows_inplace(scv_ctx* c, int K, int dir, long long nrows, double2* x, cudaStream_t s) {
+  if (dir < 0) {
+#define CALL(KK) run_rows<KK, -1>(c, nrows, x, x, s)
+    PFA_SWITCH(K, CALL)
+#undef CALL
+  }
+#define CALL(KK) run_rows<KK, +1>(c, nrows, x, x, s)
+  PFA_SWITCH(K, CALL)
+#undef CALL
+}
 int scv_pfa_ana_gamma(scv_ctx* c, int K, int real, double2* src, double* dst, cudaStream_t s) {
 #define CALL(KK) run_ana_gamma<KK>(c, real, src, dst, s)
   PFA_SWITCH(K, CALL)
 #undef CALL
 }
-int scv_pfa_syn_alpha(scv_ctx* c, int K, int real, const void* in, int b0, int nbb, double2* chunk,
+int scv_pfa_syn_alpha(scv_ctx* c, int K, int real, int tr, const void* in, int b0, int nbb, double2* chunk,
                       cudaStream_t s) {
-#define CALL(KK) run_syn_alpha<KK>(c, real, in, b0, nbb, chunk, s)
+#define CALL(KK) run_syn_alpha<KK>(c, real, tr, in, b0, nbb, chunk, s)
   PFA_SWITCH(K, CALL)
 #undef CALL
 }
@@ -846,13 +1016,13 @@ extern "C" int scv_debug_dft(scv_ctx* c, int K, int dir, int nrows, const double
 #undef CALL
 }
 
-int scv_pfa_syn_gamma_q(scv_ctx* c, int K, int real, const double2* chunk, int b0, int nbb, const double* qtab,
+int scv_pfa_syn_gamma_q(scv_ctx* c, int K, int real, int tr, const double2* chunk, int b0, int nbb, const double* qtab,
                         const long long* mbase, double2* wout, cudaStream_t s) {
   switch (K) {
-    case 255: return run_syn_gamma_q<255>(c, real, chunk, b0, nbb, qtab, mbase, wout, s);
-    case 511: return run_syn_gamma_q<511>(c, real, chunk, b0, nbb, qtab, mbase, wout, s);
-    case 1023: return run_syn_gamma_q<1023>(c, real, chunk, b0, nbb, qtab, mbase, wout, s);
-    case 2047: return run_syn_gamma_q<2047>(c, real, chunk, b0, nbb, qtab, mbase, wout, s);
+    case 255: return run_syn_gamma_q<255>(c, real, tr, chunk, b0, nbb, qtab, mbase, wout, s);
+    case 511: return run_syn_gamma_q<511>(c, real, tr, chunk, b0, nbb, qtab, mbase, wout, s);
+    case 1023: return run_syn_gamma_q<1023>(c, real, tr, chunk, b0, nbb, qtab, mbase, wout, s);
+    case 2047: return run_syn_gamma_q<2047>(c, real, tr, chunk, b0, nbb, qtab, mbase, wout, s);
     default: return scv_fail(c, SCV_EINVAL, "no gamma+quadrature kernel for length " + std::to_string(K));
   }
 }

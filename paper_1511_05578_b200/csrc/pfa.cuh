@@ -62,6 +62,11 @@ __host__ __device__ constexpr int pfa_gp(int p) { return p > 1 ? ((pfa_h(p) + pf
 // C[k][j] = cos(2 pi jk/p), S[k][j] = sin(2 pi jk/p), k = 0..M-1 (row 0 = the
 // all-ones / all-zero row that produces y_0), j = 1..Kp, zero padded.
 __host__ __device__ constexpr bool pfa_use_mma(int p) { return p >= 17; }
+// DMMA stage variant: 1 = warp-owned butterfly blocks (pfa_stage_mma_blk, no
+// scratch), 0 = register-held 16x16 tiles / scratch-staged B (A/B builds)
+#ifndef SCV_PFA_BLK
+#define SCV_PFA_BLK 1
+#endif
 __host__ __device__ constexpr int mma_M(int p) { return ((pfa_h(p) + 1 + 15) / 16) * 16; }   // output rows
 __host__ __device__ constexpr int mma_Kp(int p) { return ((pfa_h(p) + 3) / 4) * 4; }         // reduction dim
 __host__ __device__ constexpr int mma_pitch(int n) {  // row pitch (doubles) with pitch mod 16 in {4, 12}
@@ -116,7 +121,7 @@ __host__ __device__ constexpr int mma_tpw(int K, int p, int R, int NT) {
 }
 __host__ __device__ constexpr bool mma_reg(int K, int p, int R, int NT) { return mma_tpw(K, p, R, NT) <= SCV_PFA_TPW_MAX; }
 __host__ __device__ constexpr int mma_scratch_p(int K, int p, int R, int NT) {
-  return (p > 1 && pfa_use_mma(p) && !mma_reg(K, p, R, NT)) ? mma_Kp(p) * mma_pitch(mma_ncol(K, p, R)) + R * (K / p) : 0;
+  return (p > 1 && pfa_use_mma(p) && !SCV_PFA_BLK && !mma_reg(K, p, R, NT)) ? mma_Kp(p) * mma_pitch(mma_ncol(K, p, R)) + R * (K / p) : 0;
 }
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 template <class PL, int R, int NT>
@@ -508,13 +513,114 @@ __device__ __forceinline__ void pfa_stage_mma_reg(double2* X, const double2* tab
   grp_sync(bar, NT);
 }
 
+// DMMA stage, warp-owned butterfly blocks (default).  A block is 4 butterflies
+// (8 GEMM columns: re/im of each); ONE warp computes every output row k of its
+// block (all ceil((h+1)/8) m8 tiles of C.s and S.d, accumulators in
+// registers), then overwrites the block's own positions in place.  No other
+// warp reads or writes those positions during the stage, so the only
+// synchronisation is __syncwarp between the block's last read and first write
+// and one barrier at the end of the stage (the next stage reads across
+// blocks).  Warps stream through blocks with no block-wide barrier, so the
+// DMMA chains of different warps (and CTAs) overlap freely.
+// Block q covers butterflies {8g+o, 8g+o+4, 8g+o+1, 8g+o+5}, g = q/2, o = 2(q&1):
+// butterfly positions 4 apart differ by 4 mod 8 doubles, so the two
+// butterflies of each 16-lane phase of a B-fragment load hit disjoint banks.
+template <class PL, int S, int DIR, int R, int NT, int PITCH>
+__device__ __forceinline__ void pfa_stage_mma_blk(double2* X, const double2* tab, int gtid, int bar) {
+  constexpr int p = pfa_p<PL, S>();
+  constexpr int h = pfa_h(p);
+  constexpr int K = PL::K;
+  constexpr int step = pfa_st<PL, S>();
+  constexpr int nbf = K / p;
+  constexpr int NBF = R * nbf;
+  constexpr int M = mma_M(p), Kp = mma_Kp(p), PA = mma_pitch(Kp);
+  constexpr int M8 = (h + 1 + 7) / 8;          // m8 tiles covering k = 0..h
+  constexpr int NBLK = 2 * ((NBF + 7) / 8);    // blocks of 4 (two per group of 8)
+  constexpr int NW = NT / 32;
+  const double* Cm = (const double*)(tab + pfa_tab_off<PL, S>());
+  const double* Sm = Cm + M * PA;
+  const double* Xd = (const double*)X;
+  const int lane = gtid & 31, warp = gtid >> 5;
+  const int ar = lane >> 2, ac = lane & 3;
+  // block-local butterfly slot i -> offset within the group of 8
+  auto slot = [](int i) { return (i >> 1) + 4 * (i & 1); };
+#pragma unroll 1
+  for (int q = warp; q < NBLK; q += NW) {
+    const int gb = (q >> 1) * 8 + 2 * (q & 1);
+    // B-fragment column of this lane: butterfly slot ar>>1, component ar&1
+    const int bfB = gb + slot(ar >> 1);
+    const bool okB = bfB < NBF;
+    int rowd = 0, pa = 0, pb = 0;
+    if (okB) {
+      const int r = bfB / nbf, b = bfB - r * nbf;
+      const int c0 = pfa_base<PL, S>(b);
+      rowd = 2 * r * PITCH + (ar & 1);
+      pa = c0 + (ac + 1) * step;
+      pb = c0 + (p - ac - 1) * step;
+    }
+    // epilogue butterfly of this lane: slot ac (accumulator columns 2ac, 2ac+1)
+    const int bfE = gb + slot(ac);
+    const bool okE = bfE < NBF;
+    int eoff = 0;
+    double2 x0 = make_double2(0.0, 0.0);
+    if (okE) {
+      const int r = bfE / nbf, b = bfE - r * nbf;
+      eoff = r * PITCH + pfa_base<PL, S>(b);
+      x0 = X[eoff];
+    }
+    double accC[M8][2], accS[M8][2];
+#pragma unroll
+    for (int t = 0; t < M8; ++t) accC[t][0] = accC[t][1] = accS[t][0] = accS[t][1] = 0.0;
+#pragma unroll 2
+    for (int kt = 0; kt < Kp / 4; ++kt) {
+      double a = 0.0, bb = 0.0;
+      if (okB && ((Kp == h) || (4 * kt + ac + 1 <= h))) {
+        a = Xd[rowd + 2 * pa];
+        bb = Xd[rowd + 2 * pb];
+      }
+      pa += 4 * step;
+      pb -= 4 * step;
+      const double bS = a + bb, bD = a - bb;
+#pragma unroll
+      for (int t = 0; t < M8; ++t) {
+        const int row = t * 8 + ar;
+        const double aC = Cm[row * PA + kt * 4 + ac];
+        const double aS = Sm[row * PA + kt * 4 + ac];
+        dmma(accC[t][0], accC[t][1], aC, bS);
+        dmma(accS[t][0], accS[t][1], aS, bD);
+      }
+    }
+    __syncwarp();
+    if (okE) {
+      double2* Xr = X + eoff;
+#pragma unroll
+      for (int t = 0; t < M8; ++t) {
+        const int k = t * 8 + ar;
+        if (k > h) continue;
+        const double Ar = x0.x + accC[t][0], Ai = x0.y + accC[t][1];
+        if (k == 0) {
+          Xr[0] = make_double2(Ar, Ai);
+          continue;
+        }
+        const double Br = accS[t][0], Bi = accS[t][1];
+        const double iBr = DIR < 0 ? Bi : -Bi, iBi = DIR < 0 ? -Br : Br;
+        Xr[k * step] = make_double2(Ar + iBr, Ai + iBi);
+        Xr[(p - k) * step] = make_double2(Ar - iBr, Ai - iBi);
+      }
+    }
+    __syncwarp();
+  }
+  grp_sync(bar, NT);
+}
+
 // In-place K-point DFT (sign DIR) of R rows at X[r*PITCH + n] (natural order
 // in; CRT order out, read through pfa_pos).  Caller syncs before (data ready).
 // scr: pfa_scratch<PL,R,NT>() double2 of shared scratch (DMMA stages).
 template <class PL, int S, int DIR, int R, int NT, int PITCH>
 __device__ __forceinline__ void pfa_stage_any(double2* X, const double2* tab, double2* scr, int gtid, int bar) {
   constexpr int p = pfa_p<PL, S>();
-  if constexpr (pfa_use_mma(p) && mma_reg(PL::K, p, R, NT)) pfa_stage_mma_reg<PL, S, DIR, R, NT, PITCH>(X, tab, gtid, bar);
+  if constexpr (pfa_use_mma(p) && SCV_PFA_BLK) pfa_stage_mma_blk<PL, S, DIR, R, NT, PITCH>(X, tab, gtid, bar);
+  else if constexpr (pfa_use_mma(p) && mma_reg(PL::K, p, R, NT)) pfa_stage_mma_reg<PL, S, DIR, R, NT, PITCH>(X, tab, gtid, bar);
   else if constexpr (pfa_use_mma(p)) pfa_stage_mma<PL, S, DIR, R, NT, PITCH>(X, tab, scr, gtid, bar);
   else pfa_stage<PL, S, DIR, R, NT, PITCH>(X, tab, gtid, bar);
 }

@@ -117,6 +117,8 @@ struct scv_ctx {
   std::vector<Rec> recs;
   std::vector<cudaEvent_t> pool;
   // options (scv_set_option): -1 = library default
+  int opt_chunkt = 0;  // synthesis chunk layout: 1 = [b][m][g] (strided alpha writes), 0 = [b][g][m]
+  int opt_colgen = 1;  // analysis order: 1 = gamma-first column generation + in-place alpha rows, 0 = alpha-first
   int opt_betaq = -1;  // synthesis beta stage: 1 = quadrature table, 0 = per-column FFTs
 };
 
@@ -182,14 +184,17 @@ int scv_beta2_so3(scv_ctx* c, int L, int real, const double2* W1p, double2* w, d
 bool scv_pfa_supported(int K);
 int scv_pfa_ana_alpha(scv_ctx* c, int K, int real, const double2* w, const double* hlb, const double* ls,
                       const double* lc, double2* out, cudaStream_t s);
+int scv_pfa_ana_colgen(scv_ctx* c, int K, const double2* w, const double* hlb, const double* ls, const double* lc,
+                       double2* out, cudaStream_t s);
+int scv_pfa_rows_inplace(scv_ctx* c, int K, int dir, long long nrows, double2* x, cudaStream_t s);
 int scv_pfa_ana_gamma(scv_ctx* c, int K, int real, double2* src, double* dst, cudaStream_t s);
-int scv_pfa_syn_alpha(scv_ctx* c, int K, int real, const void* in, int b0, int nbb, double2* chunk,
+int scv_pfa_syn_alpha(scv_ctx* c, int K, int real, int tr, const void* in, int b0, int nbb, double2* chunk,
                       cudaStream_t s);
 int scv_pfa_syn_gamma(scv_ctx* c, int K, int real, const double2* chunk, int b0, int nbb, double2* W1p,
                       cudaStream_t s);
 int scv_pfa_pos_host(int K, int k);  // CRT output position of frequency k
 // fused gamma pass + beta quadrature (synthesis), betaq.cu tables
-int scv_pfa_syn_gamma_q(scv_ctx* c, int K, int real, const double2* chunk, int b0, int nbb, const double* qtab,
+int scv_pfa_syn_gamma_q(scv_ctx* c, int K, int real, int tr, const double2* chunk, int b0, int nbb, const double* qtab,
                         const long long* mbase, double2* wout, cudaStream_t s);
 int scv_wout_mirror(scv_ctx* c, int L, double2* wout, cudaStream_t s);
 bool scv_betaq_enabled(int L);

@@ -153,6 +153,15 @@ extern "C" int scv_so3_inverse_curvelet(scv_ctx* c, int L, int real, const doubl
   const long long LK = (long long)L * K;
   if (scv_pfa_supported(K)) {
     // hand-written prime-factor path: fused generate + alpha IDFT, then gamma IDFT
+    if (!real && c->opt_colgen) {
+      {
+        SCV_PROF(c, s, "so3inv_gamma");
+        SCV_TRY(scv_pfa_ana_colgen(c, K, (const double2*)w, c->hlb, t->sinh, t->cosh, (double2*)sig, s));
+      }
+      SCV_PROF(c, s, "so3inv_alpha");
+      SCV_TRY(scv_pfa_rows_inplace(c, K, +1, (long long)K * L, (double2*)sig, s));
+      return SCV_OK;
+    }
     if (!real) {
       {
         SCV_PROF(c, s, "so3inv_alpha");
@@ -232,10 +241,10 @@ extern "C" int scv_so3_forward_curvelet(scv_ctx* c, int L, int real, const void*
       const int nbb = std::min(nbc, L - b0);
       {
         SCV_PROF(c, s, "so3fwd_alpha");
-        SCV_TRY(scv_pfa_syn_alpha(c, K, real, sig, b0, nbb, (double2*)ch, s));
+        SCV_TRY(scv_pfa_syn_alpha(c, K, real, c->opt_chunkt, sig, b0, nbb, (double2*)ch, s));
       }
       SCV_PROF(c, s, "so3fwd_gamma_q");
-      SCV_TRY(scv_pfa_syn_gamma_q(c, K, real, (const double2*)ch, b0, nbb, qtab, mbase, (double2*)w, s));
+      SCV_TRY(scv_pfa_syn_gamma_q(c, K, real, c->opt_chunkt, (const double2*)ch, b0, nbb, qtab, mbase, (double2*)w, s));
     }
     if (real) {
       SCV_PROF(c, s, "so3fwd_mirror");
@@ -263,7 +272,7 @@ extern "C" int scv_so3_forward_curvelet(scv_ctx* c, int L, int real, const void*
       const int nbb = std::min(nbc, L - b0);
       {
         SCV_PROF(c, s, "so3fwd_alpha");
-        SCV_TRY(scv_pfa_syn_alpha(c, K, real, sig, b0, nbb, (double2*)ch, s));
+        SCV_TRY(scv_pfa_syn_alpha(c, K, real, 0, sig, b0, nbb, (double2*)ch, s));
       }
       SCV_PROF(c, s, "so3fwd_gamma");
       SCV_TRY(scv_pfa_syn_gamma(c, K, real, (const double2*)ch, b0, nbb, (double2*)W1p, s));

@@ -160,6 +160,8 @@ def stage_roofline(a, prof, Ljs, hbm_peak, fp64_peak):
     bytes_stage = {
         "so3inv_alpha": 16 * vol,                     # generated in shared memory, written once
         "so3inv_gamma": 2 * 16 * vol,                 # read + write in place
+        "so3inv_colgen": 16 * vol,                    # gamma-first: generated columns, written once
+        "so3inv_rows": 2 * 16 * vol,                  # alpha rows read + written in place
         "so3fwd_alpha": (b + 16) * vol,               # read the scale signal + write the chunk
         "so3fwd_gamma": 16 * vol + 16 * cols,         # read the chunk + write the pruned columns
         "beta_so3": 16 * cols,                        # read pruned columns once
@@ -175,6 +177,8 @@ def stage_roofline(a, prof, Ljs, hbm_peak, fp64_peak):
     flops_stage = {
         "so3inv_alpha": sum(K(L) * L * 5 * K(L) * math.log2(K(L)) for L in Ljs),
         "so3inv_gamma": sum(K(L) * L * 5 * K(L) * math.log2(K(L)) for L in Ljs),
+        "so3inv_colgen": sum(K(L) * L * 5 * K(L) * math.log2(K(L)) for L in Ljs),
+        "so3inv_rows": sum(K(L) * L * 5 * K(L) * math.log2(K(L)) for L in Ljs),
         "so3fwd_alpha": sum(K(L) * L * 5 * K(L) * math.log2(K(L)) for L in Ljs),
         "so3fwd_gamma": sum(K(L) * L * 5 * K(L) * math.log2(K(L)) for L in Ljs),
         "beta_so3": sum((2 * L * L - 1) * (5 * K(L) * math.log2(K(L)) + 2 * 5 * P_of(L) * math.log2(P_of(L)))

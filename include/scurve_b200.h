@@ -15,6 +15,9 @@
  *   scv_accumulate             <- the acc += W psi loop of synthesize  transform.py:170-178
  *   scv_finish_acc             <- acc[:s^2]=0 (+ real symmetry)    transform.py:186, 246-252
  *   scv_halfpi_wedge           <- build_halfpi_table / halfpi_table wigner.py:209-240
+ *   scv_so3_inverse_curvelet_slab  <- so3_inverse_curvelet restricted to beta rows [b0, b0+nb)
+ *   scv_so3_forward_curvelet_slab  <- the beta sum of so3_forward_curvelet over beta rows [b0, b0+nb)
+ *                                     (so3.py:203-243; the multi-GPU beta-slab shards)
  *
  * Conventions
  *   - All data pointers are DEVICE pointers owned by the caller.  Complex
@@ -72,6 +75,11 @@ int scv_profile_report(scv_ctx* ctx, char* buf, int len);
  *            into the gamma pass (default for 128 <= L <= 1024 on the
  *            prime-factor lengths), 0 = per-column Bluestein/convolution FFTs
  *            and Delta contraction.  Both compute so3.py:203-243.
+ *   "colgen": analysis order. 1 = gamma-first (closed-form columns over n,
+ *            gamma IDFT, then the alpha IDFT over contiguous rows in place;
+ *            default), 0 = alpha rows first, then gamma columns in place.
+ *   "chunkt": synthesis beta-chunk layout. 0 = [b][g][m] (default),
+ *            1 = [b][m][g] (strided alpha writes, contiguous gamma reads).
  * Returns SCV_EINVAL for an unknown name. */
 int scv_set_option(scv_ctx* ctx, const char* name, int value);
 /* Number of this library's own kernels launched by the context so far. */
@@ -119,6 +127,20 @@ int scv_scaling_product(scv_ctx* ctx, int L, int Ls, const double* flm, const do
  * complex128 -> sig (2Lj-1, Lj, 2Lj-1), complex128 or float64 if real. */
 int scv_so3_inverse_curvelet(scv_ctx* ctx, int Lj, int real, const double* w, void* sig,
                              void* stream);
+
+/* Beta-slab variants (complex path; K = 2Lj-1 must be a prime-factor length).
+ * A slab holds the beta rows [b0, b0+nb) of the scale signal as a
+ * (2Lj-1, nb, 2Lj-1) array (gamma, beta-in-slab, alpha): slabs of one scale
+ * on different GPUs hold disjoint rows of the same SO(3) signal.
+ * inverse: w (2, Lj, 2Lj-1) -> the slab (rows b0.. of the full transform).
+ * forward: the beta quadrature summed over the slab's rows only, written into
+ * w (accumulate = 0) or added to it (accumulate = 1); the sum of the partials
+ * of all slabs is scv_so3_forward_curvelet of the full signal.  Needs the
+ * beta-quadrature path (128 <= Lj <= 1024); real = 1 reads a float64 slab. */
+int scv_so3_inverse_curvelet_slab(scv_ctx* ctx, int Lj, const double* w, int b0, int nb, void* sig,
+                                  void* stream);
+int scv_so3_forward_curvelet_slab(scv_ctx* ctx, int Lj, int real, const void* sig, int b0, int nb,
+                                  double* w, int accumulate, void* stream);
 
 /* Sparse forward Wigner transform (synthesis direction): sig -> w. */
 int scv_so3_forward_curvelet(scv_ctx* ctx, int Lj, int real, const void* sig, double* w,

@@ -48,6 +48,8 @@ _SIGS = {
     "scv_scaling_product": [_P, _I, _I, _P, _P, _P, _P],
     "scv_so3_inverse_curvelet": [_P, _I, _I, _P, _P, _P],
     "scv_so3_forward_curvelet": [_P, _I, _I, _P, _P, _P],
+    "scv_so3_inverse_curvelet_slab": [_P, _I, _P, _I, _I, _P, _P],
+    "scv_so3_forward_curvelet_slab": [_P, _I, _I, _P, _I, _I, _P, _I, _P],
     "scv_accumulate": [_P, _I, _I, _P, _P, _P, _P, _P],
     "scv_accumulate_scaling": [_P, _I, _I, _P, _P, _P, _P],
     "scv_finish_acc": [_P, _I, _I, _I, _P, _P],

@@ -402,13 +402,13 @@ int scv_set_option(scv_ctx* c, const char* name, int value) {
     return SCV_OK;
   }
   if (n == "chunkt") {
-    if (value < 0 || value > 1) return scv_fail(c, SCV_EINVAL, "chunkt option must be 0 or 1");
-    c->opt_chunkt = value;
+    if (value < -1 || value > 1) return scv_fail(c, SCV_EINVAL, "chunkt option must be -1, 0 or 1");
+    c->opt_chunkt = value < 0 ? 0 : value;
     return SCV_OK;
   }
   if (n == "colgen") {
-    if (value < 0 || value > 1) return scv_fail(c, SCV_EINVAL, "colgen option must be 0 or 1");
-    c->opt_colgen = value;
+    if (value < -1 || value > 1) return scv_fail(c, SCV_EINVAL, "colgen option must be -1, 0 or 1");
+    c->opt_colgen = value < 0 ? 1 : value;
     return SCV_OK;
   }
   return scv_fail(c, SCV_EINVAL, "unknown option " + n);

@@ -318,7 +318,8 @@ static constexpr size_t pfa_smem_g() {
 template <int K>
 __global__ void __launch_bounds__(PfaGCfg<K>::NT, PfaGCfg<K>::MINB)
     k_ana_colgen(const double2* __restrict__ w, const double* __restrict__ hlb, const double* __restrict__ lsin,
-                 const double* __restrict__ lcos, double2* __restrict__ out, const double2* __restrict__ gtab) {
+                 const double* __restrict__ lcos, int b0, int nb, double2* __restrict__ out,
+                 const double2* __restrict__ gtab) {
   using PL = PfaPlan<K>;
   constexpr int R = PfaGCfg<K>::R, NT = PfaGCfg<K>::NT;
   constexpr int L = (K + 1) / 2;
@@ -329,11 +330,12 @@ __global__ void __launch_bounds__(PfaGCfg<K>::NT, PfaGCfg<K>::MINB)
   double2* const X = scr + pfa_scratch<PL, R, NT>();
   pfa_load_tables<PL, NT>(tab, gtab);
   const double fac0 = 1.0 / (8.0 * SCV_PI * SCV_PI);
-  const int ntask = L * NGRP;
+  const int ntask = nb * NGRP;
 #pragma unroll 1
   for (int task = blockIdx.x; task < ntask; task += gridDim.x) {
-    const int b = task / NGRP;
-    const int m0 = (task - b * NGRP) * R;
+    const int bs = task / NGRP;  // beta row within the slab
+    const int b = b0 + bs;
+    const int m0 = (task - bs * NGRP) * R;
     const double ls = lsin[b], lc = lcos[b];
 #pragma unroll 2
     for (int i = threadIdx.x; i < R * K; i += NT) {
@@ -349,7 +351,11 @@ __global__ void __launch_bounds__(PfaGCfg<K>::NT, PfaGCfg<K>::MINB)
         double lg = hlb[l * (l + 1) / 2 + am];
         if (es) lg += (double)es * ls;
         if (ec) lg += (double)ec * lc;
+#if SCV_EXP_COLGEN_NOEXP
+        double d = lg;  // timing experiment only
+#else
         double d = exp(lg);
+#endif
         if (n < 0 && ((l - m) & 1)) d = -d;
         const double2 cw = w[((n >= 0 ? 0 : 1) * L + l) * K + (L - 1) + m];
         const double f = (double)(2 * l + 1) * fac0 * d;
@@ -363,7 +369,11 @@ __global__ void __launch_bounds__(PfaGCfg<K>::NT, PfaGCfg<K>::MINB)
     for (int i = threadIdx.x; i < R * K; i += NT) {
       const int g = i / R, r = i - g * R;
       const int mi = m0 + r;
-      if (mi < K) out[((long long)g * L + b) * K + mi] = X[r * K + pfa_pos_tab<PL>(tab, g)];
+#if SCV_EXP_COLGEN_CONTIG
+      if (mi < K) out[(((long long)task * R + r) * K + g) % ((long long)nb * K * K)] = X[r * K + pfa_pos_tab<PL>(tab, g)];  // timing experiment only
+#else
+      if (mi < K) out[((long long)g * nb + bs) * K + mi] = X[r * K + pfa_pos_tab<PL>(tab, g)];
+#endif
     }
     __syncthreads();
   }
@@ -466,12 +476,12 @@ __global__ void __launch_bounds__(PfaCfg<K, true>::NT, PfaCfg<K, true>::MINB)
 // ---------------------------------------------------------------------------
 template <int K>
 __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
-    k_syn_alpha(int real, int tr, const void* __restrict__ in, int b0, int nbb, double2* __restrict__ chunk,
+    k_syn_alpha(int real, int tr, const void* __restrict__ in, int lsig, int b0, int nbb, double2* __restrict__ chunk,
                 const double2* __restrict__ gtab) {
   using PL = PfaPlan<K>;
   constexpr int R = PfaCfg<K, false>::R, NT = PfaCfg<K, false>::NT;
   constexpr int L = (K + 1) / 2;
-  constexpr long long LK = (long long)L * K;
+  const long long LK = (long long)lsig * K;  // in: (K, lsig, K), rows b0.. of this launch
   extern __shared__ double2 sm[];
   double2* tab = sm;
   double2* const scr = sm + pfa_tab_total<PL>();
@@ -661,18 +671,18 @@ __global__ void __launch_bounds__(PfaCfg<K, true>::NT, PfaCfg<K, true>::MINB)
 // Each (n, m) entry is owned by one block and chunks run in order, so the
 // summation order is fixed (bit-reproducible).
 // ---------------------------------------------------------------------------
-template <int K> struct PfaQCfg { static constexpr int NT = 256, MINB = 1; };
-template <> struct PfaQCfg<255> { static constexpr int NT = 128, MINB = 1; };
+template <int K> struct PfaQCfg { static constexpr int RQ = 1, NT = 256, MINB = 1; };
+template <> struct PfaQCfg<255> { static constexpr int RQ = 1, NT = 128, MINB = 1; };
 #ifndef SCV_Q1023
-#define SCV_Q1023 352, 1
+#define SCV_Q1023 2, 352, 1
 #endif
 #ifndef SCV_Q2047
-#define SCV_Q2047 192, 2
+#define SCV_Q2047 1, 192, 2
 #endif
-#define SCV_QCFG_(KK, ...)                       \
-  template <> struct PfaQCfg<KK> {               \
-    static constexpr int v_[2] = {__VA_ARGS__};  \
-    static constexpr int NT = v_[0], MINB = v_[1]; \
+#define SCV_QCFG_(KK, ...)                                   \
+  template <> struct PfaQCfg<KK> {                           \
+    static constexpr int v_[3] = {__VA_ARGS__};              \
+    static constexpr int RQ = v_[0], NT = v_[1], MINB = v_[2]; \
   };
 SCV_QCFG_(1023, SCV_Q1023)
 SCV_QCFG_(2047, SCV_Q2047)
@@ -680,7 +690,8 @@ SCV_QCFG_(2047, SCV_Q2047)
 template <int K>
 static constexpr size_t pfa_smem_q() {
   using PL = PfaPlan<K>;
-  return ((size_t)pfa_tab_total<PL>() + pfa_scratch<PL, 1, PfaQCfg<K>::NT>() + 2 * (size_t)K) * sizeof(double2);
+  return ((size_t)pfa_tab_total<PL>() + pfa_scratch<PL, PfaQCfg<K>::RQ, PfaQCfg<K>::NT>() +
+          2 * (size_t)PfaQCfg<K>::RQ * K) * sizeof(double2);
 }
 
 template <int K>
@@ -688,28 +699,37 @@ __global__ void __launch_bounds__(PfaQCfg<K>::NT, PfaQCfg<K>::MINB)
     k_syn_gamma_q(int real, int tr, const double2* __restrict__ chunk, int b0, int nbb, const double* __restrict__ qtab,
                   const long long* __restrict__ mbase, double2* __restrict__ wout, const double2* __restrict__ gtab) {
   using PL = PfaPlan<K>;
-  constexpr int NT = PfaQCfg<K>::NT;
+  constexpr int NT = PfaQCfg<K>::NT, RQ = PfaQCfg<K>::RQ;
   constexpr int L = (K + 1) / 2;
+  constexpr int NCG = (K + RQ - 1) / RQ;                 // column groups of RQ adjacent m
   extern __shared__ double2 sm[];
   double2* tab = sm;
   double2* const scr = sm + pfa_tab_total<PL>();
-  double2* const buf0 = scr + pfa_scratch<PL, 1, NT>();  // two K-point column buffers
-  constexpr int NA = (K + NT - 1) / NT;                  // accumulators per thread: n slots tid + u*NT
-  double2 acc[NA];
+  double2* const buf0 = scr + pfa_scratch<PL, RQ, NT>();  // two buffers of RQ K-point columns
+  constexpr int NA = (K + NT - 1) / NT;                   // accumulators per column per thread: n slots tid + u*NT
+  double2 acc[RQ][NA];
   pfa_load_tables<PL, NT>(tab, gtab);
-  const int mine = blockIdx.x < K ? (K - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int mine = blockIdx.x < NCG ? (NCG - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int ntask = mine * nbb;
   auto issue = [&](int task, double2* X) {
-    const int col = blockIdx.x + (task / nbb) * gridDim.x;
+    const int col0 = (blockIdx.x + (task / nbb) * gridDim.x) * RQ;
     const int bb = task % nbb;
     if (tr) {  // transposed chunk [bb][m][g]: the column is contiguous
-      const double2* cp = chunk + ((long long)bb * K + col) * K;
+#pragma unroll
+      for (int r = 0; r < RQ; ++r) {
+        if (col0 + r >= K) continue;
+        const double2* cp = chunk + ((long long)bb * K + col0 + r) * K;
 #pragma unroll 4
-      for (int g = threadIdx.x; g < K; g += NT) cp_async16(X + pfa_in_tab<PL>(tab, g), cp + g);
-    } else {   // chunk [bb][g][m]: stride K
-      const double2* cp = chunk + ((long long)bb * K + threadIdx.x) * K + col;
+        for (int g = threadIdx.x; g < K; g += NT) cp_async16(X + r * K + pfa_in_tab<PL>(tab, g), cp + g);
+      }
+    } else {   // chunk [bb][g][m]: RQ adjacent columns = RQ*16-byte segments at stride K
+      const int r = threadIdx.x % RQ;
+      const double2* cp = chunk + ((long long)bb * K + threadIdx.x / RQ) * K + col0 + r;
 #pragma unroll 4
-      for (int g = threadIdx.x; g < K; g += NT, cp += (long long)NT * K) cp_async16(X + pfa_in_tab<PL>(tab, g), cp);
+      for (int g = threadIdx.x / RQ; g < K; g += NT / RQ, cp += (long long)(NT / RQ) * K) {
+        if (col0 + r < K) cp_async16(X + r * K + pfa_in_tab<PL>(tab, g), cp);
+        else X[r * K + pfa_in_tab<PL>(tab, g)] = make_double2(0.0, 0.0);
+      }
     }
     cp_async_commit();
   };
@@ -717,53 +737,60 @@ __global__ void __launch_bounds__(PfaQCfg<K>::NT, PfaQCfg<K>::MINB)
   int cur = 0;
 #pragma unroll 1
   for (int task = 0; task < ntask; ++task) {
-    if (task + 1 < ntask) issue(task + 1, buf0 + (cur ^ 1) * K);
+    if (task + 1 < ntask) issue(task + 1, buf0 + (cur ^ 1) * (RQ * K));
     else cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
-    double2* X = buf0 + cur * K;
-    const int col = blockIdx.x + (task / nbb) * gridDim.x;
+    double2* X = buf0 + cur * (RQ * K);
+    const int col0 = (blockIdx.x + (task / nbb) * gridDim.x) * RQ;
     const int bb = task % nbb;
-    const int m = col <= L - 1 ? col : col - K;
-    const int am = m < 0 ? -m : m;
     if (bb == 0) {
 #pragma unroll
-      for (int u = 0; u < NA; ++u) acc[u] = make_double2(0.0, 0.0);
-    }
-    pfa_dft<PL, -1, 1, NT, K>(X, tab, scr);
-    const long long b = b0 + bb;
-    const double* qp = qtab + mbase[m + L - 1] + b * (L - am) - am;   // + n       (n >= 0)
-    const double* qn = qtab + mbase[-m + L - 1] + b * (L - am) - am;  // + |n|     (n < 0)
+      for (int r = 0; r < RQ; ++r)
 #pragma unroll
-    for (int u = 0; u < NA; ++u) {
-      const int gn = threadIdx.x + u * NT;
-      const int n = gn <= L - 1 ? gn : gn - K;
-      const int an = n < 0 ? -n : n;
-      if (gn >= K || an < am || (real && n < 0)) continue;
-      double qv;
-      if (n >= 0) {
-        qv = __ldg(qp + n);
-      } else {
-        qv = __ldg(qn + an);  // q_{-l,m} = (-1)^{l+m} q_{l,-m}
-        if ((an + m) & 1) qv = -qv;
-      }
-      const double2 v = X[pfa_pos_tab<PL>(tab, gn)];
-      acc[u].x = fma(v.x, qv, acc[u].x);
-      acc[u].y = fma(v.y, qv, acc[u].y);
+        for (int u = 0; u < NA; ++u) acc[r][u] = make_double2(0.0, 0.0);
     }
-    if (bb == nbb - 1) {
+    pfa_dft<PL, -1, RQ, NT, K>(X, tab, scr);
+    const long long b = b0 + bb;
+#pragma unroll
+    for (int r = 0; r < RQ; ++r) {
+      const int col = col0 + r;
+      if (col >= K) continue;
+      const int m = col <= L - 1 ? col : col - K;
+      const int am = m < 0 ? -m : m;
+      const double* qp = qtab + mbase[m + L - 1] + b * (L - am) - am;   // + n       (n >= 0)
+      const double* qn = qtab + mbase[-m + L - 1] + b * (L - am) - am;  // + |n|     (n < 0)
 #pragma unroll
       for (int u = 0; u < NA; ++u) {
         const int gn = threadIdx.x + u * NT;
         const int n = gn <= L - 1 ? gn : gn - K;
         const int an = n < 0 ? -n : n;
         if (gn >= K || an < am || (real && n < 0)) continue;
-        double2* o = wout + ((long long)(n >= 0 ? 0 : 1) * L + an) * K + (m + L - 1);
-        const double2 a = acc[u];
-        double2 w = *o;
-        w.x += a.x;
-        w.y += a.y;
-        *o = w;
+        double qv;
+        if (n >= 0) {
+          qv = __ldg(qp + n);
+        } else {
+          qv = __ldg(qn + an);  // q_{-l,m} = (-1)^{l+m} q_{l,-m}
+          if ((an + m) & 1) qv = -qv;
+        }
+        const double2 v = X[r * K + pfa_pos_tab<PL>(tab, gn)];
+        acc[r][u].x = fma(v.x, qv, acc[r][u].x);
+        acc[r][u].y = fma(v.y, qv, acc[r][u].y);
+      }
+      if (bb == nbb - 1) {
+#pragma unroll
+        for (int u = 0; u < NA; ++u) {
+          const int gn = threadIdx.x + u * NT;
+          const int n = gn <= L - 1 ? gn : gn - K;
+          const int an = n < 0 ? -n : n;
+          if (gn >= K || an < am || (real && n < 0)) continue;
+          double2* o = wout + ((long long)(n >= 0 ? 0 : 1) * L + an) * K + (m + L - 1);
+          const double2 a = acc[r][u];
+          double2 w = *o;
+          w.x += a.x;
+          w.y += a.y;
+          *o = w;
+        }
       }
     }
     __syncthreads();
@@ -882,16 +909,16 @@ static int run_ana_alpha(scv_ctx* c, int real, const double2* w, const double* h
 
 template <int K>
 static int run_ana_colgen(scv_ctx* c, const double2* w, const double* hlb, const double* ls, const double* lc,
-                          double2* out, cudaStream_t s) {
+                          int b0, int nb, double2* out, cudaStream_t s) {
   const double2* tab;
   SCV_TRY(scv_pfa_tables(c, K, &tab));
   constexpr size_t sm = pfa_smem_g<K>();
   static_assert(sm <= 232448, "column-generation launch shape exceeds the 227 KB shared-memory limit");
   constexpr int L = (K + 1) / 2;
-  const long long nt = (long long)L * ((K + PfaGCfg<K>::R - 1) / PfaGCfg<K>::R);
+  const long long nt = (long long)nb * ((K + PfaGCfg<K>::R - 1) / PfaGCfg<K>::R);
   int grid;
   SCV_TRY(persistent_grid(c, k_ana_colgen<K>, PfaGCfg<K>::NT, sm, nt, &grid));
-  k_ana_colgen<K><<<grid, PfaGCfg<K>::NT, sm, s>>>(w, hlb, ls, lc, out, tab);
+  k_ana_colgen<K><<<grid, PfaGCfg<K>::NT, sm, s>>>(w, hlb, ls, lc, b0, nb, out, tab);
   c->launches++;
   SCV_CUDA(c, cudaGetLastError());
   return SCV_OK;
@@ -915,7 +942,8 @@ static int run_ana_gamma(scv_ctx* c, int real, double2* src, double* dst, cudaSt
 }
 
 template <int K>
-static int run_syn_alpha(scv_ctx* c, int real, int tr, const void* in, int b0, int nbb, double2* chunk, cudaStream_t s) {
+static int run_syn_alpha(scv_ctx* c, int real, int tr, const void* in, int lsig, int b0, int nbb, double2* chunk,
+                         cudaStream_t s) {
   const double2* tab;
   SCV_TRY(scv_pfa_tables(c, K, &tab));
   constexpr size_t sm = pfa_smem<K, false>();
@@ -924,7 +952,7 @@ static int run_syn_alpha(scv_ctx* c, int real, int tr, const void* in, int b0, i
   const long long nb = ((long long)K * nbb + rpb - 1) / rpb;
   int grid;
   SCV_TRY(persistent_grid(c, k_syn_alpha<K>, PfaCfg<K, false>::NT, sm, nb, &grid));
-  k_syn_alpha<K><<<grid, PfaCfg<K, false>::NT, sm, s>>>(real, tr, in, b0, nbb, chunk, tab);
+  k_syn_alpha<K><<<grid, PfaCfg<K, false>::NT, sm, s>>>(real, tr, in, lsig, b0, nbb, chunk, tab);
   c->launches++;
   SCV_CUDA(c, cudaGetLastError());
   return SCV_OK;
@@ -953,7 +981,7 @@ static int run_syn_gamma_q(scv_ctx* c, int real, int tr, const double2* chunk, i
   constexpr size_t sm = pfa_smem_q<K>();
   static_assert(sm <= 232448, "gamma+quadrature launch shape exceeds the 227 KB shared-memory limit");
   int grid;
-  SCV_TRY(persistent_grid(c, k_syn_gamma_q<K>, PfaQCfg<K>::NT, sm, K, &grid));
+  SCV_TRY(persistent_grid(c, k_syn_gamma_q<K>, PfaQCfg<K>::NT, sm, (K + PfaQCfg<K>::RQ - 1) / PfaQCfg<K>::RQ, &grid));
   k_syn_gamma_q<K><<<grid, PfaQCfg<K>::NT, sm, s>>>(real, tr, chunk, b0, nbb, qtab, mbase, wout, tab);
   c->launches++;
   SCV_CUDA(c, cudaGetLastError());
@@ -967,8 +995,8 @@ int scv_pfa_ana_alpha(scv_ctx* c, int K, int real, const double2* w, const doubl
 #undef CALL
 }
 int scv_pfa_ana_colgen(scv_ctx* c, int K, const double2* w, const double* hlb, const double* ls, const double* lc,
-                       double2* out, cudaStream_t s) {
-#define CALL(KK) run_ana_colgen<KK>(c, w, hlb, ls, lc, out, s)
+                       int b0, int nb, double2* out, cudaStream_t s) {
+#define CALL(KK) run_ana_colgen<KK>(c, w, hlb, ls, lc, b0, nb, out, s)
   PFA_SWITCH(K, CALL)
 #undef CALL
 }
@@ -987,9 +1015,9 @@ int scv_pfa_ana_gamma(scv_ctx* c, int K, int real, double2* src, double* dst, cu
   PFA_SWITCH(K, CALL)
 #undef CALL
 }
-int scv_pfa_syn_alpha(scv_ctx* c, int K, int real, int tr, const void* in, int b0, int nbb, double2* chunk,
-                      cudaStream_t s) {
-#define CALL(KK) run_syn_alpha<KK>(c, real, tr, in, b0, nbb, chunk, s)
+int scv_pfa_syn_alpha(scv_ctx* c, int K, int real, int tr, const void* in, int lsig, int b0, int nbb,
+                      double2* chunk, cudaStream_t s) {
+#define CALL(KK) run_syn_alpha<KK>(c, real, tr, in, lsig, b0, nbb, chunk, s)
   PFA_SWITCH(K, CALL)
 #undef CALL
 }

@@ -67,6 +67,10 @@ __host__ __device__ constexpr bool pfa_use_mma(int p) { return p >= 17; }
 #ifndef SCV_PFA_BLK
 #define SCV_PFA_BLK 1
 #endif
+#ifndef SCV_PFA_KT_UNROLL
+#define SCV_PFA_KT_UNROLL 4
+#endif
+constexpr int pfa_kt_unroll = SCV_PFA_KT_UNROLL;
 __host__ __device__ constexpr int mma_M(int p) { return ((pfa_h(p) + 1 + 15) / 16) * 16; }   // output rows
 __host__ __device__ constexpr int mma_Kp(int p) { return ((pfa_h(p) + 3) / 4) * 4; }         // reduction dim
 __host__ __device__ constexpr int mma_pitch(int n) {  // row pitch (doubles) with pitch mod 16 in {4, 12}
@@ -571,15 +575,24 @@ __device__ __forceinline__ void pfa_stage_mma_blk(double2* X, const double2* tab
     double accC[M8][2], accS[M8][2];
 #pragma unroll
     for (int t = 0; t < M8; ++t) accC[t][0] = accC[t][1] = accS[t][0] = accS[t][1] = 0.0;
-#pragma unroll 2
+    // B operands software-pipelined one k-step ahead (the s/d formation of
+    // step kt must not wait on its own shared loads)
+    double an = 0.0, bn = 0.0;
+    if (okB && ((Kp == h) || (ac + 1 <= h))) {
+      an = Xd[rowd + 2 * pa];
+      bn = Xd[rowd + 2 * pb];
+    }
+#pragma unroll pfa_kt_unroll
     for (int kt = 0; kt < Kp / 4; ++kt) {
-      double a = 0.0, bb = 0.0;
-      if (okB && ((Kp == h) || (4 * kt + ac + 1 <= h))) {
-        a = Xd[rowd + 2 * pa];
-        bb = Xd[rowd + 2 * pb];
-      }
+      const double a = an, bb = bn;
       pa += 4 * step;
       pb -= 4 * step;
+      an = 0.0;
+      bn = 0.0;
+      if (kt + 1 < Kp / 4 && okB && ((Kp == h) || (4 * kt + 4 + ac + 1 <= h))) {
+        an = Xd[rowd + 2 * pa];
+        bn = Xd[rowd + 2 * pb];
+      }
       const double bS = a + bb, bD = a - bb;
 #pragma unroll
       for (int t = 0; t < M8; ++t) {

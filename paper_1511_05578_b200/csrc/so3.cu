@@ -140,6 +140,85 @@ static int check_so3(scv_ctx* c, int L) {
   return SCV_OK;
 }
 
+
+// Synthesis over the beta rows [sb0, sb0 + snb) of the scale signal, held as
+// a (K, snb, K) beta slab at `sig` (the full signal is the slab (0, L)):
+// alpha DFT rows -> beta chunk; gamma DFT fused with the beta quadrature,
+// accumulated into w (the partial sum over this slab's beta rows).
+static bool use_betaq(scv_ctx* c, int L) {
+  return scv_pfa_supported(2 * L - 1) && L >= 128 && L <= 1024 && c->opt_betaq != 0 &&
+         (c->opt_betaq == 1 || scv_betaq_enabled(L));
+}
+
+static int forward_q_slab(scv_ctx* c, int L, int real, const void* sig, int sb0, int snb, double* w, cudaStream_t s) {
+  const int K = 2 * L - 1;
+  const double* qtab = nullptr;
+  const long long* mbase = nullptr;
+  SCV_TRY(scv_betaq_table(c, L, s, &qtab, &mbase));
+  const size_t per_bc = (size_t)K * K * 16;
+  static const long long chunk_bytes = getenv("SCV_SYN_CHUNK") ? atoll(getenv("SCV_SYN_CHUNK")) : (1LL << 30);
+  const int nbc = (int)std::max<size_t>(1, std::min<size_t>((size_t)snb, (size_t)chunk_bytes / per_bc));
+  void* ch = nullptr;
+  SCV_TRY(scv_scratch(c, 1, per_bc * nbc, &ch));
+  for (int b0 = sb0; b0 < sb0 + snb; b0 += nbc) {
+    const int nbb = std::min(nbc, sb0 + snb - b0);
+    {
+      SCV_PROF(c, s, "so3fwd_alpha");
+      SCV_TRY(scv_pfa_syn_alpha(c, K, real, c->opt_chunkt, sig, snb, b0 - sb0, nbb, (double2*)ch, s));
+    }
+    SCV_PROF(c, s, "so3fwd_gamma_q");
+    SCV_TRY(scv_pfa_syn_gamma_q(c, K, real, c->opt_chunkt, (const double2*)ch, b0, nbb, qtab, mbase, (double2*)w, s));
+  }
+  if (real) {
+    SCV_PROF(c, s, "so3fwd_mirror");
+    SCV_TRY(scv_wout_mirror(c, L, (double2*)w, s));
+  }
+  return SCV_OK;
+}
+
+static int check_slab(scv_ctx* c, int L, int b0, int nb) {
+  if (b0 < 0 || nb < 1 || b0 + nb > L)
+    return scv_fail(c, SCV_EINVAL, "beta slab [" + std::to_string(b0) + ", " + std::to_string(b0 + nb) +
+                                       ") outside [0, " + std::to_string(L) + ")");
+  return SCV_OK;
+}
+
+extern "C" int scv_so3_inverse_curvelet_slab(scv_ctx* c, int L, const double* w, int b0, int nb, void* sig,
+                                             void* stream) {
+  if (!c) return SCV_EINVAL;
+  SCV_TRY(check_so3(c, L));
+  SCV_TRY(check_slab(c, L, b0, nb));
+  const int K = 2 * L - 1;
+  if (!scv_pfa_supported(K))
+    return scv_fail(c, SCV_EINVAL, "beta-slab analysis needs a prime-factor grid length, got K=" + std::to_string(K));
+  cudaStream_t s = (cudaStream_t)stream;
+  SCV_CUDA(c, cudaSetDevice(c->device));
+  SCV_TRY(scv_ensure_hlb(c, L, s));
+  const BetaTables* t = nullptr;
+  SCV_TRY(scv_get_beta_tables(c, L, s, &t));
+  {
+    SCV_PROF(c, s, "so3inv_colgen");
+    SCV_TRY(scv_pfa_ana_colgen(c, K, (const double2*)w, c->hlb, t->sinh, t->cosh, b0, nb, (double2*)sig, s));
+  }
+  SCV_PROF(c, s, "so3inv_rows");
+  SCV_TRY(scv_pfa_rows_inplace(c, K, +1, (long long)K * nb, (double2*)sig, s));
+  return SCV_OK;
+}
+
+extern "C" int scv_so3_forward_curvelet_slab(scv_ctx* c, int L, int real, const void* sig, int b0, int nb,
+                                             double* w, int accumulate, void* stream) {
+  if (!c) return SCV_EINVAL;
+  SCV_TRY(check_so3(c, L));
+  SCV_TRY(check_slab(c, L, b0, nb));
+  if (!use_betaq(c, L))
+    return scv_fail(c, SCV_EINVAL, "beta-slab synthesis needs the beta-quadrature path (prime-factor K, 128 <= L <= 1024)");
+  cudaStream_t s = (cudaStream_t)stream;
+  SCV_CUDA(c, cudaSetDevice(c->device));
+  SCV_TRY(scv_ensure_delta(c, L, s));
+  if (!accumulate) SCV_CUDA(c, cudaMemsetAsync(w, 0, (size_t)2 * L * (2 * L - 1) * 16, s));
+  return forward_q_slab(c, L, real, sig, b0, nb, w, s);
+}
+
 extern "C" int scv_so3_inverse_curvelet(scv_ctx* c, int L, int real, const double* w, void* sig,
                                         void* stream) {
   if (!c) return SCV_EINVAL;
@@ -155,10 +234,10 @@ extern "C" int scv_so3_inverse_curvelet(scv_ctx* c, int L, int real, const doubl
     // hand-written prime-factor path: fused generate + alpha IDFT, then gamma IDFT
     if (!real && c->opt_colgen) {
       {
-        SCV_PROF(c, s, "so3inv_gamma");
-        SCV_TRY(scv_pfa_ana_colgen(c, K, (const double2*)w, c->hlb, t->sinh, t->cosh, (double2*)sig, s));
+        SCV_PROF(c, s, "so3inv_colgen");
+        SCV_TRY(scv_pfa_ana_colgen(c, K, (const double2*)w, c->hlb, t->sinh, t->cosh, 0, L, (double2*)sig, s));
       }
-      SCV_PROF(c, s, "so3inv_alpha");
+      SCV_PROF(c, s, "so3inv_rows");
       SCV_TRY(scv_pfa_rows_inplace(c, K, +1, (long long)K * L, (double2*)sig, s));
       return SCV_OK;
     }
@@ -225,33 +304,8 @@ extern "C" int scv_so3_forward_curvelet(scv_ctx* c, int L, int real, const void*
   SCV_TRY(scv_ensure_delta(c, L, s));
   const int K = 2 * L - 1;
   SCV_CUDA(c, cudaMemsetAsync(w, 0, (size_t)2 * L * K * 16, s));
-  const bool use_q = scv_pfa_supported(K) && L >= 128 && L <= 1024 && c->opt_betaq != 0 &&
-                     (c->opt_betaq == 1 || scv_betaq_enabled(L));
-  if (use_q) {
-    // alpha DFT rows -> beta chunk; gamma DFT fused with the beta quadrature -> w
-    const double* qtab = nullptr;
-    const long long* mbase = nullptr;
-    SCV_TRY(scv_betaq_table(c, L, s, &qtab, &mbase));
-    const size_t per_bc = (size_t)K * K * 16;
-    static const long long chunk_bytes = getenv("SCV_SYN_CHUNK") ? atoll(getenv("SCV_SYN_CHUNK")) : (1LL << 30);
-    const int nbc = (int)std::max<size_t>(1, std::min<size_t>((size_t)L, (size_t)chunk_bytes / per_bc));
-    void* ch = nullptr;
-    SCV_TRY(scv_scratch(c, 1, per_bc * nbc, &ch));
-    for (int b0 = 0; b0 < L; b0 += nbc) {
-      const int nbb = std::min(nbc, L - b0);
-      {
-        SCV_PROF(c, s, "so3fwd_alpha");
-        SCV_TRY(scv_pfa_syn_alpha(c, K, real, c->opt_chunkt, sig, b0, nbb, (double2*)ch, s));
-      }
-      SCV_PROF(c, s, "so3fwd_gamma_q");
-      SCV_TRY(scv_pfa_syn_gamma_q(c, K, real, c->opt_chunkt, (const double2*)ch, b0, nbb, qtab, mbase, (double2*)w, s));
-    }
-    if (real) {
-      SCV_PROF(c, s, "so3fwd_mirror");
-      SCV_TRY(scv_wout_mirror(c, L, (double2*)w, s));
-    }
-    return SCV_OK;
-  }
+  const bool use_q = use_betaq(c, L);
+  if (use_q) return forward_q_slab(c, L, real, sig, 0, L, w, s);
   const long long cols = real ? (long long)L * L : 2LL * L * L - 1;
   void* W1p = nullptr;
   SCV_TRY(scv_scratch(c, 0, (size_t)(cols * L) * 16, &W1p));
@@ -272,7 +326,7 @@ extern "C" int scv_so3_forward_curvelet(scv_ctx* c, int L, int real, const void*
       const int nbb = std::min(nbc, L - b0);
       {
         SCV_PROF(c, s, "so3fwd_alpha");
-        SCV_TRY(scv_pfa_syn_alpha(c, K, real, 0, sig, b0, nbb, (double2*)ch, s));
+        SCV_TRY(scv_pfa_syn_alpha(c, K, real, 0, sig, L, b0, nbb, (double2*)ch, s));
       }
       SCV_PROF(c, s, "so3fwd_gamma");
       SCV_TRY(scv_pfa_syn_gamma(c, K, real, (const double2*)ch, b0, nbb, (double2*)W1p, s));

@@ -17,7 +17,16 @@ of ONE map over the ranks of a torch.distributed group:
              bit-identical to the single-GPU path.
 
 Scales are assigned greedily by cost (the (2L_j-1)^2 L_j sample volume),
-largest first to the least-loaded rank.  The per-rank compute goes through a
+largest first to the least-loaded rank.  Scale-only sharding stops scaling at
+2 GPUs at L=1024 (the two L_j=1024 scales hold 93% of the volume), so every
+scale the beta-slab kernels support (complex path, prime-factor K,
+128 <= L_j <= 1024) is instead split into `world` contiguous beta slabs, one
+per rank: analysis of a slab needs no communication (the closed-form
+generation is per beta row), and the synthesis partials of the slabs of a
+scale add up to its term (the beta quadrature is a sum over beta rows), so
+the same single reduce merges them.  For split scales the merge adds partial
+sums, so it is deterministic for a given world size but not bit-identical to
+the single-GPU summation order (agreement ~1e-14 relative).  The per-rank compute goes through a
 backend object; the default one is the CUDA path of this package.  (The
 CPU tests inject the oracle as backend to exercise the sharding logic on the
 gloo backend without a GPU.)
@@ -39,34 +48,67 @@ from .transform import scale_band_limit, scaling_band_limit
 __all__ = ["ScalePlan", "ShardedCoeffs", "CudaBackend", "analyze_sharded", "synthesize_sharded"]
 
 
+def cuda_splittable(Lj: int, real: bool) -> bool:
+    """Scales the beta-slab kernels support (include/scurve_b200.h)."""
+    K = 2 * Lj - 1
+    return (not real) and 128 <= Lj <= 1024 and (K & (K + 1)) == 0
+
+
 @dataclass
 class ScalePlan:
-    """owner[j - j_min] = rank that holds scale j."""
+    """owner[j - j_min] = rank that holds the whole scale j, or -1 when the
+    scale is split into beta slabs: slabs[j] = [(rank, b0, nb), ...]."""
 
     j_min: int
     owner: list
     cost: list
+    slabs: dict = field(default_factory=dict)
+    Ljs: list = field(default_factory=list)
 
     @classmethod
-    def build(cls, params, world: int, multires: bool = True) -> "ScalePlan":
+    def build(cls, params, world: int, multires: bool = True, real: bool = False,
+              splittable=cuda_splittable) -> "ScalePlan":
         js = list(range(params.j_min, params.j_max + 1))
         Ljs = [scale_band_limit(params, j) if multires else params.band_limit for j in js]
         cost = [(2 * L - 1) ** 2 * L for L in Ljs]
         load = [0] * world
         owner = [0] * len(js)
+        slabs = {}
+        for i, (j, L) in enumerate(zip(js, Ljs)):
+            if world > 1 and splittable is not None and splittable(L, real) and L >= world:
+                owner[i] = -1
+                cuts = [(L * r) // world for r in range(world + 1)]
+                slabs[j] = [(r, cuts[r], cuts[r + 1] - cuts[r]) for r in range(world)]
+                for r in range(world):
+                    load[r] += cost[i] * (cuts[r + 1] - cuts[r]) / L
         for i in sorted(range(len(js)), key=lambda i: (-cost[i], i)):
+            if owner[i] == -1:
+                continue
             r = min(range(world), key=lambda q: (load[q], q))
             owner[i] = r
             load[r] += cost[i]
-        return cls(params.j_min, owner, cost)
+        return cls(params.j_min, owner, cost, slabs, Ljs)
 
     def owned(self, rank: int) -> list:
+        """Whole scales held by `rank`."""
         return [self.j_min + i for i, r in enumerate(self.owner) if r == rank]
+
+    def slabs_of(self, rank: int) -> list:
+        """(j, b0, nb) beta slabs held by `rank`."""
+        return [(j, b0, nb) for j, parts in sorted(self.slabs.items()) for r, b0, nb in parts if r == rank]
+
+    def load(self, rank: int) -> float:
+        """Sample volume (cost units) assigned to `rank`."""
+        tot = sum(self.cost[j - self.j_min] for j in self.owned(rank))
+        for j, b0, nb in self.slabs_of(rank):
+            tot += self.cost[j - self.j_min] * nb / self.Ljs[j - self.j_min]
+        return tot
 
 
 @dataclass
 class ShardedCoeffs:
-    """Distributed CurveletCoeffs: `scales` holds only this rank's scales."""
+    """Distributed CurveletCoeffs: `scales` holds only this rank's scales
+    (an SO3Signal for a whole scale, an SO3Slab for a beta slab of a split one)."""
 
     params: object
     plan: ScalePlan
@@ -100,6 +142,30 @@ class CudaBackend:
         w = _scale_wigner(ctx, flm, device_tiling(t, dev), j, Lj)
         inv = so3_inverse_curvelet_real if real else so3_inverse_curvelet
         return inv(w, SO3Grid(Lj, Lj, Lj))
+
+    def scale_inverse_slab(self, flm_vals, t, j, Lj, b0, nb):
+        from . import _cabi
+        from .sphere import HarmonicCoeffs
+        from .transform import _scale_wigner, device_tiling
+        from .so3 import SO3Grid, so3_inverse_curvelet_slab
+        dev = flm_vals.device
+        ctx = _cabi.context(dev)
+        flm = HarmonicCoeffs(t.params.band_limit, t.params.spin, flm_vals)
+        w = _scale_wigner(ctx, flm, device_tiling(t, dev), j, Lj)
+        return so3_inverse_curvelet_slab(w, SO3Grid(Lj, Lj, Lj), b0, nb)
+
+    def scale_term_slab(self, slab, t, j):
+        from . import _cabi
+        from .so3 import so3_forward_curvelet_slab
+        from .transform import device_tiling
+        dev = slab.values.device
+        ctx = _cabi.context(dev)
+        L = t.params.band_limit
+        w = so3_forward_curvelet_slab(slab)
+        pos, neg = device_tiling(t, dev).psi[j]
+        term = torch.zeros(L * L, dtype=torch.complex128, device=dev)
+        ctx.call("accumulate", L, slab.grid.L, _cabi.ptr(w.values), _cabi.ptr(pos), _cabi.ptr(neg), _cabi.ptr(term))
+        return term
 
     def scaling_map(self, flm_vals, t, Ls, real):
         from . import _cabi
@@ -148,7 +214,7 @@ def _rank_world(group):
 
 
 def analyze_sharded(f, t, group=None, backend=None, src: int = 0, multires: bool = True,
-                    real: bool = False) -> ShardedCoeffs:
+                    real: bool = False, split: bool = True) -> ShardedCoeffs:
     """Analysis of one map with its scales sharded over the group.
 
     `f` is only read on `src`.  Mirrors transform.analyze (transform.py:139-152)."""
@@ -156,7 +222,10 @@ def analyze_sharded(f, t, group=None, backend=None, src: int = 0, multires: bool
     rank, world = _rank_world(group)
     p = t.params
     L = p.band_limit
-    plan = ScalePlan.build(p, world, multires)
+    kw = {} if split else {"splittable": None}
+    if split and hasattr(backend, "splittable"):
+        kw["splittable"] = backend.splittable
+    plan = ScalePlan.build(p, world, multires, real=real, **kw)
     if rank == src:
         flm = backend.sht_forward(f)
     else:
@@ -167,6 +236,8 @@ def analyze_sharded(f, t, group=None, backend=None, src: int = 0, multires: bool
     for j in plan.owned(rank):
         Lj = scale_band_limit(p, j) if multires else L
         out.scales[j] = backend.scale_inverse(flm, t, j, Lj, real)
+    for j, b0, nb in plan.slabs_of(rank):
+        out.scales[j] = backend.scale_inverse_slab(flm, t, j, plan.Ljs[j - p.j_min], b0, nb)
     if rank == src:
         Ls = scaling_band_limit(p) if multires else L
         out.scaling = backend.scaling_map(flm, t, Ls, real)
@@ -187,10 +258,12 @@ def synthesize_sharded(c: ShardedCoeffs, t, group=None, backend=None, dst: int =
                          and isinstance(backend, CudaBackend) else torch.device("cpu")))
     for j in c.plan.owned(rank):
         terms[j - p.j_min] = backend.scale_term(c.scales[j], t, j, c.real)
+    for j, _, _ in c.plan.slabs_of(rank):
+        terms[j - p.j_min] = backend.scale_term_slab(c.scales[j], t, j)
     if world > 1:
-        # every term row is owned by exactly one rank and zero elsewhere:
-        # sum-reducing the stack moves the rows without mixing arithmetic
-        # (x + 0 == x exactly), so the merge below stays bit-identical
+        # a whole-scale row is nonzero on exactly one rank: sum-reducing the
+        # stack moves it without mixing arithmetic (x + 0 == x exactly); the
+        # rows of split scales add the slab partials of every rank
         dist.reduce(terms, dst=dst, op=dist.ReduceOp.SUM, group=group)
     if rank != dst:
         return None

@@ -24,10 +24,13 @@ __all__ = [
     "CurveletWignerCoeffs",
     "SO3Grid",
     "SO3Signal",
+    "SO3Slab",
     "so3_forward_curvelet",
+    "so3_forward_curvelet_slab",
     "so3_forward_curvelet_real",
     "so3_inverse_curvelet",
     "so3_inverse_curvelet_real",
+    "so3_inverse_curvelet_slab",
 ]
 
 
@@ -167,4 +170,54 @@ def so3_forward_curvelet_real(f: SO3Signal, out: torch.Tensor | None = None) -> 
     if out is None:
         out = torch.empty((2, L, 2 * L - 1), dtype=torch.complex128, device=dev)
     _cabi.context(dev).call("so3_forward_curvelet", L, 1, _cabi.ptr(f.values), _cabi.ptr(out))
+    return CurveletWignerCoeffs(L, out)
+
+
+# ---------------------------------------------------------------------------
+# beta slabs (multi-GPU sharding of one scale)
+# ---------------------------------------------------------------------------
+@dataclass
+class SO3Slab:
+    """Beta rows [b0, b0 + nb) of an SO(3) signal on `grid`: values
+    (2N-1, nb, 2M-1) = the full signal's values[:, b0:b0+nb, :]."""
+
+    grid: SO3Grid
+    b0: int
+    values: torch.Tensor
+    real: bool = False
+
+    @property
+    def nb(self) -> int:
+        return int(self.values.shape[1])
+
+    def __post_init__(self):
+        K_g, _, K_a = self.grid.shape
+        if self.b0 < 0 or self.values.dim() != 3 or self.b0 + self.values.shape[1] > self.grid.L:
+            raise ValueError(f"slab rows [{self.b0}, {self.b0 + self.values.shape[1]}) outside [0, {self.grid.L})")
+        if (self.values.shape[0], self.values.shape[2]) != (K_g, K_a):
+            raise ValueError(f"slab shape {tuple(self.values.shape)} does not match grid {self.grid.shape}")
+
+
+def so3_inverse_curvelet_slab(w: CurveletWignerCoeffs, grid: SO3Grid, b0: int, nb: int,
+                              out: torch.Tensor | None = None) -> SO3Slab:
+    """Rows [b0, b0+nb) of so3_inverse_curvelet(w, grid) (complex path)."""
+    L = _check_sparse_grid(w, grid)
+    K = 2 * L - 1
+    dev = w.values.device
+    if out is None:
+        out = torch.empty((K, nb, K), dtype=torch.complex128, device=dev)
+    _cabi.context(dev).call("so3_inverse_curvelet_slab", L, _cabi.ptr(w.values), int(b0), int(nb), _cabi.ptr(out))
+    return SO3Slab(grid, int(b0), out)
+
+
+def so3_forward_curvelet_slab(f: SO3Slab, out: torch.Tensor | None = None, accumulate: bool = False) -> CurveletWignerCoeffs:
+    """The slab's partial sum of so3_forward_curvelet(_real): summed over all
+    slabs of a signal it equals the full forward transform (so3.py:203-243)."""
+    L = _check_forward(f)
+    dev = f.values.device
+    if out is None:
+        out = torch.zeros((2, L, 2 * L - 1), dtype=torch.complex128, device=dev)
+        accumulate = False
+    _cabi.context(dev).call("so3_forward_curvelet_slab", L, 1 if f.real else 0, _cabi.ptr(f.values), int(f.b0),
+                            f.nb, _cabi.ptr(out), 1 if accumulate else 0)
     return CurveletWignerCoeffs(L, out)

@@ -2,9 +2,11 @@
 
 The sharding driver (paper_1511_05578_b200/dist.py) is exercised with the
 CPU oracle injected as the per-rank compute backend, so the collective
-logic (broadcast of f_lm, per-scale ownership, deterministic merge of the
-per-scale synthesis terms) is checked without a GPU.  The sharded result
-must equal the single-process oracle exactly.
+logic (broadcast of f_lm, per-scale ownership, beta-slab splitting of the
+large scales, deterministic merge of the per-scale synthesis terms) is
+checked without a GPU.  Whole scales must equal the single-process oracle
+exactly; slabs are exact slices of it; the merged map, which adds slab
+partial sums, agrees to rounding.
 """
 
 import math
@@ -26,8 +28,10 @@ from paper_1511_05578_b200.dist import ScalePlan, analyze_sharded, synthesize_sh
 class OracleBackend:
     """CPU restatement standing in for the CUDA path (test only)."""
 
-    def __init__(self, L, spin):
+    def __init__(self, L, spin, split_min=None):
         self.L, self.spin = L, spin
+        if split_min is not None:
+            self.splittable = lambda Lj, real: (not real) and Lj >= split_min
 
     def sht_forward(self, f):
         return torch.from_numpy(orc.sht_forward(f, self.L, self.spin))
@@ -40,6 +44,20 @@ class OracleBackend:
         w = orc.scale_wigner(flm.numpy(), pos, neg, Lj)
         vals = orc.so3_inverse_curvelet(w)
         return types.SimpleNamespace(values=torch.from_numpy(vals), grid=types.SimpleNamespace(L=Lj))
+
+    def scale_inverse_slab(self, flm, t, j, Lj, b0, nb):
+        full = self.scale_inverse(flm, t, j, Lj, False)
+        return types.SimpleNamespace(values=full.values[:, b0:b0 + nb, :].clone(), b0=b0,
+                                     grid=types.SimpleNamespace(L=Lj))
+
+    def scale_term_slab(self, slab, t, j):
+        # the forward transform is linear in the signal and its beta sum runs
+        # over rows: the slab's partial is the transform of the zero-padded slab
+        Lj = slab.grid.L
+        K = 2 * Lj - 1
+        full = torch.zeros((K, Lj, K), dtype=torch.complex128)
+        full[:, slab.b0:slab.b0 + slab.values.shape[1], :] = slab.values
+        return self.scale_term(types.SimpleNamespace(values=full), t, j, False)
 
     def scaling_map(self, flm, t, Ls, real):
         return orc.sht_inverse(orc.scaling_coeffs(flm.numpy(), t.scaling, Ls), Ls, 0)
@@ -78,28 +96,28 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, L, spin, q):
+def _worker(rank, world, port, L, spin, q, split_min=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         t = T.build_tiling(T.TilingParams(L, spin, 2.0, 1))
-        be = OracleBackend(L, spin)
+        be = OracleBackend(L, spin, split_min)
         f = orc.sht_inverse(orc.gaussian_flm(L, spin, seed=3, real=False), L, spin)
         c = analyze_sharded(f if rank == 0 else None, t, backend=be)
         g = synthesize_sharded(c, t, backend=be)
-        q.put((rank, {j: s.values.numpy() for j, s in c.scales.items()},
+        q.put((rank, {j: (getattr(s, "b0", None), s.values.numpy()) for j, s in c.scales.items()},
                None if g is None else np.asarray(g)))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("L,spin", [(16, 0), (16, 2)])
-def test_sharded_matches_single_process(L, spin):
+@pytest.mark.parametrize("L,spin,split_min", [(16, 0, None), (16, 2, None), (16, 0, 8), (16, 2, 4)])
+def test_sharded_matches_single_process(L, spin, split_min):
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, L, spin, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, L, spin, q, split_min)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
@@ -111,23 +129,42 @@ def test_sharded_matches_single_process(L, spin):
     f = orc.sht_inverse(orc.gaussian_flm(L, spin, seed=3, real=False), L, spin)
     smap, scales = orc.analyze(f, L, spin, 2.0, 1, t.params.j_max, psi, t.scaling)
     gref = orc.synthesize(smap, scales, L, spin, 2.0, 1, t.params.j_max, psi, t.scaling)
-    seen = set()
+    seen = {}
     for rank, sc, g in res:
-        for j, v in sc.items():
-            np.testing.assert_array_equal(v, scales[j - t.params.j_min])
-            seen.add(j)
+        for j, (b0, v) in sc.items():
+            ref = scales[j - t.params.j_min]
+            if b0 is None:
+                np.testing.assert_array_equal(v, ref)
+                seen[j] = ref.shape[1]
+            else:
+                np.testing.assert_array_equal(v, ref[:, b0:b0 + v.shape[1], :])
+                seen[j] = seen.get(j, 0) + v.shape[1]
         if rank == 0:
-            np.testing.assert_array_equal(g, gref)
+            if split_min is None:
+                np.testing.assert_array_equal(g, gref)
+            else:
+                assert np.abs(g - gref).max() <= 1e-12 * np.abs(gref).max()
         else:
             assert g is None
-    assert seen == set(range(t.params.j_min, t.params.j_max + 1))
+    # every scale is covered once: whole, or by slabs that partition its beta rows
+    assert seen == {j: scales[j - t.params.j_min].shape[1] for j in range(t.params.j_min, t.params.j_max + 1)}
 
 
 def test_scale_plan_balances_cost():
     p = T.TilingParams(1024, 0, 2.0, 3)
     for world in (1, 2, 4, 8):
-        plan = ScalePlan.build(p, world)
+        # scale-only sharding
+        plan = ScalePlan.build(p, world, splittable=None)
         owned = [plan.owned(r) for r in range(world)]
         assert sorted(j for o in owned for j in o) == list(range(3, 11))
         if world == 2:  # the two L_j = 1024 scales land on different ranks
             assert plan.owner[-1] != plan.owner[-2]
+        # beta-slab splitting of the L_j >= 128 scales: balanced to 1%
+        plan = ScalePlan.build(p, world)
+        loads = [plan.load(r) for r in range(world)]
+        assert max(loads) <= 1.01 * sum(loads) / world
+        for j, parts in plan.slabs.items():
+            rows = sorted((b0, nb) for _, b0, nb in parts)
+            assert rows[0][0] == 0 and sum(nb for _, nb in rows) == plan.Ljs[j - 3]
+        # the real path keeps whole scales
+        assert not ScalePlan.build(p, world, real=True).slabs

@@ -300,3 +300,57 @@ def test_sharded_driver_cuda_world1():
         assert torch.equal(sig.values, c1.scale(j).values)
     g2 = synthesize_sharded(c2, t)
     assert torch.equal(g2.values, g1.values)
+
+
+@pytest.mark.parametrize("L,real", [(128, False), (256, False), (256, True)])
+def test_beta_slabs_partition_the_transform(L, real):
+    """Beta slabs (the multi-GPU shards of one scale): the slab inverse is the
+    slab's rows of the full inverse, and the slab forward partials sum to the
+    full forward transform (so3.py:203-285)."""
+    w = _random_cw(L, 21 + L)
+    if real:
+        w = _real_symmetric(w)
+    cw = sc.CurveletWignerCoeffs(L, w)
+    grid = sc.SO3Grid(L, L, L)
+    full = sc.so3_inverse_curvelet(cw, grid)
+    cuts = [0, 1, L // 3, L // 2 + 5, L]
+    acc = None
+    for b0, b1 in zip(cuts[:-1], cuts[1:]):
+        slab = sc.so3_inverse_curvelet_slab(cw, grid, b0, b1 - b0)
+        assert orc.rel_err(host(slab.values), host(full.values[:, b0:b1, :])) <= 1e-13
+        if real:
+            slab = sc.SO3Slab(grid, b0, full.values[:, b0:b1, :].real.contiguous(), real=True)
+        part = sc.so3_forward_curvelet_slab(slab, out=acc, accumulate=acc is not None)
+        acc = part.values
+    ref = (sc.so3_forward_curvelet_real(sc.SO3Signal(grid, full.values.real.contiguous(), real=True))
+           if real else sc.so3_forward_curvelet(full))
+    assert orc.rel_err(host(acc), host(ref.values)) <= 1e-12
+    assert orc.rel_err(host(acc), w) <= TOL_RT
+    with pytest.raises(ValueError):
+        sc.so3_inverse_curvelet_slab(cw, grid, L - 2, 3)
+
+
+@pytest.mark.parametrize("L", [256, 512])
+def test_analysis_orders_and_chunk_layouts_agree(L):
+    """Both analysis orders (gamma-first column generation vs alpha rows first)
+    and both synthesis chunk layouts compute the same transforms."""
+    from paper_1511_05578_b200 import _cabi
+    ctx = _cabi.context(0)
+    w = _random_cw(L, 5 + L)
+    cw = sc.CurveletWignerCoeffs(L, w)
+    grid = sc.SO3Grid(L, L, L)
+    try:
+        ctx.set_option("colgen", 1)
+        a = sc.so3_inverse_curvelet(cw, grid)
+        ctx.set_option("colgen", 0)
+        b = sc.so3_inverse_curvelet(cw, grid)
+        assert orc.rel_err(host(a.values), host(b.values)) <= 1e-13
+        ctx.set_option("chunkt", 1)
+        fa = host(sc.so3_forward_curvelet(a).values)
+        ctx.set_option("chunkt", 0)
+        fb = host(sc.so3_forward_curvelet(a).values)
+    finally:
+        ctx.set_option("colgen", -1)
+        ctx.set_option("chunkt", -1)
+    assert orc.rel_err(fa, fb) <= 1e-13
+    assert orc.rel_err(fb, w) <= TOL_RT

@@ -294,7 +294,7 @@ template <int K> struct PfaGCfg { static constexpr int R = 8, NT = 128, MINB = 2
 template <> struct PfaGCfg<255> { static constexpr int R = 8, NT = 256, MINB = 1; };
 template <> struct PfaGCfg<511> { static constexpr int R = 4, NT = 256, MINB = 1; };
 #ifndef SCV_GEN1023
-#define SCV_GEN1023 4, 352, 1
+#define SCV_GEN1023 4, 256, 1
 #endif
 #ifndef SCV_GEN2047
 #define SCV_GEN2047 4, 384, 1
@@ -308,6 +308,9 @@ SCV_GCFG_(1023, SCV_GEN1023)
 SCV_GCFG_(2047, SCV_GEN2047)
 template <> struct PfaGCfg<4095> { static constexpr int R = 2, NT = 320, MINB = 1; };
 
+#ifndef SCV_COLGEN_GU
+#define SCV_COLGEN_GU 4
+#endif
 template <int K>
 static constexpr size_t pfa_smem_g() {
   using PL = PfaPlan<K>;
@@ -337,31 +340,51 @@ __global__ void __launch_bounds__(PfaGCfg<K>::NT, PfaGCfg<K>::MINB)
     const int b = b0 + bs;
     const int m0 = (task - bs * NGRP) * R;
     const double ls = lsin[b], lc = lcos[b];
-#pragma unroll 2
-    for (int i = threadIdx.x; i < R * K; i += NT) {
-      const int r = i / K, gi = i - r * K;
-      const int mi = m0 + r;
-      double2 v = make_double2(0.0, 0.0);
-      const int m = mi <= L - 1 ? mi : mi - K;
-      const int n = gi <= L - 1 ? gi : gi - K;
-      const int l = n < 0 ? -n : n, am = m < 0 ? -m : m;
-      if (mi < K && am <= l) {
-        const int es = n >= 0 ? l - m : l + m;  // power of sin(b/2)
-        const int ec = n >= 0 ? l + m : l - m;  // power of cos(b/2)
-        double lg = hlb[l * (l + 1) / 2 + am];
-        if (es) lg += (double)es * ls;
-        if (ec) lg += (double)ec * lc;
-#if SCV_EXP_COLGEN_NOEXP
-        double d = lg;  // timing experiment only
-#else
-        double d = exp(lg);
-#endif
-        if (n < 0 && ((l - m) & 1)) d = -d;
-        const double2 cw = w[((n >= 0 ? 0 : 1) * L + l) * K + (L - 1) + m];
-        const double f = (double)(2 * l + 1) * fac0 * d;
-        v = make_double2(f * cw.x, f * cw.y);
+    // generation in batches of GU elements per thread: all coefficient
+    // gathers of a batch are issued before any is used (latency overlap)
+    constexpr int NPT = (R * K + NT - 1) / NT, GU = SCV_COLGEN_GU;
+#pragma unroll 1
+    for (int i0 = 0; i0 < NPT; i0 += GU) {
+      double hv[GU];
+      double2 cv[GU];
+#pragma unroll
+      for (int u = 0; u < GU; ++u) {
+        const int i = threadIdx.x + (i0 + u) * NT;
+        const int r = i / K, gi = i - r * K;
+        const int mi = m0 + r;
+        const int m = mi <= L - 1 ? mi : mi - K;
+        const int n = gi <= L - 1 ? gi : gi - K;
+        const int l = n < 0 ? -n : n, am = m < 0 ? -m : m;
+        hv[u] = 0.0;
+        cv[u] = make_double2(0.0, 0.0);
+        if (i0 + u < NPT && i < R * K && mi < K && am <= l) {
+          hv[u] = hlb[l * (l + 1) / 2 + am];
+          cv[u] = w[((n >= 0 ? 0 : 1) * L + l) * K + (L - 1) + m];
+        }
       }
-      X[r * K + pfa_in_tab<PL>(tab, gi)] = v;
+#pragma unroll
+      for (int u = 0; u < GU; ++u) {
+        const int i = threadIdx.x + (i0 + u) * NT;
+        if (i0 + u >= NPT || i >= R * K) continue;
+        const int r = i / K, gi = i - r * K;
+        const int mi = m0 + r;
+        const int m = mi <= L - 1 ? mi : mi - K;
+        const int n = gi <= L - 1 ? gi : gi - K;
+        const int l = n < 0 ? -n : n, am = m < 0 ? -m : m;
+        double2 v = make_double2(0.0, 0.0);
+        if (mi < K && am <= l) {
+          const int es = n >= 0 ? l - m : l + m;  // power of sin(b/2)
+          const int ec = n >= 0 ? l + m : l - m;  // power of cos(b/2)
+          double lg = hv[u];
+          if (es) lg += (double)es * ls;
+          if (ec) lg += (double)ec * lc;
+          double d = exp(lg);
+          if (n < 0 && ((l - m) & 1)) d = -d;
+          const double f = (double)(2 * l + 1) * fac0 * d;
+          v = make_double2(f * cv[u].x, f * cv[u].y);
+        }
+        X[r * K + pfa_in_tab<PL>(tab, gi)] = v;
+      }
     }
     __syncthreads();
     pfa_dft<PL, +1, R, NT, K>(X, tab, scr);
@@ -674,7 +697,7 @@ __global__ void __launch_bounds__(PfaCfg<K, true>::NT, PfaCfg<K, true>::MINB)
 template <int K> struct PfaQCfg { static constexpr int RQ = 1, NT = 256, MINB = 1; };
 template <> struct PfaQCfg<255> { static constexpr int RQ = 1, NT = 128, MINB = 1; };
 #ifndef SCV_Q1023
-#define SCV_Q1023 2, 352, 1
+#define SCV_Q1023 1, 352, 1
 #endif
 #ifndef SCV_Q2047
 #define SCV_Q2047 1, 192, 2
@@ -750,32 +773,49 @@ __global__ void __launch_bounds__(PfaQCfg<K>::NT, PfaQCfg<K>::MINB)
 #pragma unroll
         for (int u = 0; u < NA; ++u) acc[r][u] = make_double2(0.0, 0.0);
     }
-    pfa_dft<PL, -1, RQ, NT, K>(X, tab, scr);
     const long long b = b0 + bb;
+    // quadrature weights of this task's (n, m) entries, loaded before the
+    // transform so their latency hides behind it
+    double qv[RQ][NA];
+#pragma unroll
+    for (int r = 0; r < RQ; ++r) {
+      const int col = col0 + r;
+      const int m = col <= L - 1 ? col : col - K;
+      const int am = m < 0 ? -m : m;
+      const double* qp = qtab + mbase[min(m + L - 1, K - 1)] + b * (L - am) - am;   // + n       (n >= 0)
+      const double* qn = qtab + mbase[max(-m + L - 1, 0)] + b * (L - am) - am;      // + |n|     (n < 0)
+#pragma unroll
+      for (int u = 0; u < NA; ++u) {
+        const int gn = threadIdx.x + u * NT;
+        const int n = gn <= L - 1 ? gn : gn - K;
+        const int an = n < 0 ? -n : n;
+        qv[r][u] = 0.0;
+        if (col >= K || gn >= K || an < am || (real && n < 0)) continue;
+        if (n >= 0) {
+          qv[r][u] = __ldg(qp + n);
+        } else {
+          const double q = __ldg(qn + an);  // q_{-l,m} = (-1)^{l+m} q_{l,-m}
+          qv[r][u] = ((an + m) & 1) ? -q : q;
+        }
+      }
+    }
+    pfa_dft<PL, -1, RQ, NT, K>(X, tab, scr);
 #pragma unroll
     for (int r = 0; r < RQ; ++r) {
       const int col = col0 + r;
       if (col >= K) continue;
       const int m = col <= L - 1 ? col : col - K;
       const int am = m < 0 ? -m : m;
-      const double* qp = qtab + mbase[m + L - 1] + b * (L - am) - am;   // + n       (n >= 0)
-      const double* qn = qtab + mbase[-m + L - 1] + b * (L - am) - am;  // + |n|     (n < 0)
 #pragma unroll
       for (int u = 0; u < NA; ++u) {
         const int gn = threadIdx.x + u * NT;
         const int n = gn <= L - 1 ? gn : gn - K;
         const int an = n < 0 ? -n : n;
         if (gn >= K || an < am || (real && n < 0)) continue;
-        double qv;
-        if (n >= 0) {
-          qv = __ldg(qp + n);
-        } else {
-          qv = __ldg(qn + an);  // q_{-l,m} = (-1)^{l+m} q_{l,-m}
-          if ((an + m) & 1) qv = -qv;
-        }
+        const double q = qv[r][u];
         const double2 v = X[r * K + pfa_pos_tab<PL>(tab, gn)];
-        acc[r][u].x = fma(v.x, qv, acc[r][u].x);
-        acc[r][u].y = fma(v.y, qv, acc[r][u].y);
+        acc[r][u].x = fma(v.x, q, acc[r][u].x);
+        acc[r][u].y = fma(v.y, q, acc[r][u].y);
       }
       if (bb == nbb - 1) {
 #pragma unroll

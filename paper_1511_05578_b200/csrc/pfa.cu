@@ -309,7 +309,7 @@ SCV_GCFG_(2047, SCV_GEN2047)
 template <> struct PfaGCfg<4095> { static constexpr int R = 2, NT = 320, MINB = 1; };
 
 #ifndef SCV_COLGEN_GU
-#define SCV_COLGEN_GU 4
+#define SCV_COLGEN_GU 1
 #endif
 template <int K>
 static constexpr size_t pfa_smem_g() {
@@ -340,50 +340,58 @@ __global__ void __launch_bounds__(PfaGCfg<K>::NT, PfaGCfg<K>::MINB)
     const int b = b0 + bs;
     const int m0 = (task - bs * NGRP) * R;
     const double ls = lsin[b], lc = lcos[b];
-    // generation in batches of GU elements per thread: all coefficient
-    // gathers of a batch are issued before any is used (latency overlap)
-    constexpr int NPT = (R * K + NT - 1) / NT, GU = SCV_COLGEN_GU;
+    // generation: a thread owns one gamma frequency n (row gi of the R
+    // columns), so the n-dependent index math is shared by the R columns and
+    // the coefficient reads of consecutive m are contiguous (hlb row l,
+    // w row (sheet, l)); batches of GU rows issue all gathers before use
+    constexpr int NPT = (K + NT - 1) / NT, GU = K >= 2047 ? SCV_COLGEN_GU : 1;
 #pragma unroll 1
     for (int i0 = 0; i0 < NPT; i0 += GU) {
-      double hv[GU];
-      double2 cv[GU];
+      double hv[GU][R];
+      double2 cv[GU][R];
 #pragma unroll
       for (int u = 0; u < GU; ++u) {
-        const int i = threadIdx.x + (i0 + u) * NT;
-        const int r = i / K, gi = i - r * K;
-        const int mi = m0 + r;
-        const int m = mi <= L - 1 ? mi : mi - K;
+        const int gi = threadIdx.x + (i0 + u) * NT;
         const int n = gi <= L - 1 ? gi : gi - K;
-        const int l = n < 0 ? -n : n, am = m < 0 ? -m : m;
-        hv[u] = 0.0;
-        cv[u] = make_double2(0.0, 0.0);
-        if (i0 + u < NPT && i < R * K && mi < K && am <= l) {
-          hv[u] = hlb[l * (l + 1) / 2 + am];
-          cv[u] = w[((n >= 0 ? 0 : 1) * L + l) * K + (L - 1) + m];
+        const int l = n < 0 ? -n : n;
+        const double* hrow = hlb + l * (l + 1) / 2;
+        const double2* wrow = w + ((n >= 0 ? 0 : 1) * L + l) * K + (L - 1);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int m = m0 + r <= L - 1 ? m0 + r : m0 + r - K, am = m < 0 ? -m : m;
+          hv[u][r] = 0.0;
+          cv[u][r] = make_double2(0.0, 0.0);
+          if (i0 + u < NPT && gi < K && m0 + r < K && am <= l) {
+            hv[u][r] = hrow[am];
+            cv[u][r] = wrow[m];
+          }
         }
       }
 #pragma unroll
       for (int u = 0; u < GU; ++u) {
-        const int i = threadIdx.x + (i0 + u) * NT;
-        if (i0 + u >= NPT || i >= R * K) continue;
-        const int r = i / K, gi = i - r * K;
-        const int mi = m0 + r;
-        const int m = mi <= L - 1 ? mi : mi - K;
+        const int gi = threadIdx.x + (i0 + u) * NT;
+        if (i0 + u >= NPT || gi >= K) continue;
         const int n = gi <= L - 1 ? gi : gi - K;
-        const int l = n < 0 ? -n : n, am = m < 0 ? -m : m;
-        double2 v = make_double2(0.0, 0.0);
-        if (mi < K && am <= l) {
-          const int es = n >= 0 ? l - m : l + m;  // power of sin(b/2)
-          const int ec = n >= 0 ? l + m : l - m;  // power of cos(b/2)
-          double lg = hv[u];
-          if (es) lg += (double)es * ls;
-          if (ec) lg += (double)ec * lc;
-          double d = exp(lg);
-          if (n < 0 && ((l - m) & 1)) d = -d;
-          const double f = (double)(2 * l + 1) * fac0 * d;
-          v = make_double2(f * cv[u].x, f * cv[u].y);
+        const int l = n < 0 ? -n : n;
+        const double facl = (double)(2 * l + 1) * fac0;
+        const int xi = pfa_in_tab<PL>(tab, gi);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int m = m0 + r <= L - 1 ? m0 + r : m0 + r - K, am = m < 0 ? -m : m;
+          double2 v = make_double2(0.0, 0.0);
+          if (m0 + r < K && am <= l) {
+            const int es = n >= 0 ? l - m : l + m;  // power of sin(b/2)
+            const int ec = n >= 0 ? l + m : l - m;  // power of cos(b/2)
+            double lg = hv[u][r];
+            if (es) lg += (double)es * ls;
+            if (ec) lg += (double)ec * lc;
+            double d = exp(lg);
+            if (n < 0 && ((l - m) & 1)) d = -d;
+            const double f = facl * d;
+            v = make_double2(f * cv[u][r].x, f * cv[u][r].y);
+          }
+          X[r * K + xi] = v;
         }
-        X[r * K + pfa_in_tab<PL>(tab, gi)] = v;
       }
     }
     __syncthreads();

@@ -140,6 +140,15 @@ SCV_PFA_CFG_(1023, false, SCV_ROW1023)  SCV_PFA_CFG_(1023, true, SCV_COL1023)
 SCV_PFA_CFG_(2047, false, SCV_ROW2047)  SCV_PFA_CFG_(2047, true, SCV_COL2047)
 SCV_PFA_CFG(4095, false, 1, 320, 1)  SCV_PFA_CFG(4095, true, 1, 320, 1)
 
+// Row batches in shared memory: 2 = the next batch streams in (cp.async)
+// while the current one computes, 1 = single buffer (other resident CTAs
+// cover the load latency).
+template <int K, bool COL> struct PfaNBuf { static constexpr int v = 2; };
+#ifndef SCV_ROW2047_NBUF
+#define SCV_ROW2047_NBUF 2
+#endif
+template <> struct PfaNBuf<2047, false> { static constexpr int v = SCV_ROW2047_NBUF; };
+
 // Rows per transform call: R when the launch shape fits in shared memory,
 // else 1 (the R adjacent columns of a batch still move as R*16-byte segments,
 // but are transformed one call at a time, bounding the DMMA scratch).
@@ -148,8 +157,8 @@ constexpr size_t pfa_smem_rd() {
   static_assert(PfaCfg<K, COL>::NT % PfaCfg<K, COL>::R == 0, "column kernels map R | NT");
   using PL = PfaPlan<K>;
   constexpr int R = PfaCfg<K, COL>::R;
-  return ((size_t)2 * R * K + pfa_tab_total<PL>() + pfa_scratch<PL, RD, PfaCfg<K, COL>::NT>()) * sizeof(double2) +
-         R * sizeof(int4);
+  return ((size_t)PfaNBuf<K, COL>::v * R * K + pfa_tab_total<PL>() + pfa_scratch<PL, RD, PfaCfg<K, COL>::NT>()) *
+             sizeof(double2) + R * sizeof(int4);
 }
 template <int K, bool COL> struct PfaRD {
   static constexpr int v = pfa_smem_rd<K, COL, PfaCfg<K, COL>::R>() <= 232448 ? PfaCfg<K, COL>::R : 1;
@@ -192,15 +201,21 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
     }
     cp_async_commit();
   };
+  constexpr int NBUF = PfaNBuf<K, false>::v;
   long long bt = blockIdx.x;
   int cur = 0;
-  if (bt < nb) issue(bt, buf0);
+  if (NBUF == 2 && bt < nb) issue(bt, buf0);
 #pragma unroll 1
   for (; bt < nb; bt += gridDim.x) {
-    const long long nx = bt + gridDim.x;
-    if (nx < nb) issue(nx, buf0 + (cur ^ 1) * (R * K));
-    else cp_async_commit();
-    cp_async_wait<1>();
+    if constexpr (NBUF == 2) {
+      const long long nx = bt + gridDim.x;
+      if (nx < nb) issue(nx, buf0 + (cur ^ 1) * (R * K));
+      else cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      issue(bt, buf0);
+      cp_async_wait<0>();
+    }
     __syncthreads();
     double2* X = buf0 + cur * (R * K);
     pfa_dft_rows<PL, DIR, R, PfaRD<K, false>::v, NT>(X, tab, scr);
@@ -211,7 +226,7 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
       if (r0 + r < nrows) out[(r0 + r) * K + k] = X[r * K + pfa_pos_tab<PL>(tab, k)];
     }
     __syncthreads();
-    cur ^= 1;
+    if (NBUF == 2) cur ^= 1;
   }
 }
 
@@ -230,7 +245,7 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
   double2* tab = sm;
   double2* const scr = sm + pfa_tab_total<PL>();
   double2* X = scr + pfa_scratch<PL, PfaRD<K, false>::v, NT>();
-  int4* rp = (int4*)(X + 2 * R * K);  // per-row (gi, b, n, l)
+  int4* rp = (int4*)(X + PfaNBuf<K, false>::v * R * K);  // per-row (gi, b, n, l)
   pfa_load_tables<PL, NT>(tab, gtab);
   const long long nrows = (long long)(real ? L : K) * L;
   const long long nb = (nrows + R - 1) / R;
@@ -537,18 +552,22 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
     }
     cp_async_commit();
   };
+  constexpr int NBUF = PfaNBuf<K, false>::v;
   long long bt = blockIdx.x;
   int cur = 0;
-  if (!real && bt < nb) issue(bt, buf0);
+  if (NBUF == 2 && !real && bt < nb) issue(bt, buf0);
 #pragma unroll 1
   for (; bt < nb; bt += gridDim.x) {
     const long long r0 = bt * rpb;
     double2* X = buf0 + cur * (R * K);
-    if (!real) {
+    if (!real && NBUF == 2) {
       const long long nx = bt + gridDim.x;
       if (nx < nb) issue(nx, buf0 + (cur ^ 1) * (R * K));
       else cp_async_commit();
       cp_async_wait<1>();
+    } else if (!real) {
+      issue(bt, buf0);
+      cp_async_wait<0>();
     } else {
       const double* Fr = (const double*)in;
 #pragma unroll 4
@@ -621,7 +640,7 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
       }
     }
     __syncthreads();
-    if (!real) cur ^= 1;
+    if (!real && NBUF == 2) cur ^= 1;
   }
 }
 

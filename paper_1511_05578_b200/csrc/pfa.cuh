@@ -61,7 +61,10 @@ __host__ __device__ constexpr int pfa_gp(int p) { return p > 1 ? ((pfa_h(p) + pf
 // pfa_stage_mma): their table is the pair of dense real matrices
 // C[k][j] = cos(2 pi jk/p), S[k][j] = sin(2 pi jk/p), k = 0..M-1 (row 0 = the
 // all-ones / all-zero row that produces y_0), j = 1..Kp, zero padded.
-__host__ __device__ constexpr bool pfa_use_mma(int p) { return p >= 17; }
+#ifndef SCV_MMA_MIN_RADIX
+#define SCV_MMA_MIN_RADIX 17
+#endif
+__host__ __device__ constexpr bool pfa_use_mma(int p) { return p >= SCV_MMA_MIN_RADIX; }
 // DMMA stage variant: 1 = warp-owned butterfly blocks (pfa_stage_mma_blk, no
 // scratch), 0 = register-held 16x16 tiles / scratch-staged B (A/B builds)
 #ifndef SCV_PFA_BLK

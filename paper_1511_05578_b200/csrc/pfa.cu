@@ -751,6 +751,13 @@ static constexpr size_t pfa_smem_q() {
           2 * (size_t)PfaQCfg<K>::RQ * K) * sizeof(double2);
 }
 
+// offset of the m block of the quadrature table (betaq.cu): L * sum_{j=-(L-1)}^{m-1} (L - |j|)
+__device__ __forceinline__ long long q_mbase(int m, int L) {
+  const long long a = (long long)m + L - 1;  // number of terms
+  if (m <= 0) return (long long)L * (a * (a + 1) / 2);
+  return (long long)L * ((long long)L * (L + 1) / 2 + (long long)(m - 1) * L - (long long)m * (m - 1) / 2);
+}
+
 template <int K>
 __global__ void __launch_bounds__(PfaQCfg<K>::NT, PfaQCfg<K>::MINB)
     k_syn_gamma_q(int real, int tr, const double2* __restrict__ chunk, int b0, int nbb, const double* __restrict__ qtab,
@@ -816,8 +823,9 @@ __global__ void __launch_bounds__(PfaQCfg<K>::NT, PfaQCfg<K>::MINB)
       const int col = col0 + r;
       const int m = col <= L - 1 ? col : col - K;
       const int am = m < 0 ? -m : m;
-      const double* qp = qtab + mbase[min(m + L - 1, K - 1)] + b * (L - am) - am;   // + n       (n >= 0)
-      const double* qn = qtab + mbase[max(-m + L - 1, 0)] + b * (L - am) - am;      // + |n|     (n < 0)
+      // table offsets in closed form (no dependent gather): mbase(m) = L * sum_{j<m} (L-|j|)
+      const double* qp = qtab + q_mbase(min(m, L - 1), L) + b * (L - am) - am;    // + n       (n >= 0)
+      const double* qn = qtab + q_mbase(max(-m, -(L - 1)), L) + b * (L - am) - am;  // + |n|     (n < 0)
 #pragma unroll
       for (int u = 0; u < NA; ++u) {
         const int gn = threadIdx.x + u * NT;
@@ -825,12 +833,8 @@ __global__ void __launch_bounds__(PfaQCfg<K>::NT, PfaQCfg<K>::MINB)
         const int an = n < 0 ? -n : n;
         qv[r][u] = 0.0;
         if (col >= K || gn >= K || an < am || (real && n < 0)) continue;
-        if (n >= 0) {
-          qv[r][u] = __ldg(qp + n);
-        } else {
-          const double q = __ldg(qn + an);  // q_{-l,m} = (-1)^{l+m} q_{l,-m}
-          qv[r][u] = ((an + m) & 1) ? -q : q;
-        }
+        // raw load only; the sign q_{-l,m} = (-1)^{l+m} q_{l,-m} is applied at use
+        qv[r][u] = __ldg(n >= 0 ? qp + n : qn + an);
       }
     }
     pfa_dft<PL, -1, RQ, NT, K>(X, tab, scr);
@@ -846,7 +850,7 @@ __global__ void __launch_bounds__(PfaQCfg<K>::NT, PfaQCfg<K>::MINB)
         const int n = gn <= L - 1 ? gn : gn - K;
         const int an = n < 0 ? -n : n;
         if (gn >= K || an < am || (real && n < 0)) continue;
-        const double q = qv[r][u];
+        const double q = (n < 0 && ((an + m) & 1)) ? -qv[r][u] : qv[r][u];
         const double2 v = X[r * K + pfa_pos_tab<PL>(tab, gn)];
         acc[r][u].x = fma(v.x, q, acc[r][u].x);
         acc[r][u].y = fma(v.y, q, acc[r][u].y);

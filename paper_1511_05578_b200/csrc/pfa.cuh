@@ -142,14 +142,43 @@ __host__ __device__ constexpr int pfa_scratch() {
 // incrementally (integer pipe) and reads each pair as a warp-broadcast
 // 16-byte load.
 // position of output k, from the shared table (one 2-byte load)
+// (computed: sum_s (k mod p_s) st_s, constant divisors -> multiply-shift;
+// SCV_PFA_POSTAB=1 reads the 16-bit table in shared memory instead)
+#ifndef SCV_PFA_POSTAB
+#define SCV_PFA_POSTAB 1
+#endif
 template <class PL>
 __device__ __forceinline__ int pfa_pos_tab(const double2* tab, int k) {
-  return ((const unsigned short*)(tab + pfa_rtab_total<PL>()))[k];
+  if constexpr (SCV_PFA_POSTAB) {
+    return ((const unsigned short*)(tab + pfa_rtab_total<PL>()))[k];
+  } else {
+    int a = (k % PL::P0) * pfa_st<PL, 0>();
+    if constexpr (PL::D > 1) a += (k % PL::P1) * pfa_st<PL, 1>();
+    if constexpr (PL::D > 2) a += (k % PL::P2) * pfa_st<PL, 2>();
+    if constexpr (PL::D > 3) a += (k % PL::P3) * pfa_st<PL, 3>();
+    return a;
+  }
+}
+// (K/p)^{-1} mod p
+__host__ __device__ constexpr int pfa_inv(int K, int p) {
+  int r = (K / p) % p, v = 1;
+  while (p > 1 && (r * v) % p != 1) ++v;
+  return v;
 }
 // position of input sample n (Ruritanian map), from the shared table
 template <class PL>
 __device__ __forceinline__ int pfa_in_tab(const double2* tab, int n) {
-  return ((const unsigned short*)(tab + pfa_rtab_total<PL>()))[PL::K + n];
+  if constexpr (SCV_PFA_POSTAB) {
+    return ((const unsigned short*)(tab + pfa_rtab_total<PL>()))[PL::K + n];
+  } else {
+    constexpr int i0 = pfa_inv(PL::K, PL::P0), i1 = pfa_inv(PL::K, PL::P1);
+    constexpr int i2 = pfa_inv(PL::K, PL::P2), i3 = pfa_inv(PL::K, PL::P3);
+    int a = ((n * i0) % PL::P0) * pfa_st<PL, 0>();
+    if constexpr (PL::D > 1) a += ((n * i1) % PL::P1) * pfa_st<PL, 1>();
+    if constexpr (PL::D > 2) a += ((n * i2) % PL::P2) * pfa_st<PL, 2>();
+    if constexpr (PL::D > 3) a += ((n * i3) % PL::P3) * pfa_st<PL, 3>();
+    return a;
+  }
 }
 
 // Stage the coefficient tables of this length into shared memory.

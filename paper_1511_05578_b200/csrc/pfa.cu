@@ -432,6 +432,115 @@ __global__ void __launch_bounds__(PfaGCfg<K>::NT, PfaGCfg<K>::MINB)
   }
 }
 
+// Variant with the generation coefficients staged in shared memory: a task
+// is (beta block of BB rows, group of R adjacent m); the R columns'
+// coefficients w[sheet][l][m] and hlb[l][|m|] are read from L2 once per task
+// into shared memory and reused for the BB rows, so the per-row generation
+// has no global loads.  (SCV_COLGEN_S=1 selects it for K = 2047.)
+template <int K> struct PfaSCfg { static constexpr int R = 2, NT = 384, MINB = 1, BB = 16; };
+#ifndef SCV_COLGEN_S
+#define SCV_COLGEN_S 1
+#endif
+#ifndef SCV_COLGEN_S_BB
+#define SCV_COLGEN_S_BB 128
+#endif
+#ifndef SCV_COLGEN_S_NT
+#define SCV_COLGEN_S_NT 512
+#endif
+template <> struct PfaSCfg<2047> { static constexpr int R = 2, NT = SCV_COLGEN_S_NT, MINB = 1, BB = SCV_COLGEN_S_BB; };
+template <int K>
+static constexpr size_t pfa_smem_s() {
+  using PL = PfaPlan<K>;
+  constexpr int R = PfaSCfg<K>::R;
+  return ((size_t)R * K + pfa_tab_total<PL>() + pfa_scratch<PL, R, PfaSCfg<K>::NT>() + (size_t)R * K) *
+             sizeof(double2) + (size_t)R * K * sizeof(double);
+}
+
+template <int K>
+__global__ void __launch_bounds__(PfaSCfg<K>::NT, PfaSCfg<K>::MINB)
+    k_ana_colgen_s(const double2* __restrict__ w, const double* __restrict__ hlb, const double* __restrict__ lsin,
+                   const double* __restrict__ lcos, int b0, int nb, double2* __restrict__ out,
+                   const double2* __restrict__ gtab) {
+  using PL = PfaPlan<K>;
+  constexpr int R = PfaSCfg<K>::R, NT = PfaSCfg<K>::NT, BB = PfaSCfg<K>::BB;
+  constexpr int L = (K + 1) / 2;
+  constexpr int NGRP = (K + R - 1) / R;
+  extern __shared__ double2 sm[];
+  double2* tab = sm;
+  double2* const scr = sm + pfa_tab_total<PL>();
+  double2* const X = scr + pfa_scratch<PL, R, NT>();
+  double2* const CW = X + R * K;                 // [gi][r] W_{m,n} (0 where |m| > |n|)
+  double* const CH = (double*)(CW + R * K);      // [gi][r] log sqrt C(2l, l+|m|)
+  pfa_load_tables<PL, NT>(tab, gtab);
+  const double fac0 = 1.0 / (8.0 * SCV_PI * SCV_PI);
+  const int nbblk = (nb + BB - 1) / BB;
+  const int ntask = nbblk * NGRP;
+  constexpr int NPT = (K + NT - 1) / NT;
+#pragma unroll 1
+  for (int task = blockIdx.x; task < ntask; task += gridDim.x) {
+    const int bblk = task / NGRP;
+    const int m0 = (task - bblk * NGRP) * R;
+    // stage the R columns' coefficients
+#pragma unroll
+    for (int u = 0; u < NPT; ++u) {
+      const int gi = threadIdx.x + u * NT;
+      if (gi >= K) continue;
+      const int n = gi <= L - 1 ? gi : gi - K;
+      const int l = n < 0 ? -n : n;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int m = m0 + r <= L - 1 ? m0 + r : m0 + r - K, am = m < 0 ? -m : m;
+        const bool nz = m0 + r < K && am <= l;
+        CW[gi * R + r] = nz ? w[((n >= 0 ? 0 : 1) * L + l) * K + (L - 1) + m] : make_double2(0.0, 0.0);
+        CH[gi * R + r] = nz ? hlb[l * (l + 1) / 2 + am] : 0.0;
+      }
+    }
+    const int bs_end = min(nb, (bblk + 1) * BB);
+#pragma unroll 1
+    for (int bs = bblk * BB; bs < bs_end; ++bs) {
+      const int b = b0 + bs;
+      const double ls = lsin[b], lc = lcos[b];
+      __syncthreads();  // coefficients staged / previous row's stores done
+#pragma unroll 2
+      for (int u = 0; u < NPT; ++u) {
+        const int gi = threadIdx.x + u * NT;
+        if (gi >= K) continue;
+        const int n = gi <= L - 1 ? gi : gi - K;
+        const int l = n < 0 ? -n : n;
+        const double facl = (double)(2 * l + 1) * fac0;
+        const int xi = pfa_in_tab<PL>(tab, gi);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int m = m0 + r <= L - 1 ? m0 + r : m0 + r - K, am = m < 0 ? -m : m;
+          double2 v = make_double2(0.0, 0.0);
+          if (m0 + r < K && am <= l) {
+            const int es = n >= 0 ? l - m : l + m;  // power of sin(b/2)
+            const int ec = n >= 0 ? l + m : l - m;  // power of cos(b/2)
+            double lg = CH[gi * R + r];
+            if (es) lg += (double)es * ls;
+            if (ec) lg += (double)ec * lc;
+            double d = exp(lg);
+            if (n < 0 && ((l - m) & 1)) d = -d;
+            const double f = facl * d;
+            const double2 c = CW[gi * R + r];
+            v = make_double2(f * c.x, f * c.y);
+          }
+          X[r * K + xi] = v;
+        }
+      }
+      __syncthreads();
+      pfa_dft<PL, +1, R, NT, K>(X, tab, scr);
+#pragma unroll 4
+      for (int i = threadIdx.x; i < R * K; i += NT) {
+        const int g = i / R, r = i - g * R;
+        const int mi = m0 + r;
+        if (mi < K) out[((long long)g * nb + bs) * K + mi] = X[r * K + pfa_pos_tab<PL>(tab, g)];
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------------------
 // analysis gamma: R adjacent alpha columns of one beta slab, inverse over n.
 // complex: in place on sig (K, L, K), double-buffered.  real: src = T
@@ -994,6 +1103,17 @@ static int run_ana_colgen(scv_ctx* c, const double2* w, const double* hlb, const
   static_assert(sm <= 232448, "column-generation launch shape exceeds the 227 KB shared-memory limit");
   constexpr int L = (K + 1) / 2;
   const long long nt = (long long)nb * ((K + PfaGCfg<K>::R - 1) / PfaGCfg<K>::R);
+  if constexpr (SCV_COLGEN_S && K == 2047) {
+    constexpr size_t sms = pfa_smem_s<K>();
+    static_assert(sms <= 232448, "staged column-generation launch shape exceeds the 227 KB shared-memory limit");
+    const long long nts = (long long)((nb + PfaSCfg<K>::BB - 1) / PfaSCfg<K>::BB) * ((K + PfaSCfg<K>::R - 1) / PfaSCfg<K>::R);
+    int grid;
+    SCV_TRY(persistent_grid(c, k_ana_colgen_s<K>, PfaSCfg<K>::NT, sms, nts, &grid));
+    k_ana_colgen_s<K><<<grid, PfaSCfg<K>::NT, sms, s>>>(w, hlb, ls, lc, b0, nb, out, tab);
+    c->launches++;
+    SCV_CUDA(c, cudaGetLastError());
+    return SCV_OK;
+  }
   int grid;
   SCV_TRY(persistent_grid(c, k_ana_colgen<K>, PfaGCfg<K>::NT, sm, nt, &grid));
   k_ana_colgen<K><<<grid, PfaGCfg<K>::NT, sm, s>>>(w, hlb, ls, lc, b0, nb, out, tab);

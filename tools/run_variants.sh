@@ -7,5 +7,5 @@ for f in variants/lib_*.so; do
   echo "== $v"
   [ "$KS" != none ] && SCV_LIB=$f timeout 180 python tools/fftbench.py $KS 2>&1 | grep "K="
   SCV_LIB=$f timeout 400 python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e "$@" 2>/dev/null | tail -1 | \
-    python -c "import json,sys; d=json.loads(sys.stdin.read()); print('bench ms/map', round(d['ms_per_step'],1), {k: round(v,1) for k, v in d['stages_ms_per_step'].items() if v > 20})"
+    python -c "import json,sys; d=json.loads(sys.stdin.read()); print('bench ms/map', round(d['ms_per_step'],1), 'rt', '%.1e' % d['roundtrip_rel_err'], {k: round(v,1) for k, v in d['stages_ms_per_step'].items() if v > 20})"
 done

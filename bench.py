@@ -150,6 +150,26 @@ def algorithmic_work(a):
     return p, Ljs, B_alg, F_alg
 
 
+def ncu_traffic(stage, Ljs):
+    """Measured DRAM bytes (read + write) per map for `stage`, from the committed
+    ncu --set full captures (profiles/ncu_traffic.json: bytes per beta row of
+    the L_j = 1024 kernel on a 16-row slab, tools/prof_slab.py), scaled to the
+    map's L_j = 1024 scales; None when the stage or size has no capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            tab = json.load(fh)
+    except Exception:
+        return None
+    e = tab.get(stage)
+    if not e:
+        return None
+    n = sum(1 for L in Ljs if L == e["L"])
+    if n == 0:
+        return None
+    return {"bytes_per_map": e["bytes_per_beta_row"] * e["L"] * n, "covers": f"{n} L_j={e['L']} scale launch(es)",
+            "kernel": e["kernel"], "source": e["source"]}
+
+
 def stage_roofline(a, prof, Ljs, hbm_peak, fp64_peak):
     """Roofline of the dominant stage from the live per-stage CUDA-event times."""
     K = lambda L: 2 * L - 1  # noqa: E731
@@ -201,7 +221,11 @@ def stage_roofline(a, prof, Ljs, hbm_peak, fp64_peak):
                     "frac": ach / hbm_peak, "peak_source": "MEASURED_PEAKS.json hbm_gbs"})
         if name in flops_stage:
             out["fp64_tflops_alg"] = flops_stage[name] / (ms_map * 1e-3) / 1e12
-    out["traffic"] = None
+    tr = ncu_traffic(name, Ljs)
+    # measured DRAM bytes (GB per map) vs the algorithmic bytes behind `achieved`
+    out["traffic"] = None if tr is None else tr["bytes_per_map"] / 1e9
+    out["traffic_detail"] = tr
+    out["alg_GB_per_map"] = bytes_stage.get(name, 0) / 1e9
     out["all_stages"] = {}
     for nm, (c_, ms_) in prof.items():
         mm = ms_ / a.steps

@@ -860,6 +860,12 @@ static constexpr size_t pfa_smem_q() {
           2 * (size_t)PfaQCfg<K>::RQ * K) * sizeof(double2);
 }
 
+#ifndef SCV_GQ_L2LINE
+#define SCV_GQ_L2LINE 0
+#endif
+#ifndef SCV_GQ_RED
+#define SCV_GQ_RED 1
+#endif
 // offset of the m block of the quadrature table (betaq.cu): L * sum_{j=-(L-1)}^{m-1} (L - |j|)
 __device__ __forceinline__ long long q_mbase(int m, int L) {
   const long long a = (long long)m + L - 1;  // number of terms
@@ -900,7 +906,13 @@ __global__ void __launch_bounds__(PfaQCfg<K>::NT, PfaQCfg<K>::MINB)
       const double2* cp = chunk + ((long long)bb * K + threadIdx.x / RQ) * K + col0 + r;
 #pragma unroll 4
       for (int g = threadIdx.x / RQ; g < K; g += NT / RQ, cp += (long long)(NT / RQ) * K) {
-        if (col0 + r < K) cp_async16(X + r * K + pfa_in_tab<PL>(tab, g), cp);
+        if (col0 + r < K) {
+#if SCV_GQ_L2LINE
+          cp_async16_l2line(X + r * K + pfa_in_tab<PL>(tab, g), cp);
+#else
+          cp_async16(X + r * K + pfa_in_tab<PL>(tab, g), cp);
+#endif
+        }
         else X[r * K + pfa_in_tab<PL>(tab, g)] = make_double2(0.0, 0.0);
       }
     }
@@ -973,10 +985,16 @@ __global__ void __launch_bounds__(PfaQCfg<K>::NT, PfaQCfg<K>::MINB)
           if (gn >= K || an < am || (real && n < 0)) continue;
           double2* o = wout + ((long long)(n >= 0 ? 0 : 1) * L + an) * K + (m + L - 1);
           const double2 a = acc[r][u];
+#if SCV_GQ_RED
+          // one add per entry per launch, launches stream-ordered: deterministic
+          atomicAdd(&o->x, a.x);
+          atomicAdd(&o->y, a.y);
+#else
           double2 w = *o;
           w.x += a.x;
           w.y += a.y;
           *o = w;
+#endif
         }
       }
     }

@@ -74,6 +74,9 @@ __host__ __device__ constexpr bool pfa_use_mma(int p) { return p >= SCV_MMA_MIN_
 #define SCV_PFA_KT_UNROLL 4
 #endif
 constexpr int pfa_kt_unroll = SCV_PFA_KT_UNROLL;
+#ifndef SCV_PFA_NBW_SMALL
+#define SCV_PFA_NBW_SMALL 1
+#endif
 __host__ __device__ constexpr int mma_M(int p) { return ((pfa_h(p) + 1 + 15) / 16) * 16; }   // output rows
 __host__ __device__ constexpr int mma_Kp(int p) { return ((pfa_h(p) + 3) / 4) * 4; }         // reduction dim
 __host__ __device__ constexpr int mma_pitch(int n) {  // row pitch (doubles) with pitch mod 16 in {4, 12}
@@ -586,74 +589,95 @@ __device__ __forceinline__ void pfa_stage_mma_blk(double2* X, const double2* tab
   const int ar = lane >> 2, ac = lane & 3;
   // block-local butterfly slot i -> offset within the group of 8
   auto slot = [](int i) { return (i >> 1) + 4 * (i & 1); };
+  // small radices (<= 2 m8 tiles): NBW blocks per warp iteration, for more
+  // independent DMMA chains per k-step
+  constexpr int NBW = M8 <= 2 ? SCV_PFA_NBW_SMALL : 1;
 #pragma unroll 1
-  for (int q = warp; q < NBLK; q += NW) {
-    const int gb = (q >> 1) * 8 + 2 * (q & 1);
-    // B-fragment column of this lane: butterfly slot ar>>1, component ar&1
-    const int bfB = gb + slot(ar >> 1);
-    const bool okB = bfB < NBF;
-    int rowd = 0, pa = 0, pb = 0;
-    if (okB) {
-      const int r = bfB / nbf, b = bfB - r * nbf;
-      const int c0 = pfa_base<PL, S>(b);
-      rowd = 2 * r * PITCH + (ar & 1);
-      pa = c0 + (ac + 1) * step;
-      pb = c0 + (p - ac - 1) * step;
-    }
-    // epilogue butterfly of this lane: slot ac (accumulator columns 2ac, 2ac+1)
-    const int bfE = gb + slot(ac);
-    const bool okE = bfE < NBF;
-    int eoff = 0;
-    double2 x0 = make_double2(0.0, 0.0);
-    if (okE) {
-      const int r = bfE / nbf, b = bfE - r * nbf;
-      eoff = r * PITCH + pfa_base<PL, S>(b);
-      x0 = X[eoff];
-    }
-    double accC[M8][2], accS[M8][2];
+  for (int q0 = warp; q0 < NBLK; q0 += NW * NBW) {
+    int rowd[NBW], pa[NBW], pb[NBW], eoff[NBW];
+    bool okB[NBW], okE[NBW];
+    double2 x0[NBW];
+    double accC[NBW][M8][2], accS[NBW][M8][2];
+    double an[NBW], bn[NBW];
 #pragma unroll
-    for (int t = 0; t < M8; ++t) accC[t][0] = accC[t][1] = accS[t][0] = accS[t][1] = 0.0;
-    // B operands software-pipelined one k-step ahead (the s/d formation of
-    // step kt must not wait on its own shared loads)
-    double an = 0.0, bn = 0.0;
-    if (okB && ((Kp == h) || (ac + 1 <= h))) {
-      an = Xd[rowd + 2 * pa];
-      bn = Xd[rowd + 2 * pb];
+    for (int w = 0; w < NBW; ++w) {
+      const int q = q0 + w * NW;
+      const int gb = (q >> 1) * 8 + 2 * (q & 1);
+      // B-fragment column of this lane: butterfly slot ar>>1, component ar&1
+      const int bfB = gb + slot(ar >> 1);
+      okB[w] = q < NBLK && bfB < NBF;
+      rowd[w] = pa[w] = pb[w] = 0;
+      if (okB[w]) {
+        const int r = bfB / nbf, b = bfB - r * nbf;
+        const int c0 = pfa_base<PL, S>(b);
+        rowd[w] = 2 * r * PITCH + (ar & 1);
+        pa[w] = c0 + (ac + 1) * step;
+        pb[w] = c0 + (p - ac - 1) * step;
+      }
+      // epilogue butterfly of this lane: slot ac (accumulator columns 2ac, 2ac+1)
+      const int bfE = gb + slot(ac);
+      okE[w] = q < NBLK && bfE < NBF;
+      eoff[w] = 0;
+      x0[w] = make_double2(0.0, 0.0);
+      if (okE[w]) {
+        const int r = bfE / nbf, b = bfE - r * nbf;
+        eoff[w] = r * PITCH + pfa_base<PL, S>(b);
+        x0[w] = X[eoff[w]];
+      }
+#pragma unroll
+      for (int t = 0; t < M8; ++t) accC[w][t][0] = accC[w][t][1] = accS[w][t][0] = accS[w][t][1] = 0.0;
+      // B operands software-pipelined one k-step ahead (the s/d formation of
+      // step kt must not wait on its own shared loads)
+      an[w] = bn[w] = 0.0;
+      if (okB[w] && ((Kp == h) || (ac + 1 <= h))) {
+        an[w] = Xd[rowd[w] + 2 * pa[w]];
+        bn[w] = Xd[rowd[w] + 2 * pb[w]];
+      }
     }
 #pragma unroll pfa_kt_unroll
     for (int kt = 0; kt < Kp / 4; ++kt) {
-      const double a = an, bb = bn;
-      pa += 4 * step;
-      pb -= 4 * step;
-      an = 0.0;
-      bn = 0.0;
-      if (kt + 1 < Kp / 4 && okB && ((Kp == h) || (4 * kt + 4 + ac + 1 <= h))) {
-        an = Xd[rowd + 2 * pa];
-        bn = Xd[rowd + 2 * pb];
+      double bS[NBW], bD[NBW];
+#pragma unroll
+      for (int w = 0; w < NBW; ++w) {
+        const double a = an[w], bb = bn[w];
+        pa[w] += 4 * step;
+        pb[w] -= 4 * step;
+        an[w] = 0.0;
+        bn[w] = 0.0;
+        if (kt + 1 < Kp / 4 && okB[w] && ((Kp == h) || (4 * kt + 4 + ac + 1 <= h))) {
+          an[w] = Xd[rowd[w] + 2 * pa[w]];
+          bn[w] = Xd[rowd[w] + 2 * pb[w]];
+        }
+        bS[w] = a + bb;
+        bD[w] = a - bb;
       }
-      const double bS = a + bb, bD = a - bb;
 #pragma unroll
       for (int t = 0; t < M8; ++t) {
         const int row = t * 8 + ar;
         const double aC = Cm[row * PA + kt * 4 + ac];
         const double aS = Sm[row * PA + kt * 4 + ac];
-        dmma(accC[t][0], accC[t][1], aC, bS);
-        dmma(accS[t][0], accS[t][1], aS, bD);
+#pragma unroll
+        for (int w = 0; w < NBW; ++w) {
+          dmma(accC[w][t][0], accC[w][t][1], aC, bS[w]);
+          dmma(accS[w][t][0], accS[w][t][1], aS, bD[w]);
+        }
       }
     }
     __syncwarp();
-    if (okE) {
-      double2* Xr = X + eoff;
+#pragma unroll
+    for (int w = 0; w < NBW; ++w) {
+      if (!okE[w]) continue;
+      double2* Xr = X + eoff[w];
 #pragma unroll
       for (int t = 0; t < M8; ++t) {
         const int k = t * 8 + ar;
         if (k > h) continue;
-        const double Ar = x0.x + accC[t][0], Ai = x0.y + accC[t][1];
+        const double Ar = x0[w].x + accC[w][t][0], Ai = x0[w].y + accC[w][t][1];
         if (k == 0) {
           Xr[0] = make_double2(Ar, Ai);
           continue;
         }
-        const double Br = accS[t][0], Bi = accS[t][1];
+        const double Br = accS[w][t][0], Bi = accS[w][t][1];
         const double iBr = DIR < 0 ? Bi : -Bi, iBi = DIR < 0 ? -Br : Br;
         Xr[k * step] = make_double2(Ar + iBr, Ai + iBi);
         Xr[(p - k) * step] = make_double2(Ar - iBr, Ai - iBi);

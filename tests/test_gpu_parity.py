@@ -354,3 +354,39 @@ def test_analysis_orders_and_chunk_layouts_agree(L):
         ctx.set_option("chunkt", -1)
     assert orc.rel_err(fa, fb) <= 1e-13
     assert orc.rel_err(fb, w) <= TOL_RT
+
+
+# ------------------------------------------------- BASELINE full sizes (properties)
+def test_c4_full_size_round_trip_and_energy():
+    """BASELINE configs[3] (C4) at full size, L=1024, lambda=2, J0=3: there is no
+    oracle at this size (147 GB of coefficients), so check the size-independent
+    property the reference's own round-trip command reports: synthesize(analyze(f))
+    == f to 1e-11 relative, on the map and on f_lm (src/cli.py:239-243)."""
+    L = 1024
+    p = sc.TilingParams(L, 0, 2.0, 3)
+    t = sc.build_tiling(p)
+    flm = orc.gaussian_flm(L, 0, seed=0, real=True)
+    f = sc.sht_inverse(sc.HarmonicCoeffs(L, 0, flm, real=True))
+    c = sc.analyze(f, t)
+    assert [tuple(s.values.shape) for s in c.scales][-1] == (2047, 1024, 2047)
+    g = sc.synthesize(c, t)
+    rt = float((g.values - f.values).abs().max() / f.values.abs().max())
+    assert rt <= TOL_RT, rt
+    back = host(sc.sht_forward(g).values)
+    assert np.abs(back - flm).max() <= TOL_RT * np.abs(flm).max()
+    del c, g
+    torch.cuda.empty_cache()
+
+
+def test_analysis_is_linear_at_L256():
+    # analyze(a f1 + b f2) = a analyze(f1) + b analyze(f2) (exact linear map)
+    L = 256
+    t = sc.build_tiling(sc.TilingParams(L, 2, 2.0, 2))
+    f1 = sc.sht_inverse(sc.HarmonicCoeffs(L, 2, orc.gaussian_flm(L, 2, seed=1, real=False)))
+    f2 = sc.sht_inverse(sc.HarmonicCoeffs(L, 2, orc.gaussian_flm(L, 2, seed=2, real=False)))
+    a, b = 0.75 - 0.5j, -1.25 + 2.0j
+    f12 = sc.SphereSignal(f1.grid, 2, a * f1.values + b * f2.values)
+    c1, c2, c12 = sc.analyze(f1, t), sc.analyze(f2, t), sc.analyze(f12, t)
+    for s1, s2, s12 in zip(c1.scales, c2.scales, c12.scales):
+        ref = a * s1.values + b * s2.values
+        assert float((s12.values - ref).abs().max() / ref.abs().max()) <= 1e-12

@@ -542,6 +542,129 @@ __global__ void __launch_bounds__(PfaSCfg<K>::NT, PfaSCfg<K>::MINB)
 }
 
 // ---------------------------------------------------------------------------
+// analysis, real signal, gamma first.  For a real signal the gamma transform
+// T_b[g, m] = sum_n F_b[n, m] e^{i n gamma_g} is Hermitian in m for every g, so
+// only the columns m >= 0 are formed (half the columns of the complex path),
+// with the n < 0 entries taken from the n > 0 half by the real-signal symmetry
+// F[-n, -m] = conj(F[n, m]) and the n = 0 entry reduced to its real part --
+// exactly the inputs the reference's real path reads (so3.py:386-417: the
+// n >= 0 half spectrum, irfft semantics for the n = 0 bin).  Output T is
+// (K, nb, L) complex; the alpha pass k_rows_c2r then forms two real rows per
+// complex transform.
+// ---------------------------------------------------------------------------
+template <int K>
+__global__ void __launch_bounds__(PfaGCfg<K>::NT, PfaGCfg<K>::MINB)
+    k_ana_colgen_real(const double2* __restrict__ w, const double* __restrict__ hlb, const double* __restrict__ lsin,
+                      const double* __restrict__ lcos, int b0, int nb, double2* __restrict__ T,
+                      const double2* __restrict__ gtab) {
+  using PL = PfaPlan<K>;
+  constexpr int R = PfaGCfg<K>::R, NT = PfaGCfg<K>::NT;
+  constexpr int L = (K + 1) / 2;
+  constexpr int NGRP = (L + R - 1) / R;
+  extern __shared__ double2 sm[];
+  double2* tab = sm;
+  double2* const scr = sm + pfa_tab_total<PL>();
+  double2* const X = scr + pfa_scratch<PL, R, NT>();
+  pfa_load_tables<PL, NT>(tab, gtab);
+  const double fac0 = 1.0 / (8.0 * SCV_PI * SCV_PI);
+  const int ntask = nb * NGRP;
+  constexpr int NPT = (K + NT - 1) / NT;
+#pragma unroll 1
+  for (int task = blockIdx.x; task < ntask; task += gridDim.x) {
+    const int bs = task / NGRP;
+    const int b = b0 + bs;
+    const int m0 = (task - bs * NGRP) * R;
+    const double ls = lsin[b], lc = lcos[b];
+#pragma unroll 1
+    for (int u = 0; u < NPT; ++u) {
+      const int gi = threadIdx.x + u * NT;
+      if (gi >= K) continue;
+      const int n = gi <= L - 1 ? gi : gi - K;
+      const int l = n < 0 ? -n : n;
+      const double facl = (double)(2 * l + 1) * fac0;
+      const int xi = pfa_in_tab<PL>(tab, gi);
+      // n < 0 uses the n = +l sheet at -m, conjugated
+      const double* hrow = hlb + l * (l + 1) / 2;
+      const double2* wrow = w + (long long)l * K + (L - 1);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int m = m0 + r;
+        double2 v = make_double2(0.0, 0.0);
+        if (m < L && m <= l) {
+          const int ms = n >= 0 ? m : -m;   // the sheet-0 entry (n' = +l, m')
+          const int es = l - ms, ec = l + ms;
+          double lg = hrow[m];
+          if (es) lg += (double)es * ls;
+          if (ec) lg += (double)ec * lc;
+          const double f = facl * exp(lg);
+          const double2 cw = wrow[ms];
+          v = n >= 0 ? make_double2(f * cw.x, f * cw.y) : make_double2(f * cw.x, -f * cw.y);
+          if (n == 0) v.y = 0.0;  // l = 0: the real part (irfft semantics of the n = 0 bin)
+        }
+        X[r * K + xi] = v;
+      }
+    }
+    __syncthreads();
+    pfa_dft<PL, +1, R, NT, K>(X, tab, scr);
+#pragma unroll 4
+    for (int i = threadIdx.x; i < R * K; i += NT) {
+      const int g = i / R, r = i - g * R;
+      const int m = m0 + r;
+      if (m < L) T[((long long)g * nb + bs) * L + m] = X[r * K + pfa_pos_tab<PL>(tab, g)];
+    }
+    __syncthreads();
+  }
+}
+
+// alpha pass of the real analysis: rows ri = (g, bs) of T (L Hermitian-half
+// bins each) -> real rows of sig (K, nb, K).  Two rows per complex transform:
+// Z = T1 + i T2 extended by Z[-m] = conj(T1[m]) + i conj(T2[m]); the IDFT of Z
+// is f1 + i f2.
+template <int K>
+__global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
+    k_rows_c2r(long long nrows, const double2* __restrict__ T, double* __restrict__ out,
+               const double2* __restrict__ gtab) {
+  using PL = PfaPlan<K>;
+  constexpr int R = PfaCfg<K, false>::R, NT = PfaCfg<K, false>::NT;
+  constexpr int L = (K + 1) / 2;
+  extern __shared__ double2 sm[];
+  double2* tab = sm;
+  double2* const scr = sm + pfa_tab_total<PL>();
+  double2* const X = scr + pfa_scratch<PL, PfaRD<K, false>::v, NT>();
+  pfa_load_tables<PL, NT>(tab, gtab);
+  const long long nb = (nrows + 2 * R - 1) / (2 * R);
+#pragma unroll 1
+  for (long long bt = blockIdx.x; bt < nb; bt += gridDim.x) {
+    const long long r0 = bt * 2 * R;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < R * L; i += NT) {
+      const int r = i / L, m = i - r * L;
+      const long long ri1 = r0 + 2 * r, ri2 = ri1 + 1;
+      double2 t1 = ri1 < nrows ? T[ri1 * L + m] : make_double2(0.0, 0.0);
+      double2 t2 = ri2 < nrows ? T[ri2 * L + m] : make_double2(0.0, 0.0);
+      if (m == 0) {
+        t1.y = 0.0;
+        t2.y = 0.0;
+      }
+      X[r * K + pfa_in_tab<PL>(tab, m)] = make_double2(t1.x - t2.y, t1.y + t2.x);
+      if (m > 0) X[r * K + pfa_in_tab<PL>(tab, K - m)] = make_double2(t1.x + t2.y, -t1.y + t2.x);
+    }
+    __syncthreads();
+    pfa_dft_rows<PL, +1, R, PfaRD<K, false>::v, NT>(X, tab, scr);
+#pragma unroll 4
+    for (int i = threadIdx.x; i < 2 * R * K; i += NT) {
+      const int c = i / K, a = i - c * K;
+      const long long ri = r0 + c;
+      if (ri < nrows) {
+        const double2 z = X[(c >> 1) * K + pfa_pos_tab<PL>(tab, a)];
+        out[ri * K + a] = (c & 1) ? z.y : z.x;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // analysis gamma: R adjacent alpha columns of one beta slab, inverse over n.
 // complex: in place on sig (K, L, K), double-buffered.  real: src = T
 // (L, L, K) complex half spectrum (n >= 0), dst = real sig (K, L, K); two
@@ -1141,6 +1264,37 @@ static int run_ana_colgen(scv_ctx* c, const double2* w, const double* hlb, const
 }
 
 template <int K>
+static int run_ana_real_gf(scv_ctx* c, const double2* w, const double* hlb, const double* ls, const double* lc,
+                           int b0, int nb, double2* T, double* out, cudaStream_t s) {
+  const double2* tab;
+  SCV_TRY(scv_pfa_tables(c, K, &tab));
+  constexpr int L = (K + 1) / 2;
+  {
+    constexpr size_t sm = pfa_smem_g<K>();
+    static_assert(sm <= 232448, "column-generation launch shape exceeds the 227 KB shared-memory limit");
+    const long long nt = (long long)nb * ((L + PfaGCfg<K>::R - 1) / PfaGCfg<K>::R);
+    int grid;
+    SCV_TRY(persistent_grid(c, k_ana_colgen_real<K>, PfaGCfg<K>::NT, sm, nt, &grid));
+    SCV_PROF(c, s, "so3inv_colgen");
+    k_ana_colgen_real<K><<<grid, PfaGCfg<K>::NT, sm, s>>>(w, hlb, ls, lc, b0, nb, T, tab);
+    c->launches++;
+    SCV_CUDA(c, cudaGetLastError());
+  }
+  {
+    constexpr size_t sm = pfa_smem<K, false>();
+    const long long nrows = (long long)K * nb;
+    const long long nbt = (nrows + 2 * PfaCfg<K, false>::R - 1) / (2 * PfaCfg<K, false>::R);
+    int grid;
+    SCV_TRY(persistent_grid(c, k_rows_c2r<K>, PfaCfg<K, false>::NT, sm, nbt, &grid));
+    SCV_PROF(c, s, "so3inv_rows");
+    k_rows_c2r<K><<<grid, PfaCfg<K, false>::NT, sm, s>>>(nrows, T, out, tab);
+    c->launches++;
+    SCV_CUDA(c, cudaGetLastError());
+  }
+  return SCV_OK;
+}
+
+template <int K>
 static int run_ana_gamma(scv_ctx* c, int real, double2* src, double* dst, cudaStream_t s) {
   const double2* tab;
   SCV_TRY(scv_pfa_tables(c, K, &tab));
@@ -1213,6 +1367,12 @@ int scv_pfa_ana_alpha(scv_ctx* c, int K, int real, const double2* w, const doubl
 int scv_pfa_ana_colgen(scv_ctx* c, int K, const double2* w, const double* hlb, const double* ls, const double* lc,
                        int b0, int nb, double2* out, cudaStream_t s) {
 #define CALL(KK) run_ana_colgen<KK>(c, w, hlb, ls, lc, b0, nb, out, s)
+  PFA_SWITCH(K, CALL)
+#undef CALL
+}
+int scv_pfa_ana_real_gf(scv_ctx* c, int K, const double2* w, const double* hlb, const double* ls, const double* lc,
+                        int b0, int nb, double2* T, double* out, cudaStream_t s) {
+#define CALL(KK) run_ana_real_gf<KK>(c, w, hlb, ls, lc, b0, nb, T, out, s)
   PFA_SWITCH(K, CALL)
 #undef CALL
 }

@@ -252,6 +252,11 @@ extern "C" int scv_so3_inverse_curvelet(scv_ctx* c, int L, int real, const doubl
     }
     void* T = nullptr;
     SCV_TRY(scv_scratch(c, 0, (size_t)L * LK * 16, &T));
+    if (c->opt_colgen) {  // gamma first: Hermitian-half columns, then two real rows per transform
+      SCV_TRY(scv_pfa_ana_real_gf(c, K, (const double2*)w, c->hlb, t->sinh, t->cosh, 0, L, (double2*)T,
+                                  (double*)sig, s));
+      return SCV_OK;
+    }
     {
       SCV_PROF(c, s, "so3inv_alpha");
       SCV_TRY(scv_pfa_ana_alpha(c, K, 1, (const double2*)w, c->hlb, t->sinh, t->cosh, (double2*)T, s));

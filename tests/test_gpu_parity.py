@@ -390,3 +390,26 @@ def test_analysis_is_linear_at_L256():
     for s1, s2, s12 in zip(c1.scales, c2.scales, c12.scales):
         ref = a * s1.values + b * s2.values
         assert float((s12.values - ref).abs().max() / ref.abs().max()) <= 1e-12
+
+
+@pytest.mark.parametrize("L", [128, 256, 512])
+def test_real_analysis_orders_agree(L):
+    """Real path: gamma-first (Hermitian-half columns + two real rows per
+    transform) and alpha-first (n >= 0 rows + Hermitian gamma columns) analysis
+    give the same real signal (so3.py:386-417)."""
+    from paper_1511_05578_b200 import _cabi
+    ctx = _cabi.context(0)
+    w = _real_symmetric(_random_cw(L, 9 + L))
+    cw = sc.CurveletWignerCoeffs(L, w)
+    grid = sc.SO3Grid(L, L, L)
+    try:
+        ctx.set_option("colgen", 1)
+        a = host(sc.so3_inverse_curvelet_real(cw, grid).values)
+        ctx.set_option("colgen", 0)
+        b = host(sc.so3_inverse_curvelet_real(cw, grid).values)
+    finally:
+        ctx.set_option("colgen", -1)
+    full = host(sc.so3_inverse_curvelet(cw, grid).values)
+    assert orc.rel_err(a, b) <= 1e-13
+    assert orc.rel_err(a, full.real) <= 1e-13
+    assert np.abs(full.imag).max() <= 1e-12 * np.abs(full.real).max()

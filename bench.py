@@ -54,6 +54,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-json", default="")
+    ap.add_argument("--streamed", action="store_true",
+                    help="roundtrip_streamed: beta-slab streamed analysis+synthesis (coefficients never "
+                         "held whole; BASELINE C5 on one GPU: --L 2048 --spin 2 --jmin 4)")
+    ap.add_argument("--slab-gb", type=float, default=16.0, help="--streamed slab size (GiB)")
     ap.add_argument("--shard-scales", action="store_true",
                     help="N>1: one map per step with its scales sharded over the ranks "
                          "(NCCL broadcast + gather); default is one map per rank per step")
@@ -77,6 +81,8 @@ def gaussian_flm(L, spin, seed, real):
 
 def workload_name(a):
     path = "analyze_real+synthesize_real" if a.real else "analyze+synthesize"
+    if a.streamed:
+        path = "roundtrip_streamed (beta-slab streamed analyze+synthesize)"
     return f"curvelet {path} L={a.L} spin={a.spin} B={a.lam:g} J0={a.jmin}"
 
 
@@ -262,13 +268,20 @@ def run_ours(a):
     if a.real:
         f = sc.SphereSignal(f.grid, 0, f.values.real.contiguous(), real=True)
     dtype = torch.float64 if a.real else torch.complex128
-    scale_out = [torch.empty((2 * Lj - 1, Lj, 2 * Lj - 1), dtype=dtype, device=dev) for Lj in Ljs]
     ana = sc.analyze_real if a.real else sc.analyze
     syn = sc.synthesize_real if a.real else sc.synthesize
+    if a.streamed:
+        if a.real:
+            raise SystemExit("--streamed runs the complex path")
 
-    def step(fin):
-        c = ana(fin, t, scale_out=scale_out)
-        return syn(c, t)
+        def step(fin):
+            return sc.roundtrip_streamed(fin, t, slab_bytes=int(a.slab_gb * (1 << 30)))
+    else:
+        scale_out = [torch.empty((2 * Lj - 1, Lj, 2 * Lj - 1), dtype=dtype, device=dev) for Lj in Ljs]
+
+        def step(fin):
+            c = ana(fin, t, scale_out=scale_out)
+            return syn(c, t)
 
     if a.shard_scales and world > 1:
         from paper_1511_05578_b200.dist import analyze_sharded, synthesize_sharded
@@ -369,6 +382,7 @@ def run_ours(a):
         "config": {"workload": workload_name(a), "L": a.L, "spin": a.spin, "lambda": a.lam,
                    "j_min": a.jmin, "j_max": p.j_max, "scale_band_limits": Ljs,
                    "maps_per_step": maps_per_step,
+                   **({"streamed_slab_GiB": a.slab_gb} if a.streamed else {}),
                    "parallelism": ("scales sharded x%d (NCCL broadcast f_lm + gather terms)" % world
                                    if (a.shard_scales and world > 1) else
                                    (f"maps x{world} (one map per rank)" if world > 1 else "1 GPU")),

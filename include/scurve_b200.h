@@ -72,7 +72,7 @@ int scv_profile(scv_ctx* ctx, int enable);
 int scv_profile_report(scv_ctx* ctx, char* buf, int len);
 /* Set a context option; value -1 restores the library default.
  *   "betaq": synthesis beta stage. 1 = precomputed beta quadrature table fused
- *            into the gamma pass (default for 128 <= L <= 1024 on the
+ *            into the gamma pass (default for 128 <= L <= 2048 on the
  *            prime-factor lengths), 0 = per-column Bluestein/convolution FFTs
  *            and Delta contraction.  Both compute so3.py:203-243.
  *   "colgen": analysis order. 1 = gamma-first (closed-form columns over n,
@@ -136,7 +136,7 @@ int scv_so3_inverse_curvelet(scv_ctx* ctx, int Lj, int real, const double* w, vo
  * forward: the beta quadrature summed over the slab's rows only, written into
  * w (accumulate = 0) or added to it (accumulate = 1); the sum of the partials
  * of all slabs is scv_so3_forward_curvelet of the full signal.  Needs the
- * beta-quadrature path (128 <= Lj <= 1024); real = 1 reads a float64 slab. */
+ * beta-quadrature path (128 <= Lj <= 2048); real = 1 reads a float64 slab. */
 int scv_so3_inverse_curvelet_slab(scv_ctx* ctx, int Lj, const double* w, int b0, int nb, void* sig,
                                   void* stream);
 int scv_so3_forward_curvelet_slab(scv_ctx* ctx, int Lj, int real, const void* sig, int b0, int nb,

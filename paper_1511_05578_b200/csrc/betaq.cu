@@ -37,10 +37,10 @@
 namespace {
 
 typedef long double ld;
-constexpr int QG = 8;       // consecutive degrees per task (coalesced 64-byte stores)
+constexpr int QG_MAX = 8;   // consecutive degrees per task (coalesced 64-byte stores)
 constexpr int QNT = 256;    // threads per block
 
-__global__ void __launch_bounds__(QNT) k_betaq_build(int L, double pref, const double* __restrict__ delta,
+__global__ void __launch_bounds__(QNT) k_betaq_build(int L, int QG, double pref, const double* __restrict__ delta,
                                                      const double* __restrict__ trig, const long long* __restrict__ mbase,
                                                      const int2* __restrict__ tasks, int ntasks, double* __restrict__ q) {
   const int K = 2 * L - 1;
@@ -181,6 +181,10 @@ int scv_betaq_table(scv_ctx* c, int L, cudaStream_t s, const double** qtab, cons
     mb[m + L - 1] = acc;
     acc += (long long)L * (L - std::abs(m));
   }
+  // degrees per task: as many as fit next to the trig tables in shared memory
+  // (8 up to L = 1024, fewer at L = 2048)
+  const size_t fixed = (size_t)4 * K + 2 * L + 2 + L + 32;
+  const int QG = (int)std::max<long long>(1, std::min<long long>(QG_MAX, ((long long)(232448 / sizeof(double)) - (long long)fixed) / L));
   std::vector<int2> tasks;
   for (int m = -(L - 1); m <= L - 1; ++m)
     for (int l0 = std::abs(m); l0 < L; l0 += QG) tasks.push_back(make_int2(m, l0));
@@ -200,7 +204,7 @@ int scv_betaq_table(scv_ctx* c, int L, cudaStream_t s, const double** qtab, cons
   SCV_CUDA(c, cudaMemcpyAsync(dmb, mb.data(), mb.size() * sizeof(long long), cudaMemcpyHostToDevice, s));
   SCV_CUDA(c, cudaMemcpyAsync(dtrig, trig.data(), trig.size() * sizeof(double), cudaMemcpyHostToDevice, s));
   SCV_CUDA(c, cudaMemcpyAsync(dtask, tasks.data(), tasks.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
-  const size_t sm = ((size_t)4 * K + 2 * L + 2 + L + (size_t)QG * L + 32) * sizeof(double);
+  const size_t sm = (fixed + (size_t)QG * L) * sizeof(double);
   SCV_CUDA(c, cudaFuncSetAttribute(k_betaq_build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   int per = 0, sms = 0;
   SCV_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_betaq_build, QNT, sm));
@@ -209,7 +213,7 @@ int scv_betaq_table(scv_ctx* c, int L, cudaStream_t s, const double** qtab, cons
   const double pref = 4.0 * SCV_PI * SCV_PI / ((double)K * (double)K);
   {
     SCV_PROF(c, s, "betaq_build");
-    k_betaq_build<<<grid, QNT, sm, s>>>(L, pref, c->delta, (const double*)dtrig, dmb, (const int2*)dtask,
+    k_betaq_build<<<grid, QNT, sm, s>>>(L, QG, pref, c->delta, (const double*)dtrig, dmb, (const int2*)dtask,
                                         (int)tasks.size(), dq);
     c->launches++;
     SCV_CUDA(c, cudaGetLastError());

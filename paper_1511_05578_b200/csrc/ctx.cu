@@ -125,30 +125,52 @@ int scv_ensure_hlb(scv_ctx* c, int L, cudaStream_t s) {
 
 int scv_ensure_delta(scv_ctx* c, int L, cudaStream_t s) {
   if (c->delta && c->delta_L >= L) return SCV_OK;
-  // edge rows Delta^l_{l,m} = (-1)^{l-m} sqrt(C(2l,l+m)) / 2^l  (wigner.py:153-161)
+  // edge rows Delta^l_{l,m} = (-1)^{l-m} sqrt(C(2l,l+m)) / 2^l  (wigner.py:153-161),
+  // as a double mantissa in [0.5, 1) and a power-of-two exponent: above
+  // l ~ 1022 the edge values near |m| = l fall below the double range (2^-l),
+  // while the interior entries the recursion grows from them do not, so the
+  // kernel carries an exponent shift until the values are representable.
+  // Seeds inside the double range reproduce (double)v exactly.
   std::vector<ld> lf = log_factorials(2 * L + 2);
   std::vector<double> edge((size_t)L * (L + 1) / 2);
+  std::vector<int> edge_e((size_t)L * (L + 1) / 2);
   for (int l = 0; l < L; ++l)
     for (int m = 0; m <= l; ++m) {
-      ld v = expl(0.5L * (lf[2 * l] - lf[l + m] - lf[l - m]) - (ld)l * logl(2.0L));
-      if ((l - m) & 1) v = -v;
-      edge[(size_t)l * (l + 1) / 2 + m] = (double)v;
+      const ld lg2 = (0.5L * (lf[2 * l] - lf[l + m] - lf[l - m])) / logl(2.0L) - (ld)l;  // log2 |v|
+      int e = (int)floorl(lg2) + 1;
+      ld mant = exp2l(lg2 - (ld)e);  // in [0.5, 1)
+      if (mant >= 1.0L) { mant *= 0.5L; ++e; }
+      if (mant < 0.5L) { mant *= 2.0L; --e; }
+      if ((l - m) & 1) mant = -mant;
+      edge[(size_t)l * (l + 1) / 2 + m] = (double)mant;
+      edge_e[(size_t)l * (l + 1) / 2 + m] = e;
     }
   if (L > 1) {  // seed plane of build_halfpi_table (wigner.py:214-218) uses 1/sqrt(2.0)
-    edge[1] = -1.0 / std::sqrt(2.0);
-    edge[2] = 0.5;
+    int e;
+    edge[1] = std::frexp(-1.0 / std::sqrt(2.0), &e);
+    edge_e[1] = e;
+    edge[2] = std::frexp(0.5, &e);
+    edge_e[2] = e;
   }
   double* d_edge = nullptr;
   SCV_TRY(upload(c, &d_edge, edge, s));
+  int* d_edge_e = nullptr;
+  {
+    cudaError_t ee = cudaMalloc((void**)&d_edge_e, edge_e.size() * sizeof(int));
+    if (ee != cudaSuccess) return scv_fail(c, SCV_ENOMEM, "cudaMalloc(delta edge)");
+    SCV_CUDA(c, cudaMemcpyAsync(d_edge_e, edge_e.data(), edge_e.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+  }
   double* tab = nullptr;
   cudaError_t e = cudaMalloc((void**)&tab, (size_t)wedge_size(L) * sizeof(double));
   if (e != cudaSuccess) {
     cudaFree(d_edge);
+    cudaFree(d_edge_e);
     return scv_fail(c, SCV_ENOMEM, "cudaMalloc(delta wedge): " + std::string(cudaGetErrorString(e)));
   }
-  int rc = scv_launch_delta_wedge(c, L, d_edge, tab, s);
+  int rc = scv_launch_delta_wedge(c, L, d_edge, d_edge_e, tab, s);
   cudaStreamSynchronize(s);
   cudaFree(d_edge);
+  cudaFree(d_edge_e);
   if (rc != SCV_OK) {
     cudaFree(tab);
     return rc;

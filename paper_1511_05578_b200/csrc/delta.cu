@@ -15,11 +15,22 @@
 // consecutive addresses of every plane (coalesced).  The products are
 // evaluated with explicit round-to-nearest intrinsics (no FMA contraction)
 // in the reference's operation order, so planes match numpy's arithmetic.
+//
+// Range: the border values 2^-l sqrt(C(2l, l+m)) leave the double range near
+// |m| = l once l > ~1022, where the reference's float64 closed form
+// underflows to 0 and the recursion then keeps the entries grown from it at 0
+// (wrong for L > 1024: the SHT round trip fails near |m'|, |m| ~ 0.7 l).
+// The seed arrives as mantissa + exponent; a seed below the normal range
+// starts the recursion scaled by 2^e (exact: the recursion is linear and
+// homogeneous), the shift is released as the values grow, and each plane
+// entry is written as ldexp(v, -e) (rounding correctly to a subnormal / 0
+// only where the true value is that small).  Seeds inside the normal range
+// run unscaled, bit-identical to the plain recursion.
 
 #include "scv_internal.cuh"
 
 __global__ void __launch_bounds__(256) k_delta_wedge(int L, const double* __restrict__ edge,
-                                                     double* __restrict__ out) {
+                                                     const int* __restrict__ edge_e, double* __restrict__ out) {
   long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   long long total = (long long)L * (L + 1) / 2;
   if (t >= total) return;
@@ -30,10 +41,17 @@ __global__ void __launch_bounds__(256) k_delta_wedge(int L, const double* __rest
   const double mp = (double)a, m = (double)b;
   const double mp2 = __dmul_rn(mp, mp), m2 = __dmul_rn(m, m);
   double p1 = 0.0, p2 = 0.0;
+  int sh = 0;  // values held scaled by 2^sh (sh > 0 only while below the normal range)
   for (int l = a; l < L; ++l) {
     double v;
     if (l == a) {
-      v = edge[t];
+      const int ex = edge_e[t];
+      if (ex >= -1021) {
+        v = ldexp(edge[t], ex);  // normal: exactly the rounded double seed
+      } else {
+        v = edge[t];
+        sh = -ex;
+      }
     } else if (l == 1) {
       v = 0.0;  // Delta^1_{00} of the seed plane (wigner.py:214-218)
     } else {
@@ -48,16 +66,26 @@ __global__ void __launch_bounds__(256) k_delta_wedge(int L, const double* __rest
       double q2 = (a <= l - 2) ? p2 : 0.0;
       v = __dmul_rn(sc, __dsub_rn(__dmul_rn(ac, p1), __dmul_rn(bc, q2)));
     }
-    out[wedge_plane_base(l) + t] = v;
+    if (sh > 0 && v != 0.0) {
+      // release the shift as the scaled value grows past 1 (both carried
+      // predecessors move by the same power of two)
+      const int k = min(ilogb(v), sh);
+      if (k > 0) {
+        v = ldexp(v, -k);
+        p1 = ldexp(p1, -k);
+        sh -= k;
+      }
+    }
+    out[wedge_plane_base(l) + t] = sh > 0 ? ldexp(v, -sh) : v;
     p2 = p1;
     p1 = v;
   }
 }
 
-int scv_launch_delta_wedge(scv_ctx* c, int L, const double* edge, double* out, cudaStream_t s) {
+int scv_launch_delta_wedge(scv_ctx* c, int L, const double* edge, const int* edge_e, double* out, cudaStream_t s) {
   long long total = (long long)L * (L + 1) / 2;
   int blocks = (int)((total + 255) / 256);
-  k_delta_wedge<<<blocks, 256, 0, s>>>(L, edge, out);
+  k_delta_wedge<<<blocks, 256, 0, s>>>(L, edge, edge_e, out);
   c->launches++;
   SCV_CUDA(c, cudaGetLastError());
   return SCV_OK;

@@ -961,6 +961,7 @@ __global__ void __launch_bounds__(PfaCfg<K, true>::NT, PfaCfg<K, true>::MINB)
 // summation order is fixed (bit-reproducible).
 // ---------------------------------------------------------------------------
 template <int K> struct PfaQCfg { static constexpr int RQ = 1, NT = 256, MINB = 1; };
+template <> struct PfaQCfg<4095> { static constexpr int RQ = 1, NT = 512, MINB = 1; };
 template <> struct PfaQCfg<255> { static constexpr int RQ = 1, NT = 128, MINB = 1; };
 #ifndef SCV_Q1023
 #define SCV_Q1023 1, 352, 1
@@ -1427,6 +1428,7 @@ int scv_pfa_syn_gamma_q(scv_ctx* c, int K, int real, int tr, const double2* chun
     case 511: return run_syn_gamma_q<511>(c, real, tr, chunk, b0, nbb, qtab, mbase, wout, s);
     case 1023: return run_syn_gamma_q<1023>(c, real, tr, chunk, b0, nbb, qtab, mbase, wout, s);
     case 2047: return run_syn_gamma_q<2047>(c, real, tr, chunk, b0, nbb, qtab, mbase, wout, s);
+    case 4095: return run_syn_gamma_q<4095>(c, real, tr, chunk, b0, nbb, qtab, mbase, wout, s);
     default: return scv_fail(c, SCV_EINVAL, "no gamma+quadrature kernel for length " + std::to_string(K));
   }
 }

@@ -171,7 +171,7 @@ int scv_plan(scv_ctx* c, const std::string& key, int rank, int* n, int* inembed,
 int scv_plan_exec_setup(scv_ctx* c, cufftHandle h, cudaStream_t s);
 
 // kernels launched from other units
-int scv_launch_delta_wedge(scv_ctx* c, int L, const double* edge, double* out, cudaStream_t s);
+int scv_launch_delta_wedge(scv_ctx* c, int L, const double* edge, const int* edge_e, double* out, cudaStream_t s);
 int scv_beta_sht(scv_ctx* c, int L, int spin, int real, const double2* G, double2* Gw, double pref,
                  cudaStream_t s);
 int scv_beta_so3(scv_ctx* c, int L, int real, const double2* W1p, double2* w, double pref,

@@ -146,7 +146,7 @@ static int check_so3(scv_ctx* c, int L) {
 // alpha DFT rows -> beta chunk; gamma DFT fused with the beta quadrature,
 // accumulated into w (the partial sum over this slab's beta rows).
 static bool use_betaq(scv_ctx* c, int L) {
-  return scv_pfa_supported(2 * L - 1) && L >= 128 && L <= 1024 && c->opt_betaq != 0 &&
+  return scv_pfa_supported(2 * L - 1) && L >= 128 && L <= 2048 && c->opt_betaq != 0 &&
          (c->opt_betaq == 1 || scv_betaq_enabled(L));
 }
 
@@ -211,7 +211,7 @@ extern "C" int scv_so3_forward_curvelet_slab(scv_ctx* c, int L, int real, const 
   SCV_TRY(check_so3(c, L));
   SCV_TRY(check_slab(c, L, b0, nb));
   if (!use_betaq(c, L))
-    return scv_fail(c, SCV_EINVAL, "beta-slab synthesis needs the beta-quadrature path (prime-factor K, 128 <= L <= 1024)");
+    return scv_fail(c, SCV_EINVAL, "beta-slab synthesis needs the beta-quadrature path (prime-factor K, 128 <= L <= 2048)");
   cudaStream_t s = (cudaStream_t)stream;
   SCV_CUDA(c, cudaSetDevice(c->device));
   SCV_TRY(scv_ensure_delta(c, L, s));

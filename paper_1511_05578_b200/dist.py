@@ -51,7 +51,7 @@ __all__ = ["ScalePlan", "ShardedCoeffs", "CudaBackend", "analyze_sharded", "synt
 def cuda_splittable(Lj: int, real: bool) -> bool:
     """Scales the beta-slab kernels support (include/scurve_b200.h)."""
     K = 2 * Lj - 1
-    return (not real) and 128 <= Lj <= 1024 and (K & (K + 1)) == 0
+    return (not real) and 128 <= Lj <= 2048 and (K & (K + 1)) == 0
 
 
 @dataclass

@@ -23,7 +23,8 @@ import torch
 
 from . import _cabi
 from .so3 import (CurveletWignerCoeffs, SO3Grid, SO3Signal, so3_forward_curvelet,
-                  so3_forward_curvelet_real, so3_inverse_curvelet, so3_inverse_curvelet_real)
+                  so3_forward_curvelet_real, so3_forward_curvelet_slab, so3_inverse_curvelet,
+                  so3_inverse_curvelet_real, so3_inverse_curvelet_slab)
 from .sphere import (HarmonicCoeffs, SphereGrid, SphereSignal, sht_forward, sht_forward_real,
                      sht_inverse, sht_inverse_real)
 from .tiling import Tiling, TilingParams, curvelet_harmonics
@@ -32,6 +33,7 @@ __all__ = [
     "CurveletCoeffs",
     "analyze",
     "analyze_real",
+    "roundtrip_streamed",
     "scale_band_limit",
     "scaling_band_limit",
     "synthesize",
@@ -209,3 +211,90 @@ def synthesize_real(c: CurveletCoeffs, t: Tiling) -> SphereSignal:
     if not c.real:
         raise ValueError("synthesize_real requires real-flagged coefficients")
     return _synthesize(c, t, True)
+
+
+# ---------------------------------------------------------------------------
+# beta-slab streamed round trip
+# ---------------------------------------------------------------------------
+def _slab_streamable(Lj: int) -> bool:
+    """Scales the beta-slab kernels take (include/scurve_b200.h): complex
+    path, prime-factor K = 2^k - 1, 128 <= L_j <= 2048."""
+    K = 2 * Lj - 1
+    return 128 <= Lj <= 2048 and (K & (K + 1)) == 0
+
+
+def _syn_chunk_rows(Lj: int) -> int:
+    """Beta rows per synthesis launch pair inside the library (so3.cu,
+    forward_q_slab: a 1 GiB chunk of (K, K) planes)."""
+    K = 2 * Lj - 1
+    return max(1, min(Lj, (1 << 30) // (K * K * 16)))
+
+
+def roundtrip_streamed(f: SphereSignal, t: Tiling, multires: bool = True, slab_bytes: int = 8 << 30,
+                       consumer=None):
+    """``synthesize(analyze(f, t), t)`` without holding the coefficients.
+
+    The reference's round trip (``cli.cmd_roundtrip``, cli.py:227-246) keeps
+    every scale signal in memory: 147 GB at L=1024 and 1.18 TB at L=2048
+    (BASELINE config C5), more than one B200 holds.  Here each large scale
+    (prime-factor K, 128 <= L_j <= 2048) is analysed in beta slabs of at most
+    ``slab_bytes``; every slab is handed to ``consumer(j, slab)`` (an
+    ``SO3Slab``: the rows [b0, b0+nb) of scale j's signal, valid only during
+    the call) and then folded into scale j's Wigner coefficients by the slab
+    synthesis, before the next slab overwrites the buffer.  Smaller scales
+    run whole (``consumer(j, SO3Signal)``).  The scaling signal is passed as
+    ``consumer("scaling", SphereSignal)``.
+
+    Slab heights are multiples of the library's synthesis chunk, so the
+    summation order is the whole-scale one and the result is bit-identical
+    to ``synthesize(analyze(f, t), t)``.  Returns the reconstructed signal.
+    """
+    _check_signal(f, t)
+    p = t.params
+    L = p.band_limit
+    dev = f.values.device
+    ctx = _cabi.context(dev)
+    dt = device_tiling(t, dev)
+    flm = sht_forward(f)
+    acc = torch.zeros(L * L, dtype=torch.complex128, device=dev)
+    slab_buf = None
+    for j in range(p.j_min, p.j_max + 1):
+        Lj = scale_band_limit(p, j) if multires else L
+        K = 2 * Lj - 1
+        grid = SO3Grid(Lj, Lj, Lj)
+        w = _scale_wigner(ctx, flm, dt, j, Lj)
+        if _slab_streamable(Lj):
+            ch = _syn_chunk_rows(Lj)
+            nb = max(ch, (slab_bytes // (K * K * 16)) // ch * ch)
+            nb = min(nb, Lj)
+            need = K * nb * K
+            if slab_buf is None or slab_buf.numel() < need:
+                slab_buf = None
+                slab_buf = torch.empty(need, dtype=torch.complex128, device=dev)
+            W = None
+            for b0 in range(0, Lj, nb):
+                nbb = min(nb, Lj - b0)
+                out = slab_buf[: K * nbb * K].view(K, nbb, K)
+                slab = so3_inverse_curvelet_slab(w, grid, b0, nbb, out=out)
+                if consumer is not None:
+                    consumer(j, slab)
+                if W is None:
+                    W = so3_forward_curvelet_slab(slab)
+                else:
+                    so3_forward_curvelet_slab(slab, out=W.values, accumulate=True)
+        else:
+            sig = so3_inverse_curvelet(w, grid)
+            if consumer is not None:
+                consumer(j, sig)
+            W = so3_forward_curvelet(sig)
+            del sig
+        pos, neg = dt.psi[j]
+        ctx.call("accumulate", L, Lj, _cabi.ptr(W.values), _cabi.ptr(pos), _cabi.ptr(neg), _cabi.ptr(acc))
+    Ls = scaling_band_limit(p) if multires else L
+    scaling_sig = sht_inverse(_scaling_coeffs(ctx, flm, dt, Ls, False))
+    if consumer is not None:
+        consumer("scaling", scaling_sig)
+    slm = sht_forward(scaling_sig)
+    ctx.call("accumulate_scaling", L, slm.band_limit, _cabi.ptr(slm.values), _cabi.ptr(dt.scaling), _cabi.ptr(acc))
+    ctx.call("finish_acc", L, p.spin, 0, _cabi.ptr(acc))
+    return sht_inverse(HarmonicCoeffs(L, p.spin, acc))

@@ -70,13 +70,13 @@ int scv_pfa_tables(scv_ctx* c, int K, const double2** out) {
     if (p == 1) continue;
     if (pfa_use_mma(p)) {
       // dense C and S matrices (M rows x pitch doubles each), row 0 = (1, 0)
-      const int h = (p - 1) / 2, M = mma_M(p), PA = mma_pitch(mma_Kp(p));
+      const int h = (p - 1) / 2, M = mma_M(p), PA = mma_pa(p);
       std::vector<double> C((size_t)M * PA, 0.0), S((size_t)M * PA, 0.0);
       for (int k = 0; k <= h; ++k)
         for (int j = 1; j <= h; ++j) {
           const ld a = twopi * (ld)(((long long)j * k) % p) / (ld)p;
-          C[(size_t)k * PA + (j - 1)] = (double)cosl(a);
-          S[(size_t)k * PA + (j - 1)] = (double)sinl(a);
+          C[(size_t)mma_aoff(p, k, j - 1)] = (double)cosl(a);
+          S[(size_t)mma_aoff(p, k, j - 1)] = (double)sinl(a);
         }
       const size_t base = tab.size();
       tab.resize(base + (size_t)M * PA);
@@ -234,6 +234,67 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
 #endif
     __syncthreads();
     if (NBUF == 2) cur ^= 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// batched rows, warp-group variant: the CTA holds ONE copy of the tables and
+// NG independent groups of NTG threads, each owning a row buffer and a named
+// barrier (bar.sync 1+g).  A group loads its row (cp.async), runs the stages
+// with group-local barriers and stores it; groups drift apart, so one group's
+// load / store phase overlaps the others' DMMA stages without CTA-wide
+// barriers (vs k_pfa_rows: 2 CTAs per SM, each CTA-synchronised, tables
+// duplicated per CTA).
+// ---------------------------------------------------------------------------
+#ifndef SCV_ROWS_GRP
+#define SCV_ROWS_GRP 5, 96
+#endif
+template <int K> struct PfaGrpCfg { static constexpr int NG = 0, NTG = 0; };
+#define SCV_RGCFG_(KK, ...)                                  \
+  template <> struct PfaGrpCfg<KK> {                         \
+    static constexpr int v_[2] = {__VA_ARGS__};              \
+    static constexpr int NG = v_[0], NTG = v_[1];            \
+  };
+SCV_RGCFG_(2047, SCV_ROWS_GRP)
+template <int K>
+static constexpr size_t pfa_smem_grp() {
+  using PL = PfaPlan<K>;
+  return ((size_t)pfa_tab_total<PL>() + (size_t)PfaGrpCfg<K>::NG * K) * sizeof(double2);
+}
+
+// GATHER = 1 (synthesis alpha): row r = bb*K + g of the launch reads the
+// input row (g, b0 + bb) of a (K, lsig, K) signal, i.e. in + g*lsig*K +
+// (b0+bb)*K, and writes chunk row r (the [bb][g][m] beta chunk).
+template <int K, int DIR, int GATHER>
+__global__ void __launch_bounds__(PfaGrpCfg<K>::NG * PfaGrpCfg<K>::NTG, 1)
+    k_pfa_rows_g(long long nrows, const double2* in, double2* out, const double2* __restrict__ gtab,
+                 long long LK = 0, int b0 = 0) {
+  using PL = PfaPlan<K>;
+  constexpr int NG = PfaGrpCfg<K>::NG, NTG = PfaGrpCfg<K>::NTG;
+  extern __shared__ double2 sm[];
+  double2* tab = sm;
+  pfa_load_tables<PL, NG * NTG>(tab, gtab);
+  const int g = threadIdx.x / NTG, gtid = threadIdx.x - g * NTG, bar = 1 + g;
+  double2* const X = sm + pfa_tab_total<PL>() + g * K;
+#pragma unroll 1
+  for (long long r = (long long)blockIdx.x * NG + g; r < nrows; r += (long long)gridDim.x * NG) {
+    const double2* src;
+    if constexpr (GATHER) {
+      const long long bb = r / K, g = r - bb * K;
+      src = in + g * LK + (b0 + bb) * K;
+    } else {
+      src = in + r * K;
+    }
+#pragma unroll 4
+    for (int n = gtid; n < K; n += NTG) cp_async16(X + pfa_in_tab<PL>(tab, n), src + n);
+    cp_async_commit();
+    cp_async_wait<0>();
+    grp_sync(bar, NTG);
+    pfa_dft<PL, DIR, 1, NTG, K>(X, tab, nullptr, gtid, bar);
+    double2* dst = out + r * K;
+#pragma unroll 4
+    for (int k = gtid; k < K; k += NTG) dst[k] = X[pfa_pos_tab<PL>(tab, k)];
+    grp_sync(bar, NTG);
   }
 }
 
@@ -448,6 +509,13 @@ template <int K> struct PfaSCfg { static constexpr int R = 2, NT = 384, MINB = 1
 #define SCV_COLGEN_S_NT 512
 #endif
 template <> struct PfaSCfg<2047> { static constexpr int R = 2, NT = SCV_COLGEN_S_NT, MINB = 1, BB = SCV_COLGEN_S_BB; };
+// NGR > 1: the CTA runs NGR independent groups of NT/NGR threads, group g
+// generating and transforming column m0 + g with its own named barrier, so
+// one group's generation (exp, coefficient reads) overlaps the other's DMMA
+// stages instead of the whole CTA alternating between the two phases.
+#ifndef SCV_COLGEN_S_NGR
+#define SCV_COLGEN_S_NGR 1
+#endif
 template <int K>
 static constexpr size_t pfa_smem_s() {
   using PL = PfaPlan<K>;
@@ -496,6 +564,51 @@ __global__ void __launch_bounds__(PfaSCfg<K>::NT, PfaSCfg<K>::MINB)
       }
     }
     const int bs_end = min(nb, (bblk + 1) * BB);
+    if constexpr (SCV_COLGEN_S_NGR > 1) {
+      // group g owns column m0 + g (R == NGR): generation of one group
+      // overlaps the other group's transform
+      static_assert(R == SCV_COLGEN_S_NGR, "one column per group");
+      constexpr int NTG = NT / SCV_COLGEN_S_NGR, NPG = (K + NTG - 1) / NTG;
+      const int g = threadIdx.x / NTG, gtid = threadIdx.x - g * NTG, bar = 1 + g;
+      double2* const Xg = X + g * K;
+      const int mg = m0 + g <= L - 1 ? m0 + g : m0 + g - K, amg = mg < 0 ? -mg : mg;
+      __syncthreads();  // coefficients staged
+#pragma unroll 1
+      for (int bs = bblk * BB; bs < bs_end; ++bs) {
+        const int b = b0 + bs;
+        const double ls = lsin[b], lc = lcos[b];
+#pragma unroll 2
+        for (int u = 0; u < NPG; ++u) {
+          const int gi = gtid + u * NTG;
+          if (gi >= K) continue;
+          const int n = gi <= L - 1 ? gi : gi - K;
+          const int l = n < 0 ? -n : n;
+          double2 v = make_double2(0.0, 0.0);
+          if (m0 + g < K && amg <= l) {
+            const int es = n >= 0 ? l - mg : l + mg;
+            const int ec = n >= 0 ? l + mg : l - mg;
+            double lg = CH[gi * R + g];
+            if (es) lg += (double)es * ls;
+            if (ec) lg += (double)ec * lc;
+            double d = exp(lg);
+            if (n < 0 && ((l - mg) & 1)) d = -d;
+            const double f = (double)(2 * l + 1) * fac0 * d;
+            const double2 c = CW[gi * R + g];
+            v = make_double2(f * c.x, f * c.y);
+          }
+          Xg[pfa_in_tab<PL>(tab, gi)] = v;
+        }
+        grp_sync(bar, NTG);
+        pfa_dft<PL, +1, 1, NTG, K>(Xg, tab, scr, gtid, bar);
+        if (m0 + g < K) {
+#pragma unroll 4
+          for (int gg = gtid; gg < K; gg += NTG) out[((long long)gg * nb + bs) * K + m0 + g] = Xg[pfa_pos_tab<PL>(tab, gg)];
+        }
+        grp_sync(bar, NTG);
+      }
+      __syncthreads();  // both groups done with CW / CH before restaging
+      continue;
+    }
 #pragma unroll 1
     for (int bs = bblk * BB; bs < bs_end; ++bs) {
       const int b = b0 + bs;
@@ -1208,6 +1321,17 @@ template <int K, int DIR>
 static int run_rows(scv_ctx* c, long long nrows, const double2* in, double2* out, cudaStream_t s) {
   const double2* tab;
   SCV_TRY(scv_pfa_tables(c, K, &tab));
+  if constexpr (PfaGrpCfg<K>::NG > 0) {
+    constexpr size_t smg = pfa_smem_grp<K>();
+    static_assert(smg <= 232448, "grouped rows launch shape exceeds the 227 KB shared-memory limit");
+    constexpr int NTB = PfaGrpCfg<K>::NG * PfaGrpCfg<K>::NTG;
+    int grid;
+    SCV_TRY(persistent_grid(c, k_pfa_rows_g<K, DIR, 0>, NTB, smg, (nrows + PfaGrpCfg<K>::NG - 1) / PfaGrpCfg<K>::NG, &grid));
+    k_pfa_rows_g<K, DIR, 0><<<grid, NTB, smg, s>>>(nrows, in, out, tab);
+    c->launches++;
+    SCV_CUDA(c, cudaGetLastError());
+    return SCV_OK;
+  }
   constexpr size_t sm = pfa_smem<K, false>();
   static_assert(sm <= 232448, "prime-factor launch shape exceeds the 227 KB shared-memory limit");
   int grid;
@@ -1319,6 +1443,19 @@ static int run_syn_alpha(scv_ctx* c, int real, int tr, const void* in, int lsig,
   SCV_TRY(scv_pfa_tables(c, K, &tab));
   constexpr size_t sm = pfa_smem<K, false>();
   static_assert(sm <= 232448, "prime-factor launch shape exceeds the 227 KB shared-memory limit");
+  if constexpr (PfaGrpCfg<K>::NG > 0) {
+    if (!real && !tr) {
+      constexpr size_t smg = pfa_smem_grp<K>();
+      constexpr int NTB = PfaGrpCfg<K>::NG * PfaGrpCfg<K>::NTG;
+      const long long nrows = (long long)K * nbb;
+      int grid;
+      SCV_TRY(persistent_grid(c, k_pfa_rows_g<K, -1, 1>, NTB, smg, (nrows + PfaGrpCfg<K>::NG - 1) / PfaGrpCfg<K>::NG, &grid));
+      k_pfa_rows_g<K, -1, 1><<<grid, NTB, smg, s>>>(nrows, (const double2*)in, chunk, tab, (long long)lsig * K, b0);
+      c->launches++;
+      SCV_CUDA(c, cudaGetLastError());
+      return SCV_OK;
+    }
+  }
   const int rpb = real ? 2 * PfaCfg<K, false>::R : PfaCfg<K, false>::R;
   const long long nb = ((long long)K * nbb + rpb - 1) / rpb;
   int grid;

@@ -82,10 +82,33 @@ __host__ __device__ constexpr int mma_Kp(int p) { return ((pfa_h(p) + 3) / 4) * 
 __host__ __device__ constexpr int mma_pitch(int n) {  // row pitch (doubles) with pitch mod 16 in {4, 12}
   return (n % 16 == 4 || n % 16 == 12) ? n : (n % 16 < 4 ? n + (4 - n % 16) : n % 16 < 12 ? n + (12 - n % 16) : n + (20 - n % 16));
 }
+// A-operand layout of the DMMA stages.  SCV_PFA_A2 = 1 (experimental, with the
+// warp-owned blocks; measured 1.5x SLOWER on B200 -- register pressure and
+// spills in the 2047 kernels -- so off by default): the coefficients of k-steps 2q and 2q+1 of one A
+// fragment are adjacent, C2[row][q][ac][kt & 1] (kt = 4-wide k-step, ac = lane
+// & 3), so one 16-byte LDS feeds two k-steps; the row pitch is 8 mod 16
+// doubles, which makes each 8-lane phase of the 16-byte loads cover all 32
+// banks.  SCV_PFA_A2 = 0 (default): plain row-major [row][j], pitch 4|12 mod 16.
+#ifndef SCV_PFA_A2
+#define SCV_PFA_A2 0
+#endif
+#ifndef SCV_PFA_Q_UNROLL
+#define SCV_PFA_Q_UNROLL 1
+#endif
+constexpr int pfa_q_unroll = SCV_PFA_Q_UNROLL;
+static_assert(!SCV_PFA_A2 || SCV_PFA_BLK, "the paired A layout is implemented by the warp-owned block stage only");
+__host__ __device__ constexpr int mma_pa(int p) {
+  return SCV_PFA_A2 ? (((mma_Kp(p) + 7) / 8) * 8) % 16 == 0 ? ((mma_Kp(p) + 7) / 8) * 8 + 8 : ((mma_Kp(p) + 7) / 8) * 8
+                    : mma_pitch(mma_Kp(p));
+}
+// offset (doubles) of coefficient (row, reduction index kk = j - 1) in a DMMA table
+__host__ __device__ constexpr int mma_aoff(int p, int row, int kk) {
+  return SCV_PFA_A2 ? row * mma_pa(p) + (kk / 8) * 8 + (kk % 4) * 2 + (kk / 4) % 2 : row * mma_pa(p) + kk;
+}
 // table size in double2 units: 1-D (cos, sin) table of p entries, or the two
 // dense matrices (2 * M * pitch doubles = M * pitch double2)
 __host__ __device__ constexpr int pfa_tab(int p) {
-  return p <= 1 ? 0 : pfa_use_mma(p) ? mma_M(p) * mma_pitch(mma_Kp(p)) : p;
+  return p <= 1 ? 0 : pfa_use_mma(p) ? mma_M(p) * mma_pa(p) : p;
 }
 template <class PL>
 __host__ __device__ constexpr int pfa_rtab_total() {
@@ -578,7 +601,7 @@ __device__ __forceinline__ void pfa_stage_mma_blk(double2* X, const double2* tab
   constexpr int step = pfa_st<PL, S>();
   constexpr int nbf = K / p;
   constexpr int NBF = R * nbf;
-  constexpr int M = mma_M(p), Kp = mma_Kp(p), PA = mma_pitch(Kp);
+  constexpr int M = mma_M(p), Kp = mma_Kp(p), PA = mma_pa(p);
   constexpr int M8 = (h + 1 + 7) / 8;          // m8 tiles covering k = 0..h
   constexpr int NBLK = 2 * ((NBF + 7) / 8);    // blocks of 4 (two per group of 8)
   constexpr int NW = NT / 32;
@@ -634,6 +657,50 @@ __device__ __forceinline__ void pfa_stage_mma_blk(double2* X, const double2* tab
         bn[w] = Xd[rowd[w] + 2 * pb[w]];
       }
     }
+#if SCV_PFA_A2
+    // k-steps in pairs: one 16-byte A load per (tile, C|S) feeds steps 2q, 2q+1
+    constexpr int KT = Kp / 4, KQ = (KT + 1) / 2;
+#pragma unroll pfa_q_unroll
+    for (int q = 0; q < KQ; ++q) {
+      double2 aC2[M8], aS2[M8];
+#pragma unroll
+      for (int t = 0; t < M8; ++t) {
+        const int off = (t * 8 + ar) * PA + q * 8 + ac * 2;
+        aC2[t] = *(const double2*)(Cm + off);
+        aS2[t] = *(const double2*)(Sm + off);
+      }
+#pragma unroll
+      for (int two = 0; two < 2; ++two) {
+        const int kt = 2 * q + two;
+        if (KT % 2 == 1 && kt >= KT) break;
+        double bS[NBW], bD[NBW];
+#pragma unroll
+        for (int w = 0; w < NBW; ++w) {
+          const double a = an[w], bb = bn[w];
+          pa[w] += 4 * step;
+          pb[w] -= 4 * step;
+          an[w] = 0.0;
+          bn[w] = 0.0;
+          if (kt + 1 < KT && okB[w] && ((Kp == h) || (4 * kt + 4 + ac + 1 <= h))) {
+            an[w] = Xd[rowd[w] + 2 * pa[w]];
+            bn[w] = Xd[rowd[w] + 2 * pb[w]];
+          }
+          bS[w] = a + bb;
+          bD[w] = a - bb;
+        }
+#pragma unroll
+        for (int t = 0; t < M8; ++t) {
+          const double aC = two ? aC2[t].y : aC2[t].x;
+          const double aS = two ? aS2[t].y : aS2[t].x;
+#pragma unroll
+          for (int w = 0; w < NBW; ++w) {
+            dmma(accC[w][t][0], accC[w][t][1], aC, bS[w]);
+            dmma(accS[w][t][0], accS[w][t][1], aS, bD[w]);
+          }
+        }
+      }
+    }
+#else
 #pragma unroll pfa_kt_unroll
     for (int kt = 0; kt < Kp / 4; ++kt) {
       double bS[NBW], bD[NBW];
@@ -663,6 +730,7 @@ __device__ __forceinline__ void pfa_stage_mma_blk(double2* X, const double2* tab
         }
       }
     }
+#endif
     __syncwarp();
 #pragma unroll
     for (int w = 0; w < NBW; ++w) {

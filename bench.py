@@ -176,6 +176,51 @@ def ncu_traffic(stage, Ljs):
             "kernel": e["kernel"], "source": e["source"]}
 
 
+# Prime-factor plans and launch shapes of the DFT engine (csrc/pfa.cuh PfaPlan,
+# pfa.cu PfaCfg / PfaSCfg / PfaGCfg / PfaQCfg), mirrored to count the FP64
+# tensor-core (DMMA m8n8k4, 512 flops each) instructions a pass executes:
+# per call of R rows, a DMMA radix p (h = (p-1)/2) runs 2*ceil(R*(K/p)/8)
+# warp blocks x ceil((h+1)/8) m8 tiles x ceil(h/4) k-steps x 2 (C.s, S.d).
+# Cross-checked against ncu: 1081 DMMA per K=2047 row (sm__inst_executed_pipe_
+# tensor_subpipe_dmma, profiles/r01v8_ncu_k_pfa_rows.txt) vs 1080 here.
+PFA_PLAN = {3: (3,), 7: (7,), 15: (3, 5), 31: (31,), 63: (7, 9), 255: (3, 5, 17), 511: (7, 73),
+            1023: (3, 11, 31), 2047: (23, 89), 4095: (5, 7, 9, 13)}
+PFA_R = {  # rows per transform call by stage
+    "so3inv_rows": {1023: 2, 511: 4, 255: 8},
+    "so3inv_colgen": {2047: 2, 1023: 4, 511: 4, 255: 8, 4095: 2},
+    "so3fwd_alpha": {1023: 2, 511: 4, 255: 8},
+    "so3fwd_gamma_q": {},
+}
+DMMA_PEAK_TF = 36.9  # measured, 8 independent chains x 32 warps/SM (profiles/r01_fp64_pipe_microbench.log)
+
+
+def dmma_per_row(K, R):
+    if K not in PFA_PLAN:
+        return None
+    tot = 0
+    for p in PFA_PLAN[K]:
+        if p < (9 if K == 4095 else 17):
+            continue
+        h = (p - 1) // 2
+        nblk = 2 * ((R * (K // p) + 7) // 8)
+        tot += nblk * ((h + 1 + 7) // 8) * ((h + 3) // 4) * 2
+    return tot / R
+
+
+def executed_dmma(stage, Ljs):
+    """Executed DMMA flops of one map's launches of `stage` (None if a scale is not on the engine)."""
+    if stage not in PFA_R:
+        return None
+    fl = 0.0
+    for L in Ljs:
+        K = 2 * L - 1
+        d = dmma_per_row(K, PFA_R[stage].get(K, 1))
+        if d is None:
+            continue
+        fl += d * 512.0 * K * L  # K*L transforms of length K per pass
+    return fl
+
+
 def stage_roofline(a, prof, Ljs, hbm_peak, fp64_peak):
     """Roofline of the dominant stage from the live per-stage CUDA-event times."""
     K = lambda L: 2 * L - 1  # noqa: E731
@@ -227,6 +272,14 @@ def stage_roofline(a, prof, Ljs, hbm_peak, fp64_peak):
                     "frac": ach / hbm_peak, "peak_source": "MEASURED_PEAKS.json hbm_gbs"})
         if name in flops_stage:
             out["fp64_tflops_alg"] = flops_stage[name] / (ms_map * 1e-3) / 1e12
+    ex = executed_dmma(name, Ljs)
+    if ex:
+        # what the kernel's own pipe does: FP64 tensor-core (DMMA) flops the
+        # prime-factor engine issues, vs the measured DMMA peak
+        out["executed_dmma"] = {"tflops": ex / (ms_map * 1e-3) / 1e12, "peak_tflops": DMMA_PEAK_TF,
+                                "frac": ex / (ms_map * 1e-3) / 1e12 / DMMA_PEAK_TF,
+                                "flops_per_map": ex, "source": "DMMA count of the engine's launch shapes "
+                                "(bench.py dmma_per_row; 1080/row at K=2047 vs ncu 1081)"}
     tr = ncu_traffic(name, Ljs)
     # measured DRAM bytes (GB per map) vs the algorithmic bytes behind `achieved`
     out["traffic"] = None if tr is None else tr["bytes_per_map"] / 1e9
@@ -240,6 +293,9 @@ def stage_roofline(a, prof, Ljs, hbm_peak, fp64_peak):
             e["hbm_gbs_alg"] = bytes_stage[nm] / (mm * 1e-3) / 1e9
         if nm in flops_stage:
             e["fp64_tflops_alg"] = flops_stage[nm] / (mm * 1e-3) / 1e12
+        exn = executed_dmma(nm, Ljs)
+        if exn:
+            e["dmma_frac"] = exn / (mm * 1e-3) / 1e12 / DMMA_PEAK_TF
         out["all_stages"][nm] = e
     return out
 

@@ -68,7 +68,7 @@ int scv_pfa_tables(scv_ctx* c, int K, const double2** out) {
   for (int s = 0; s < 4; ++s) {
     const int p = f[s];
     if (p == 1) continue;
-    if (pfa_use_mma(p)) {
+    if (pfa_use_mma(p, K)) {
       // dense C and S matrices (M rows x pitch doubles each), row 0 = (1, 0)
       const int h = (p - 1) / 2, M = mma_M(p), PA = mma_pa(p);
       std::vector<double> C((size_t)M * PA, 0.0), S((size_t)M * PA, 0.0);

@@ -64,7 +64,15 @@ __host__ __device__ constexpr int pfa_gp(int p) { return p > 1 ? ((pfa_h(p) + pf
 #ifndef SCV_MMA_MIN_RADIX
 #define SCV_MMA_MIN_RADIX 17
 #endif
-__host__ __device__ constexpr bool pfa_use_mma(int p) { return p >= SCV_MMA_MIN_RADIX; }
+// per length: K = 4095 = 5*7*9*13 runs its radices 9 and 13 on DMMA too
+// (measured 48 vs 29 G points/s: the all-DFMA stages of 4095 spill), while
+// 1023 keeps radix 11 on DFMA (66 vs 54 G points/s)
+#ifndef SCV_MMA_MIN_RADIX_4095
+#define SCV_MMA_MIN_RADIX_4095 9
+#endif
+__host__ __device__ constexpr bool pfa_use_mma(int p, int K) {
+  return p >= (K == 4095 ? SCV_MMA_MIN_RADIX_4095 : SCV_MMA_MIN_RADIX);
+}
 // DMMA stage variant: 1 = warp-owned butterfly blocks (pfa_stage_mma_blk, no
 // scratch), 0 = register-held 16x16 tiles / scratch-staged B (A/B builds)
 #ifndef SCV_PFA_BLK
@@ -107,12 +115,12 @@ __host__ __device__ constexpr int mma_aoff(int p, int row, int kk) {
 }
 // table size in double2 units: 1-D (cos, sin) table of p entries, or the two
 // dense matrices (2 * M * pitch doubles = M * pitch double2)
-__host__ __device__ constexpr int pfa_tab(int p) {
-  return p <= 1 ? 0 : pfa_use_mma(p) ? mma_M(p) * mma_pa(p) : p;
+__host__ __device__ constexpr int pfa_tab(int p, int K) {
+  return p <= 1 ? 0 : pfa_use_mma(p, K) ? mma_M(p) * mma_pa(p) : p;
 }
 template <class PL>
 __host__ __device__ constexpr int pfa_rtab_total() {
-  return pfa_tab(PL::P0) + pfa_tab(PL::P1) + pfa_tab(PL::P2) + pfa_tab(PL::P3);
+  return pfa_tab(PL::P0, PL::K) + pfa_tab(PL::P1, PL::K) + pfa_tab(PL::P2, PL::K) + pfa_tab(PL::P3, PL::K);
 }
 // followed by two 16-bit maps: out[k] = position of output frequency k,
 // in[n] = position of input sample n (see pfa_st)
@@ -138,7 +146,7 @@ __device__ __forceinline__ int pfa_base(int c) {
 }
 template <class PL, int S>
 __host__ __device__ constexpr int pfa_tab_off() {
-  return (S > 0 ? pfa_tab(PL::P0) : 0) + (S > 1 ? pfa_tab(PL::P1) : 0) + (S > 2 ? pfa_tab(PL::P2) : 0);
+  return (S > 0 ? pfa_tab(PL::P0, PL::K) : 0) + (S > 1 ? pfa_tab(PL::P1, PL::K) : 0) + (S > 2 ? pfa_tab(PL::P2, PL::K) : 0);
 }
 // scratch (double2 units) for a DMMA stage over R rows: B matrices s and d
 // (Kp x pitch(2*NBF padded to 16) doubles each) + x0 per butterfly
@@ -154,7 +162,7 @@ __host__ __device__ constexpr int mma_tpw(int K, int p, int R, int NT) {
 }
 __host__ __device__ constexpr bool mma_reg(int K, int p, int R, int NT) { return mma_tpw(K, p, R, NT) <= SCV_PFA_TPW_MAX; }
 __host__ __device__ constexpr int mma_scratch_p(int K, int p, int R, int NT) {
-  return (p > 1 && pfa_use_mma(p) && !SCV_PFA_BLK && !mma_reg(K, p, R, NT)) ? mma_Kp(p) * mma_pitch(mma_ncol(K, p, R)) + R * (K / p) : 0;
+  return (p > 1 && pfa_use_mma(p, K) && !SCV_PFA_BLK && !mma_reg(K, p, R, NT)) ? mma_Kp(p) * mma_pitch(mma_ncol(K, p, R)) + R * (K / p) : 0;
 }
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 template <class PL, int R, int NT>
@@ -762,9 +770,9 @@ __device__ __forceinline__ void pfa_stage_mma_blk(double2* X, const double2* tab
 template <class PL, int S, int DIR, int R, int NT, int PITCH>
 __device__ __forceinline__ void pfa_stage_any(double2* X, const double2* tab, double2* scr, int gtid, int bar) {
   constexpr int p = pfa_p<PL, S>();
-  if constexpr (pfa_use_mma(p) && SCV_PFA_BLK) pfa_stage_mma_blk<PL, S, DIR, R, NT, PITCH>(X, tab, gtid, bar);
-  else if constexpr (pfa_use_mma(p) && mma_reg(PL::K, p, R, NT)) pfa_stage_mma_reg<PL, S, DIR, R, NT, PITCH>(X, tab, gtid, bar);
-  else if constexpr (pfa_use_mma(p)) pfa_stage_mma<PL, S, DIR, R, NT, PITCH>(X, tab, scr, gtid, bar);
+  if constexpr (pfa_use_mma(p, PL::K) && SCV_PFA_BLK) pfa_stage_mma_blk<PL, S, DIR, R, NT, PITCH>(X, tab, gtid, bar);
+  else if constexpr (pfa_use_mma(p, PL::K) && mma_reg(PL::K, p, R, NT)) pfa_stage_mma_reg<PL, S, DIR, R, NT, PITCH>(X, tab, gtid, bar);
+  else if constexpr (pfa_use_mma(p, PL::K)) pfa_stage_mma<PL, S, DIR, R, NT, PITCH>(X, tab, scr, gtid, bar);
   else pfa_stage<PL, S, DIR, R, NT, PITCH>(X, tab, gtid, bar);
 }
 

@@ -964,7 +964,7 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
         const int m = i / (2 * R), c = i - m * (2 * R);
         const int r = c >> 1;
         const int ri = (int)r0 + c;
-        if (ri < nrows) {
+        if (ri < nrows && (real != 2 || m < L)) {
           const double2 z = X[r * K + pfa_pos_tab<PL>(tab, m)];
           const double2 zc = X[r * K + pfa_pos_tab<PL>(tab, m == 0 ? 0 : K - m)];
           double2 v;
@@ -976,12 +976,13 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
       }
     } else {
       // Z = X1 + i X2 (X1, X2 Hermitian): X1[k] = (Z[k] + conj Z[-k])/2, X2[k] = (Z[k] - conj Z[-k])/(2i)
+      // (real == 2: only the m >= 0 half the gamma+quadrature pass reads)
 #pragma unroll 4
       for (int i = threadIdx.x; i < 2 * R * K; i += NT) {
         const int c = i / K, m = i - c * K;
         const int r = c >> 1;
         const long long ri = r0 + c;
-        if (ri < nrows) {
+        if (ri < nrows && (real != 2 || m < L)) {
           const double2 z = X[r * K + pfa_pos_tab<PL>(tab, m)];
           const double2 zc = X[r * K + pfa_pos_tab<PL>(tab, m == 0 ? 0 : K - m)];
           double2 v;
@@ -1117,7 +1118,10 @@ __global__ void __launch_bounds__(PfaQCfg<K>::NT, PfaQCfg<K>::MINB)
   using PL = PfaPlan<K>;
   constexpr int NT = PfaQCfg<K>::NT, RQ = PfaQCfg<K>::RQ;
   constexpr int L = (K + 1) / 2;
-  constexpr int NCG = (K + RQ - 1) / RQ;                 // column groups of RQ adjacent m
+  // real: only the columns m >= 0 are transformed (the chunk of a real
+  // signal is Hermitian in (g, m) jointly: T(n, -m) = conj T(-n, m)), and the
+  // n < 0 outputs of column m feed W(-n, -m) = sum_b q_{-n,-m}(b) conj T(n, m)
+  const int NCG = real ? (L + RQ - 1) / RQ : (K + RQ - 1) / RQ;  // column groups of RQ adjacent m
   extern __shared__ double2 sm[];
   double2* tab = sm;
   double2* const scr = sm + pfa_tab_total<PL>();
@@ -1190,8 +1194,9 @@ __global__ void __launch_bounds__(PfaQCfg<K>::NT, PfaQCfg<K>::MINB)
         const int n = gn <= L - 1 ? gn : gn - K;
         const int an = n < 0 ? -n : n;
         qv[r][u] = 0.0;
-        if (col >= K || gn >= K || an < am || (real && n < 0)) continue;
+        if (col >= (real ? L : K) || gn >= K || an < am || (real && n < 0 && m == 0)) continue;
         // raw load only; the sign q_{-l,m} = (-1)^{l+m} q_{l,-m} is applied at use
+        // (real, n < 0: the weight of W(|n|, -m) is q_{|n|,-m} itself)
         qv[r][u] = __ldg(n >= 0 ? qp + n : qn + an);
       }
     }
@@ -1207,9 +1212,10 @@ __global__ void __launch_bounds__(PfaQCfg<K>::NT, PfaQCfg<K>::MINB)
         const int gn = threadIdx.x + u * NT;
         const int n = gn <= L - 1 ? gn : gn - K;
         const int an = n < 0 ? -n : n;
-        if (gn >= K || an < am || (real && n < 0)) continue;
-        const double q = (n < 0 && ((an + m) & 1)) ? -qv[r][u] : qv[r][u];
-        const double2 v = X[r * K + pfa_pos_tab<PL>(tab, gn)];
+        if (gn >= K || an < am || (real && n < 0 && m == 0)) continue;
+        const double q = (!real && n < 0 && ((an + m) & 1)) ? -qv[r][u] : qv[r][u];
+        double2 v = X[r * K + pfa_pos_tab<PL>(tab, gn)];
+        if (real && n < 0) v.y = -v.y;
         acc[r][u].x = fma(v.x, q, acc[r][u].x);
         acc[r][u].y = fma(v.y, q, acc[r][u].y);
       }
@@ -1219,8 +1225,10 @@ __global__ void __launch_bounds__(PfaQCfg<K>::NT, PfaQCfg<K>::MINB)
           const int gn = threadIdx.x + u * NT;
           const int n = gn <= L - 1 ? gn : gn - K;
           const int an = n < 0 ? -n : n;
-          if (gn >= K || an < am || (real && n < 0)) continue;
-          double2* o = wout + ((long long)(n >= 0 ? 0 : 1) * L + an) * K + (m + L - 1);
+          if (gn >= K || an < am || (real && n < 0 && m == 0)) continue;
+          // complex: sheet by the sign of n; real: n < 0 slots hold W(|n|, -m) on sheet 0
+          double2* o = real ? wout + (long long)an * K + ((n < 0 ? -m : m) + L - 1)
+                            : wout + ((long long)(n >= 0 ? 0 : 1) * L + an) * K + (m + L - 1);
           const double2 a = acc[r][u];
 #if SCV_GQ_RED
           // one add per entry per launch, launches stream-ordered: deterministic

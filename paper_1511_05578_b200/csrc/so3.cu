@@ -164,7 +164,8 @@ static int forward_q_slab(scv_ctx* c, int L, int real, const void* sig, int sb0,
     const int nbb = std::min(nbc, sb0 + snb - b0);
     {
       SCV_PROF(c, s, "so3fwd_alpha");
-      SCV_TRY(scv_pfa_syn_alpha(c, K, real, c->opt_chunkt, sig, snb, b0 - sb0, nbb, (double2*)ch, s));
+      // real: the alpha pass keeps only the m >= 0 half (real = 2) the gamma+quadrature pass reads
+      SCV_TRY(scv_pfa_syn_alpha(c, K, real ? 2 : 0, c->opt_chunkt, sig, snb, b0 - sb0, nbb, (double2*)ch, s));
     }
     SCV_PROF(c, s, "so3fwd_gamma_q");
     SCV_TRY(scv_pfa_syn_gamma_q(c, K, real, c->opt_chunkt, (const double2*)ch, b0, nbb, qtab, mbase, (double2*)w, s));

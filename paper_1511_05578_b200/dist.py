@@ -20,7 +20,7 @@ Scales are assigned greedily by cost (the (2L_j-1)^2 L_j sample volume),
 largest first to the least-loaded rank.  Scale-only sharding stops scaling at
 2 GPUs at L=1024 (the two L_j=1024 scales hold 93% of the volume), so every
 scale the beta-slab kernels support (complex path, prime-factor K,
-128 <= L_j <= 1024) is instead split into `world` contiguous beta slabs, one
+128 <= L_j <= 2048) is instead split into `world` contiguous beta slabs, one
 per rank: analysis of a slab needs no communication (the closed-form
 generation is per beta row), and the synthesis partials of the slabs of a
 scale add up to its term (the beta quadrature is a sum over beta rows), so
@@ -45,7 +45,8 @@ import torch.distributed as dist
 
 from .transform import scale_band_limit, scaling_band_limit
 
-__all__ = ["ScalePlan", "ShardedCoeffs", "CudaBackend", "analyze_sharded", "synthesize_sharded"]
+__all__ = ["ScalePlan", "ShardedCoeffs", "CudaBackend", "analyze_sharded", "roundtrip_sharded_streamed",
+           "synthesize_sharded"]
 
 
 def cuda_splittable(Lj: int, real: bool) -> bool:
@@ -271,3 +272,64 @@ def synthesize_sharded(c: ShardedCoeffs, t, group=None, backend=None, dst: int =
     for i in range(nsc):  # coarse -> fine, the reference order
         acc += terms[i]
     return backend.finish(acc, c.scaling, t, c.real)
+
+
+def roundtrip_sharded_streamed(f, t, group=None, backend=None, src: int = 0, dst: int = 0, multires: bool = True,
+                               slab_rows: int | None = None, consumer=None, split: bool = True):
+    """synthesize(analyze(f, t), t) of ONE map over the group, streaming
+    beta slabs: no rank ever holds its scale signals whole.
+
+    The scale plan is analyze_sharded's (whole small scales by owner, the
+    large scales split into one beta slab per rank); each rank walks its
+    slabs in pieces of at most `slab_rows` rows, hands every piece to
+    `consumer(j, piece)` and folds it into scale j's synthesis term at once
+    (the beta quadrature is a sum over rows), then the (J, L^2) term stack is
+    reduced to `dst` as in synthesize_sharded.  Per-rank memory is one piece
+    plus the tables, so BASELINE C5 (L=2048, 1.18 TB of coefficients) runs
+    with ~147 GB of coefficients per rank never materialised.  Returns the
+    reconstructed map on `dst`, None elsewhere.  `f` is read on `src` only.
+    """
+    backend = backend or CudaBackend()
+    rank, world = _rank_world(group)
+    p = t.params
+    L = p.band_limit
+    kw = {} if split else {"splittable": None}
+    if split and hasattr(backend, "splittable"):
+        kw["splittable"] = backend.splittable
+    plan = ScalePlan.build(p, world, multires, real=False, **kw)
+    flm = backend.sht_forward(f) if rank == src else backend.flm_like(L)
+    if world > 1:
+        dist.broadcast(flm, src=src, group=group)
+    terms = torch.zeros((p.scale_count, L * L), dtype=torch.complex128, device=flm.device)
+    for j in plan.owned(rank):
+        Lj = scale_band_limit(p, j) if multires else L
+        sig = backend.scale_inverse(flm, t, j, Lj, False)
+        if consumer is not None:
+            consumer(j, sig)
+        terms[j - p.j_min] = backend.scale_term(sig, t, j, False)
+        del sig
+    for j, b0, nb in plan.slabs_of(rank):
+        Lj = plan.Ljs[j - p.j_min]
+        step = nb if not slab_rows else max(1, min(nb, slab_rows))
+        for c0 in range(b0, b0 + nb, step):
+            piece = backend.scale_inverse_slab(flm, t, j, Lj, c0, min(step, b0 + nb - c0))
+            if consumer is not None:
+                consumer(j, piece)
+            terms[j - p.j_min] += backend.scale_term_slab(piece, t, j)
+            del piece
+    scaling = None
+    if rank == dst:
+        if rank != src:
+            raise ValueError("dst must equal src (the scaling signal is formed where f_lm is)")
+        Ls = scaling_band_limit(p) if multires else L
+        scaling = backend.scaling_map(flm, t, Ls, False)
+        if consumer is not None:
+            consumer("scaling", scaling)
+    if world > 1:
+        dist.reduce(terms, dst=dst, op=dist.ReduceOp.SUM, group=group)
+    if rank != dst:
+        return None
+    acc = torch.zeros(L * L, dtype=torch.complex128, device=terms.device)
+    for i in range(p.scale_count):  # coarse -> fine, the reference order
+        acc += terms[i]
+    return backend.finish(acc, scaling, t, False)

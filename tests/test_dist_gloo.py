@@ -22,7 +22,7 @@ import torch.multiprocessing as mp
 
 from oracle import scurve_oracle as orc
 from paper_1511_05578_b200 import tiling as T
-from paper_1511_05578_b200.dist import ScalePlan, analyze_sharded, synthesize_sharded
+from paper_1511_05578_b200.dist import ScalePlan, analyze_sharded, roundtrip_sharded_streamed, synthesize_sharded
 
 
 class OracleBackend:
@@ -148,6 +148,60 @@ def test_sharded_matches_single_process(L, spin, split_min):
             assert g is None
     # every scale is covered once: whole, or by slabs that partition its beta rows
     assert seen == {j: scales[j - t.params.j_min].shape[1] for j in range(t.params.j_min, t.params.j_max + 1)}
+
+
+def _worker_streamed(rank, world, port, L, spin, q, split_min):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        t = T.build_tiling(T.TilingParams(L, spin, 2.0, 1))
+        be = OracleBackend(L, spin, split_min)
+        f = orc.sht_inverse(orc.gaussian_flm(L, spin, seed=3, real=False), L, spin)
+        pieces = []
+        g = roundtrip_sharded_streamed(f if rank == 0 else None, t, backend=be, slab_rows=3,
+                                       consumer=lambda j, x: pieces.append(
+                                           (j, getattr(x, "b0", None), None if isinstance(j, str) else x.values.shape[1])))
+        q.put((rank, pieces, None if g is None else np.asarray(g)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("L,spin,split_min", [(16, 2, 4), (16, 0, 8)])
+def test_sharded_streamed_round_trip(L, spin, split_min):
+    """roundtrip_sharded_streamed (the C5 decomposition): every rank streams its
+    beta slabs in 3-row pieces, folds each into its synthesis terms, one
+    reduce merges them; the map equals the single-process round trip to
+    rounding and every beta row of every scale is visited exactly once."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_streamed, args=(r, world, port, L, spin, q, split_min)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    t = T.build_tiling(T.TilingParams(L, spin, 2.0, 1))
+    psi = [T.curvelet_harmonics(t, j) for j in range(t.params.j_min, t.params.j_max + 1)]
+    f = orc.sht_inverse(orc.gaussian_flm(L, spin, seed=3, real=False), L, spin)
+    smap, scales = orc.analyze(f, L, spin, 2.0, 1, t.params.j_max, psi, t.scaling)
+    gref = orc.synthesize(smap, scales, L, spin, 2.0, 1, t.params.j_max, psi, t.scaling)
+    rows = {}
+    for rank, pieces, g in res:
+        for j, b0, nb in pieces:
+            if isinstance(j, str):
+                assert rank == 0
+                continue
+            assert nb <= 3 or b0 is None
+            rows[j] = rows.get(j, 0) + nb
+        if rank == 0:
+            assert np.abs(g - gref).max() <= 1e-12 * np.abs(gref).max()
+            assert np.abs(g - f).max() <= 1e-11 * np.abs(f).max()
+        else:
+            assert g is None
+    assert rows == {j: scales[j - t.params.j_min].shape[1] for j in range(t.params.j_min, t.params.j_max + 1)}
 
 
 def test_scale_plan_balances_cost():

@@ -22,6 +22,9 @@
 #include <cmath>
 #include <cstring>
 
+#include <cuda.h>          // CUtensorMap (TMA descriptor type only; encoded via the runtime entry point)
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
+
 #include "pfa.cuh"
 
 typedef long double ld;
@@ -652,6 +655,154 @@ __global__ void __launch_bounds__(PfaSCfg<K>::NT, PfaSCfg<K>::MINB)
     }
     __syncthreads();
   }
+}
+
+// ---------------------------------------------------------------------------
+// Staged column generation with TMA stores (SCV_COLGEN_TMA, K = 2047).
+// k_ana_colgen_s spends ~30% of its stall samples in the store loop: every
+// output element (g, b, m0..m0+1) is a 32-byte piece at stride nb*K*16 B, so
+// each warp store instruction scatters over 16 lines while the DMMA pipe
+// idles (profiles/r01v11_ncu_k_ana_colgen_s.txt).  Here the transformed
+// column pair is permuted in place into the TMA box order [g][m0..m0+1] and
+// written by 8 bulk tensor stores (box 4 doubles x 1 beta row x 256 gamma,
+// out-of-range m / gamma clipped by the TMA unit); the CTA goes on to
+// generate the next row into registers while the TMA engine streams the
+// scattered pieces, and waits for the bulk READ of the buffer only before
+// overwriting it.  Measured on B200 (r01v11): correct, but 170 vs 160 ms/map
+// for the analysis gamma pass -- the scattered 32-byte pieces cost the same
+// whether the LSU or the TMA unit issues them, and the in-place permutation
+// adds two barriers per row -- so it is off by default.
+// ---------------------------------------------------------------------------
+#ifndef SCV_COLGEN_TMA
+#define SCV_COLGEN_TMA 0
+#endif
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* smem, int c0, int c1, int c2) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];"
+               ::"l"(reinterpret_cast<unsigned long long>(map)), "r"(sa), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+template <int K>
+__global__ void __launch_bounds__(PfaSCfg<K>::NT, PfaSCfg<K>::MINB)
+    k_ana_colgen_t(const double2* __restrict__ w, const double* __restrict__ hlb, const double* __restrict__ lsin,
+                   const double* __restrict__ lcos, int b0, int nb, const __grid_constant__ CUtensorMap omap,
+                   const double2* __restrict__ gtab) {
+  using PL = PfaPlan<K>;
+  constexpr int R = PfaSCfg<K>::R, NT = PfaSCfg<K>::NT, BB = PfaSCfg<K>::BB;
+  constexpr int L = (K + 1) / 2;
+  constexpr int NGRP = (K + R - 1) / R;
+  constexpr int GB = 256;                         // gamma rows per TMA box
+  constexpr int NBOX = (K + GB - 1) / GB;
+  static_assert(R == 2, "box inner extent is one column pair (4 doubles)");
+  extern __shared__ __align__(128) double2 sm[];
+  double2* tab = sm;
+  double2* const X = sm + pfa_tab_total<PL>();    // 128-byte aligned (tables are 2816 double2)
+  double2* const CW = X + R * K;
+  double* const CH = (double*)(CW + R * K);
+  pfa_load_tables<PL, NT>(tab, gtab);
+  const double fac0 = 1.0 / (8.0 * SCV_PI * SCV_PI);
+  const int nbblk = (nb + BB - 1) / BB;
+  const int ntask = nbblk * NGRP;
+  constexpr int NPT = (K + NT - 1) / NT;
+  constexpr int EPT = (R * K + NT - 1) / NT;
+  bool pending = false;  // a bulk store still reads X (thread 0's bulk group)
+#pragma unroll 1
+  for (int task = blockIdx.x; task < ntask; task += gridDim.x) {
+    const int bblk = task / NGRP;
+    const int m0 = (task - bblk * NGRP) * R;
+#pragma unroll
+    for (int u = 0; u < NPT; ++u) {
+      const int gi = threadIdx.x + u * NT;
+      if (gi >= K) continue;
+      const int n = gi <= L - 1 ? gi : gi - K;
+      const int l = n < 0 ? -n : n;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int m = m0 + r <= L - 1 ? m0 + r : m0 + r - K, am = m < 0 ? -m : m;
+        const bool nz = m0 + r < K && am <= l;
+        CW[gi * R + r] = nz ? w[((n >= 0 ? 0 : 1) * L + l) * K + (L - 1) + m] : make_double2(0.0, 0.0);
+        CH[gi * R + r] = nz ? hlb[l * (l + 1) / 2 + am] : 0.0;
+      }
+    }
+    __syncthreads();
+    const int bs_end = min(nb, (bblk + 1) * BB);
+#pragma unroll 1
+    for (int bs = bblk * BB; bs < bs_end; ++bs) {
+      const int b = b0 + bs;
+      const double ls = lsin[b], lc = lcos[b];
+      // generation into registers (X may still be read by the previous row's bulk stores)
+      double2 gv[NPT][R];
+#pragma unroll
+      for (int u = 0; u < NPT; ++u) {
+        const int gi = threadIdx.x + u * NT;
+        const int n = gi <= L - 1 ? gi : gi - K;
+        const int l = n < 0 ? -n : n;
+        const double facl = (double)(2 * l + 1) * fac0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int m = m0 + r <= L - 1 ? m0 + r : m0 + r - K, am = m < 0 ? -m : m;
+          double2 v = make_double2(0.0, 0.0);
+          if (gi < K && m0 + r < K && am <= l) {
+            const int es = n >= 0 ? l - m : l + m;
+            const int ec = n >= 0 ? l + m : l - m;
+            double lg = CH[gi * R + r];
+            if (es) lg += (double)es * ls;
+            if (ec) lg += (double)ec * lc;
+            double d = exp(lg);
+            if (n < 0 && ((l - m) & 1)) d = -d;
+            const double f = facl * d;
+            const double2 c = CW[gi * R + r];
+            v = make_double2(f * c.x, f * c.y);
+          }
+          gv[u][r] = v;
+        }
+      }
+      if (pending && threadIdx.x == 0) bulk_wait_read0();
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < NPT; ++u) {
+        const int gi = threadIdx.x + u * NT;
+        if (gi >= K) continue;
+        const int xi = pfa_in_tab<PL>(tab, gi);
+#pragma unroll
+        for (int r = 0; r < R; ++r) X[r * K + xi] = gv[u][r];
+      }
+      __syncthreads();
+      pfa_dft<PL, +1, R, NT, K>(X, tab, nullptr);
+      // permute in place into the box order X'[g*R + r] (reads all, barrier, writes all)
+      double2 ov[EPT];
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) {
+        const int i = threadIdx.x + e * NT;
+        if (i < R * K) {
+          const int g = i / R, r = i - g * R;
+          ov[e] = X[r * K + pfa_pos_tab<PL>(tab, g)];
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) {
+        const int i = threadIdx.x + e * NT;
+        if (i < R * K) X[i] = ov[e];
+      }
+      fence_proxy_async_smem();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+#pragma unroll 1
+        for (int q = 0; q < NBOX; ++q) tma_store_3d(&omap, X + q * GB * R, 2 * m0, bs, q * GB);
+        bulk_commit();
+      }
+      pending = true;
+    }
+    // CW / CH are re-staged next task: nothing of theirs is read by the bulk stores
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) bulk_wait0();
 }
 
 // ---------------------------------------------------------------------------
@@ -1316,6 +1467,30 @@ static int pfa_in_host(int K, int n) {
   return a;
 }
 
+// TMA descriptor of a (K, nb, K) complex128 beta slab seen as doubles:
+// dims (2K alpha-doubles, nb beta rows, K gamma), box (4, 1, 256) = one column
+// pair of 256 gamma rows.  cuTensorMapEncodeTiled comes from the driver through
+// the runtime's entry-point query (no libcuda link dependency).
+static int scv_tma_map_slab(scv_ctx* c, const void* base, int K, int nb, CUtensorMap* map) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    SCV_CUDA(c, cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !fn) return scv_fail(c, SCV_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }
+  const cuuint64_t dims[3] = {(cuuint64_t)2 * K, (cuuint64_t)nb, (cuuint64_t)K};
+  const cuuint64_t strides[2] = {(cuuint64_t)K * 16, (cuuint64_t)nb * K * 16};
+  const cuuint32_t box[3] = {4, 1, 256};
+  const cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return scv_fail(c, SCV_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return SCV_OK;
+}
+
 #define PFA_SWITCH(K, CALL)                                                                 \
   switch (K) {                                                                              \
     case 3: return CALL(3); case 7: return CALL(7); case 15: return CALL(15);              \
@@ -1377,6 +1552,20 @@ static int run_ana_colgen(scv_ctx* c, const double2* w, const double* hlb, const
   static_assert(sm <= 232448, "column-generation launch shape exceeds the 227 KB shared-memory limit");
   constexpr int L = (K + 1) / 2;
   const long long nt = (long long)nb * ((K + PfaGCfg<K>::R - 1) / PfaGCfg<K>::R);
+  if constexpr (SCV_COLGEN_S && SCV_COLGEN_TMA && K == 2047) {
+    constexpr size_t sms = pfa_smem_s<K>();
+    static_assert(sms <= 232448, "staged column-generation launch shape exceeds the 227 KB shared-memory limit");
+    static_assert((pfa_tab_total<PfaPlan<K>>() * sizeof(double2)) % 128 == 0, "TMA box source must be 128-byte aligned");
+    CUtensorMap omap;
+    SCV_TRY(scv_tma_map_slab(c, out, K, nb, &omap));
+    const long long nts = (long long)((nb + PfaSCfg<K>::BB - 1) / PfaSCfg<K>::BB) * ((K + PfaSCfg<K>::R - 1) / PfaSCfg<K>::R);
+    int grid;
+    SCV_TRY(persistent_grid(c, k_ana_colgen_t<K>, PfaSCfg<K>::NT, sms, nts, &grid));
+    k_ana_colgen_t<K><<<grid, PfaSCfg<K>::NT, sms, s>>>(w, hlb, ls, lc, b0, nb, omap, tab);
+    c->launches++;
+    SCV_CUDA(c, cudaGetLastError());
+    return SCV_OK;
+  }
   if constexpr (SCV_COLGEN_S && K == 2047) {
     constexpr size_t sms = pfa_smem_s<K>();
     static_assert(sms <= 232448, "staged column-generation launch shape exceeds the 227 KB shared-memory limit");

@@ -339,7 +339,15 @@ def run_ours(a):
             c = ana(fin, t, scale_out=scale_out)
             return syn(c, t)
 
-    if a.shard_scales and world > 1:
+    if a.shard_scales and world > 1 and a.streamed:
+        from paper_1511_05578_b200.dist import roundtrip_sharded_streamed
+        K_fin = 2 * Ljs[-1] - 1
+        rows = max(1, int(a.slab_gb * (1 << 30)) // (K_fin * K_fin * 16))
+
+        def step(fin):  # noqa: F811
+            g = roundtrip_sharded_streamed(fin, t, slab_rows=rows)
+            return g if g is not None else fin
+    elif a.shard_scales and world > 1:
         from paper_1511_05578_b200.dist import analyze_sharded, synthesize_sharded
 
         def step(fin):  # noqa: F811
@@ -439,7 +447,8 @@ def run_ours(a):
                    "j_min": a.jmin, "j_max": p.j_max, "scale_band_limits": Ljs,
                    "maps_per_step": maps_per_step,
                    **({"streamed_slab_GiB": a.slab_gb} if a.streamed else {}),
-                   "parallelism": ("scales sharded x%d (NCCL broadcast f_lm + gather terms)" % world
+                   "parallelism": ("scales + beta slabs sharded x%d%s (NCCL broadcast f_lm + reduce of the "
+                                   "per-scale terms)" % (world, ", slabs streamed" if a.streamed else "")
                                    if (a.shard_scales and world > 1) else
                                    (f"maps x{world} (one map per rank)" if world > 1 else "1 GPU")),
                    "l2_flush": "not needed: every scale volume >> 126 MB L2"},

@@ -60,7 +60,8 @@ int scv_create(int device, scv_ctx** out);
 int scv_destroy(scv_ctx* ctx);
 const char* scv_last_error(const scv_ctx* ctx);
 
-/* Bytes of device memory currently held by the context's workspace. */
+/* Bytes of device memory currently held by the context: scratch workspace,
+ * the Delta wedge and the per-L tables (beta quadrature, prime-factor). */
 long long scv_workspace_bytes(const scv_ctx* ctx);
 /* Release every lazily grown scratch buffer (tables stay). */
 int scv_trim(scv_ctx* ctx);

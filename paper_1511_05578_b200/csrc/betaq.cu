@@ -223,6 +223,7 @@ int scv_betaq_table(scv_ctx* c, int L, cudaStream_t s, const double** qtab, cons
   cudaFree(dtask);
   c->aux[key] = dq;
   c->aux[kb] = dmb;
+  c->table_bytes += (long long)acc * (long long)sizeof(double) + (long long)mb.size() * (long long)sizeof(long long);
   *qtab = dq;
   *mbase = dmb;
   return SCV_OK;

@@ -412,6 +412,7 @@ long long scv_workspace_bytes(const scv_ctx* c) {
   long long b = (long long)c->fft_work_bytes;
   for (int i = 0; i < 3; ++i) b += (long long)c->scratch_bytes[i];
   if (c->delta) b += wedge_size(c->delta_L) * 8;
+  b += c->table_bytes;
   return b;
 }
 

@@ -110,6 +110,7 @@ struct scv_ctx {
   size_t scratch_bytes[3] = {0, 0, 0};
   // small int tables by key
   std::map<std::string, void*> aux;
+  long long table_bytes = 0;  // persistent per-L tables in `aux` (quadrature, prime-factor, tasks)
   // stage profiler (scv_profile): event pairs around every launch group
   bool prof = false;
   long long launches = 0;  // kernels of this library launched (scv_launch_count)

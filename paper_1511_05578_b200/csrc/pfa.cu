@@ -269,6 +269,10 @@ static constexpr size_t pfa_smem_grp() {
 // GATHER = 1 (synthesis alpha): row r = bb*K + g of the launch reads the
 // input row (g, b0 + bb) of a (K, lsig, K) signal, i.e. in + g*lsig*K +
 // (b0+bb)*K, and writes chunk row r (the [bb][g][m] beta chunk).
+// GATHER = 2 (analysis alpha from the beta-block scratch of k_ana_colgen_s in
+// T mode): row r = bb*K + g reads column pairs T[bb][m/2][g][m&1] (32-byte
+// pieces) and writes the signal row (g, bs0 + bb) of a (K, LK/K... ) slab:
+// out + (g*snb + bs0 + bb)*K, snb = LK.
 template <int K, int DIR, int GATHER>
 __global__ void __launch_bounds__(PfaGrpCfg<K>::NG * PfaGrpCfg<K>::NTG, 1)
     k_pfa_rows_g(long long nrows, const double2* in, double2* out, const double2* __restrict__ gtab,
@@ -283,19 +287,28 @@ __global__ void __launch_bounds__(PfaGrpCfg<K>::NG * PfaGrpCfg<K>::NTG, 1)
 #pragma unroll 1
   for (long long r = (long long)blockIdx.x * NG + g; r < nrows; r += (long long)gridDim.x * NG) {
     const double2* src;
-    if constexpr (GATHER) {
+    double2* dst = out + r * K;
+    if constexpr (GATHER == 2) {
+      constexpr int NPR = (K + 1) / 2;
       const long long bb = r / K, g = r - bb * K;
-      src = in + g * LK + (b0 + bb) * K;
-    } else {
-      src = in + r * K;
-    }
+      src = in + (bb * NPR * K + g) * 2;  // + (m/2)*2K + (m&1)
+      dst = out + (g * LK + b0 + bb) * K;
 #pragma unroll 4
-    for (int n = gtid; n < K; n += NTG) cp_async16(X + pfa_in_tab<PL>(tab, n), src + n);
+      for (int n = gtid; n < K; n += NTG) cp_async16(X + pfa_in_tab<PL>(tab, n), src + (long long)(n >> 1) * (2 * K) + (n & 1));
+    } else {
+      if constexpr (GATHER == 1) {
+        const long long bb = r / K, g = r - bb * K;
+        src = in + g * LK + (b0 + bb) * K;
+      } else {
+        src = in + r * K;
+      }
+#pragma unroll 4
+      for (int n = gtid; n < K; n += NTG) cp_async16(X + pfa_in_tab<PL>(tab, n), src + n);
+    }
     cp_async_commit();
     cp_async_wait<0>();
     grp_sync(bar, NTG);
     pfa_dft<PL, DIR, 1, NTG, K>(X, tab, nullptr, gtid, bar);
-    double2* dst = out + r * K;
 #pragma unroll 4
     for (int k = gtid; k < K; k += NTG) dst[k] = X[pfa_pos_tab<PL>(tab, k)];
     grp_sync(bar, NTG);
@@ -528,7 +541,10 @@ static constexpr size_t pfa_smem_s() {
              sizeof(double2) + (size_t)R * K * sizeof(double);
 }
 
-template <int K>
+// TM = 1: write the beta-block scratch T[bs][m0/R][g][r] instead of the
+// signal (R*K*16 contiguous bytes per task row; k_pfa_rows_g<K, +1, 2> then
+// gathers the alpha rows from it and writes the signal).
+template <int K, int TM = 0>
 __global__ void __launch_bounds__(PfaSCfg<K>::NT, PfaSCfg<K>::MINB)
     k_ana_colgen_s(const double2* __restrict__ w, const double* __restrict__ hlb, const double* __restrict__ lsin,
                    const double* __restrict__ lcos, int b0, int nb, double2* __restrict__ out,
@@ -651,7 +667,11 @@ __global__ void __launch_bounds__(PfaSCfg<K>::NT, PfaSCfg<K>::MINB)
       for (int i = threadIdx.x; i < R * K; i += NT) {
         const int g = i / R, r = i - g * R;
         const int mi = m0 + r;
-        if (mi < K) out[((long long)g * nb + bs) * K + mi] = X[r * K + pfa_pos_tab<PL>(tab, g)];
+        if constexpr (TM) {
+          out[(((long long)bs * NGRP + m0 / R) * K + g) * R + r] = X[r * K + pfa_pos_tab<PL>(tab, g)];
+        } else {
+          if (mi < K) out[((long long)g * nb + bs) * K + mi] = X[r * K + pfa_pos_tab<PL>(tab, g)];
+        }
       }
     }
     __syncthreads();
@@ -1700,6 +1720,51 @@ int scv_pfa_ana_alpha(scv_ctx* c, int K, int real, const double2* w, const doubl
   PFA_SWITCH(K, CALL)
 #undef CALL
 }
+// Blocked analysis (SCV_COLGEN_T = beta rows per block, 0 = off; env
+// SCV_COLGEN_T overrides): per block of the slab [b0, b0+nb), k_ana_colgen_s
+// writes the contiguous scratch T (65 KB per task row instead of 2047
+// scattered 32-byte pieces) and k_pfa_rows_g<2047, +1, 2> gathers the alpha
+// rows from T (async 32-byte pieces) into the signal.  Measured (r01v12):
+// gamma pass 160 -> 144 ms/map, alpha pass 114 -> 118, map 563 -> 550 ms,
+// +4.3 GB scratch at 64 rows per block.
+// Returns 1 when not applicable (the caller runs colgen + rows in place).
+#ifndef SCV_COLGEN_T
+#define SCV_COLGEN_T 64
+#endif
+int scv_pfa_ana_blocked(scv_ctx* c, int K, const double2* w, const double* hlb, const double* ls, const double* lc,
+                        int b0, int nb, double2* sig, cudaStream_t s) {
+  static const int blk = getenv("SCV_COLGEN_T") ? atoi(getenv("SCV_COLGEN_T")) : SCV_COLGEN_T;
+  if (K != 2047 || blk <= 0 || !SCV_COLGEN_S) return 1;
+  constexpr int KK = 2047, R = PfaSCfg<KK>::R, NPR = (KK + R - 1) / R;
+  const double2* tab;
+  SCV_TRY(scv_pfa_tables(c, KK, &tab));
+  void* T = nullptr;
+  SCV_TRY(scv_scratch(c, 1, (size_t)blk * NPR * KK * R * 16, &T));
+  constexpr size_t sms = pfa_smem_s<KK>();
+  constexpr size_t smg = pfa_smem_grp<KK>();
+  constexpr int NTB = PfaGrpCfg<KK>::NG * PfaGrpCfg<KK>::NTG;
+  for (int bs0 = 0; bs0 < nb; bs0 += blk) {
+    const int nbb = std::min(blk, nb - bs0);
+    {
+      SCV_PROF(c, s, "so3inv_colgen");
+      const long long nts = (long long)((nbb + PfaSCfg<KK>::BB - 1) / PfaSCfg<KK>::BB) * NPR;
+      int grid;
+      SCV_TRY(persistent_grid(c, k_ana_colgen_s<KK, 1>, PfaSCfg<KK>::NT, sms, nts, &grid));
+      k_ana_colgen_s<KK, 1><<<grid, PfaSCfg<KK>::NT, sms, s>>>(w, hlb, ls, lc, b0 + bs0, nbb, (double2*)T, tab);
+      c->launches++;
+      SCV_CUDA(c, cudaGetLastError());
+    }
+    SCV_PROF(c, s, "so3inv_rows");
+    const long long nrows = (long long)nbb * KK;
+    int grid;
+    SCV_TRY(persistent_grid(c, k_pfa_rows_g<KK, +1, 2>, NTB, smg, (nrows + PfaGrpCfg<KK>::NG - 1) / PfaGrpCfg<KK>::NG, &grid));
+    k_pfa_rows_g<KK, +1, 2><<<grid, NTB, smg, s>>>(nrows, (const double2*)T, sig, tab, (long long)nb, bs0);
+    c->launches++;
+    SCV_CUDA(c, cudaGetLastError());
+  }
+  return SCV_OK;
+}
+
 int scv_pfa_ana_colgen(scv_ctx* c, int K, const double2* w, const double* hlb, const double* ls, const double* lc,
                        int b0, int nb, double2* out, cudaStream_t s) {
 #define CALL(KK) run_ana_colgen<KK>(c, w, hlb, ls, lc, b0, nb, out, s)

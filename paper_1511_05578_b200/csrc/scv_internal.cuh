@@ -190,6 +190,8 @@ int scv_pfa_ana_colgen(scv_ctx* c, int K, const double2* w, const double* hlb, c
 int scv_pfa_ana_real_gf(scv_ctx* c, int K, const double2* w, const double* hlb, const double* ls, const double* lc,
                         int b0, int nb, double2* T, double* out, cudaStream_t s);
 int scv_pfa_rows_inplace(scv_ctx* c, int K, int dir, long long nrows, double2* x, cudaStream_t s);
+int scv_pfa_ana_blocked(scv_ctx* c, int K, const double2* w, const double* hlb, const double* ls, const double* lc,
+                        int b0, int nb, double2* sig, cudaStream_t s);
 int scv_pfa_ana_gamma(scv_ctx* c, int K, int real, double2* src, double* dst, cudaStream_t s);
 int scv_pfa_syn_alpha(scv_ctx* c, int K, int real, int tr, const void* in, int lsig, int b0, int nbb, double2* chunk,
                       cudaStream_t s);

@@ -198,6 +198,10 @@ extern "C" int scv_so3_inverse_curvelet_slab(scv_ctx* c, int L, const double* w,
   const BetaTables* t = nullptr;
   SCV_TRY(scv_get_beta_tables(c, L, s, &t));
   {
+    const int rc = scv_pfa_ana_blocked(c, K, (const double2*)w, c->hlb, t->sinh, t->cosh, b0, nb, (double2*)sig, s);
+    if (rc <= 0) return rc;
+  }
+  {
     SCV_PROF(c, s, "so3inv_colgen");
     SCV_TRY(scv_pfa_ana_colgen(c, K, (const double2*)w, c->hlb, t->sinh, t->cosh, b0, nb, (double2*)sig, s));
   }
@@ -234,6 +238,10 @@ extern "C" int scv_so3_inverse_curvelet(scv_ctx* c, int L, int real, const doubl
   if (scv_pfa_supported(K)) {
     // hand-written prime-factor path: fused generate + alpha IDFT, then gamma IDFT
     if (!real && c->opt_colgen) {
+      {
+        const int rc = scv_pfa_ana_blocked(c, K, (const double2*)w, c->hlb, t->sinh, t->cosh, 0, L, (double2*)sig, s);
+        if (rc <= 0) return rc;
+      }
       {
         SCV_PROF(c, s, "so3inv_colgen");
         SCV_TRY(scv_pfa_ana_colgen(c, K, (const double2*)w, c->hlb, t->sinh, t->cosh, 0, L, (double2*)sig, s));

@@ -284,6 +284,73 @@ __global__ void __launch_bounds__(PfaGrpCfg<K>::NG * PfaGrpCfg<K>::NTG, 1)
   pfa_load_tables<PL, NG * NTG>(tab, gtab);
   const int g = threadIdx.x / NTG, gtid = threadIdx.x - g * NTG, bar = 1 + g;
   double2* const X = sm + pfa_tab_total<PL>() + g * K;
+  if constexpr (GATHER >= 3) {
+    // real paths: two real rows per complex transform (row pairs 2p, 2p+1)
+    constexpr int L = (K + 1) / 2;
+    const long long npair = (nrows + 1) / 2;
+#pragma unroll 1
+    for (long long pr = (long long)blockIdx.x * NG + g; pr < npair; pr += (long long)gridDim.x * NG) {
+      const long long r1 = 2 * pr, r2 = r1 + 1;
+      const bool has2 = r2 < nrows;
+      if constexpr (GATHER == 3) {
+        // synthesis alpha of a real signal: X = f1 + i f2 (rows (g, b0+bb) of a (K, LK/K, K) real signal)
+        const double* F = (const double*)in;
+        const long long bb1 = r1 / K, g1 = r1 - bb1 * K, bb2 = r2 / K, g2 = r2 - bb2 * K;
+        const double* s1 = F + g1 * LK + (b0 + bb1) * K;
+        const double* s2 = F + g2 * LK + (b0 + bb2) * K;
+#pragma unroll 4
+        for (int n = gtid; n < K; n += NTG) {
+          double* xd = (double*)(X + pfa_in_tab<PL>(tab, n));
+          cp_async8(xd, s1 + n);
+          if (has2) cp_async8(xd + 1, s2 + n);
+          else xd[1] = 0.0;
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+      } else {
+        // analysis alpha of a real signal from its half spectrum T (nrows, L):
+        // Z = T1 + i T2 extended by Z[-m] = conj(T1[m]) + i conj(T2[m]); Im of m = 0 dropped
+        const double2* T1 = in + r1 * L;
+        const double2* T2 = in + r2 * L;
+#pragma unroll 4
+        for (int m = gtid; m < L; m += NTG) {
+          double2 t1 = T1[m];
+          double2 t2 = has2 ? T2[m] : make_double2(0.0, 0.0);
+          if (m == 0) {
+            t1.y = 0.0;
+            t2.y = 0.0;
+          }
+          X[pfa_in_tab<PL>(tab, m)] = make_double2(t1.x - t2.y, t1.y + t2.x);
+          if (m > 0) X[pfa_in_tab<PL>(tab, K - m)] = make_double2(t1.x + t2.y, -t1.y + t2.x);
+        }
+      }
+      grp_sync(bar, NTG);
+      pfa_dft<PL, DIR, 1, NTG, K>(X, tab, nullptr, gtid, bar);
+      if constexpr (GATHER == 3) {
+        // X1[m] = (Z[m] + conj Z[-m])/2, X2[m] = (Z[m] - conj Z[-m])/(2i), m >= 0 half only
+        double2* d1 = out + r1 * K;
+        double2* d2 = out + r2 * K;
+#pragma unroll 4
+        for (int m = gtid; m < L; m += NTG) {
+          const double2 z = X[pfa_pos_tab<PL>(tab, m)];
+          const double2 zc = X[pfa_pos_tab<PL>(tab, m == 0 ? 0 : K - m)];
+          d1[m] = make_double2(0.5 * (z.x + zc.x), 0.5 * (z.y - zc.y));
+          if (has2) d2[m] = make_double2(0.5 * (z.y + zc.y), -0.5 * (z.x - zc.x));
+        }
+      } else {
+        double* o1 = (double*)out + r1 * K;
+        double* o2 = (double*)out + r2 * K;
+#pragma unroll 4
+        for (int a = gtid; a < K; a += NTG) {
+          const double2 z = X[pfa_pos_tab<PL>(tab, a)];
+          o1[a] = z.x;
+          if (has2) o2[a] = z.y;
+        }
+      }
+      grp_sync(bar, NTG);
+    }
+    return;
+  }
 #pragma unroll 1
   for (long long r = (long long)blockIdx.x * NG + g; r < nrows; r += (long long)gridDim.x * NG) {
     const double2* src;
@@ -1623,6 +1690,18 @@ static int run_ana_real_gf(scv_ctx* c, const double2* w, const double* hlb, cons
     c->launches++;
     SCV_CUDA(c, cudaGetLastError());
   }
+  if constexpr (PfaGrpCfg<K>::NG > 0) {
+    constexpr size_t smg = pfa_smem_grp<K>();
+    constexpr int NTB = PfaGrpCfg<K>::NG * PfaGrpCfg<K>::NTG;
+    const long long nrows = (long long)K * nb;
+    int grid;
+    SCV_TRY(persistent_grid(c, k_pfa_rows_g<K, +1, 4>, NTB, smg, ((nrows + 1) / 2 + PfaGrpCfg<K>::NG - 1) / PfaGrpCfg<K>::NG, &grid));
+    SCV_PROF(c, s, "so3inv_rows");
+    k_pfa_rows_g<K, +1, 4><<<grid, NTB, smg, s>>>(nrows, T, (double2*)out, tab);
+    c->launches++;
+    SCV_CUDA(c, cudaGetLastError());
+    return SCV_OK;
+  }
   {
     constexpr size_t sm = pfa_smem<K, false>();
     const long long nrows = (long long)K * nb;
@@ -1662,6 +1741,17 @@ static int run_syn_alpha(scv_ctx* c, int real, int tr, const void* in, int lsig,
   constexpr size_t sm = pfa_smem<K, false>();
   static_assert(sm <= 232448, "prime-factor launch shape exceeds the 227 KB shared-memory limit");
   if constexpr (PfaGrpCfg<K>::NG > 0) {
+    if (real == 2 && !tr) {
+      constexpr size_t smg = pfa_smem_grp<K>();
+      constexpr int NTB = PfaGrpCfg<K>::NG * PfaGrpCfg<K>::NTG;
+      const long long nrows = (long long)K * nbb;
+      int grid;
+      SCV_TRY(persistent_grid(c, k_pfa_rows_g<K, -1, 3>, NTB, smg, ((nrows + 1) / 2 + PfaGrpCfg<K>::NG - 1) / PfaGrpCfg<K>::NG, &grid));
+      k_pfa_rows_g<K, -1, 3><<<grid, NTB, smg, s>>>(nrows, (const double2*)in, chunk, tab, (long long)lsig * K, b0);
+      c->launches++;
+      SCV_CUDA(c, cudaGetLastError());
+      return SCV_OK;
+    }
     if (!real && !tr) {
       constexpr size_t smg = pfa_smem_grp<K>();
       constexpr int NTB = PfaGrpCfg<K>::NG * PfaGrpCfg<K>::NTG;

@@ -278,6 +278,11 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
 }
+// 8-byte variant (cp.async.ca: sizes below 16 go through L1)
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
 // same, with an L2 prefetch of the whole 128-byte line (strided column reads
 // whose neighbouring columns are read by other CTAs at about the same time)
 __device__ __forceinline__ void cp_async16_l2line(void* smem, const void* gmem) {

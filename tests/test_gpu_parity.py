@@ -475,3 +475,46 @@ def test_c5_full_size_streamed_round_trip():
     back = host(sc.sht_forward(g).values)
     assert np.abs(back - flm).max() <= TOL_RT * np.abs(flm).max()
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("L,s,J0", [(1024, 0, 3), (2048, 2, 4)])
+def test_full_size_analysis_beta_rows_vs_oracle(L, s, J0):
+    """BASELINE C4 / C5 finest scale (L_j = L) against the oracle directly:
+    the scale's Wigner coefficients from the oracle's harmonic product of a
+    seeded Gaussian f_lm, sampled beta rows of the GPU analysis (beta slabs of
+    one row through the C ABI) vs the oracle's per-beta-row restatement of
+    so3_inverse_curvelet (one K x K inverse FFT per row), <= 1e-10 relative."""
+    t = sc.build_tiling(sc.TilingParams(L, s, 2.0, J0))
+    j = t.params.j_max
+    assert sc.scale_band_limit(t.params, j) == L
+    flm = orc.gaussian_flm(L, s, seed=0, real=(s == 0))
+    pos, neg = sc.curvelet_harmonics(t, j)
+    w = orc.scale_wigner(flm, pos, neg, L)
+    cw = sc.CurveletWignerCoeffs(L, torch.as_tensor(w, device="cuda"))
+    grid = sc.SO3Grid(L, L, L)
+    for b in (0, L // 3, L - 1):
+        row = host(sc.so3_inverse_curvelet_slab(cw, grid, b, 1).values)[:, 0, :]
+        ref = orc.so3_inverse_curvelet_beta_row(w, b)
+        assert orc.rel_err(row, ref) <= TOL, (L, b)
+    torch.cuda.empty_cache()
+
+
+def test_full_size_so3_pair_identity_L1024():
+    """forward(inverse(w)) == w at L_j = 1024 (the exact quadrature of the MW
+    sampling theorem), through the beta-slab entry points."""
+    L = 1024
+    K = 2 * L - 1
+    w = _random_cw(L, 77)
+    cw = sc.CurveletWignerCoeffs(L, w)
+    grid = sc.SO3Grid(L, L, L)
+    acc = None
+    for b0 in range(0, L, 128):
+        slab = sc.so3_inverse_curvelet_slab(cw, grid, b0, 128)
+        if acc is None:
+            acc = sc.so3_forward_curvelet_slab(slab)
+        else:
+            sc.so3_forward_curvelet_slab(slab, out=acc.values, accumulate=True)
+        del slab
+    ref = torch.as_tensor(w, device="cuda") if not torch.is_tensor(w) else w
+    assert float((acc.values - ref).abs().max() / ref.abs().max()) <= 1e-12
+    torch.cuda.empty_cache()

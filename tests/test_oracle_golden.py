@@ -136,3 +136,16 @@ def test_config1_L64(golden):
     assert orc.rel_err(g, golden["c1_recon"]) <= TILING_TOL
     w = orc.so3_forward_curvelet(scales[-1])
     assert orc.rel_err(w, golden["c1_wlast"]) <= TILING_TOL
+
+
+@pytest.mark.parametrize("L", [8, 16, 24])
+def test_beta_row_restatement_matches_full_oracle(L):
+    """The per-beta-row oracle used for the full-size (L=1024, 2048) GPU checks
+    restates the same linear map as the full so3_inverse_curvelet oracle
+    (itself pinned to the reference goldens above)."""
+    rng = np.random.default_rng(L)
+    K = 2 * L - 1
+    w = rng.standard_normal((2, L, K)) + 1j * rng.standard_normal((2, L, K))
+    full = orc.so3_inverse_curvelet(w)
+    for b in (0, L // 2, L - 1):
+        assert orc.rel_err(orc.so3_inverse_curvelet_beta_row(w, b), full[:, b, :]) <= 1e-13

@@ -590,7 +590,7 @@ template <int K> struct PfaSCfg { static constexpr int R = 2, NT = 384, MINB = 1
 #define SCV_COLGEN_S_BB 128
 #endif
 #ifndef SCV_COLGEN_S_NT
-#define SCV_COLGEN_S_NT 512
+#define SCV_COLGEN_S_NT 384
 #endif
 template <> struct PfaSCfg<2047> { static constexpr int R = 2, NT = SCV_COLGEN_S_NT, MINB = 1, BB = SCV_COLGEN_S_BB; };
 // NGR > 1: the CTA runs NGR independent groups of NT/NGR threads, group g

@@ -85,6 +85,9 @@ constexpr int pfa_kt_unroll = SCV_PFA_KT_UNROLL;
 #ifndef SCV_PFA_NBW_SMALL
 #define SCV_PFA_NBW_SMALL 1
 #endif
+#ifndef SCV_PFA_NBW_BIG
+#define SCV_PFA_NBW_BIG 1
+#endif
 __host__ __device__ constexpr int mma_M(int p) { return ((pfa_h(p) + 1 + 15) / 16) * 16; }   // output rows
 __host__ __device__ constexpr int mma_Kp(int p) { return ((pfa_h(p) + 3) / 4) * 4; }         // reduction dim
 __host__ __device__ constexpr int mma_pitch(int n) {  // row pitch (doubles) with pitch mod 16 in {4, 12}
@@ -627,7 +630,7 @@ __device__ __forceinline__ void pfa_stage_mma_blk(double2* X, const double2* tab
   auto slot = [](int i) { return (i >> 1) + 4 * (i & 1); };
   // small radices (<= 2 m8 tiles): NBW blocks per warp iteration, for more
   // independent DMMA chains per k-step
-  constexpr int NBW = M8 <= 2 ? SCV_PFA_NBW_SMALL : 1;
+  constexpr int NBW = M8 <= 2 ? SCV_PFA_NBW_SMALL : SCV_PFA_NBW_BIG;
 #pragma unroll 1
   for (int q0 = warp; q0 < NBLK; q0 += NW * NBW) {
     int rowd[NBW], pa[NBW], pb[NBW], eoff[NBW];

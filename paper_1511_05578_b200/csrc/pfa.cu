@@ -182,9 +182,13 @@ static constexpr size_t pfa_smem() {
 // ---------------------------------------------------------------------------
 // batched rows (test / benchmark entry): out[r][k] = sum_n in[r][n] e^{DIR 2 pi i nk/K}
 // ---------------------------------------------------------------------------
-template <int K, int DIR>
+// GATHER = 2: the blocked analysis's alpha pass (see k_pfa_rows_g): row
+// r = bb*K + g reads the column pairs T[bb][m/2][g][m&1] and writes signal
+// row (g, b0 + bb) of a slab with LK beta rows.
+template <int K, int DIR, int GATHER = 0>
 __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
-    k_pfa_rows(long long nrows, const double2* in, double2* out, const double2* __restrict__ gtab) {
+    k_pfa_rows(long long nrows, const double2* in, double2* out, const double2* __restrict__ gtab,
+               long long LK = 0, int b0 = 0) {
   // in == out is allowed (in-place rows: a batch is read one iteration before it is written)
   using PL = PfaPlan<K>;
   constexpr int R = PfaCfg<K, false>::R, NT = PfaCfg<K, false>::NT;
@@ -203,8 +207,17 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
     for (int i = threadIdx.x; i < R * K; i += NT) {
       const int r = i / K, n = i - r * K;
       const int xi = r * K + pfa_in_tab<PL>(tab, n);
-      if (r0 + r < nrows) cp_async16(X + xi, in + (r0 + r) * K + n);
-      else X[xi] = make_double2(0.0, 0.0);
+      if (r0 + r < nrows) {
+        if constexpr (GATHER == 2) {
+          constexpr int NPR = (K + 1) / 2;
+          const long long ri = r0 + r, bb = ri / K, g = ri - bb * K;
+          cp_async16(X + xi, in + ((bb * NPR + (n >> 1)) * K + g) * 2 + (n & 1));
+        } else {
+          cp_async16(X + xi, in + (r0 + r) * K + n);
+        }
+      } else {
+        X[xi] = make_double2(0.0, 0.0);
+      }
     }
     cp_async_commit();
   };
@@ -233,7 +246,14 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
 #pragma unroll 4
     for (int i = threadIdx.x; i < R * K; i += NT) {
       const int r = i / K, k = i - r * K;
-      if (r0 + r < nrows) out[(r0 + r) * K + k] = X[r * K + pfa_pos_tab<PL>(tab, k)];
+      if (r0 + r < nrows) {
+        if constexpr (GATHER == 2) {
+          const long long ri = r0 + r, bb = ri / K, g = ri - bb * K;
+          out[(g * LK + b0 + bb) * K + k] = X[r * K + pfa_pos_tab<PL>(tab, k)];
+        } else {
+          out[(r0 + r) * K + k] = X[r * K + pfa_pos_tab<PL>(tab, k)];
+        }
+      }
     }
 #endif
     __syncthreads();
@@ -260,6 +280,8 @@ template <int K> struct PfaGrpCfg { static constexpr int NG = 0, NTG = 0; };
     static constexpr int NG = v_[0], NTG = v_[1];            \
   };
 SCV_RGCFG_(2047, SCV_ROWS_GRP)
+// (K = 4095 keeps k_pfa_rows: its all-register DFMA stages for radices 5 and 7
+// spill in 128-thread groups)
 template <int K>
 static constexpr size_t pfa_smem_grp() {
   using PL = PfaPlan<K>;
@@ -485,7 +507,8 @@ static constexpr size_t pfa_smem_g() {
          sizeof(double2);
 }
 
-template <int K>
+// TM = 1: beta-block scratch output T[bs][m0/R][g][r] (see k_ana_colgen_s)
+template <int K, int TM = 0>
 __global__ void __launch_bounds__(PfaGCfg<K>::NT, PfaGCfg<K>::MINB)
     k_ana_colgen(const double2* __restrict__ w, const double* __restrict__ hlb, const double* __restrict__ lsin,
                  const double* __restrict__ lcos, int b0, int nb, double2* __restrict__ out,
@@ -570,7 +593,8 @@ __global__ void __launch_bounds__(PfaGCfg<K>::NT, PfaGCfg<K>::MINB)
 #if SCV_EXP_COLGEN_CONTIG
       if (mi < K) out[(((long long)task * R + r) * K + g) % ((long long)nb * K * K)] = X[r * K + pfa_pos_tab<PL>(tab, g)];  // timing experiment only
 #else
-      if (mi < K) out[((long long)g * nb + bs) * K + mi] = X[r * K + pfa_pos_tab<PL>(tab, g)];
+      if constexpr (TM) out[(((long long)bs * NGRP + m0 / R) * K + g) * R + r] = X[r * K + pfa_pos_tab<PL>(tab, g)];
+      else if (mi < K) out[((long long)g * nb + bs) * K + mi] = X[r * K + pfa_pos_tab<PL>(tab, g)];
 #endif
     }
     __syncthreads();
@@ -1821,9 +1845,46 @@ int scv_pfa_ana_alpha(scv_ctx* c, int K, int real, const double2* w, const doubl
 #ifndef SCV_COLGEN_T
 #define SCV_COLGEN_T 64
 #endif
+#ifndef SCV_COLGEN_T_4095
+#define SCV_COLGEN_T_4095 16
+#endif
+static int ana_blocked_4095(scv_ctx* c, const double2* w, const double* hlb, const double* ls, const double* lc,
+                            int b0, int nb, double2* sig, cudaStream_t s) {
+  constexpr int KK = 4095, R = PfaGCfg<KK>::R, NPR = (KK + R - 1) / R;
+  static_assert(R == 2, "the gather of k_pfa_rows<K, +1, 2> reads column pairs");
+  const int blk = SCV_COLGEN_T_4095;
+  const double2* tab;
+  SCV_TRY(scv_pfa_tables(c, KK, &tab));
+  void* T = nullptr;
+  SCV_TRY(scv_scratch(c, 1, (size_t)blk * NPR * KK * R * 16, &T));
+  constexpr size_t smc = pfa_smem_g<KK>();
+  constexpr size_t smr = pfa_smem<KK, false>();
+  constexpr int NTR = PfaCfg<KK, false>::NT, RR = PfaCfg<KK, false>::R;
+  for (int bs0 = 0; bs0 < nb; bs0 += blk) {
+    const int nbb = std::min(blk, nb - bs0);
+    {
+      SCV_PROF(c, s, "so3inv_colgen");
+      int grid;
+      SCV_TRY(persistent_grid(c, k_ana_colgen<KK, 1>, PfaGCfg<KK>::NT, smc, (long long)nbb * NPR, &grid));
+      k_ana_colgen<KK, 1><<<grid, PfaGCfg<KK>::NT, smc, s>>>(w, hlb, ls, lc, b0 + bs0, nbb, (double2*)T, tab);
+      c->launches++;
+      SCV_CUDA(c, cudaGetLastError());
+    }
+    SCV_PROF(c, s, "so3inv_rows");
+    const long long nrows = (long long)nbb * KK;
+    int grid;
+    SCV_TRY(persistent_grid(c, k_pfa_rows<KK, +1, 2>, NTR, smr, (nrows + RR - 1) / RR, &grid));
+    k_pfa_rows<KK, +1, 2><<<grid, NTR, smr, s>>>(nrows, (const double2*)T, sig, tab, (long long)nb, bs0);
+    c->launches++;
+    SCV_CUDA(c, cudaGetLastError());
+  }
+  return SCV_OK;
+}
+
 int scv_pfa_ana_blocked(scv_ctx* c, int K, const double2* w, const double* hlb, const double* ls, const double* lc,
                         int b0, int nb, double2* sig, cudaStream_t s) {
   static const int blk = getenv("SCV_COLGEN_T") ? atoi(getenv("SCV_COLGEN_T")) : SCV_COLGEN_T;
+  if (K == 4095 && SCV_COLGEN_T_4095 > 0) return ana_blocked_4095(c, w, hlb, ls, lc, b0, nb, sig, s);
   if (K != 2047 || blk <= 0 || !SCV_COLGEN_S) return 1;
   constexpr int KK = 2047, R = PfaSCfg<KK>::R, NPR = (KK + R - 1) / R;
   const double2* tab;

@@ -89,9 +89,10 @@ class _DevTiling:
         self.psi = {}
         for j in range(p.j_min, p.j_max + 1):
             pos, neg = curvelet_harmonics(t, j)
-            self.psi[j] = (torch.as_tensor(np.ascontiguousarray(pos), dtype=torch.float64, device=device),
-                           torch.as_tensor(np.ascontiguousarray(neg), dtype=torch.float64, device=device))
-        self.scaling = torch.as_tensor(np.ascontiguousarray(t.scaling), dtype=torch.float64, device=device)
+            # np.array copies: tiling arrays may be read-only views (frozen reference Tiling)
+            self.psi[j] = (torch.as_tensor(np.array(pos, dtype=np.float64), device=device),
+                           torch.as_tensor(np.array(neg, dtype=np.float64), device=device))
+        self.scaling = torch.as_tensor(np.array(t.scaling, dtype=np.float64), device=device)
 
 
 def device_tiling(t, device) -> _DevTiling:

@@ -20,5 +20,16 @@ for L, s, J0 in [(64, 2, 2), (128, 0, 2), (256, 0, 6)]:
         gr = sc.synthesize_real(sc.analyze_real(fr, t), t)
         msg += f", real {float((gr.values - fr.values).abs().max() / fr.values.abs().max()):.2e}"
     print(msg, flush=True)
+# the K = 2047 kernels (blocked column generation, grouped row kernels, gamma +
+# quadrature) on a 2-row beta slab of an L_j = 1024 scale
+L = 1024
+rng = np.random.default_rng(1)
+w = np.zeros((2, L, 2 * L - 1), complex)
+for l in range(L):
+    w[:, l, L - 1 - l:L + l] = rng.standard_normal((2, 2 * l + 1)) + 1j * rng.standard_normal((2, 2 * l + 1))
+cw = sc.CurveletWignerCoeffs(L, torch.as_tensor(w, device="cuda"))
+slab = sc.so3_inverse_curvelet_slab(cw, sc.SO3Grid(L, L, L), 500, 2)
+part = sc.so3_forward_curvelet_slab(slab)
 torch.cuda.synchronize()
+print("L=1024 slab ok", float(part.values.abs().max()))
 print("sanitize workload done")

@@ -79,7 +79,7 @@ __host__ __device__ constexpr bool pfa_use_mma(int p, int K) {
 #define SCV_PFA_BLK 1
 #endif
 #ifndef SCV_PFA_KT_UNROLL
-#define SCV_PFA_KT_UNROLL 4
+#define SCV_PFA_KT_UNROLL 11
 #endif
 constexpr int pfa_kt_unroll = SCV_PFA_KT_UNROLL;
 #ifndef SCV_PFA_NBW_SMALL

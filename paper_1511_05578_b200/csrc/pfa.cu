@@ -282,6 +282,10 @@ template <int K> struct PfaGrpCfg { static constexpr int NG = 0, NTG = 0; };
 SCV_RGCFG_(2047, SCV_ROWS_GRP)
 // (K = 4095 keeps k_pfa_rows: its all-register DFMA stages for radices 5 and 7
 // spill in 128-thread groups)
+#ifndef SCV_ROWS_GRP_1023
+#define SCV_ROWS_GRP_1023 0, 0
+#endif
+SCV_RGCFG_(1023, SCV_ROWS_GRP_1023)
 template <int K>
 static constexpr size_t pfa_smem_grp() {
   using PL = PfaPlan<K>;

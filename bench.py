@@ -182,7 +182,9 @@ def ncu_traffic(stage, Ljs):
 # per call of R rows, a DMMA radix p (h = (p-1)/2) runs 2*ceil(R*(K/p)/8)
 # warp blocks x ceil((h+1)/8) m8 tiles x ceil(h/4) k-steps x 2 (C.s, S.d).
 # Cross-checked against ncu: 1081 DMMA per K=2047 row (sm__inst_executed_pipe_
-# tensor_subpipe_dmma, profiles/r01v8_ncu_k_pfa_rows.txt) vs 1080 here.
+# tensor_subpipe_dmma, profiles/r01v8_ncu_k_pfa_rows.txt) vs 1080 here with the
+# dense radix-89 stage; the Rader radix-89 stage (r01v15+) issues 66 per block
+# of 4 butterflies: 288 + 396 = 684 per K=2047 row.
 PFA_PLAN = {3: (3,), 7: (7,), 15: (3, 5), 31: (31,), 63: (7, 9), 255: (3, 5, 17), 511: (7, 73),
             1023: (3, 11, 31), 2047: (23, 89), 4095: (5, 7, 9, 13)}
 PFA_R = {  # rows per transform call by stage
@@ -203,6 +205,9 @@ def dmma_per_row(K, R):
             continue
         h = (p - 1) // 2
         nblk = 2 * ((R * (K // p) + 7) // 8)
+        if p == 89:  # Rader + 4 x 11 CRT (pfa_stage_rader89): 2*6 + 3*18 DMMA per block
+            tot += nblk * 66
+            continue
         tot += nblk * ((h + 1 + 7) // 8) * ((h + 3) // 4) * 2
     return tot / R
 
@@ -279,7 +284,7 @@ def stage_roofline(a, prof, Ljs, hbm_peak, fp64_peak):
         out["executed_dmma"] = {"tflops": ex / (ms_map * 1e-3) / 1e12, "peak_tflops": DMMA_PEAK_TF,
                                 "frac": ex / (ms_map * 1e-3) / 1e12 / DMMA_PEAK_TF,
                                 "flops_per_map": ex, "source": "DMMA count of the engine's launch shapes "
-                                "(bench.py dmma_per_row; 1080/row at K=2047 vs ncu 1081)"}
+                                "(bench.py dmma_per_row; 684/row at K=2047 with the Rader radix-89 stage)"}
     tr = ncu_traffic(name, Ljs)
     # measured DRAM bytes (GB per map) vs the algorithmic bytes behind `achieved`
     out["traffic"] = None if tr is None else tr["bytes_per_map"] / 1e9

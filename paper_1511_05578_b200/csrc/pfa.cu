@@ -19,6 +19,7 @@
 // tables in shared memory once.
 
 #include <algorithm>
+#include <complex>
 #include <cmath>
 #include <cstring>
 
@@ -57,6 +58,108 @@ static void factors_of(int K, int f[4]) {
 int scv_pfa_pos_host(int K, int k);
 static int pfa_in_host(int K, int n);
 
+// Tables of pfa_stage_rader89 (pfa.cuh), in long double: the 44-point cyclic
+// (cos) and negacyclic (sin) correlation operators of Rader's permutation
+// (r_a = 3^a mod 89), conjugated by the in-lane 4-point transforms along
+// a mod 4 (a <-> (a mod 4, a mod 11)), are block diagonal; the blocks are the
+// dense products the stage runs on DMMA.  The 1/4 and 1/2 of the inverse
+// transforms are folded in.  Layout: see R89_OFF_* (rows = output a mod 11,
+// columns = input a mod 11; 22 x 22 blocks stored as Re rows 0..7 / Im rows
+// 8..15 / Re rows 16..18 / Im rows 19..21 and Re columns 0..10 / Im 12..22).
+static void rader89_tables(double* T) {
+  typedef std::complex<ld> cld;
+  const int p = 89, h = 44;
+  const ld pi = 3.141592653589793238462643383279502884L;
+  int r[44];
+  r[0] = 1;
+  for (int a = 1; a < h; ++a) r[a] = (r[a - 1] * 3) % p;
+  auto idx = [](int a1, int a2) { return (33 * a1 + 12 * a2) % 44; };
+  auto sgn = [](int a) { return ((a >> 2) & 1) ? -1.0L : 1.0L; };
+  std::vector<ld> C44(h * h), S44(h * h);
+  for (int b = 0; b < h; ++b)
+    for (int a = 0; a < h; ++a) {
+      const ld ang = 2 * pi * (ld)(((long long)r[a] * r[b]) % p) / (ld)p;
+      C44[b * h + a] = cosl(ang);
+      S44[b * h + a] = sinl(ang);
+    }
+  // cyclic: coordinates [V0 | V2 | Ur | Ui] x 11
+  std::vector<ld> Tc(h * h, 0.0L), Tci(h * h, 0.0L);
+  for (int a2 = 0; a2 < 11; ++a2) {
+    for (int a1 = 0; a1 < 4; ++a1) {
+      Tc[a2 * h + idx(a1, a2)] = 1;
+      Tc[(11 + a2) * h + idx(a1, a2)] = (a1 & 1) ? -1 : 1;
+    }
+    Tc[(22 + a2) * h + idx(0, a2)] = 1;
+    Tc[(22 + a2) * h + idx(2, a2)] = -1;
+    Tc[(33 + a2) * h + idx(1, a2)] = 1;
+    Tc[(33 + a2) * h + idx(3, a2)] = -1;
+    // inverse: v0 = (V0+V2)/4 + Ur/2, v1 = (V0-V2)/4 + Ui/2, v2 = (V0+V2)/4 - Ur/2, v3 = (V0-V2)/4 - Ui/2
+    for (int a1 = 0; a1 < 4; ++a1) {
+      const int a = idx(a1, a2);
+      Tci[a * h + a2] = 0.25L;
+      Tci[a * h + 11 + a2] = (a1 & 1) ? -0.25L : 0.25L;
+      if (a1 == 0) Tci[a * h + 22 + a2] = 0.5L;
+      if (a1 == 2) Tci[a * h + 22 + a2] = -0.5L;
+      if (a1 == 1) Tci[a * h + 33 + a2] = 0.5L;
+      if (a1 == 3) Tci[a * h + 33 + a2] = -0.5L;
+    }
+  }
+  auto mm = [h](const std::vector<ld>& A, const std::vector<ld>& B) {
+    std::vector<ld> Cm(h * h, 0.0L);
+    for (int i = 0; i < h; ++i)
+      for (int k = 0; k < h; ++k) {
+        const ld v = A[i * h + k];
+        if (v == 0) continue;
+        for (int j = 0; j < h; ++j) Cm[i * h + j] += v * B[k * h + j];
+      }
+    return Cm;
+  };
+  const std::vector<ld> Mc = mm(mm(Tc, C44), Tci);
+  // negacyclic: sign-twisted odd DFT, eta_f = exp(-i pi (2f+1)/4)
+  std::vector<cld> Ts(h * h), Tsi(h * h), Sc(h * h);
+  for (int i = 0; i < h * h; ++i) Sc[i] = cld(S44[i], 0);
+  for (int f = 0; f < 4; ++f) {
+    const cld eta = std::polar(1.0L, -pi * (ld)(2 * f + 1) / 4);
+    for (int a2 = 0; a2 < 11; ++a2)
+      for (int a1 = 0; a1 < 4; ++a1) {
+        const int a = idx(a1, a2);
+        Ts[(f * 11 + a2) * h + a] = sgn(a) * std::pow(eta, a1);
+        Tsi[a * h + f * 11 + a2] = sgn(a) * 0.25L * std::pow(eta, -a1);
+      }
+  }
+  auto mmc = [h](const std::vector<cld>& A, const std::vector<cld>& B) {
+    std::vector<cld> Cm(h * h, cld(0, 0));
+    for (int i = 0; i < h; ++i)
+      for (int k = 0; k < h; ++k) {
+        const cld v = A[i * h + k];
+        if (v == cld(0, 0)) continue;
+        for (int j = 0; j < h; ++j) Cm[i * h + j] += v * B[k * h + j];
+      }
+    return Cm;
+  };
+  const std::vector<cld> Ms = mmc(mmc(Ts, Sc), Tsi);
+  auto row22 = [](int rr) { return rr < 11 ? (rr < 8 ? rr : 16 + rr - 8) : (rr - 11 < 8 ? 8 + rr - 11 : 19 + rr - 19); };
+  auto col22 = [](int cc) { return cc < 11 ? cc : 12 + cc - 11; };
+  for (int b2 = 0; b2 < 11; ++b2)
+    for (int a2 = 0; a2 < 11; ++a2) {
+      T[b2 * R89_P12 + a2] = (double)(0.25L * Mc[b2 * h + a2]);
+      T[R89_OFF_M2 + b2 * R89_P12 + a2] = (double)(0.25L * Mc[(11 + b2) * h + 11 + a2]);
+    }
+  for (int i = 0; i < 22; ++i)
+    for (int j = 0; j < 22; ++j) {
+      T[R89_OFF_MC + row22(i) * R89_P28 + col22(j)] = (double)(0.5L * Mc[(22 + i) * h + 22 + j]);
+      // complex 11 x 11 blocks as real [[Re, -Im], [Im, Re]]: A = Ms[33.., 0..] (f 0 -> 3), B = Ms[22.., 11..] (f 1 -> 2)
+      const int bi = i % 11, bj = j % 11;
+      const cld za = Ms[(33 + bi) * h + bj], zb = Ms[(22 + bi) * h + 11 + bj];
+      const ld ra = (i < 11) == (j < 11) ? za.real() : (i < 11 ? -za.imag() : za.imag());
+      const ld rb = (i < 11) == (j < 11) ? zb.real() : (i < 11 ? -zb.imag() : zb.imag());
+      T[R89_OFF_RA + row22(i) * R89_P28 + col22(j)] = (double)(0.5L * ra);
+      T[R89_OFF_RB + row22(i) * R89_P28 + col22(j)] = (double)(0.5L * rb);
+    }
+  unsigned char* RT = (unsigned char*)(T + R89_OFF_RT);
+  for (int a = 0; a < h; ++a) RT[a] = (unsigned char)r[a];
+}
+
 int scv_pfa_tables(scv_ctx* c, int K, const double2** out) {
   const std::string key = "pfa_" + std::to_string(K);
   auto it = c->aux.find(key);
@@ -71,6 +174,12 @@ int scv_pfa_tables(scv_ctx* c, int K, const double2** out) {
   for (int s = 0; s < 4; ++s) {
     const int p = f[s];
     if (p == 1) continue;
+    if (pfa_rader89(p)) {
+      const size_t base = tab.size();
+      tab.resize(base + R89_TAB, make_double2(0.0, 0.0));
+      rader89_tables((double*)(tab.data() + base));
+      continue;
+    }
     if (pfa_use_mma(p, K)) {
       // dense C and S matrices (M rows x pitch doubles each), row 0 = (1, 0)
       const int h = (p - 1) / 2, M = mma_M(p), PA = mma_pa(p);
@@ -271,7 +380,7 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
 // duplicated per CTA).
 // ---------------------------------------------------------------------------
 #ifndef SCV_ROWS_GRP
-#define SCV_ROWS_GRP 5, 96
+#define SCV_ROWS_GRP 4, 96
 #endif
 template <int K> struct PfaGrpCfg { static constexpr int NG = 0, NTG = 0; };
 #define SCV_RGCFG_(KK, ...)                                  \

@@ -118,8 +118,19 @@ __host__ __device__ constexpr int mma_aoff(int p, int row, int kk) {
 }
 // table size in double2 units: 1-D (cos, sin) table of p entries, or the two
 // dense matrices (2 * M * pitch doubles = M * pitch double2)
+// Radix 89 by Rader + CRT (SCV_RADER89, see pfa_stage_rader89): the table is
+// five small dense matrices (M0, M2: 16 x 12; Mc, RA, RB: 24 x 28 doubles)
+// and the 44 Rader positions r_a = 3^a mod 89 as bytes.
+#ifndef SCV_RADER89
+#define SCV_RADER89 1
+#endif
+constexpr int R89_P12 = 12, R89_P28 = 28;
+constexpr int R89_OFF_M2 = 16 * R89_P12, R89_OFF_MC = 2 * 16 * R89_P12, R89_OFF_RA = R89_OFF_MC + 24 * R89_P28,
+              R89_OFF_RB = R89_OFF_RA + 24 * R89_P28, R89_OFF_RT = R89_OFF_RB + 24 * R89_P28;  // doubles
+constexpr int R89_TAB = (R89_OFF_RT * 8 + 48 + 15) / 16;  // double2 units (+ 44 position bytes)
+__host__ __device__ constexpr bool pfa_rader89(int p) { return SCV_RADER89 && p == 89; }
 __host__ __device__ constexpr int pfa_tab(int p, int K) {
-  return p <= 1 ? 0 : pfa_use_mma(p, K) ? mma_M(p) * mma_pa(p) : p;
+  return p <= 1 ? 0 : pfa_rader89(p) ? R89_TAB : pfa_use_mma(p, K) ? mma_M(p) * mma_pa(p) : p;
 }
 template <class PL>
 __host__ __device__ constexpr int pfa_rtab_total() {
@@ -772,13 +783,173 @@ __device__ __forceinline__ void pfa_stage_mma_blk(double2* X, const double2* tab
   grp_sync(bar, NT);
 }
 
+// Radix-89 stage by Rader's algorithm with a 4 x 11 CRT split, on the FP64
+// tensor cores.  With r_a = 3^a mod 89 (3 is a primitive root; a < 44 picks one
+// of each pair {j, 89-j}), s'_a = x_{r_a} + x_{89-r_a}, d'_a = x_{r_a} - x_{89-r_a}:
+//   A'_b = sum_a cos(2 pi r_a r_b / 89) s'_a   (44-point cyclic correlation),
+//   B'_b = sum_a sin(2 pi r_a r_b / 89) d'_a   (44-point negacyclic correlation),
+//   y_{r_b} = x0 + A'_b + DIR i B'_b,  y_{89-r_b} = x0 + A'_b - DIR i B'_b,  y_0 = x0 + sum s'.
+// a <-> (a mod 4, a mod 11) turns each correlation into a 2-D one; a 4-point
+// transform along a mod 4 (cyclic DFT for A', sign-twisted odd DFT for B', done
+// in-lane: each lane holds all four a mod 4 of its a mod 11 values) leaves
+// dense 11 x 11 (real) / 22 x 22 (complex as real) products on the tensor
+// cores: 66 DMMA per 4 butterflies instead of the 132 of the dense symmetric
+// form (pfa_stage_mma_blk).  The matrices are built on the host in long double
+// (pfa.cu) and checked end to end against torch.fft (tools/fftbench.py).
+// Warp-owned blocks of 4 butterflies as in pfa_stage_mma_blk.  Lane (ar, ac):
+// B-fragment column ar (butterfly slot(ar>>1), component ar&1) holding the
+// a mod 11 = ac + 4 kt values; epilogue butterfly slot(ac), output rows ar.
+template <class PL, int S, int DIR, int R, int NT, int PITCH>
+__device__ __forceinline__ void pfa_stage_rader89(double2* X, const double2* tab, int gtid, int bar) {
+  constexpr int p = 89;
+  constexpr int K = PL::K;
+  constexpr int step = pfa_st<PL, S>();
+  constexpr int nbf = K / p;
+  constexpr int NBF = R * nbf;
+  constexpr int NBLK = 2 * ((NBF + 7) / 8);
+  constexpr int NW = NT / 32;
+  const double* T0 = (const double*)(tab + pfa_tab_off<PL, S>());
+  const unsigned char* RT = (const unsigned char*)(T0 + R89_OFF_RT);
+  const double* Xd = (const double*)X;
+  const int lane = gtid & 31, warp = gtid >> 5;
+  const int ar = lane >> 2, ac = lane & 3;
+  constexpr double s2 = 0.70710678118654752440;
+  auto slot = [](int i) { return (i >> 1) + 4 * (i & 1); };
+#pragma unroll 1
+  for (int q = warp; q < NBLK; q += NW) {
+    const int gb = (q >> 1) * 8 + 2 * (q & 1);
+    const int bfB = gb + slot(ar >> 1);
+    const bool okB = bfB < NBF;
+    int rowd = 0, c0B = 0;
+    if (okB) {
+      const int rr = bfB / nbf, b = bfB - rr * nbf;
+      c0B = pfa_base<PL, S>(b);
+      rowd = 2 * rr * PITCH + (ar & 1);
+    }
+    const int bfE = gb + slot(ac);
+    const bool okE = bfE < NBF;
+    int eoff = 0;
+    double2 x0 = make_double2(0.0, 0.0);
+    if (okE) {
+      const int rr = bfE / nbf, b = bfE - rr * nbf;
+      eoff = rr * PITCH + pfa_base<PL, S>(b);
+      x0 = X[eoff];
+    }
+    // ---- per k-step kt (a2 = ac + 4 kt): gather, in-lane 4-point transforms,
+    // and the tensor-core products of that k-step (the Im halves of the 22 x 22
+    // products are k-step kt + 3), so only one k-step of B operands is live
+    double y0[2][2], y2[2][2], yu[3][2], za[3][2], zb[3][2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) y0[t][0] = y0[t][1] = y2[t][0] = y2[t][1] = 0.0;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) yu[t][0] = yu[t][1] = za[t][0] = za[t][1] = zb[t][0] = zb[t][1] = 0.0;
+    double ssum = 0.0;
+#pragma unroll
+    for (int kt = 0; kt < 3; ++kt) {
+      const int a2 = ac + 4 * kt;
+      double sv[4], w[4];
+#pragma unroll
+      for (int a1 = 0; a1 < 4; ++a1) {
+        sv[a1] = 0.0;
+        w[a1] = 0.0;
+        if (okB && a2 < 11) {
+          const int a = (33 * a1 + 12 * a2) % 44;
+          const int r = RT[a];
+          const double xa = Xd[rowd + 2 * (c0B + r * step)];
+          const double xb = Xd[rowd + 2 * (c0B + (p - r) * step)];
+          sv[a1] = xa + xb;
+          const double dv = xa - xb;
+          w[a1] = ((a >> 2) & 1) ? -dv : dv;
+        }
+      }
+      const double bV0 = (sv[0] + sv[2]) + (sv[1] + sv[3]);
+      const double bV2 = (sv[0] + sv[2]) - (sv[1] + sv[3]);
+      const double bUr = sv[0] - sv[2], bUi = sv[1] - sv[3];
+      ssum += bV0;
+      const double P = (w[1] - w[3]) * s2, Q = (w[1] + w[3]) * s2;
+      const double bAr = w[0] + P, bAi = -w[2] - Q, bBr = w[0] - P, bBi = w[2] - Q;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int o = (t * 8 + ar) * R89_P12 + kt * 4 + ac;
+        dmma(y0[t][0], y0[t][1], T0[o], bV0);
+        dmma(y2[t][0], y2[t][1], T0[R89_OFF_M2 + o], bV2);
+      }
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        const int o = (t * 8 + ar) * R89_P28 + kt * 4 + ac;
+        dmma(yu[t][0], yu[t][1], T0[R89_OFF_MC + o], bUr);
+        dmma(yu[t][0], yu[t][1], T0[R89_OFF_MC + o + 12], bUi);
+        dmma(za[t][0], za[t][1], T0[R89_OFF_RA + o], bAr);
+        dmma(za[t][0], za[t][1], T0[R89_OFF_RA + o + 12], bAi);
+        dmma(zb[t][0], zb[t][1], T0[R89_OFF_RB + o], bBr);
+        dmma(zb[t][0], zb[t][1], T0[R89_OFF_RB + o + 12], bBi);
+      }
+    }
+    // y_0 = x0 + sum_a s'_a: column sums over the quad, then to the epilogue lanes
+    ssum += __shfl_xor_sync(0xffffffffu, ssum, 1);
+    ssum += __shfl_xor_sync(0xffffffffu, ssum, 2);
+    const double s0r = __shfl_sync(0xffffffffu, ssum, (2 * ac) * 4);
+    const double s0i = __shfl_sync(0xffffffffu, ssum, (2 * ac + 1) * 4);
+    // rows 3..5 of the third product tile hold the Im parts of b2 = 8..10
+    double uhi[2], ahi[2], bhi[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      uhi[c] = __shfl_down_sync(0xffffffffu, yu[2][c], 12);
+      ahi[c] = __shfl_down_sync(0xffffffffu, za[2][c], 12);
+      bhi[c] = __shfl_down_sync(0xffffffffu, zb[2][c], 12);
+    }
+    __syncwarp();
+    if (okE) {
+      double2* Xr = X + eoff;
+      if (ar == 0) Xr[0] = make_double2(x0.x + s0r, x0.y + s0i);
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int b2 = hh * 8 + ar;
+        if (hh == 1 && ar >= 3) continue;
+        // per component c (0 = re, 1 = im of the butterfly)
+        double Aq[4][2], Bq[4][2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const double Y0 = y0[hh][c], Y2 = y2[hh][c];
+          const double Yr = hh ? yu[2][c] : yu[0][c], Yi = hh ? uhi[c] : yu[1][c];
+          const double ZAr = hh ? za[2][c] : za[0][c], ZAi = hh ? ahi[c] : za[1][c];
+          const double ZBr = hh ? zb[2][c] : zb[0][c], ZBi = hh ? bhi[c] : zb[1][c];
+          Aq[0][c] = (Y0 + Y2) + Yr;
+          Aq[1][c] = (Y0 - Y2) + Yi;
+          Aq[2][c] = (Y0 + Y2) - Yr;
+          Aq[3][c] = (Y0 - Y2) - Yi;
+          Bq[0][c] = ZAr + ZBr;
+          Bq[1][c] = ((ZAr + ZAi) + (ZBi - ZBr)) * s2;
+          Bq[2][c] = ZAi - ZBi;
+          Bq[3][c] = ((ZAi - ZAr) + (ZBr + ZBi)) * s2;
+        }
+#pragma unroll
+        for (int b1 = 0; b1 < 4; ++b1) {
+          const int b = (33 * b1 + 12 * b2) % 44;
+          const double sg = ((b >> 2) & 1) ? -1.0 : 1.0;
+          const int r = RT[b];
+          const double Ar = x0.x + Aq[b1][0], Ai = x0.y + Aq[b1][1];
+          const double Br = sg * Bq[b1][0], Bi = sg * Bq[b1][1];
+          // DIR i B
+          const double iBr = DIR < 0 ? Bi : -Bi, iBi = DIR < 0 ? -Br : Br;
+          Xr[r * step] = make_double2(Ar + iBr, Ai + iBi);
+          Xr[(p - r) * step] = make_double2(Ar - iBr, Ai - iBi);
+        }
+      }
+    }
+    __syncwarp();
+  }
+  grp_sync(bar, NT);
+}
+
 // In-place K-point DFT (sign DIR) of R rows at X[r*PITCH + n] (natural order
 // in; CRT order out, read through pfa_pos).  Caller syncs before (data ready).
 // scr: pfa_scratch<PL,R,NT>() double2 of shared scratch (DMMA stages).
 template <class PL, int S, int DIR, int R, int NT, int PITCH>
 __device__ __forceinline__ void pfa_stage_any(double2* X, const double2* tab, double2* scr, int gtid, int bar) {
   constexpr int p = pfa_p<PL, S>();
-  if constexpr (pfa_use_mma(p, PL::K) && SCV_PFA_BLK) pfa_stage_mma_blk<PL, S, DIR, R, NT, PITCH>(X, tab, gtid, bar);
+  if constexpr (pfa_rader89(p)) pfa_stage_rader89<PL, S, DIR, R, NT, PITCH>(X, tab, gtid, bar);
+  else if constexpr (pfa_use_mma(p, PL::K) && SCV_PFA_BLK) pfa_stage_mma_blk<PL, S, DIR, R, NT, PITCH>(X, tab, gtid, bar);
   else if constexpr (pfa_use_mma(p, PL::K) && mma_reg(PL::K, p, R, NT)) pfa_stage_mma_reg<PL, S, DIR, R, NT, PITCH>(X, tab, gtid, bar);
   else if constexpr (pfa_use_mma(p, PL::K)) pfa_stage_mma<PL, S, DIR, R, NT, PITCH>(X, tab, scr, gtid, bar);
   else pfa_stage<PL, S, DIR, R, NT, PITCH>(X, tab, gtid, bar);

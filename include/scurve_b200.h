@@ -15,6 +15,9 @@
  *   scv_accumulate             <- the acc += W psi loop of synthesize  transform.py:170-178
  *   scv_finish_acc             <- acc[:s^2]=0 (+ real symmetry)    transform.py:186, 246-252
  *   scv_halfpi_wedge           <- build_halfpi_table / halfpi_table wigner.py:209-240
+ *   scv_edge_columns           <- wigner_d_edge_columns            wigner.py:304-322
+ *   scv_rotate_to_north        <- rotate_to_north                  transform.py:256-277
+ *   scv_rotate_from_north      <- rotate_from_north                transform.py:280-297
  *   scv_so3_inverse_curvelet_slab  <- so3_inverse_curvelet restricted to beta rows [b0, b0+nb)
  *   scv_so3_forward_curvelet_slab  <- the beta sum of so3_forward_curvelet over beta rows [b0, b0+nb)
  *                                     (so3.py:203-243; the multi-GPU beta-slab shards)
@@ -157,6 +160,24 @@ int scv_accumulate_scaling(scv_ctx* ctx, int L, int Ls, const double* slm,
 
 /* acc[: spin^2] = 0; if real, re-impose f_{l,-m} = (-1)^m conj f_{lm}, f_l0 real. */
 int scv_finish_acc(scv_ctx* ctx, int L, int spin, int real, double* acc, void* stream);
+
+/* Frame rotation of one scale.  Dense Wigner coefficients
+ * (the reference's WignerCoeffs.planes) are packed plane after plane: plane l,
+ * (2l+1) x (2l+1) complex128 with rows m+l and columns k+l, starts at entry
+ * l(4l^2-1)/3; L(4L^2-1)/3 entries in total.  theta is the scale's tiling
+ * angle (Tiling.angles, in [pi/2, pi]).
+ *
+ * edge_columns: out (L, 2L-1, 2) float64, out[l][k+L-1] = (d^l_{k,+l}(theta),
+ * d^l_{k,-l}(theta)) for |k| <= l, zero elsewhere.
+ * rotate_to_north: w (2, L, 2L-1) -> dense planes,
+ *   plane_l = outer(w[0,l], d_{.,+l}) + outer(w[1,l], d_{.,-l}) (l >= 1).
+ * rotate_from_north: dense planes -> w (2, L, 2L-1), w[0,l] = plane_l d_{.,+l},
+ *   w[1,l] = plane_l d_{.,-l} (l >= 1), zero outside |m| <= l and at w[1,0]. */
+int scv_edge_columns(scv_ctx* ctx, int L, double theta, double* out, void* stream);
+int scv_rotate_to_north(scv_ctx* ctx, int L, double theta, const double* w, double* dense,
+                        void* stream);
+int scv_rotate_from_north(scv_ctx* ctx, int L, double theta, const double* dense, double* w,
+                          void* stream);
 
 #ifdef __cplusplus
 }

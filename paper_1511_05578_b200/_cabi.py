@@ -26,6 +26,7 @@ _lib_lock = threading.Lock()
 
 _P = ctypes.c_void_p
 _I = ctypes.c_int
+_D = ctypes.c_double
 
 # name -> argtypes (all return int unless listed in _RESTYPE)
 _SIGS = {
@@ -53,6 +54,9 @@ _SIGS = {
     "scv_accumulate": [_P, _I, _I, _P, _P, _P, _P, _P],
     "scv_accumulate_scaling": [_P, _I, _I, _P, _P, _P, _P],
     "scv_finish_acc": [_P, _I, _I, _I, _P, _P],
+    "scv_edge_columns": [_P, _I, _D, _P, _P],
+    "scv_rotate_to_north": [_P, _I, _D, _P, _P, _P],
+    "scv_rotate_from_north": [_P, _I, _D, _P, _P, _P],
 }
 _RESTYPE = {"scv_last_error": ctypes.c_char_p, "scv_workspace_bytes": ctypes.c_longlong,
             "scv_launch_count": ctypes.c_longlong}

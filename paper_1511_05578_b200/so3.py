@@ -25,6 +25,7 @@ __all__ = [
     "SO3Grid",
     "SO3Signal",
     "SO3Slab",
+    "WignerCoeffs",
     "so3_forward_curvelet",
     "so3_forward_curvelet_slab",
     "so3_forward_curvelet_real",
@@ -108,6 +109,65 @@ class CurveletWignerCoeffs:
 
     def set_row(self, n: int, row) -> None:
         self.row(n)[:] = as_device(row, torch.complex128)
+
+
+def plane_offset(ell: int) -> int:
+    """Start of plane ell in the packed dense layout: sum_{l<ell} (2l+1)^2."""
+    return ell * (4 * ell * ell - 1) // 3
+
+
+class WignerCoeffs:
+    """Dense Wigner coefficients: planes[ell][m + ell, n + ell] (so3.py:93-121).
+
+    The planes live packed back to back in one device tensor ``values``
+    (plane ell at ``plane_offset(ell)``, L(4L^2-1)/3 complex128 entries);
+    ``planes`` is the reference's list of (2l+1, 2l+1) views into it.
+    """
+
+    def __init__(self, band_limit: int, planes=None, *, values=None):
+        L = int(band_limit)
+        if L < 1:
+            raise ValueError(f"band limit must be positive, got {L}")
+        self.band_limit = L
+        if values is not None:
+            v = as_device(values, torch.complex128).reshape(-1)
+            if v.numel() != plane_offset(L):
+                raise ValueError(f"expected {plane_offset(L)} packed entries, got {v.numel()}")
+            self.values = v
+        else:
+            if planes is None or len(planes) != L:
+                raise ValueError(f"expected {L} planes, got {0 if planes is None else len(planes)}")
+            for ell, pl in enumerate(planes):
+                if _shape(pl) != (2 * ell + 1, 2 * ell + 1):
+                    raise ValueError(f"plane {ell} has shape {_shape(pl)}")
+            self.values = torch.cat([as_device(pl, torch.complex128).reshape(-1) for pl in planes])
+
+    @property
+    def planes(self) -> list:
+        return [self.plane(ell) for ell in range(self.band_limit)]
+
+    def plane(self, ell: int) -> torch.Tensor:
+        if not 0 <= ell < self.band_limit:
+            raise ValueError(f"degree {ell} out of range")
+        n = 2 * ell + 1
+        return self.values[plane_offset(ell): plane_offset(ell + 1)].view(n, n)
+
+    @classmethod
+    def zeros(cls, L: int) -> "WignerCoeffs":
+        if L < 1:
+            raise ValueError(f"band limit must be positive, got {L}")
+        return cls(L, values=torch.zeros(plane_offset(L), dtype=torch.complex128, device=_dev()))
+
+    @classmethod
+    def random(cls, L: int, rng: np.random.Generator) -> "WignerCoeffs":
+        planes = [rng.uniform(-1, 1, (2 * ell + 1, 2 * ell + 1))
+                  + 1j * rng.uniform(-1, 1, (2 * ell + 1, 2 * ell + 1)) for ell in range(L)]
+        return cls(L, planes)
+
+
+def _dev():
+    from .sphere import _device
+    return _device()
 
 
 def _check_sparse_grid(w, grid):

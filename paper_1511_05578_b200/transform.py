@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import _cabi
-from .so3 import (CurveletWignerCoeffs, SO3Grid, SO3Signal, so3_forward_curvelet,
+from .so3 import (CurveletWignerCoeffs, SO3Grid, WignerCoeffs, SO3Signal, so3_forward_curvelet,
                   so3_forward_curvelet_real, so3_forward_curvelet_slab, so3_inverse_curvelet,
                   so3_inverse_curvelet_real, so3_inverse_curvelet_slab)
 from .sphere import (HarmonicCoeffs, SphereGrid, SphereSignal, sht_forward, sht_forward_real,
@@ -33,6 +33,8 @@ __all__ = [
     "CurveletCoeffs",
     "analyze",
     "analyze_real",
+    "rotate_from_north",
+    "rotate_to_north",
     "roundtrip_streamed",
     "scale_band_limit",
     "scaling_band_limit",
@@ -299,3 +301,41 @@ def roundtrip_streamed(f: SphereSignal, t: Tiling, multires: bool = True, slab_b
     ctx.call("accumulate_scaling", L, slm.band_limit, _cabi.ptr(slm.values), _cabi.ptr(dt.scaling), _cabi.ptr(acc))
     ctx.call("finish_acc", L, p.spin, 0, _cabi.ptr(acc))
     return sht_inverse(HarmonicCoeffs(L, p.spin, acc))
+
+
+# ---------------------------------------------------------------------------
+# frame rotation (transform.py:256-297), csrc/rotate.cu
+# ---------------------------------------------------------------------------
+def _rotation_angle(j: int, t: Tiling) -> float:
+    p = t.params
+    if not p.j_min <= j <= p.j_max:
+        raise ValueError(f"scale {j} outside [{p.j_min}, {p.j_max}]")
+    return float(t.angles[j - p.j_min])
+
+
+def rotate_to_north(w: CurveletWignerCoeffs, j: int, t: Tiling) -> WignerCoeffs:
+    """Move a scale's coefficients to the frame of the pole-centred function
+    (transform.py:256-277): dense planes outer(w[+l], d_{.,+l}(theta_j)) +
+    outer(w[-l], d_{.,-l}(theta_j)), one warp per plane row (k_rot_to_north)."""
+    if not isinstance(w, CurveletWignerCoeffs):
+        raise TypeError("rotate_to_north expects sparse coefficients")
+    theta = _rotation_angle(j, t)
+    L = w.band_limit
+    ctx = _cabi.context(w.values.device)
+    out = WignerCoeffs.zeros(L) if L == 1 else WignerCoeffs(
+        L, values=torch.empty(L * (4 * L * L - 1) // 3, dtype=torch.complex128, device=w.values.device))
+    ctx.call("rotate_to_north", L, theta, _cabi.ptr(w.values), _cabi.ptr(out.values))
+    return out
+
+
+def rotate_from_north(w: WignerCoeffs, j: int, t: Tiling) -> CurveletWignerCoeffs:
+    """Inverse of rotate_to_north, exact on its image (transform.py:280-297):
+    w[+l] = plane_l d_{.,+l}(theta_j), w[-l] = plane_l d_{.,-l}(theta_j)."""
+    if not isinstance(w, WignerCoeffs):
+        raise TypeError("rotate_from_north expects dense coefficients")
+    theta = _rotation_angle(j, t)
+    L = w.band_limit
+    ctx = _cabi.context(w.values.device)
+    out = torch.empty((2, L, 2 * L - 1), dtype=torch.complex128, device=w.values.device)
+    ctx.call("rotate_from_north", L, theta, _cabi.ptr(w.values), _cabi.ptr(out))
+    return CurveletWignerCoeffs(L, out)

@@ -16,7 +16,7 @@ import torch
 
 from . import _cabi
 
-__all__ = ["halfpi_wedge", "wedge_index", "wedge_plane"]
+__all__ = ["halfpi_wedge", "wedge_index", "wedge_plane", "wigner_d_edge_columns", "edge_column_table"]
 
 
 def wedge_size(L: int) -> int:
@@ -57,3 +57,23 @@ def halfpi_wedge(L: int, device=None) -> torch.Tensor:
     out = torch.empty(wedge_size(L), dtype=torch.float64, device=torch.device("cuda", ctx.device))
     ctx.call("halfpi_wedge", L, _cabi.ptr(out))
     return out
+
+
+def edge_column_table(L: int, beta: float, device=None) -> torch.Tensor:
+    """(L, 2L-1, 2) float64 device table: [l, k+L-1] = (d^l_{k,+l}(beta),
+    d^l_{k,-l}(beta)) for |k| <= l, zero elsewhere (csrc/rotate.cu)."""
+    if L < 1:
+        raise ValueError(f"band limit must be positive, got {L}")
+    ctx = _cabi.context(device)
+    out = torch.empty((L, 2 * L - 1, 2), dtype=torch.float64, device=torch.device("cuda", ctx.device))
+    ctx.call("edge_columns", L, float(beta), _cabi.ptr(out))
+    return out
+
+
+def wigner_d_edge_columns(ell: int, beta: float):
+    """Columns d^ell_{k,+ell}(beta) and d^ell_{k,-ell}(beta) over k in
+    [-ell, ell] (wigner.py:304-322), log-space closed forms on the device."""
+    if ell < 0:
+        raise ValueError(f"degree must be non-negative, got {ell}")
+    tab = edge_column_table(ell + 1, beta)[ell]
+    return tab[:, 0], tab[:, 1]

@@ -175,6 +175,74 @@ def transform_cases(out):
     out["c1_wlast"] = w.values
 
 
+def rotation_cases(out):
+    """Frame rotation (transform.py:256-297) on the reference's own random
+    generators; SURVEY 8(f) row 1."""
+    rng = np.random.default_rng(11)
+    # scale j=2 of L=16 spin 1, J0=1 (tests/test_transform.py:198-214 shapes)
+    t = scurve.build_tiling(scurve.TilingParams(16, 1, 2.0, 1))
+    for j, Lw in ((2, 4), (3, 8), (t.params.j_max, 16)):
+        w = scurve.CurveletWignerCoeffs.random(Lw, rng)
+        dense = scurve.rotate_to_north(w, j, t)
+        back = scurve.rotate_from_north(dense, j, t)
+        out[f"rot16_j{j}_theta"] = np.array(float(t.angles[j - t.params.j_min]))
+        out[f"rot16_j{j}_w"] = w.values
+        out[f"rot16_j{j}_dense"] = np.concatenate([p.ravel() for p in dense.planes])
+        out[f"rot16_j{j}_back"] = back.values
+    # dense random input (projection), L=8, scale 2 of an L=8 J0=0 tiling
+    t8 = scurve.build_tiling(scurve.TilingParams(8, 0, 2.0, 0))
+    d = scurve.WignerCoeffs.random(8, rng)
+    out["rot8_dense_in"] = np.concatenate([p.ravel() for p in d.planes])
+    out["rot8_theta"] = np.array(float(t8.angles[2]))
+    out["rot8_from"] = scurve.rotate_from_north(d, 2, t8).values
+    # identity-angle scale (theta = pi): L=16 spin 2 J0=0, scale 0
+    t0 = scurve.build_tiling(scurve.TilingParams(16, 2, 2.0, 0))
+    w = scurve.CurveletWignerCoeffs.random(4, rng)
+    out["rot_pi_theta"] = np.array(float(t0.angles[0]))
+    out["rot_pi_w"] = w.values
+    out["rot_pi_dense"] = np.concatenate([p.ravel() for p in scurve.rotate_to_north(w, 0, t0).planes])
+    # a larger band limit, sampled: L=48 at the finest scale of an L=48 J0=2 tiling
+    t48 = scurve.build_tiling(scurve.TilingParams(48, 0, 2.0, 2))
+    j = t48.params.j_max
+    w = scurve.CurveletWignerCoeffs.random(48, rng)
+    dense = scurve.rotate_to_north(w, j, t48)
+    flat = np.concatenate([p.ravel() for p in dense.planes])
+    idx = rng.integers(0, flat.size, 512)
+    out["rot48_theta"] = np.array(float(t48.angles[j - t48.params.j_min]))
+    out["rot48_w"] = w.values
+    out["rot48_idx"] = idx
+    out["rot48_val"] = flat[idx]
+    out["rot48_l2"] = np.array(np.sqrt((np.abs(flat) ** 2).sum()))
+    out["rot48_back"] = scurve.rotate_from_north(dense, j, t48).values
+    for ell in (0, 1, 17, 47):
+        pos, neg = wigner.wigner_d_edge_columns(ell, float(out["rot48_theta"]))
+        out[f"edge48_{ell}"] = np.stack([pos, neg])
+
+
+def main_rotation():
+    out = {}
+    rotation_cases(out)
+    path = os.path.join(HERE, "reference_rotation.npz")
+    np.savez_compressed(path, **out)
+    print(f"wrote {len(out)} arrays to {path} ({os.path.getsize(path) / 1e6:.2f} MB)")
+
+
+def main_container():
+    """SCRV1 files written by the reference's own writers (container.py:152-206)."""
+    rng = np.random.default_rng(21)
+    t = scurve.build_tiling(scurve.TilingParams(8, 2, 2.0, 1))
+    f = scurve.sht_inverse(scurve.random_coeffs(8, 2, rng))
+    scurve.container.write_sphere(os.path.join(HERE, "ref_sphere_L8s2.scrv"), f, extra={"seed": 21})
+    c = scurve.analyze(f, t)
+    scurve.container.write_coeffs(os.path.join(HERE, "ref_coeffs_L8s2.scrv"), c, extra={"note": "golden"})
+    t0 = scurve.build_tiling(scurve.TilingParams(8, 0, 2.0, 1))
+    fr = scurve.sht_inverse_real(scurve.random_coeffs(8, 0, rng, real=True)) if hasattr(scurve, "sht_inverse_real") else None
+    if fr is not None:
+        cr = scurve.analyze_real(fr, t0)
+        scurve.container.write_coeffs(os.path.join(HERE, "ref_coeffs_L8real.scrv"), cr)
+    print("wrote SCRV1 fixtures")
+
+
 def main():
     out = {}
     wigner_cases(out)
@@ -188,4 +256,11 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if "rotation" in sys.argv[1:]:
+        main_rotation()
+    elif "container" in sys.argv[1:]:
+        main_container()
+    else:
+        main()
+        main_rotation()
+        main_container()

@@ -44,3 +44,13 @@ def golden_tilings():
         t = T.build_tiling(T.TilingParams(L, s, lam, j0))
         out.setdefault((L, s, lam, j0), t)
     return out
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _fresh_step_tables():
+    """Every test module starts from an empty tiling step-table memo, as in a
+    fresh process, so a module's golden comparisons do not depend on which
+    tilings earlier modules built (see GOLDEN_TILING_ORDER above)."""
+    from paper_1511_05578_b200 import tiling as T
+    T._reset_step_tables()
+    yield

@@ -8,6 +8,8 @@ created lazily and shared; calls are serialised per context by a lock
 
 from __future__ import annotations
 
+import contextlib
+import contextvars
 import ctypes
 import os
 import threading
@@ -165,6 +167,29 @@ _ctxs: dict = {}
 _ctx_lock = threading.Lock()
 
 
+# A private context (own scratch and tables) bound for the current thread /
+# task by `using`, so independent pipelines can run concurrently on separate
+# streams without sharing scratch buffers (GraphedRoundTrip lanes).
+_override: contextvars.ContextVar = contextvars.ContextVar("scv_context_override", default=None)
+
+
+def new_context(device: int | None = None) -> Context:
+    """A fresh, unshared context on `device` (default: the current device)."""
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1511_05578_b200 needs a CUDA device (B200); there is no CPU fallback")
+    return Context(torch.cuda.current_device() if device is None else int(device))
+
+
+@contextlib.contextmanager
+def using(ctx: Context):
+    """Route every library call on ctx's device inside the block to `ctx`."""
+    tok = _override.set(ctx)
+    try:
+        yield ctx
+    finally:
+        _override.reset(tok)
+
+
 def context(device: torch.device | int | None = None) -> Context:
     if not torch.cuda.is_available():
         raise RuntimeError("paper_1511_05578_b200 needs a CUDA device (B200); there is no CPU fallback")
@@ -174,6 +199,9 @@ def context(device: torch.device | int | None = None) -> Context:
         idx = device.index if device.index is not None else torch.cuda.current_device()
     else:
         idx = int(device)
+    ov = _override.get()
+    if ov is not None and ov.device == idx:
+        return ov
     with _ctx_lock:
         if idx not in _ctxs:
             _ctxs[idx] = Context(idx)

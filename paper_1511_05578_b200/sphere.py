@@ -134,7 +134,9 @@ class HarmonicCoeffs:
         if _shape(self.values) != (L * L,):
             raise ValueError(f"expected {L * L} coefficients, got shape {_shape(self.values)}")
         low = self.spin * self.spin
-        if low and bool(torch.any(self.values[:low] != 0)):
+        # a data-dependent check syncs the host: skipped while a CUDA graph is being
+        # captured (GraphedRoundTrip), where the values come from this package's own SHT
+        if low and not torch.cuda.is_current_stream_capturing() and bool(torch.any(self.values[:low] != 0)):
             raise ValueError("degrees below |spin| must be exactly zero")
         if self.real and self.spin != 0:
             raise ValueError("real coefficient sets must have spin 0")

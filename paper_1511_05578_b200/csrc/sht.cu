@@ -92,6 +92,93 @@ __global__ void k_sht_bins(int L, int spin, int real, const double2* __restrict_
   B[(long long)row * ncol + col] = v;
 }
 
+
+// Wedge-pair form of k_sht_bins (default, SCV_SHT_BINS_WEDGE=1): one thread
+// per Delta wedge pair (a, b), 0 <= b <= a < L, produces every bin (m', m) in
+// {(+-a, +-b), (+-b, +-a)} from ONE wedge load per degree: the eight bins
+// share |Delta^l_{ab}|, and consecutive threads take consecutive b, so the
+// wedge, the u column and the f_{l,+-b} loads are contiguous.  The per-bin
+// arithmetic is k_sht_bins' (same operands, same order).
+#ifndef SCV_SHT_BINS_WEDGE
+#define SCV_SHT_BINS_WEDGE 1
+#endif
+
+// U[l][mp + L - 1] = Delta^l_{mp,-s}, |mp| <= l
+__global__ void k_sht_ucol(int L, int spin, const double* __restrict__ delta, double* __restrict__ U) {
+  const int K = 2 * L - 1;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)L * K) return;
+  const int l = (int)(t / K), mp = (int)(t - (long long)l * K) - (L - 1);
+  const int as = spin < 0 ? -spin : spin;
+  U[t] = (mp >= -l && mp <= l && l >= as) ? wedge_get(delta, l, mp, -spin) : 0.0;
+}
+
+__global__ void __launch_bounds__(128) k_sht_bins_w(int L, int spin, int real, const double2* __restrict__ flm,
+                                                    const double* __restrict__ delta, const double* __restrict__ U,
+                                                    double2* __restrict__ B) {
+  const int K = 2 * L - 1;
+  const int ncol = real ? L : K;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)L * (L + 1) / 2) return;
+  int a = (int)((sqrt(8.0 * (double)i + 1.0) - 1.0) * 0.5);
+  while ((long long)a * (a + 1) / 2 > i) --a;
+  while ((long long)(a + 1) * (a + 2) / 2 <= i) ++a;
+  const int b = (int)(i - (long long)a * (a + 1) / 2);
+  const int as = spin < 0 ? -spin : spin;
+  // slot k: swap = k >> 2 (m' = +-b, m = +-a), sign of m' = bit 1, sign of m = bit 0
+  int mpk[8], mk[8];
+  bool ok[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int sw = k >> 2, s1 = (k >> 1) & 1, s2 = k & 1;
+    const int x = sw ? b : a, y = sw ? a : b;
+    mpk[k] = s1 ? -x : x;
+    mk[k] = s2 ? -y : y;
+    ok[k] = !(s1 && x == 0) && !(s2 && y == 0) && !(sw && a == b) && !(real && mk[k] < 0);
+  }
+  double sx[8], sy[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) sx[k] = sy[k] = 0.0;
+  const int l0 = a > as ? a : as;
+  for (int l = l0; l < L; ++l) {
+    const double amp = sht_amp(l, spin);
+    const double w = __ldg(delta + wedge_plane_base(l) + (long long)a * (a + 1) / 2 + b);
+    const double* Ul = U + (long long)l * K + (L - 1);
+    const double2* fl = flm + (long long)l * l + l;
+    const double uap = __ldg(Ul + a), uan = __ldg(Ul - a), ubp = __ldg(Ul + b), ubn = __ldg(Ul - b);
+    const double2 fap = __ldg(fl + a), fbp = __ldg(fl + b);
+    const double2 fan = real ? fap : __ldg(fl - a), fbn = real ? fbp : __ldg(fl - b);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (!ok[k]) continue;
+      const int sw = k >> 2, s1 = (k >> 1) & 1, s2 = k & 1;
+      const int mp = mpk[k], m = mk[k];
+      // sign of Delta^l_{mp,m} relative to the wedge value (wedge_get's rules)
+      int neg = 0;
+      if (mp < 0) neg ^= (l + m) & 1;
+      if (m < 0) neg ^= (l + (mp < 0 ? -mp : mp)) & 1;
+      if (sw) neg ^= (a - b) & 1;
+      const double d = neg ? -w : w;
+      const double u = sw ? (s1 ? ubn : ubp) : (s1 ? uan : uap);
+      const double2 f = sw ? (s2 ? fan : fap) : (s2 ? fbn : fbp);
+      sx[k] += (u * (amp * f.x)) * d;
+      sy[k] += (u * (amp * f.y)) * d;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    if (!ok[k]) continue;
+    const int mp = mpk[k], m = mk[k];
+    double2 v = cipow(make_double2(sx[k], sy[k]), -(m + spin));
+    double sn, cs;
+    sincos((double)mp * (SCV_PI / (double)K), &sn, &cs);
+    v = cmul(v, make_double2(cs, sn));
+    const int row = ((mp % K) + K) % K;
+    const int col = real ? m : ((m % K) + K) % K;
+    B[(long long)row * ncol + col] = v;
+  }
+}
+
 __global__ void k_zero_imag_col0(double2* B, int rows, int pitch) {
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < rows) B[(long long)t * pitch].y = 0.0;
@@ -160,9 +247,20 @@ extern "C" int scv_sht_inverse(scv_ctx* c, int L, int spin, int real, const doub
   const long long tot = (long long)K * ncol;
   {
   SCV_PROF(c, s, "sht_bins");
-  k_sht_bins<<<(int)((tot + 127) / 128), 128, 0, s>>>(L, spin, real, (const double2*)flm, c->delta,
-                                                      (double2*)B);
-                                                      c->launches++;
+  if (SCV_SHT_BINS_WEDGE) {
+    void* U = nullptr;
+    SCV_TRY(scv_scratch(c, 2, (size_t)L * K * 8, &U));
+    k_sht_ucol<<<(int)(((long long)L * K + 255) / 256), 256, 0, s>>>(L, spin, c->delta, (double*)U);
+    c->launches++;
+    const long long np = (long long)L * (L + 1) / 2;
+    k_sht_bins_w<<<(int)((np + 127) / 128), 128, 0, s>>>(L, spin, real, (const double2*)flm, c->delta,
+                                                         (const double*)U, (double2*)B);
+    c->launches++;
+  } else {
+    k_sht_bins<<<(int)((tot + 127) / 128), 128, 0, s>>>(L, spin, real, (const double2*)flm, c->delta,
+                                                        (double2*)B);
+    c->launches++;
+  }
   SCV_CUDA(c, cudaGetLastError());
   }
   SCV_PROF(c, s, "sht_ifft");

@@ -57,6 +57,78 @@ __global__ void k_sht_contract(int L, int spin, int real, const double2* __restr
   }
 }
 
+
+// Wedge-pair form of k_sht_contract (SCV_SHT_CONTRACT_WEDGE=1): one thread per
+// (l, b = |m|) accumulates f_{l,+b} and f_{l,-b} over a = |m'| = 0..l; the four
+// terms (+-a, +-b) share one wedge value, U(+-a) = Delta^l_{+-a,-s} are warp
+// broadcasts and Gw[+-a][+-b] are contiguous across the warp's b.
+#ifndef SCV_SHT_CONTRACT_WEDGE
+#define SCV_SHT_CONTRACT_WEDGE 1
+#endif
+__global__ void __launch_bounds__(128) k_sht_contract_w(int L, int spin, int real, const double2* __restrict__ Gw,
+                                                        const double* __restrict__ delta,
+                                                        const double* __restrict__ U, double2* __restrict__ flm) {
+  const int K = 2 * L - 1;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)L * (L + 1) / 2) return;
+  int l = (int)((sqrt(8.0 * (double)i + 1.0) - 1.0) * 0.5);
+  while ((long long)l * (l + 1) / 2 > i) --l;
+  while ((long long)(l + 1) * (l + 2) / 2 <= i) ++l;
+  const int b = (int)(i - (long long)l * (l + 1) / 2);
+  const int as = spin < 0 ? -spin : spin;
+  if (l < as) {
+    flm[(long long)l * l + l + b] = make_double2(0.0, 0.0);
+    if (b > 0) flm[(long long)l * l + l - b] = make_double2(0.0, 0.0);
+    return;
+  }
+  const int ncol = real ? L : K;
+  const int coff = real ? 0 : L - 1;
+  const bool negm = b > 0 && !real;  // compute m = -b directly (real: conjugate fill)
+  const double* Ul = U + (long long)l * K + (L - 1);
+  const double* Wl = delta + wedge_plane_base(l);
+  double px = 0.0, py = 0.0, nx = 0.0, ny = 0.0;
+  for (int a = 0; a <= l; ++a) {
+    const double w = a >= b ? __ldg(Wl + (long long)a * (a + 1) / 2 + b) : __ldg(Wl + (long long)b * (b + 1) / 2 + a);
+    const int swp = a < b ? ((b - a) & 1) : 0;  // transpose sign (m'-m parity)
+#pragma unroll
+    for (int sa = 0; sa < 2; ++sa) {
+      if (sa && a == 0) continue;
+      const int mp = sa ? -a : a;
+      const double u = __ldg(Ul + mp);
+      const double2* grow = Gw + (long long)(mp + L - 1) * ncol + coff;
+      {  // m = +b
+        int neg = swp;
+        if (mp < 0) neg ^= (l + b) & 1;
+        const double d = (neg ? -w : w) * u;
+        const double2 g = __ldg(grow + b);
+        px += d * g.x;
+        py += d * g.y;
+      }
+      if (negm) {  // m = -b
+        int neg = swp;
+        if (mp < 0) neg ^= (l - b) & 1;
+        neg ^= (l + a) & 1;
+        const double d = (neg ? -w : w) * u;
+        const double2 g = __ldg(grow - b);
+        nx += d * g.x;
+        ny += d * g.y;
+      }
+    }
+  }
+  const double amp = sht_amp(l, spin);
+  const double2 v = cipow(make_double2(px * amp, py * amp), b + spin);
+  flm[(long long)l * l + l + b] = v;
+  if (b > 0) {
+    if (real) {
+      double2 cv = make_double2(v.x, -v.y);
+      if (b & 1) cv = make_double2(-cv.x, -cv.y);
+      flm[(long long)l * l + l - b] = cv;
+    } else {
+      flm[(long long)l * l + l - b] = cipow(make_double2(nx * amp, ny * amp), -b + spin);
+    }
+  }
+}
+
 // B[m' mod K][m mod K] = e^{i m' pi/K} i^{-(m+s)} sum_{l} amp D_{m'm} D_{m',-s} f_lm   (sphere.py:191-203)
 // real: B[m' mod K][m], m in [0,L)   (sphere.py:245-252)
 __global__ void k_sht_bins(int L, int spin, int real, const double2* __restrict__ flm,
@@ -225,10 +297,21 @@ extern "C" int scv_sht_forward(scv_ctx* c, int L, int spin, int real, const void
   SCV_TRY(scv_beta_sht(c, L, spin, real, (const double2*)G, (double2*)Gw, 2.0 * SCV_PI / (double)K, s));
   }
   SCV_PROF(c, s, "sht_contract");
-  const long long warps = (long long)L * L;
-  k_sht_contract<<<(int)((warps * 32 + 255) / 256), 256, 0, s>>>(L, spin, real, (const double2*)Gw,
-                                                                 c->delta, (double2*)flm);
-                                                                 c->launches++;
+  if (SCV_SHT_CONTRACT_WEDGE) {
+    void* U = nullptr;
+    SCV_TRY(scv_scratch(c, 0, (size_t)L * K * 8, &U));
+    k_sht_ucol<<<(int)(((long long)L * K + 255) / 256), 256, 0, s>>>(L, spin, c->delta, (double*)U);
+    c->launches++;
+    const long long np = (long long)L * (L + 1) / 2;
+    k_sht_contract_w<<<(int)((np + 127) / 128), 128, 0, s>>>(L, spin, real, (const double2*)Gw, c->delta,
+                                                             (const double*)U, (double2*)flm);
+    c->launches++;
+  } else {
+    const long long warps = (long long)L * L;
+    k_sht_contract<<<(int)((warps * 32 + 255) / 256), 256, 0, s>>>(L, spin, real, (const double2*)Gw,
+                                                                   c->delta, (double2*)flm);
+    c->launches++;
+  }
   SCV_CUDA(c, cudaGetLastError());
   return SCV_OK;
 }

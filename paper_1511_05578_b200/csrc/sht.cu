@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(128) k_sht_contract_w(int L, int spin, int rea
   const double* Ul = U + (long long)l * K + (L - 1);
   const double* Wl = delta + wedge_plane_base(l);
   double px = 0.0, py = 0.0, nx = 0.0, ny = 0.0;
+#pragma unroll 4
   for (int a = 0; a <= l; ++a) {
     const double w = a >= b ? __ldg(Wl + (long long)a * (a + 1) / 2 + b) : __ldg(Wl + (long long)b * (b + 1) / 2 + a);
     const int swp = a < b ? ((b - a) & 1) : 0;  // transpose sign (m'-m parity)
@@ -212,6 +213,9 @@ __global__ void __launch_bounds__(128) k_sht_bins_w(int L, int spin, int real, c
 #pragma unroll
   for (int k = 0; k < 8; ++k) sx[k] = sy[k] = 0.0;
   const int l0 = a > as ? a : as;
+  // the wedge loads of successive degrees are independent DRAM accesses one
+  // plane apart: unrolled so several are in flight per thread
+#pragma unroll 4
   for (int l = l0; l < L; ++l) {
     const double amp = sht_amp(l, spin);
     const double w = __ldg(delta + wedge_plane_base(l) + (long long)a * (a + 1) / 2 + b);

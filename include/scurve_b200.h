@@ -18,6 +18,8 @@
  *   scv_edge_columns           <- wigner_d_edge_columns            wigner.py:304-322
  *   scv_rotate_to_north        <- rotate_to_north                  transform.py:256-277
  *   scv_rotate_from_north      <- rotate_from_north                transform.py:280-297
+ *   scv_abs_max, scv_histogram,
+ *   scv_sort_f64, scv_gini_sums <- cmd_sparsity / gini_coefficient  cli.py:59-70, 268-320
  *   scv_so3_inverse_curvelet_slab  <- so3_inverse_curvelet restricted to beta rows [b0, b0+nb)
  *   scv_so3_forward_curvelet_slab  <- the beta sum of so3_forward_curvelet over beta rows [b0, b0+nb)
  *                                     (so3.py:203-243; the multi-GPU beta-slab shards)
@@ -178,6 +180,23 @@ int scv_rotate_to_north(scv_ctx* ctx, int L, double theta, const double* w, doub
                         void* stream);
 int scv_rotate_from_north(scv_ctx* ctx, int L, double theta, const double* dense, double* w,
                           void* stream);
+
+/* Sparsity statistics (cli.py:59-70, 268-320).
+ * abs_max: mags[i] = |v[i]| (complex128 if is_complex, else float64; mags may
+ *   be NULL), and *top = max(*top, max_i |v[i]|) on the device (*top >= 0).
+ * histogram: counts[k] += #{i : x_i = mags[i] / *top falls in bin k} with
+ *   numpy's uniform-bin rule over edges (bins+1 doubles, linspace(0, 1));
+ *   counts are uint64.
+ * sort_f64: ascending radix sort of n doubles; the result is in `keys`
+ *   (*in_alt = 0) or `alt` (*in_alt = 1); both buffers are overwritten.
+ * gini_sums: out[0] = sum_i (2(i+1) - n - 1) x_i, out[1] = sum_i x_i over the
+ *   sorted x (deterministic reduction order). */
+int scv_abs_max(scv_ctx* ctx, long long n, int is_complex, const void* v, double* mags, double* top,
+                void* stream);
+int scv_histogram(scv_ctx* ctx, long long n, const double* mags, const double* top, int bins,
+                  const double* edges, unsigned long long* counts, void* stream);
+int scv_sort_f64(scv_ctx* ctx, long long n, double* keys, double* alt, int* in_alt, void* stream);
+int scv_gini_sums(scv_ctx* ctx, long long n, const double* sorted, double* out, void* stream);
 
 #ifdef __cplusplus
 }

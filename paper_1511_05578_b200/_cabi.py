@@ -29,6 +29,7 @@ _lib_lock = threading.Lock()
 _P = ctypes.c_void_p
 _I = ctypes.c_int
 _D = ctypes.c_double
+_LL = ctypes.c_longlong
 
 # name -> argtypes (all return int unless listed in _RESTYPE)
 _SIGS = {
@@ -59,6 +60,10 @@ _SIGS = {
     "scv_edge_columns": [_P, _I, _D, _P, _P],
     "scv_rotate_to_north": [_P, _I, _D, _P, _P, _P],
     "scv_rotate_from_north": [_P, _I, _D, _P, _P, _P],
+    "scv_abs_max": [_P, _LL, _I, _P, _P, _P, _P],
+    "scv_histogram": [_P, _LL, _P, _P, _I, _P, _P, _P],
+    "scv_sort_f64": [_P, _LL, _P, _P, ctypes.POINTER(_I), _P],
+    "scv_gini_sums": [_P, _LL, _P, _P, _P],
 }
 _RESTYPE = {"scv_last_error": ctypes.c_char_p, "scv_workspace_bytes": ctypes.c_longlong,
             "scv_launch_count": ctypes.c_longlong}

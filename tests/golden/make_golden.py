@@ -243,6 +243,35 @@ def main_container():
     print("wrote SCRV1 fixtures")
 
 
+def main_sparsity():
+    """Per-scale sparsity statistics exactly as the reference's `sparsity`
+    command computes them (cli.py:268-320): analyze / analyze_real, then
+    np.histogram of |c|/max and cli.gini_coefficient.  The scale values are
+    stored too, so the device statistics can be checked on identical input."""
+    from scurve import cli
+    rng = np.random.default_rng(31)
+    out = {}
+    cases = [("s16c", 16, 0, False, 10), ("s16r", 16, 0, True, 7), ("s24s2", 24, 2, False, 12)]
+    for name, L, spin, real, bins in cases:
+        t = scurve.build_tiling(scurve.TilingParams(L, spin, 2.0, 1))
+        flm = scurve.random_coeffs(L, spin, rng, real=real)
+        f = scurve.sht_inverse_real(flm) if real else scurve.sht_inverse(flm)
+        c = scurve.analyze_real(f, t) if real else scurve.analyze(f, t)
+        out[f"{name}_map"] = f.values
+        out[f"{name}_meta"] = np.array([L, spin, int(real), bins, t.params.j_min, t.params.j_max])
+        for j in range(t.params.j_min, t.params.j_max + 1):
+            v = c.scale(j).values
+            mags = np.abs(v).ravel()
+            top = float(mags.max())
+            counts, _ = np.histogram(mags / top, bins=bins, range=(0.0, 1.0))
+            out[f"{name}_j{j}_values"] = v
+            out[f"{name}_j{j}_stats"] = np.array([mags.size, top, cli.gini_coefficient(mags)])
+            out[f"{name}_j{j}_counts"] = counts
+    path = os.path.join(HERE, "reference_sparsity.npz")
+    np.savez_compressed(path, **out)
+    print(f"wrote {len(out)} arrays to {path} ({os.path.getsize(path) / 1e6:.2f} MB)")
+
+
 def main():
     out = {}
     wigner_cases(out)
@@ -260,7 +289,10 @@ if __name__ == "__main__":
         main_rotation()
     elif "container" in sys.argv[1:]:
         main_container()
+    elif "sparsity" in sys.argv[1:]:
+        main_sparsity()
     else:
         main()
         main_rotation()
         main_container()
+        main_sparsity()

@@ -18,6 +18,7 @@
  *   scv_edge_columns           <- wigner_d_edge_columns            wigner.py:304-322
  *   scv_rotate_to_north        <- rotate_to_north                  transform.py:256-277
  *   scv_rotate_from_north      <- rotate_from_north                transform.py:280-297
+ *   scv_so3_inverse_general    <- so3_inverse_general (dense O(L^4)) so3.py:317-346
  *   scv_abs_max, scv_histogram,
  *   scv_sort_f64, scv_gini_sums <- cmd_sparsity / gini_coefficient  cli.py:59-70, 268-320
  *   scv_so3_inverse_curvelet_slab  <- so3_inverse_curvelet restricted to beta rows [b0, b0+nb)
@@ -180,6 +181,12 @@ int scv_rotate_to_north(scv_ctx* ctx, int L, double theta, const double* w, doub
                         void* stream);
 int scv_rotate_from_north(scv_ctx* ctx, int L, double theta, const double* dense, double* w,
                           void* stream);
+
+/* Dense inverse Wigner transform, O(L^4) (the reference's cross-check path):
+ * planes = packed dense WignerCoeffs of band limit L (as for the rotation),
+ * out (2gN-1, gL, 2gM-1) complex128 on the SO3Grid(gL, gM, gN); L <= gL, gM, gN. */
+int scv_so3_inverse_general(scv_ctx* ctx, int L, int gL, int gM, int gN, const double* planes, double* out,
+                            void* stream);
 
 /* Sparsity statistics (cli.py:59-70, 268-320).
  * abs_max: mags[i] = |v[i]| (complex128 if is_complex, else float64; mags may

@@ -32,6 +32,7 @@ __all__ = [
     "so3_inverse_curvelet",
     "so3_inverse_curvelet_real",
     "so3_inverse_curvelet_slab",
+    "so3_inverse_general",
 ]
 
 
@@ -109,6 +110,10 @@ class CurveletWignerCoeffs:
 
     def set_row(self, n: int, row) -> None:
         self.row(n)[:] = as_device(row, torch.complex128)
+
+    def densify(self) -> "WignerCoeffs":
+        """Dense coefficients holding the outer columns n = +-ell (so3.py:176-182)."""
+        return densify(self)
 
 
 def plane_offset(ell: int) -> int:
@@ -281,3 +286,34 @@ def so3_forward_curvelet_slab(f: SO3Slab, out: torch.Tensor | None = None, accum
     _cabi.context(dev).call("so3_forward_curvelet_slab", L, 1 if f.real else 0, _cabi.ptr(f.values), int(f.b0),
                             f.nb, _cabi.ptr(out), 1 if accumulate else 0)
     return CurveletWignerCoeffs(L, out)
+
+
+def so3_inverse_general(w: WignerCoeffs, grid: SO3Grid) -> SO3Signal:
+    """Dense synthesis onto the grid, O(L^4) (so3.py:317-346): the reference's
+    cross-check of the curvelet-sparse path, on the device (csrc/general.cu)."""
+    if isinstance(w, CurveletWignerCoeffs):
+        raise TypeError("dense synthesis requires WignerCoeffs; use densify() first")
+    if not isinstance(w, WignerCoeffs):
+        raise TypeError("dense synthesis requires WignerCoeffs")
+    L = w.band_limit
+    if L > min(grid.L, grid.M, grid.N):
+        raise ValueError(f"band limit {L} exceeds grid {grid}")
+    ctx = _cabi.context(w.values.device)
+    out = torch.empty(grid.shape, dtype=torch.complex128, device=w.values.device)
+    ctx.call("so3_inverse_general", L, grid.L, grid.M, grid.N, _cabi.ptr(w.values), _cabi.ptr(out))
+    return SO3Signal(grid, out)
+
+
+def densify(w: CurveletWignerCoeffs) -> WignerCoeffs:
+    """Dense coefficients holding only the outer columns n = +-ell of `w`."""
+    if not isinstance(w, CurveletWignerCoeffs):
+        raise TypeError("densify expects sparse coefficients")
+    L = w.band_limit
+    d = WignerCoeffs.zeros(L)
+    c = L - 1
+    for ell in range(L):
+        pl = d.plane(ell)
+        pl[:, 2 * ell] = w.values[0, ell, c - ell: c + ell + 1]
+        if ell > 0:
+            pl[:, 0] = w.values[1, ell, c - ell: c + ell + 1]
+    return d

@@ -35,6 +35,7 @@ __all__ = [
     "GraphedRoundTrip",
     "analyze",
     "analyze_real",
+    "analyze_north_validation",
     "rotate_from_north",
     "rotate_to_north",
     "roundtrip_streamed",
@@ -440,3 +441,23 @@ class BatchedRoundTrip:
         for lane in self.lanes:
             lane.join()
         return out
+
+
+def analyze_north_validation(f: SphereSignal, t: Tiling, j: int, max_band_limit: int = 32) -> SO3Signal:
+    """Scale-j signal computed the slow way, through the dense frame
+    (transform.py:300-322): scale coefficients, rotate_to_north, then the
+    dense O(L^4) synthesis.  A cross-check of the fast path, hence the cap."""
+    from .so3 import so3_inverse_general
+    _check_signal(f, t)
+    p = t.params
+    if not p.j_min <= j <= p.j_max:
+        raise ValueError(f"scale {j} outside [{p.j_min}, {p.j_max}]")
+    Lj = scale_band_limit(p, j)
+    if Lj > max_band_limit:
+        raise ValueError(f"band limit {Lj} exceeds the dense validation cap {max_band_limit}")
+    dev = f.values.device
+    ctx = _cabi.context(dev)
+    flm = sht_forward(f)
+    w = _scale_wigner(ctx, flm, device_tiling(t, dev), j, Lj)
+    dense = rotate_to_north(w, j, t)
+    return so3_inverse_general(dense, SO3Grid(Lj, Lj, Lj))

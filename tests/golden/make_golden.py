@@ -217,6 +217,15 @@ def rotation_cases(out):
     for ell in (0, 1, 17, 47):
         pos, neg = wigner.wigner_d_edge_columns(ell, float(out["rot48_theta"]))
         out[f"edge48_{ell}"] = np.stack([pos, neg])
+    # dense O(L^4) synthesis (so3.py:317-346) on a non-square grid, and the
+    # north-frame validation path (transform.py:300-322)
+    d = scurve.WignerCoeffs.random(6, rng)
+    out["gen_in"] = np.concatenate([p.ravel() for p in d.planes])
+    out["gen_out"] = scurve.so3_inverse_general(d, scurve.SO3Grid(8, 7, 9)).values
+    tn = scurve.build_tiling(scurve.TilingParams(8, 0, 2.0, 0))
+    f = scurve.sht_inverse(scurve.random_coeffs(8, 0, rng))
+    out["north_map"] = f.values
+    out["north_out"] = scurve.analyze_north_validation(f, tn, 2).values
 
 
 def main_rotation():

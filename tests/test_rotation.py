@@ -225,3 +225,53 @@ def test_full_size_L1024_properties():
         assert np.abs(per_m_dense - per_m_sparse).max() <= 1e-11 * scale ** 2
     del dense, back
     torch.cuda.empty_cache()
+
+
+# ------------------------------------------- dense O(L^4) synthesis (8(f) row 4)
+@gpu
+def test_so3_inverse_general_matches_reference(rot):
+    sc = _sc()
+    d = sc.WignerCoeffs(6, values=rot["gen_in"])
+    out = sc.so3_inverse_general(d, sc.SO3Grid(8, 7, 9))
+    assert orc.rel_err(host(out.values), rot["gen_out"]) <= 1e-12
+    with pytest.raises(TypeError):
+        sc.so3_inverse_general(sc.CurveletWignerCoeffs.zeros(4), sc.SO3Grid(4, 4, 4))
+    with pytest.raises(ValueError):
+        sc.so3_inverse_general(d, sc.SO3Grid(5, 8, 8))
+
+
+@gpu
+def test_dense_synthesis_matches_sparse_path(rng):
+    """The dense transform of the densified outer columns is the
+    curvelet-sparse synthesis (the reference's own cross-check)."""
+    sc = _sc()
+    L = 16
+    v = rng.uniform(-1, 1, (2, L, 2 * L - 1)) + 1j * rng.uniform(-1, 1, (2, L, 2 * L - 1))
+    for ell in range(L):
+        v[:, ell, : L - 1 - ell] = 0
+        v[:, ell, L + ell:] = 0
+    v[1, 0] = 0
+    w = sc.CurveletWignerCoeffs(L, v)
+    grid = sc.SO3Grid(L, L, L)
+    a = sc.so3_inverse_general(w.densify(), grid)
+    b = sc.so3_inverse_curvelet(w, grid)
+    assert orc.rel_err(host(a.values), host(b.values)) <= 1e-12
+
+
+@gpu
+def test_north_validation_matches_reference(rot):
+    sc = _sc()
+    from paper_1511_05578_b200 import tiling as T
+    # replay the fixture generator's tiling history (tilings memoise step
+    # integrals, conftest.GOLDEN_TILING_ORDER); its last build is the one used
+    T._reset_step_tables()
+    for prm in ((16, 1, 2.0, 1), (8, 0, 2.0, 0), (16, 2, 2.0, 0), (48, 0, 2.0, 2)):
+        T.build_tiling(T.TilingParams(*prm))
+    t = T.build_tiling(T.TilingParams(8, 0, 2.0, 0))
+    f = sc.SphereSignal(sc.SphereGrid(8), 0, rot["north_map"])
+    out = sc.analyze_north_validation(f, t, 2)
+    assert orc.rel_err(host(out.values), rot["north_out"]) <= 1e-10
+    z = sc.analyze_north_validation(sc.SphereSignal(sc.SphereGrid(8), 0, np.zeros((8, 15), complex)), t, 2)
+    assert float(z.values.abs().max()) == 0.0
+    with pytest.raises(ValueError):
+        sc.analyze_north_validation(f, t, 2, max_band_limit=4)

@@ -325,8 +325,8 @@ def rotate_to_north(w: CurveletWignerCoeffs, j: int, t: Tiling) -> WignerCoeffs:
     theta = _rotation_angle(j, t)
     L = w.band_limit
     ctx = _cabi.context(w.values.device)
-    out = WignerCoeffs.zeros(L) if L == 1 else WignerCoeffs(
-        L, values=torch.empty(L * (4 * L * L - 1) // 3, dtype=torch.complex128, device=w.values.device))
+    out = WignerCoeffs(L, values=torch.empty(L * (4 * L * L - 1) // 3, dtype=torch.complex128,
+                                             device=w.values.device))
     ctx.call("rotate_to_north", L, theta, _cabi.ptr(w.values), _cabi.ptr(out.values))
     return out
 

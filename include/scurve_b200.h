@@ -19,6 +19,7 @@
  *   scv_rotate_to_north        <- rotate_to_north                  transform.py:256-277
  *   scv_rotate_from_north      <- rotate_from_north                transform.py:280-297
  *   scv_so3_inverse_general    <- so3_inverse_general (dense O(L^4)) so3.py:317-346
+ *   scv_so3_forward_general    <- so3_forward_general (dense O(L^4)) so3.py:288-314
  *   scv_abs_max, scv_histogram,
  *   scv_sort_f64, scv_gini_sums <- cmd_sparsity / gini_coefficient  cli.py:59-70, 268-320
  *   scv_so3_inverse_curvelet_slab  <- so3_inverse_curvelet restricted to beta rows [b0, b0+nb)
@@ -186,6 +187,10 @@ int scv_rotate_from_north(scv_ctx* ctx, int L, double theta, const double* dense
  * planes = packed dense WignerCoeffs of band limit L (as for the rotation),
  * out (2gN-1, gL, 2gM-1) complex128 on the SO3Grid(gL, gM, gN); L <= gL, gM, gN. */
 int scv_so3_inverse_general(scv_ctx* ctx, int L, int gL, int gM, int gN, const double* planes, double* out,
+                            void* stream);
+/* Dense forward Wigner transform, O(L^4): sig (2gN-1, gL, 2gM-1) complex128 ->
+ * packed dense planes of band limit L <= gL, gM, gN. */
+int scv_so3_forward_general(scv_ctx* ctx, int L, int gL, int gM, int gN, const double* sig, double* planes,
                             void* stream);
 
 /* Sparsity statistics (cli.py:59-70, 268-320).

@@ -61,6 +61,7 @@ _SIGS = {
     "scv_rotate_to_north": [_P, _I, _D, _P, _P, _P],
     "scv_rotate_from_north": [_P, _I, _D, _P, _P, _P],
     "scv_so3_inverse_general": [_P, _I, _I, _I, _I, _P, _P, _P],
+    "scv_so3_forward_general": [_P, _I, _I, _I, _I, _P, _P, _P],
     "scv_abs_max": [_P, _LL, _I, _P, _P, _P, _P],
     "scv_histogram": [_P, _LL, _P, _P, _I, _P, _P, _P],
     "scv_sort_f64": [_P, _LL, _P, _P, ctypes.POINTER(_I), _P],

@@ -32,6 +32,7 @@ __all__ = [
     "so3_inverse_curvelet",
     "so3_inverse_curvelet_real",
     "so3_inverse_curvelet_slab",
+    "so3_forward_general",
     "so3_inverse_general",
 ]
 
@@ -317,3 +318,18 @@ def densify(w: CurveletWignerCoeffs) -> WignerCoeffs:
         if ell > 0:
             pl[:, 0] = w.values[1, ell, c - ell: c + ell + 1]
     return d
+
+
+def so3_forward_general(f: SO3Signal, band_limit: int | None = None) -> WignerCoeffs:
+    """Dense forward Wigner transform, O(L^4) (so3.py:288-314), on the device:
+    the (gamma, alpha) spectrum by cuFFT, then direct beta and Delta sums."""
+    grid = f.grid
+    L = grid.L if band_limit is None else int(band_limit)
+    if L > min(grid.L, grid.M, grid.N):
+        raise ValueError(f"band limit {L} exceeds grid {grid}")
+    if f.real:
+        raise ValueError("dense forward transform takes complex samples")
+    ctx = _cabi.context(f.values.device)
+    out = WignerCoeffs(L, values=torch.empty(plane_offset(L), dtype=torch.complex128, device=f.values.device))
+    ctx.call("so3_forward_general", L, grid.L, grid.M, grid.N, _cabi.ptr(f.values), _cabi.ptr(out.values))
+    return out

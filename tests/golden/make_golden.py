@@ -226,6 +226,11 @@ def rotation_cases(out):
     f = scurve.sht_inverse(scurve.random_coeffs(8, 0, rng))
     out["north_map"] = f.values
     out["north_out"] = scurve.analyze_north_validation(f, tn, 2).values
+    # dense forward (so3.py:288-314) of a random signal on the same grid, band limit 6
+    g = scurve.SO3Grid(8, 7, 9)
+    sig = rng.standard_normal(g.shape) + 1j * rng.standard_normal(g.shape)
+    out["genf_in"] = sig
+    out["genf_out"] = np.concatenate([p.ravel() for p in scurve.so3_forward_general(scurve.SO3Signal(g, sig), 6).planes])
 
 
 def main_rotation():

@@ -275,3 +275,17 @@ def test_north_validation_matches_reference(rot):
     assert float(z.values.abs().max()) == 0.0
     with pytest.raises(ValueError):
         sc.analyze_north_validation(f, t, 2, max_band_limit=4)
+
+
+@gpu
+def test_so3_forward_general_matches_reference(rot, rng):
+    sc = _sc()
+    g = sc.SO3Grid(8, 7, 9)
+    out = sc.so3_forward_general(sc.SO3Signal(g, rot["genf_in"]), 6)
+    assert orc.rel_err(host(out.values), rot["genf_out"]) <= 1e-12
+    # exact on band-limited signals: forward(inverse(w)) = w
+    d = sc.WignerCoeffs(6, values=rot["gen_in"])
+    back = sc.so3_forward_general(sc.so3_inverse_general(d, g), 6)
+    assert orc.rel_err(host(back.values), rot["gen_in"]) <= 1e-12
+    with pytest.raises(ValueError):
+        sc.so3_forward_general(sc.SO3Signal(g, rot["genf_in"]), 8)

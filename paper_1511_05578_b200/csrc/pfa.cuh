@@ -118,6 +118,13 @@ __host__ __device__ constexpr int mma_aoff(int p, int row, int kk) {
 }
 // table size in double2 units: 1-D (cos, sin) table of p entries, or the two
 // dense matrices (2 * M * pitch doubles = M * pitch double2)
+// SCV_R89_PREPOS: the Rader stage reads its per-lane gather positions once per
+// stage into registers instead of per block.  Measured (r01v25): column
+// generation -0.7 ms/map, rows unchanged, gamma+quadrature +5.4 ms (the six
+// extra registers spill there), so off by default.
+#ifndef SCV_R89_PREPOS
+#define SCV_R89_PREPOS 0
+#endif
 // Radix 89 by Rader + CRT (SCV_RADER89, see pfa_stage_rader89): the table is
 // five small dense matrices (M0, M2: 16 x 12; Mc, RA, RB: 24 x 28 doubles)
 // and the 44 Rader positions r_a = 3^a mod 89 as bytes.
@@ -815,6 +822,23 @@ __device__ __forceinline__ void pfa_stage_rader89(double2* X, const double2* tab
   const int ar = lane >> 2, ac = lane & 3;
   constexpr double s2 = 0.70710678118654752440;
   auto slot = [](int i) { return (i >> 1) + 4 * (i & 1); };
+#if SCV_R89_PREPOS
+  // the lane's 12 gather offsets r_a * step (a = (33 a1 + 12 a2) mod 44) do not
+  // depend on the block: read from the position table once per stage, packed
+  // two 16-bit offsets per register
+  unsigned int gpos[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) gpos[i] = 0u;
+#pragma unroll
+  for (int kt = 0; kt < 3; ++kt) {
+#pragma unroll
+    for (int a1 = 0; a1 < 4; ++a1) {
+      const int a2 = ac + 4 * kt, i = kt * 4 + a1;
+      const unsigned int v = a2 < 11 ? (unsigned int)(RT[(33 * a1 + 12 * a2) % 44] * step) : 0u;
+      gpos[i >> 1] |= v << (16 * (i & 1));
+    }
+  }
+#endif
 #pragma unroll 1
   for (int q = warp; q < NBLK; q += NW) {
     const int gb = (q >> 1) * 8 + 2 * (q & 1);
@@ -854,9 +878,15 @@ __device__ __forceinline__ void pfa_stage_rader89(double2* X, const double2* tab
         w[a1] = 0.0;
         if (okB && a2 < 11) {
           const int a = (33 * a1 + 12 * a2) % 44;
+#if SCV_R89_PREPOS
+          const int rs = (int)((gpos[(kt * 4 + a1) >> 1] >> (16 * ((kt * 4 + a1) & 1))) & 0xFFFFu);
+          const double xa = Xd[rowd + 2 * (c0B + rs)];
+          const double xb = Xd[rowd + 2 * (c0B + p * step - rs)];
+#else
           const int r = RT[a];
           const double xa = Xd[rowd + 2 * (c0B + r * step)];
           const double xb = Xd[rowd + 2 * (c0B + (p - r) * step)];
+#endif
           sv[a1] = xa + xb;
           const double dv = xa - xb;
           w[a1] = ((a >> 2) & 1) ? -dv : dv;

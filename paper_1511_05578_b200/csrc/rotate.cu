@@ -78,16 +78,9 @@ __global__ void __launch_bounds__(256) k_rot_to_north(int L, const double2* __re
     const double2 b = l > 0 ? w[((long long)L + l) * K + (L - 1) + m] : make_double2(0.0, 0.0);
     const double2* e = E + (long long)l * K + (L - 1) - l;
     double2* o = out + plane_off(l) + (long long)(m + l) * n;
-    // four edge-table loads (L2 hits) in flight per lane before the streaming stores
-    int k = lane;
-    for (; k + 96 < n; k += 128) {
-      double2 d[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) d[u] = __ldg(e + k + 32 * u);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) __stcs(o + k + 32 * u, rot_entry(l, a, b, d[u]));
-    }
-    for (; k < n; k += 32) __stcs(o + k, rot_entry(l, a, b, __ldg(e + k)));
+    // (a four-deep batch of edge-table loads before the stores measured 2% slower:
+    // 4.37 vs 4.28 ms at L=1024)
+    for (int k = lane; k < n; k += 32) __stcs(o + k, rot_entry(l, a, b, __ldg(e + k)));
   }
 }
 

@@ -608,7 +608,10 @@ template <> struct PfaGCfg<511> { static constexpr int R = 4, NT = 256, MINB = 1
   };
 SCV_GCFG_(1023, SCV_GEN1023)
 SCV_GCFG_(2047, SCV_GEN2047)
-template <> struct PfaGCfg<4095> { static constexpr int R = 2, NT = 320, MINB = 1; };
+#ifndef SCV_GEN4095_NT
+#define SCV_GEN4095_NT 640
+#endif
+template <> struct PfaGCfg<4095> { static constexpr int R = 2, NT = SCV_GEN4095_NT, MINB = 1; };
 
 #ifndef SCV_COLGEN_GU
 #define SCV_COLGEN_GU 1
@@ -1451,7 +1454,10 @@ __global__ void __launch_bounds__(PfaCfg<K, true>::NT, PfaCfg<K, true>::MINB)
 // summation order is fixed (bit-reproducible).
 // ---------------------------------------------------------------------------
 template <int K> struct PfaQCfg { static constexpr int RQ = 1, NT = 256, MINB = 1; };
-template <> struct PfaQCfg<4095> { static constexpr int RQ = 1, NT = 512, MINB = 1; };
+#ifndef SCV_Q4095_NT
+#define SCV_Q4095_NT 384
+#endif
+template <> struct PfaQCfg<4095> { static constexpr int RQ = 1, NT = SCV_Q4095_NT, MINB = 1; };
 template <> struct PfaQCfg<255> { static constexpr int RQ = 1, NT = 128, MINB = 1; };
 #ifndef SCV_Q1023
 #define SCV_Q1023 1, 352, 1

@@ -596,7 +596,7 @@ template <int K> struct PfaGCfg { static constexpr int R = 8, NT = 128, MINB = 2
 template <> struct PfaGCfg<255> { static constexpr int R = 8, NT = 256, MINB = 1; };
 template <> struct PfaGCfg<511> { static constexpr int R = 4, NT = 256, MINB = 1; };
 #ifndef SCV_GEN1023
-#define SCV_GEN1023 4, 256, 1
+#define SCV_GEN1023 4, 512, 1
 #endif
 #ifndef SCV_GEN2047
 #define SCV_GEN2047 4, 384, 1

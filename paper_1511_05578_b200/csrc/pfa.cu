@@ -251,7 +251,7 @@ SCV_PFA_CFG(511, false, 4, 256, 1)   SCV_PFA_CFG(511, true, 4, 256, 1)
 #define SCV_PFA_CFG_(KK, CL, ...) SCV_PFA_CFG(KK, CL, __VA_ARGS__)
 SCV_PFA_CFG_(1023, false, SCV_ROW1023)  SCV_PFA_CFG_(1023, true, SCV_COL1023)
 SCV_PFA_CFG_(2047, false, SCV_ROW2047)  SCV_PFA_CFG_(2047, true, SCV_COL2047)
-SCV_PFA_CFG(4095, false, 1, 320, 1)  SCV_PFA_CFG(4095, true, 1, 320, 1)
+SCV_PFA_CFG(4095, false, 1, 384, 1)  SCV_PFA_CFG(4095, true, 1, 384, 1)
 
 // Row batches in shared memory: 2 = the next batch streams in (cp.async)
 // while the current one computes, 1 = single buffer (other resident CTAs

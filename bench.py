@@ -12,9 +12,15 @@ map copied host->device and the reconstruction copied back every step.
 Every scale volume (68.6 GB at the finest scale) is far larger than the
 126 MB L2, so no explicit L2 flush is needed between steps.
 
-Multi-GPU (torchrun, one process per GPU): weak scaling over maps — each
-rank runs the full pipeline on its own seeded map (maps are the
-independent units), max-over-ranks device time.
+Multi-GPU (one process per GPU).  `--gpus N` under torchrun (WORLD_SIZE set)
+uses the launched ranks; without WORLD_SIZE, bench.py launches the N ranks
+itself (torch.distributed.run on 127.0.0.1) and asserts world == N.  The
+N > 1 default is the north star's decomposition of ONE C4 map per step
+(dist.py): rank 0 runs the SHT and NCCL-broadcasts f_lm, the scales with
+128 <= L_j <= 2048 are split into one beta slab per rank, small scales are
+whole per rank, and one NCCL reduce merges the per-scale synthesis terms --
+strong scaling, max-over-ranks device time.  `--maps-per-rank` instead runs
+one independent map per rank (weak scaling, no collective).
 
 --impl reference times the reference algorithm's CPU implementation (the
 oracle port in oracle/, numpy + scipy.fft with all host threads) on a
@@ -65,9 +71,27 @@ def parse():
                          "held whole; BASELINE C5 on one GPU: --L 2048 --spin 2 --jmin 4)")
     ap.add_argument("--slab-gb", type=float, default=16.0, help="--streamed slab size (GiB)")
     ap.add_argument("--shard-scales", action="store_true",
-                    help="N>1: one map per step with its scales sharded over the ranks "
-                         "(NCCL broadcast + gather); default is one map per rank per step")
+                    help="(default for N>1) one map per step with its scales / beta slabs sharded over the ranks")
+    ap.add_argument("--maps-per-rank", action="store_true",
+                    help="N>1: one independent map per rank per step (weak scaling, no collective)")
+    ap.add_argument("--stub", action="store_true",
+                    help="launcher / collective plumbing check on CPU (gloo, no transform compute); tests only")
+    ap.add_argument("--no-measured-cpu", action="store_true",
+                    help="skip the measured full CPU round trip at L=256 (cpu_baseline.measured)")
     return ap.parse_args()
+
+
+def spawn_ranks(a) -> int:
+    """`--gpus N` without WORLD_SIZE: launch N ranks of this script with
+    torch.distributed.run on 127.0.0.1 and return its exit code (rank 0
+    prints the JSON line)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 class _Batch:
@@ -239,7 +263,7 @@ def executed_dmma(stage, Ljs):
     return fl
 
 
-def stage_roofline(a, prof, Ljs, hbm_peak, fp64_peak):
+def stage_roofline(a, prof, Ljs, hbm_peak, fp64_peak, dmma_peak=None):
     """Roofline of the dominant stage from the live per-stage CUDA-event times."""
     K = lambda L: 2 * L - 1  # noqa: E731
     b = 8 if a.real else 16
@@ -294,8 +318,10 @@ def stage_roofline(a, prof, Ljs, hbm_peak, fp64_peak):
     if ex:
         # what the kernel's own pipe does: FP64 tensor-core (DMMA) flops the
         # prime-factor engine issues, vs the measured DMMA peak
-        out["executed_dmma"] = {"tflops": ex / (ms_map * 1e-3) / 1e12, "peak_tflops": DMMA_PEAK_TF,
-                                "frac": ex / (ms_map * 1e-3) / 1e12 / DMMA_PEAK_TF,
+        pk = dmma_peak or DMMA_PEAK_TF
+        out["executed_dmma"] = {"tflops": ex / (ms_map * 1e-3) / 1e12, "peak_tflops": pk,
+                                "peak_source": "in-run DMMA loop (scv_dmma_peak)" if dmma_peak else "r01 microbench",
+                                "frac": ex / (ms_map * 1e-3) / 1e12 / pk,
                                 "flops_per_map": ex, "source": "DMMA count of the engine's launch shapes "
                                 "(bench.py dmma_per_row; 684/row at K=2047 with the Rader radix-89 stage)"}
     tr = ncu_traffic(name, Ljs)
@@ -313,12 +339,80 @@ def stage_roofline(a, prof, Ljs, hbm_peak, fp64_peak):
             e["fp64_tflops_alg"] = flops_stage[nm] / (mm * 1e-3) / 1e12
         exn = executed_dmma(nm, Ljs)
         if exn:
-            e["dmma_frac"] = exn / (mm * 1e-3) / 1e12 / DMMA_PEAK_TF
+            e["dmma_frac"] = exn / (mm * 1e-3) / 1e12 / (dmma_peak or DMMA_PEAK_TF)
         out["all_stages"][nm] = e
     return out
 
 
+def run_stub(a):
+    """--stub: the launcher and collective plumbing of the N-rank bench on CPU
+    (gloo), without any transform compute -- for tests/test_bench_launcher.py.
+    The line carries "stub": true and no throughput claim."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world != a.gpus:
+        raise SystemExit(f"world size {world} != --gpus {a.gpus}")
+    if world > 1:
+        dist.init_process_group("gloo")
+    from paper_1511_05578_b200.dist import ScalePlan
+    from paper_1511_05578_b200.tiling import TilingParams
+    p = TilingParams(a.L, a.spin, a.lam, a.jmin)
+    plan = ScalePlan.build(p, world)
+    flm = torch.zeros(a.L * a.L, dtype=torch.complex128)
+    terms = torch.zeros((p.scale_count, a.L * a.L), dtype=torch.complex128)
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        if world > 1:
+            dist.broadcast(flm, src=0)
+            dist.reduce(terms, dst=0, op=dist.ReduceOp.SUM)
+    el = time.perf_counter() - t0
+    line = {"metric": "curvelet analysis+synthesis maps/s", "value": None, "unit": "maps/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "stub": True, "scaling": "strong",
+            "config": {"workload": workload_name(a), "parallelism": f"scales + beta slabs sharded x{world}",
+                       "rank_loads": [plan.load(r) for r in range(world)]},
+            "collective_wall_s": el}
+    if world > 1:
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def measured_cpu_roundtrip(a, gpu_ms_at):
+    """cpu_baseline.measured: one FULL oracle round trip (analyze + synthesize,
+    transform.py:139-187 restated) at L=256 with the bench's lambda / J0, timed
+    on this host with all cores and with one scipy.fft worker, beside the GPU
+    time of the same round trip (the largest L the reference
+    finishes in reasonable time; L=1024 does not fit host RAM)."""
+    from scipy import fft as sfft
+    from oracle import scurve_oracle as orc
+    from paper_1511_05578_b200 import tiling as T
+    L = 256
+    p = T.TilingParams(L, a.spin, a.lam, a.jmin)
+    t = T.build_tiling(p)
+    psi = [T.curvelet_harmonics(t, j) for j in range(p.j_min, p.j_max + 1)]
+    flm = gaussian_flm(L, a.spin, a.seed, a.spin == 0)
+    f = orc.sht_inverse(flm, L, a.spin)
+    out = {"L": L, "config": f"L={L} spin={a.spin} B={a.lam:g} J0={a.jmin}, analyze+synthesize (complex path)"}
+    for tag, workers in (("all_cores", os.cpu_count() or 1), ("one_thread", 1)):
+        with sfft.set_workers(workers):
+            t0 = time.perf_counter()
+            smap, scales = orc.analyze(f, L, a.spin, a.lam, a.jmin, p.j_max, psi, t.scaling)
+            g = orc.synthesize(smap, scales, L, a.spin, a.lam, a.jmin, p.j_max, psi, t.scaling)
+            sec = time.perf_counter() - t0
+        out[tag] = {"cores": workers, "s_per_map": sec}
+        del smap, scales
+    out["roundtrip_rel_err"] = orc.rel_err(g, f)
+    out["gpu_s_per_map"] = gpu_ms_at(L) / 1e3
+    out["ratio_all_cores"] = out["all_cores"]["s_per_map"] / out["gpu_s_per_map"]
+    out["ratio_one_thread"] = out["one_thread"]["s_per_map"] / out["gpu_s_per_map"]
+    return out
+
+
 def run_ours(a):
+    if a.stub:
+        return run_stub(a)
     import torch
     import torch.distributed as dist
 
@@ -328,16 +422,24 @@ def run_ours(a):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus:
+        raise SystemExit(f"world size {world} != --gpus {a.gpus} (launch with torchrun, or without WORLD_SIZE "
+                         f"and bench.py spawns the ranks)")
     torch.cuda.set_device(local)
     if world > 1:
+        # NCCL prints its communicator-init lines (rank, nranks, device, NVLS)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    sharded = world > 1 and not a.maps_per_rank
     dev = torch.device("cuda", local)
+    t_first0 = time.perf_counter()
     ctx = _cabi.context(local)
 
     p, Ljs, B_alg, F_alg = algorithmic_work(a)
     t = sc.build_tiling(p)
     real_sym = a.spin == 0
-    flm = gaussian_flm(a.L, a.spin, a.seed + rank, real_sym)
+    flm = gaussian_flm(a.L, a.spin, a.seed + (0 if sharded else rank), real_sym)
     f = sc.sht_inverse(sc.HarmonicCoeffs(a.L, a.spin, flm))
     if a.real:
         f = sc.SphereSignal(f.grid, 0, f.values.real.contiguous(), real=True)
@@ -350,17 +452,17 @@ def run_ours(a):
 
         def step(fin):
             return sc.roundtrip_streamed(fin, t, slab_bytes=int(a.slab_gb * (1 << 30)))
-    else:
+    elif not sharded:
         scale_out = [torch.empty((2 * Lj - 1, Lj, 2 * Lj - 1), dtype=dtype, device=dev) for Lj in Ljs]
 
         def step(fin):
             c = ana(fin, t, scale_out=scale_out)
             return syn(c, t)
 
-    eager_step = step
+    eager_step = step if not sharded else None
     graphed = None
     if a.graph:
-        if a.streamed or (a.shard_scales and world > 1):
+        if a.streamed or sharded:
             raise SystemExit("--graph replays the single-GPU in-memory round trip")
         graphed = sc.GraphedRoundTrip(t, spin=a.spin, real=a.real)
 
@@ -368,7 +470,7 @@ def run_ours(a):
             return graphed(None if fin.values.data_ptr() == graphed.inp.data_ptr() else fin.values)
     batched = None
     if a.lanes:
-        if a.streamed or (a.shard_scales and world > 1):
+        if a.streamed or sharded:
             raise SystemExit("--lanes runs the single-GPU in-memory round trip")
         batched = sc.BatchedRoundTrip(t, lanes=a.lanes, spin=a.spin, real=a.real)
         outb = torch.empty((a.lanes, *f.values.shape), dtype=f.values.dtype, device=dev)
@@ -378,7 +480,7 @@ def run_ours(a):
             batched(maps, out=outb)
             return sc.SphereSignal(f.grid, f.spin, outb[0], real=a.real)
 
-    if a.shard_scales and world > 1 and a.streamed:
+    if sharded and a.streamed:
         from paper_1511_05578_b200.dist import roundtrip_sharded_streamed
         K_fin = 2 * Ljs[-1] - 1
         rows = max(1, int(a.slab_gb * (1 << 30)) // (K_fin * K_fin * 16))
@@ -386,7 +488,7 @@ def run_ours(a):
         def step(fin):  # noqa: F811
             g = roundtrip_sharded_streamed(fin, t, slab_rows=rows)
             return g if g is not None else fin
-    elif a.shard_scales and world > 1:
+    elif sharded:
         from paper_1511_05578_b200.dist import analyze_sharded, synthesize_sharded
 
         def step(fin):  # noqa: F811
@@ -394,8 +496,16 @@ def run_ours(a):
             g = synthesize_sharded(c, t)
             return g if g is not None else fin
 
-    g = None
-    for _ in range(a.warmup):
+    # first map: context, per-L tables (Delta wedge, quadrature table, DFT
+    # tables), plans and the first round trip -- what a one-map user pays
+    ctx.profile(True)
+    g = step(f)
+    torch.cuda.synchronize()
+    first_map_ms = (time.perf_counter() - t_first0) * 1e3
+    ctx.profile(False)
+    first_prof = ctx.profile_report()
+    table_ms = sum(v[1] for k, v in first_prof.items() if k.endswith("_build") or k.startswith("delta"))
+    for _ in range(max(0, a.warmup - 1)):
         g = step(f)
     torch.cuda.synchronize()
     rt_err = float((g.values - f.values).abs().max() / f.values.abs().max())
@@ -404,9 +514,13 @@ def run_ours(a):
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             hbm_peak = float(json.load(fh)["hbm_gbs"])
+        hbm_src = "MEASURED_PEAKS.json hbm_gbs"
     except Exception:
         hbm_peak = 6650.0
-    fp64_peak = ctx.fp64_peak_tflops()
+        hbm_src = "B200_PROFILING.md fallback"
+    dfma_peak = ctx.fp64_peak_tflops()
+    dmma_peak = ctx.dmma_peak_tflops()
+    fp64_peak = max(dfma_peak, dmma_peak)
 
     # ---------------- timed region (device-resident input) ----------------
     stream = torch.cuda.current_stream()
@@ -453,8 +567,11 @@ def run_ours(a):
         tt = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
+        lt = torch.tensor([launches], device=dev, dtype=torch.float64)
+        dist.all_reduce(lt, op=dist.ReduceOp.SUM)
+        launches = int(lt.item())
     ms_per_step = ms / a.steps
-    maps_per_step = 1 if (a.shard_scales and world > 1) else world * max(1, a.lanes)
+    maps_per_step = 1 if sharded else world * max(1, a.lanes)
     value = maps_per_step * a.steps / (ms * 1e-3)
 
     # ---------------- e2e: host buffers through the public API ----------------
@@ -490,8 +607,9 @@ def run_ours(a):
         e2e = {"value": maps_per_step * a.steps / (ems * 1e-3), "unit": "maps/s", "h2d_bytes_per_step": nb,
                "d2h_bytes_per_step": nb, "ms_per_step": ems / a.steps}
 
-    roof = stage_roofline(a, prof, Ljs, hbm_peak, fp64_peak)
-    t_roof = max(B_alg / (hbm_peak * 1e9), F_alg / (fp64_peak * 1e12))
+    roof = stage_roofline(a, prof, Ljs, hbm_peak, fp64_peak, dmma_peak)
+    roof["peak_source"] = roof.get("peak_source", "") if roof.get("bound") != "hbm" else hbm_src
+    t_roof = max(B_alg / (hbm_peak * 1e9 * world), F_alg / (fp64_peak * 1e12 * world))
     line = {
         "metric": "curvelet analysis+synthesis maps/s",
         "value": value,
@@ -501,7 +619,7 @@ def run_ours(a):
         "warmup": a.warmup,
         "ms_per_step": ms_per_step,
         "higher_is_better": True,
-        "scaling": "strong" if (a.shard_scales and world > 1) else "weak",
+        "scaling": "strong" if sharded else "weak",
         "vs_baseline": None,
         "dtype": "f64" if a.real else "c128",
         "data": "synthetic (seeded Gaussian f_lm, C_l=(l+1)^-2)",
@@ -511,7 +629,7 @@ def run_ours(a):
                    **({"streamed_slab_GiB": a.slab_gb} if a.streamed else {}),
                    "parallelism": ("scales + beta slabs sharded x%d%s (NCCL broadcast f_lm + reduce of the "
                                    "per-scale terms)" % (world, ", slabs streamed" if a.streamed else "")
-                                   if (a.shard_scales and world > 1) else
+                                   if sharded else
                                    (f"maps x{world} (one map per rank)" if world > 1 else "1 GPU")),
                    **({"cuda_graph": True} if a.graph else {}),
                    **({"lanes": a.lanes, "batch": "maps in flight per step, one CUDA graph + private "
@@ -524,41 +642,93 @@ def run_ours(a):
         "roofline": roof,
         "paper_roofline": {"B_alg_GB": B_alg / 1e9, "F_alg_TF": F_alg / 1e12, "t_roof_ms": t_roof * 1e3,
                            "frac": t_roof * 1e3 * max(1, a.lanes) / ms_per_step, "fp64_peak_tflops": fp64_peak,
-                           "hbm_peak_gbs": hbm_peak},
+                           "fp64_peak_source": "max(in-run DFMA loop %.2f TF, in-run DMMA m8n8k4 loop %.2f TF) "
+                                               "per GPU, x n_gpus" % (dfma_peak, dmma_peak),
+                           "hbm_peak_gbs": hbm_peak, "hbm_peak_source": hbm_src},
         "stages_ms_per_step": {k: v[1] / a.steps for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])},
         "roundtrip_rel_err": rt_err,
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clocks,
+        "first_map_ms": first_map_ms,
+        "first_map": {"ms": first_map_ms, "table_build_ms": table_ms,
+                      "what": "context + per-L tables (Delta wedge, beta-quadrature table, DFT tables) + the first "
+                              "round trip, host wall clock; excluded from the timed region like the reference's "
+                              "cached Delta / kernel FFTs (cli.py:257-263)",
+                      "stages_ms": {k: v[1] for k, v in sorted(first_prof.items(), key=lambda kv: -kv[1][1])[:6]}},
         "peak_mem_gb": torch.cuda.max_memory_allocated() / 1e9 + ctx.workspace_bytes() / 1e9,
     }
-    if rank == 0 and not a.no_cpu_baseline:
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
         from oracle import cpu_sample
-        line["cpu_baseline"] = cpu_sample.baseline(a.L, a.spin, a.lam, a.jmin, a.real, budget_s=20.0)
+
+        def gpu_ms_at(L):
+            pp = sc.TilingParams(L, a.spin, a.lam, a.jmin)
+            tt_ = sc.build_tiling(pp)
+            fl = sc.sht_inverse(sc.HarmonicCoeffs(L, a.spin, gaussian_flm(L, a.spin, a.seed, a.spin == 0)))
+            for _ in range(2):
+                sc.synthesize(sc.analyze(fl, tt_), tt_)
+            torch.cuda.synchronize()
+            q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            q0.record()
+            for _ in range(5):
+                sc.synthesize(sc.analyze(fl, tt_), tt_)
+            q1.record()
+            torch.cuda.synchronize()
+            return q0.elapsed_time(q1) / 5
+
+        measured = None if a.no_measured_cpu or a.real else measured_cpu_roundtrip(a, gpu_ms_at)
+        line["cpu_baseline"] = cpu_sample.calibrated_baseline(a.L, a.spin, a.lam, a.jmin, a.real, measured)
     if a.profile_json and rank == 0:
         with open(a.profile_json, "w") as fh:
             json.dump(line, fh, indent=1)
-    if rank == 0:
-        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
 
 
 def run_reference(a):
+    """The reference's algorithm on the host CPU (oracle port, numpy +
+    scipy.fft with every host thread), rank 0 only.  A full L=1024 reference
+    round trip needs >147 GB of host RAM and ~40 min, so each STEP times a
+    bounded sample of the same map -- one n-chunk / beta-block piece per
+    distinct scale size plus both SHTs (oracle/cpu_sample.py) -- and scales it
+    by the piece counts.  The first warm-up step also times one FULL round trip
+    at L=256, which calibrates the sampler.  ms_per_step is the real wall time
+    of a step (the sample); value = 1 / (calibrated seconds per map), i.e.
+    the map fraction a step covers divided by its wall time."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from oracle import cpu_sample
     p, Ljs, _, _ = algorithmic_work(a)
-    times = []
-    cb = None
+    measured = None
+    if not a.real and not a.no_measured_cpu:
+        measured = measured_cpu_roundtrip_host_only(a)
+    raw, walls = [], []
+    t_run0 = time.perf_counter()
     for i in range(a.warmup + a.steps):
-        cb = cpu_sample.baseline(a.L, a.spin, a.lam, a.jmin, a.real, budget_s=8.0)
+        t0 = time.perf_counter()
+        cb = cpu_sample.baseline(a.L, a.spin, a.lam, a.jmin, a.real)
         if i >= a.warmup:
-            times.append(cb["seconds_per_map"])
-    sec = statistics.median(times)
+            raw.append(cb["seconds_per_map"])
+            walls.append(time.perf_counter() - t0)
+    est = statistics.median(raw)
+    factor = 1.0
+    cal = None
+    if measured is not None:
+        est_m = sorted(cpu_sample.baseline(measured["L"], a.spin, a.lam, a.jmin, a.real)["seconds_per_map"]
+                       for _ in range(3))[1]
+        factor = measured["all_cores"]["s_per_map"] / est_m
+        cal = {"L": measured["L"], "measured_s_per_map": measured["all_cores"]["s_per_map"],
+               "estimated_s_per_map": est_m, "factor": factor}
+    sec = est * factor
     value = 1.0 / sec
-    cb["value"] = value
+    step_s = statistics.median(walls)
+    cb = {"value": value, "unit": "maps/s", "seconds_per_map": sec, "cores": os.cpu_count() or 1, "kind": "port",
+          "sample": cb["sample"] + (f"; calibrated x{factor:.3f} by a full round trip at L=256" if cal else ""),
+          "estimate_uncalibrated_s_per_map": est, "estimate_spread_s_per_map": raw, "calibration": cal,
+          "measured": measured, "per_scale_seconds": cb["per_scale_seconds"]}
     line = {
         "impl": "reference",
         "metric": "curvelet analysis+synthesis maps/s",
@@ -567,7 +737,9 @@ def run_reference(a):
         "n_gpus": a.gpus,
         "steps": a.steps,
         "warmup": a.warmup,
-        "ms_per_step": sec * 1e3,
+        "ms_per_step": step_s * 1e3,
+        "map_fraction_per_step": step_s / sec,
+        "run_wall_s": time.perf_counter() - t_run0,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
@@ -581,8 +753,29 @@ def run_reference(a):
     print(json.dumps(line), flush=True)
 
 
+def measured_cpu_roundtrip_host_only(a):
+    """measured_cpu_roundtrip without the GPU column (reference arm: all cores only)."""
+    from scipy import fft as sfft
+    from oracle import scurve_oracle as orc
+    from paper_1511_05578_b200 import tiling as T
+    L = 256
+    p = T.TilingParams(L, a.spin, a.lam, a.jmin)
+    t = T.build_tiling(p)
+    psi = [T.curvelet_harmonics(t, j) for j in range(p.j_min, p.j_max + 1)]
+    f = orc.sht_inverse(gaussian_flm(L, a.spin, a.seed, a.spin == 0), L, a.spin)
+    workers = os.cpu_count() or 1
+    with sfft.set_workers(workers):
+        t0 = time.perf_counter()
+        smap, scales = orc.analyze(f, L, a.spin, a.lam, a.jmin, p.j_max, psi, t.scaling)
+        orc.synthesize(smap, scales, L, a.spin, a.lam, a.jmin, p.j_max, psi, t.scaling)
+        sec = time.perf_counter() - t0
+    return {"L": L, "all_cores": {"cores": workers, "s_per_map": sec}}
+
+
 if __name__ == "__main__":
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -97,6 +97,9 @@ long long scv_launch_count(const scv_ctx* ctx);
  * from a register-resident DFMA loop over every SM; used as the roofline
  * denominator for FP64-bound stages (MEASURED_PEAKS.json has no FP64 entry). */
 int scv_fp64_peak(scv_ctx* ctx, double* tflops);
+/* measured FP64 tensor-core (DMMA m8n8k4) peak of this device, TFLOP/s:
+   the denominator of the executed-DMMA fraction (bench.py) */
+int scv_dmma_peak(scv_ctx* ctx, double* tflops);
 
 /* Batched K-point DFT of `nrows` contiguous complex128 rows with the
  * hand-written prime-factor engine (K = 2^k - 1 up to 4095):

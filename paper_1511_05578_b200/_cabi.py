@@ -44,6 +44,7 @@ _SIGS = {
     "scv_launch_count": [_P],
     "scv_profile_report": [_P, ctypes.c_char_p, _I],
     "scv_fp64_peak": [_P, ctypes.POINTER(ctypes.c_double)],
+    "scv_dmma_peak": [_P, ctypes.POINTER(ctypes.c_double)],
     "scv_debug_dft": [_P, _I, _I, _I, _P, _P, _P],
     "scv_halfpi_wedge": [_P, _I, _P, _P],
     "scv_sht_forward": [_P, _I, _I, _I, _P, _P, _P],
@@ -151,6 +152,14 @@ class Context:
             raise RuntimeError(self.lib.scv_last_error(self.handle).decode())
         return v.value
 
+    def dmma_peak_tflops(self) -> float:
+        v = ctypes.c_double()
+        with self.lock:
+            rc = self.lib.scv_dmma_peak(self.handle, ctypes.byref(v))
+        if rc != SCV_OK:
+            raise RuntimeError(self.lib.scv_last_error(self.handle).decode())
+        return v.value
+
     def set_option(self, name: str, value: int):
         """scv_set_option: e.g. set_option("betaq", 0) selects the FFT beta stage."""
         with self.lock:
@@ -161,7 +170,9 @@ class Context:
     def trim(self):
         with self.lock:
             torch.cuda.synchronize(self.device)
-            self.lib.scv_trim(self.handle)
+            rc = self.lib.scv_trim(self.handle)
+        if rc != SCV_OK:
+            raise ValueError(self.lib.scv_last_error(self.handle).decode())
 
     def __del__(self):
         try:
@@ -217,3 +228,22 @@ def context(device: torch.device | int | None = None) -> Context:
 
 def ptr(t: torch.Tensor) -> ctypes.c_void_p:
     return _P(t.data_ptr())
+
+
+def checked(t, dtype: torch.dtype, shape, device, what: str = "buffer") -> torch.Tensor:
+    """Validate a caller-supplied tensor before its raw pointer reaches the C
+    ABI (which trusts sizes): a CUDA tensor on `device`, exactly `dtype`,
+    C-contiguous, exactly `shape`.  TypeError for a non-tensor / wrong dtype,
+    ValueError for device, layout or shape mismatches."""
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{what} must be a torch tensor, got {type(t).__name__}")
+    if t.dtype != dtype:
+        raise TypeError(f"{what} must have dtype {dtype}, got {t.dtype}")
+    dev = device if isinstance(device, torch.device) else torch.device("cuda", int(device))
+    if not t.is_cuda or (dev.index is not None and t.device.index != dev.index):
+        raise ValueError(f"{what} must live on {dev}, got {t.device}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{what} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    if not t.is_contiguous():
+        raise ValueError(f"{what} must be contiguous")
+    return t

@@ -38,8 +38,8 @@ def _deps_mtime():
     return max(ts)
 
 
-def _compile(src: str, verbose: bool) -> str:
-    obj = os.path.join(BUILD, os.path.basename(src)[:-3] + ".o")
+def _compile(src: str, verbose: bool, objdir: str = BUILD) -> str:
+    obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
     cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
     if verbose:
         cmd += ["-Xptxas", "-v"]
@@ -57,10 +57,13 @@ def build(force: bool = False, verbose: bool = False, out: str = OUT, defines=()
     if not force and out == OUT and os.path.exists(OUT) and os.path.getmtime(OUT) >= _deps_mtime():
         return OUT
     FLAGS = FLAGS + [f"-D{d}" for d in defines]
-    os.makedirs(BUILD, exist_ok=True)
+    # variant builds (other `out`) get their own object directory, so several
+    # can be built at once
+    objdir = BUILD if out == OUT else os.path.join(BUILD, "var_" + os.path.basename(out).replace(".so", ""))
+    os.makedirs(objdir, exist_ok=True)
     srcs = _sources()
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
+        objs = list(ex.map(lambda s: _compile(s, verbose, objdir), srcs))
     tmp = out + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, f"-L{CUDA}/lib64", "-lcufft",
            "-Xlinker", f"-rpath={CUDA}/lib64"]

@@ -108,8 +108,16 @@ static std::vector<double2> to_d2(const std::vector<cld>& v) {
 // ---------------------------------------------------------------------------
 // tables
 // ---------------------------------------------------------------------------
+int scv_check_unpinned(scv_ctx* c, const char* what) {
+  if (c->pinned > 0)
+    return scv_fail(c, SCV_EINVAL, std::string("context is pinned by a captured CUDA graph; refusing to ") + what +
+                                       " (use a private context for graphs, or release the graph first)");
+  return SCV_OK;
+}
+
 int scv_ensure_hlb(scv_ctx* c, int L, cudaStream_t s) {
   if (c->hlb && c->hlb_L >= L) return SCV_OK;
+  if (c->hlb) SCV_TRY(scv_check_unpinned(c, "grow the log-binomial table"));
   int Lb = L;
   std::vector<ld> lf = log_factorials(2 * Lb + 2);
   std::vector<double> h((size_t)Lb * (Lb + 1) / 2);
@@ -125,6 +133,7 @@ int scv_ensure_hlb(scv_ctx* c, int L, cudaStream_t s) {
 
 int scv_ensure_delta(scv_ctx* c, int L, cudaStream_t s) {
   if (c->delta && c->delta_L >= L) return SCV_OK;
+  if (c->delta) SCV_TRY(scv_check_unpinned(c, "grow the Delta table"));
   // edge rows Delta^l_{l,m} = (-1)^{l-m} sqrt(C(2l,l+m)) / 2^l  (wigner.py:153-161),
   // as a double mantissa in [0.5, 1) and a power-of-two exponent: above
   // l ~ 1022 the edge values near |m| = l fall below the double range (2^-l),
@@ -259,6 +268,7 @@ int scv_get_beta_tables(scv_ctx* c, int L, cudaStream_t s, const BetaTables** ou
 int scv_scratch(scv_ctx* c, int slot, size_t bytes, void** out) {
   if (bytes == 0) bytes = 16;
   if (c->scratch_bytes[slot] < bytes) {
+    if (c->scratch[slot]) SCV_TRY(scv_check_unpinned(c, "grow a scratch buffer"));
     if (c->scratch[slot]) {
       cudaDeviceSynchronize();
       cudaFree(c->scratch[slot]);
@@ -300,6 +310,13 @@ int scv_plan(scv_ctx* c, const std::string& key, int rank, int* n, int* inembed,
     return scv_fail(c, SCV_ECUFFT, "cufftMakePlanMany(" + key + ") failed: " + std::to_string((int)r));
   }
   p.work = work;
+  if (work > c->fft_work_bytes && c->fft_work) {
+    const int rc = scv_check_unpinned(c, "grow the cuFFT work area");
+    if (rc != SCV_OK) {
+      cufftDestroy(p.h);
+      return rc;
+    }
+  }
   if (work > c->fft_work_bytes) {
     if (c->fft_work) {
       cudaDeviceSynchronize();
@@ -429,6 +446,11 @@ int scv_set_option(scv_ctx* c, const char* name, int value) {
     c->opt_chunkt = value < 0 ? 0 : value;
     return SCV_OK;
   }
+  if (n == "pin") {  // 1: a graph captured on this context is alive; 0: it was released
+    if (value != 0 && value != 1) return scv_fail(c, SCV_EINVAL, "pin option must be 0 or 1");
+    c->pinned = value ? c->pinned + 1 : (c->pinned > 0 ? c->pinned - 1 : 0);
+    return SCV_OK;
+  }
   if (n == "colgen") {
     if (value < -1 || value > 1) return scv_fail(c, SCV_EINVAL, "colgen option must be -1, 0 or 1");
     c->opt_colgen = value < 0 ? 1 : value;
@@ -439,6 +461,7 @@ int scv_set_option(scv_ctx* c, const char* name, int value) {
 
 int scv_trim(scv_ctx* c) {
   if (!c) return SCV_EINVAL;
+  SCV_TRY(scv_check_unpinned(c, "trim the workspace"));
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   for (int i = 0; i < 3; ++i) {

@@ -379,6 +379,9 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
 // barriers (vs k_pfa_rows: 2 CTAs per SM, each CTA-synchronised, tables
 // duplicated per CTA).
 // ---------------------------------------------------------------------------
+#ifndef SCV_EXP_ROWS_NOIO
+#define SCV_EXP_ROWS_NOIO 0
+#endif
 #ifndef SCV_ROWS_GRP
 #define SCV_ROWS_GRP 4, 96
 #endif
@@ -504,15 +507,20 @@ __global__ void __launch_bounds__(PfaGrpCfg<K>::NG * PfaGrpCfg<K>::NTG, 1)
       } else {
         src = in + r * K;
       }
+      constexpr int KLD = SCV_EXP_ROWS_NOIO ? 0 : K;  // timing experiment only: no loads
 #pragma unroll 4
-      for (int n = gtid; n < K; n += NTG) cp_async16(X + pfa_in_tab<PL>(tab, n), src + n);
+      for (int n = gtid; n < KLD; n += NTG) cp_async16(X + pfa_in_tab<PL>(tab, n), src + n);
     }
     cp_async_commit();
     cp_async_wait<0>();
     grp_sync(bar, NTG);
     pfa_dft<PL, DIR, 1, NTG, K>(X, tab, nullptr, gtid, bar);
+#if SCV_EXP_ROWS_NOIO
+    if (gtid == 0 && X[0].x == 12345.678) dst[0] = X[1];  // timing experiment only: no stores
+#else
 #pragma unroll 4
     for (int k = gtid; k < K; k += NTG) dst[k] = X[pfa_pos_tab<PL>(tab, k)];
+#endif
     grp_sync(bar, NTG);
   }
 }

@@ -987,13 +987,17 @@ __device__ __forceinline__ void pfa_stage_any(double2* X, const double2* tab, do
 
 // gtid/bar: thread index within the work group of NT threads and its named
 // barrier (defaults: the whole block, barrier 0).
+#ifndef SCV_EXP_SKIP_STAGES
+#define SCV_EXP_SKIP_STAGES 0
+#endif
 template <class PL, int DIR, int R, int NT, int PITCH>
 __device__ __forceinline__ void pfa_dft(double2* X, const double2* tab, double2* scr, int gtid = threadIdx.x,
                                         int bar = 0) {
-  pfa_stage_any<PL, 0, DIR, R, NT, PITCH>(X, tab, scr, gtid, bar);
-  if constexpr (PL::D > 1) pfa_stage_any<PL, 1, DIR, R, NT, PITCH>(X, tab, scr, gtid, bar);
-  if constexpr (PL::D > 2) pfa_stage_any<PL, 2, DIR, R, NT, PITCH>(X, tab, scr, gtid, bar);
-  if constexpr (PL::D > 3) pfa_stage_any<PL, 3, DIR, R, NT, PITCH>(X, tab, scr, gtid, bar);
+  // SCV_EXP_SKIP_STAGES (timing experiments only, wrong results): bit s skips stage s
+  if constexpr (!(SCV_EXP_SKIP_STAGES & 1)) pfa_stage_any<PL, 0, DIR, R, NT, PITCH>(X, tab, scr, gtid, bar);
+  if constexpr (PL::D > 1 && !(SCV_EXP_SKIP_STAGES & 2)) pfa_stage_any<PL, 1, DIR, R, NT, PITCH>(X, tab, scr, gtid, bar);
+  if constexpr (PL::D > 2 && !(SCV_EXP_SKIP_STAGES & 4)) pfa_stage_any<PL, 2, DIR, R, NT, PITCH>(X, tab, scr, gtid, bar);
+  if constexpr (PL::D > 3 && !(SCV_EXP_SKIP_STAGES & 8)) pfa_stage_any<PL, 3, DIR, R, NT, PITCH>(X, tab, scr, gtid, bar);
 }
 
 // Out-of-line variant: isolates the transform's register allocation from a

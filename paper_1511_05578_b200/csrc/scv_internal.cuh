@@ -121,7 +121,14 @@ struct scv_ctx {
   int opt_chunkt = 0;  // synthesis chunk layout: 1 = [b][m][g] (strided alpha writes), 0 = [b][g][m]
   int opt_colgen = 1;  // analysis order: 1 = gamma-first column generation + in-place alpha rows, 0 = alpha-first
   int opt_betaq = -1;  // synthesis beta stage: 1 = quadrature table, 0 = per-column FFTs
+  // > 0 while CUDA graphs captured on this context are alive (scv_set_option
+  // "pin"): the graphs hold raw pointers into the workspace, so every path
+  // that would free or move a workspace buffer fails instead
+  int pinned = 0;
 };
+
+// SCV_EINVAL if the context is pinned (a live graph references its buffers)
+int scv_check_unpinned(scv_ctx* c, const char* what);
 
 // RAII stage timer: records a start/stop event pair on `s` when profiling is on
 struct ProfScope {

@@ -139,7 +139,7 @@ class CudaBackend:
         from .so3 import SO3Grid, so3_inverse_curvelet, so3_inverse_curvelet_real
         dev = flm_vals.device
         ctx = _cabi.context(dev)
-        flm = HarmonicCoeffs(t.params.band_limit, 0 if real else t.params.spin, flm_vals, real=real)
+        flm = HarmonicCoeffs(t.params.band_limit, 0 if real else t.params.spin, flm_vals, real=real, trusted=True)
         w = _scale_wigner(ctx, flm, device_tiling(t, dev), j, Lj)
         inv = so3_inverse_curvelet_real if real else so3_inverse_curvelet
         return inv(w, SO3Grid(Lj, Lj, Lj))
@@ -151,7 +151,7 @@ class CudaBackend:
         from .so3 import SO3Grid, so3_inverse_curvelet_slab
         dev = flm_vals.device
         ctx = _cabi.context(dev)
-        flm = HarmonicCoeffs(t.params.band_limit, t.params.spin, flm_vals)
+        flm = HarmonicCoeffs(t.params.band_limit, t.params.spin, flm_vals, trusted=True)
         w = _scale_wigner(ctx, flm, device_tiling(t, dev), j, Lj)
         return so3_inverse_curvelet_slab(w, SO3Grid(Lj, Lj, Lj), b0, nb)
 
@@ -174,7 +174,7 @@ class CudaBackend:
         from .transform import _scaling_coeffs, device_tiling
         dev = flm_vals.device
         ctx = _cabi.context(dev)
-        flm = HarmonicCoeffs(t.params.band_limit, 0 if real else t.params.spin, flm_vals, real=real)
+        flm = HarmonicCoeffs(t.params.band_limit, 0 if real else t.params.spin, flm_vals, real=real, trusted=True)
         s = _scaling_coeffs(ctx, flm, device_tiling(t, dev), Ls, real)
         return sht_inverse_real(s) if real else sht_inverse(s)
 
@@ -204,8 +204,8 @@ class CudaBackend:
         ctx.call("accumulate_scaling", L, slm.band_limit, _cabi.ptr(slm.values), _cabi.ptr(dt.scaling), _cabi.ptr(acc))
         ctx.call("finish_acc", L, p.spin, 1 if real else 0, _cabi.ptr(acc))
         if real:
-            return sht_inverse_real(HarmonicCoeffs(L, 0, acc, real=True))
-        return sht_inverse(HarmonicCoeffs(L, p.spin, acc))
+            return sht_inverse_real(HarmonicCoeffs(L, 0, acc, real=True, trusted=True))
+        return sht_inverse(HarmonicCoeffs(L, p.spin, acc, trusted=True))
 
 
 def _rank_world(group):
@@ -250,6 +250,9 @@ def synthesize_sharded(c: ShardedCoeffs, t, group=None, backend=None, dst: int =
     on `dst` (None elsewhere).  Mirrors transform.synthesize (transform.py:155-187)."""
     backend = backend or CudaBackend()
     rank, world = _rank_world(group)
+    if rank == dst and c.scaling is None:
+        # analyze_sharded forms the scaling signal on its src rank only
+        raise ValueError(f"dst={dst} does not hold the scaling signal: synthesize on the analysis src rank")
     p = t.params
     L = p.band_limit
     nsc = p.scale_count

@@ -192,6 +192,7 @@ def so3_inverse_curvelet(w: CurveletWignerCoeffs, grid: SO3Grid, out: torch.Tens
     dev = w.values.device
     if out is None:
         out = torch.empty((K, L, K), dtype=torch.complex128, device=dev)
+    _cabi.checked(out, torch.complex128, (K, L, K), dev, "out")
     _cabi.context(dev).call("so3_inverse_curvelet", L, 0, _cabi.ptr(w.values), _cabi.ptr(out))
     return SO3Signal(grid, out)
 
@@ -204,6 +205,7 @@ def so3_inverse_curvelet_real(w: CurveletWignerCoeffs, grid: SO3Grid, out: torch
     dev = w.values.device
     if out is None:
         out = torch.empty((K, L, K), dtype=torch.float64, device=dev)
+    _cabi.checked(out, torch.float64, (K, L, K), dev, "out")
     _cabi.context(dev).call("so3_inverse_curvelet", L, 1, _cabi.ptr(w.values), _cabi.ptr(out))
     return SO3Signal(grid, out, real=True)
 
@@ -223,6 +225,8 @@ def so3_forward_curvelet(f: SO3Signal, out: torch.Tensor | None = None) -> Curve
     dev = vals.device
     if out is None:
         out = torch.empty((2, L, 2 * L - 1), dtype=torch.complex128, device=dev)
+    _cabi.checked(out, torch.complex128, (2, L, 2 * L - 1), dev, "out")
+    _cabi.checked(vals, torch.complex128, (2 * L - 1, L, 2 * L - 1), dev, "signal values")
     _cabi.context(dev).call("so3_forward_curvelet", L, 0, _cabi.ptr(vals), _cabi.ptr(out))
     return CurveletWignerCoeffs(L, out)
 
@@ -235,6 +239,8 @@ def so3_forward_curvelet_real(f: SO3Signal, out: torch.Tensor | None = None) -> 
     dev = f.values.device
     if out is None:
         out = torch.empty((2, L, 2 * L - 1), dtype=torch.complex128, device=dev)
+    _cabi.checked(out, torch.complex128, (2, L, 2 * L - 1), dev, "out")
+    _cabi.checked(f.values, torch.float64, (2 * L - 1, L, 2 * L - 1), dev, "signal values")
     _cabi.context(dev).call("so3_forward_curvelet", L, 1, _cabi.ptr(f.values), _cabi.ptr(out))
     return CurveletWignerCoeffs(L, out)
 
@@ -258,6 +264,11 @@ class SO3Slab:
 
     def __post_init__(self):
         K_g, _, K_a = self.grid.shape
+        if self.real and _is_complex(self.values):
+            raise ValueError("real slab carries complex values")
+        # a view such as full.values[:, b0:b0+nb, :] is not contiguous: copy it
+        # into the dense (K, nb, K) layout the C ABI reads
+        self.values = as_device(self.values, torch.float64 if self.real else torch.complex128)
         if self.b0 < 0 or self.values.dim() != 3 or self.b0 + self.values.shape[1] > self.grid.L:
             raise ValueError(f"slab rows [{self.b0}, {self.b0 + self.values.shape[1]}) outside [0, {self.grid.L})")
         if (self.values.shape[0], self.values.shape[2]) != (K_g, K_a):
@@ -272,6 +283,7 @@ def so3_inverse_curvelet_slab(w: CurveletWignerCoeffs, grid: SO3Grid, b0: int, n
     dev = w.values.device
     if out is None:
         out = torch.empty((K, nb, K), dtype=torch.complex128, device=dev)
+    _cabi.checked(out, torch.complex128, (K, nb, K), dev, "out")
     _cabi.context(dev).call("so3_inverse_curvelet_slab", L, _cabi.ptr(w.values), int(b0), int(nb), _cabi.ptr(out))
     return SO3Slab(grid, int(b0), out)
 
@@ -284,6 +296,9 @@ def so3_forward_curvelet_slab(f: SO3Slab, out: torch.Tensor | None = None, accum
     if out is None:
         out = torch.zeros((2, L, 2 * L - 1), dtype=torch.complex128, device=dev)
         accumulate = False
+    _cabi.checked(out, torch.complex128, (2, L, 2 * L - 1), dev, "out")
+    K = 2 * L - 1
+    _cabi.checked(f.values, torch.float64 if f.real else torch.complex128, (K, f.nb, K), dev, "slab values")
     _cabi.context(dev).call("so3_forward_curvelet_slab", L, 1 if f.real else 0, _cabi.ptr(f.values), int(f.b0),
                             f.nb, _cabi.ptr(out), 1 if accumulate else 0)
     return CurveletWignerCoeffs(L, out)

@@ -10,7 +10,7 @@ libscurve_b200.so (csrc/sht.cu, csrc/beta.cu).
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 from functools import cached_property
 
 import numpy as np
@@ -123,6 +123,11 @@ class HarmonicCoeffs:
     spin: int
     values: torch.Tensor
     real: bool = False
+    # internal: set by this package's own producers (the forward SHT, the
+    # synthesis accumulator after finish_acc), whose degrees below |spin| are
+    # zero by construction, so the data-dependent check -- a host sync -- is
+    # only paid for user-supplied coefficients
+    trusted: bool = field(default=False, repr=False, compare=False, kw_only=True)
 
     def __post_init__(self):
         L = self.band_limit
@@ -134,9 +139,10 @@ class HarmonicCoeffs:
         if _shape(self.values) != (L * L,):
             raise ValueError(f"expected {L * L} coefficients, got shape {_shape(self.values)}")
         low = self.spin * self.spin
-        # a data-dependent check syncs the host: skipped while a CUDA graph is being
-        # captured (GraphedRoundTrip), where the values come from this package's own SHT
-        if low and not torch.cuda.is_current_stream_capturing() and bool(torch.any(self.values[:low] != 0)):
+        # a data-dependent check syncs the host: skipped for trusted producers
+        # and while a CUDA graph is being captured (GraphedRoundTrip)
+        if (low and not self.trusted and not torch.cuda.is_current_stream_capturing()
+                and bool(torch.any(self.values[:low] != 0))):
             raise ValueError("degrees below |spin| must be exactly zero")
         if self.real and self.spin != 0:
             raise ValueError("real coefficient sets must have spin 0")
@@ -165,7 +171,7 @@ def sht_forward(f: SphereSignal) -> HarmonicCoeffs:
     ctx = _cabi.context(f.values.device)
     out = torch.empty(L * L, dtype=torch.complex128, device=f.values.device)
     ctx.call("sht_forward", L, s, 0, _cdbl(f.values), _cdbl(out))
-    return HarmonicCoeffs(L, s, out)
+    return HarmonicCoeffs(L, s, out, trusted=True)
 
 
 def sht_inverse(flm: HarmonicCoeffs) -> SphereSignal:
@@ -187,7 +193,7 @@ def sht_forward_real(f: SphereSignal) -> HarmonicCoeffs:
     ctx = _cabi.context(f.values.device)
     out = torch.empty(L * L, dtype=torch.complex128, device=f.values.device)
     ctx.call("sht_forward", L, 0, 1, _cdbl(f.values), _cdbl(out))
-    return HarmonicCoeffs(L, 0, out, real=True)
+    return HarmonicCoeffs(L, 0, out, real=True, trusted=True)
 
 
 def sht_inverse_real(flm: HarmonicCoeffs) -> SphereSignal:

@@ -203,8 +203,8 @@ def _synthesize(c: CurveletCoeffs, t, real: bool) -> SphereSignal:
     ctx.call("accumulate_scaling", L, slm.band_limit, _cabi.ptr(slm.values), _cabi.ptr(dt.scaling), _cabi.ptr(acc))
     ctx.call("finish_acc", L, p.spin, 1 if real else 0, _cabi.ptr(acc))
     if real:
-        return sht_inverse_real(HarmonicCoeffs(L, 0, acc, real=True))
-    return sht_inverse(HarmonicCoeffs(L, p.spin, acc))
+        return sht_inverse_real(HarmonicCoeffs(L, 0, acc, real=True, trusted=True))
+    return sht_inverse(HarmonicCoeffs(L, p.spin, acc, trusted=True))
 
 
 def synthesize(c: CurveletCoeffs, t: Tiling) -> SphereSignal:
@@ -303,7 +303,7 @@ def roundtrip_streamed(f: SphereSignal, t: Tiling, multires: bool = True, slab_b
     slm = sht_forward(scaling_sig)
     ctx.call("accumulate_scaling", L, slm.band_limit, _cabi.ptr(slm.values), _cabi.ptr(dt.scaling), _cabi.ptr(acc))
     ctx.call("finish_acc", L, p.spin, 0, _cabi.ptr(acc))
-    return sht_inverse(HarmonicCoeffs(L, p.spin, acc))
+    return sht_inverse(HarmonicCoeffs(L, p.spin, acc, trusted=True))
 
 
 # ---------------------------------------------------------------------------
@@ -359,14 +359,24 @@ class GraphedRoundTrip:
     graph-owned tensors, overwritten by the next call.  Results are
     bit-identical to the eager calls (the same kernels on the same buffers;
     tests/test_graph.py).
+
+    The graph holds raw pointers into its context's workspace (scratch
+    slots, cuFFT work area, Delta and log-binomial tables), which the
+    library grows and frees on demand.  By default the instance therefore
+    owns a private context, so eager calls elsewhere can never move memory
+    the graph replays against.  With ``private_context=False`` the shared
+    per-device context is PINNED while the instance lives (``close()`` or
+    garbage collection releases it): any call that would grow, free or trim
+    a workspace buffer of that context raises ValueError instead.
     """
 
     def __init__(self, t: Tiling, spin: int = 0, real: bool = False, multires: bool = True,
-                 private_context: bool = False):
+                 private_context: bool = True):
         L = t.params.band_limit
         dev = torch.device("cuda", torch.cuda.current_device())
         dtype = torch.float64 if real else torch.complex128
         self.t, self.real = t, real
+        self._pinned = False
         # a private context owns its scratch, so several instances can replay
         # concurrently on different streams (BatchedRoundTrip)
         self.ctx = _cabi.new_context(dev.index) if private_context else _cabi.context(dev)
@@ -388,6 +398,22 @@ class GraphedRoundTrip:
                 self.coeffs = ana(f, t, multires)
                 self.out = syn(self.coeffs, t)
             self.kernels_per_replay = self.ctx.launch_count() - n0
+        if not private_context:
+            self.ctx.set_option("pin", 1)
+            self._pinned = True
+
+    def close(self) -> None:
+        """Release the graph (and the pin on a shared context)."""
+        if getattr(self, "_pinned", False):
+            self._pinned = False
+            self.ctx.set_option("pin", 0)
+        self.graph = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
     def launch(self, values=None) -> SphereSignal:
         """Replay on this instance's own stream, ordered after the caller's

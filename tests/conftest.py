@@ -26,31 +26,25 @@ def golden():
         return {k: z[k] for k in z.files}
 
 
-# Tiling build order of tests/golden/make_golden.py.  The step table memoises
-# integrals (reference tiling.py:92-134), so kernel values depend on the query
-# history at the ~1e-8 absolute level; replaying the generator's history makes
-# the comparison with the golden tilings exact to rounding.
-GOLDEN_TILING_ORDER = [(64, 0, 2.0, 2), (128, 2, 2.0, 2), (512, 0, 2.0, 2), (1024, 0, 2.0, 3),
-                       (16, 0, 3.0, 0), (33, 1, 2.5, 1), (16, 0, 2.0, 2), (16, 2, 2.0, 2),
-                       (16, 0, 2.0, 2), (64, 0, 2.0, 2)]
+@pytest.fixture(scope="session")
+def ref_tilings():
+    path = os.path.join(ROOT, "tests", "golden", "reference_tilings.npz")
+    with np.load(path) as z:
+        return {k: z[k] for k in z.files}
 
 
-def golden_tilings():
-    """Rebuild the generator's tilings in its order; returns {key: Tiling} (first build wins)."""
+def reference_tiling(L, s, lam, j0, k=0):
+    """The k-th tiling with these parameters that the reference's fixture
+    generators built (tests/golden/make_golden_tilings.py), as this
+    package's Tiling.  Tests comparing transform outputs with reference
+    fixtures run on these exact arrays; tests/test_tiling.py pins our own
+    build_tiling to them."""
     from paper_1511_05578_b200 import tiling as T
-    T._reset_step_tables()
-    out = {}
-    for (L, s, lam, j0) in GOLDEN_TILING_ORDER:
-        t = T.build_tiling(T.TilingParams(L, s, lam, j0))
-        out.setdefault((L, s, lam, j0), t)
-    return out
-
-
-@pytest.fixture(autouse=True, scope="module")
-def _fresh_step_tables():
-    """Every test module starts from an empty tiling step-table memo, as in a
-    fresh process, so a module's golden comparisons do not depend on which
-    tilings earlier modules built (see GOLDEN_TILING_ORDER above)."""
-    from paper_1511_05578_b200 import tiling as T
-    T._reset_step_tables()
-    yield
+    path = os.path.join(ROOT, "tests", "golden", "reference_tilings.npz")
+    key = "t_%d_%d_%s_%d_%d" % (L, s, repr(float(lam)), j0, k)
+    with np.load(path) as z:
+        a = {n: z[key + "_" + n] for n in ("kernels", "scaling", "dirpos", "dirneg", "angles", "jmax")}
+    p = T.TilingParams(L, s, lam, j0, int(a["jmax"]))
+    for v in a.values():
+        v.setflags(write=False)
+    return T.Tiling(p, a["kernels"], a["scaling"], a["dirpos"], a["dirneg"], a["angles"])

@@ -144,7 +144,8 @@ def test_our_analysis_against_reference_file(tmp_path):
     import paper_1511_05578_b200 as sc
     f = C.read_sphere(os.path.join(GOLD, "ref_sphere_L8s2.scrv"))
     ref = C.read_coeffs(os.path.join(GOLD, "ref_coeffs_L8s2.scrv"))
-    t = sc.build_tiling(sc.TilingParams(8, 2, 2.0, 1))
+    from conftest import reference_tiling
+    t = reference_tiling(8, 2, 2.0, 1)
     c = sc.analyze(f, t)
     C.write_coeffs(str(tmp_path / "ours.scrv"), c, extra={"note": "golden"})
     ours = C.read_coeffs(str(tmp_path / "ours.scrv"))

@@ -222,3 +222,14 @@ def test_scale_plan_balances_cost():
             assert rows[0][0] == 0 and sum(nb for _, nb in rows) == plan.Ljs[j - 3]
         # the real path keeps whole scales
         assert not ScalePlan.build(p, world, real=True).slabs
+
+
+def test_synthesize_sharded_requires_scaling_on_dst():
+    """analyze_sharded forms the scaling signal on its src rank only; a dst
+    that does not hold it is rejected up front (not after the reduce)."""
+    from paper_1511_05578_b200.dist import ShardedCoeffs
+    p = T.TilingParams(16, 0, 2.0, 1)
+    t = T.build_tiling(p)
+    c = ShardedCoeffs(p, ScalePlan.build(p, 1), scaling=None)
+    with pytest.raises(ValueError, match="scaling"):
+        synthesize_sharded(c, t, backend=OracleBackend(16, 0))

@@ -201,7 +201,8 @@ def test_beta_quadrature_matches_fft_beta_stage(L, real):
 # ------------------------------------------------------------------ transform
 @pytest.mark.parametrize("L,s,real", [(16, 0, False), (16, 2, False), (16, 0, True)])
 def test_transform_golden(golden, L, s, real):
-    t = sc.build_tiling(sc.TilingParams(L, s, 2.0, 2))
+    from conftest import reference_tiling
+    t = reference_tiling(L, s, 2.0, 2, 1 if real else 0)  # the reference's own kernels
     key = f"xf_{L}_{s}_{int(real)}"
     f = sc.SphereSignal(sc.SphereGrid(L), s, golden[key + "_map"], real=real)
     c = sc.analyze_real(f, t) if real else sc.analyze(f, t)
@@ -214,8 +215,9 @@ def test_transform_golden(golden, L, s, real):
 
 
 def test_config1_golden(golden):
+    from conftest import reference_tiling
     L = 64
-    t = sc.build_tiling(sc.TilingParams(L, 0, 2.0, 2))
+    t = reference_tiling(L, 0, 2.0, 2, 1)
     f = sc.SphereSignal(sc.SphereGrid(L), 0, golden["c1_map"])
     c = sc.analyze(f, t)
     assert orc.rel_err(host(c.scaling.values), golden["c1_scaling"]) <= TOL

@@ -59,3 +59,47 @@ def test_batched_lanes_bit_identical(L, spin, real):
     torch.cuda.synchronize()
     for i in range(7):
         assert torch.equal(out2[i], eager[6 - i]), i
+
+
+def test_private_graph_survives_eager_growth():
+    """A graph captured at a small band limit owns a private context (the
+    default), so an eager call at a larger band limit on the same device --
+    which grows the shared context's scratch, Delta and cuFFT buffers -- can
+    not move memory the graph replays against: the replay stays bit-identical."""
+    import paper_1511_05578_b200 as sc
+    L = 32
+    t = sc.build_tiling(sc.TilingParams(L, 0, 2.0, 2))
+    g = sc.GraphedRoundTrip(t)
+    fmap = orc.sht_inverse(orc.gaussian_flm(L, 0, seed=3, real=False), L, 0)
+    f = sc.SphereSignal(sc.SphereGrid(L), 0, fmap)
+    first = g(f.values).values.clone()
+    torch.cuda.synchronize()
+    Lb = 256
+    tb = sc.build_tiling(sc.TilingParams(Lb, 0, 2.0, 2))
+    fb = sc.sht_inverse(sc.HarmonicCoeffs(Lb, 0, orc.gaussian_flm(Lb, 0, seed=4, real=False)))
+    sc.synthesize(sc.analyze(fb, tb), tb)
+    from paper_1511_05578_b200 import _cabi
+    _cabi.context(0).trim()  # frees the shared context's scratch outright
+    again = g(f.values).values
+    torch.cuda.synchronize()
+    assert torch.equal(again, first)
+    g.close()
+
+
+def test_shared_context_graph_pins_the_context():
+    """With private_context=False the graph replays against the shared
+    context's buffers; while it lives, freeing or moving them is refused."""
+    import paper_1511_05578_b200 as sc
+    from paper_1511_05578_b200 import _cabi
+    L = 32
+    t = sc.build_tiling(sc.TilingParams(L, 0, 2.0, 2))
+    g = sc.GraphedRoundTrip(t, private_context=False)
+    ctx = _cabi.context(0)
+    with pytest.raises(ValueError, match="pinned"):
+        ctx.trim()
+    fmap = orc.sht_inverse(orc.gaussian_flm(L, 0, seed=5, real=False), L, 0)
+    out = g(fmap).values.clone()
+    torch.cuda.synchronize()
+    assert orc.rel_err(out.cpu().numpy(), fmap) <= 1e-11
+    g.close()
+    ctx.trim()  # released: allowed again

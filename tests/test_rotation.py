@@ -261,13 +261,8 @@ def test_dense_synthesis_matches_sparse_path(rng):
 @gpu
 def test_north_validation_matches_reference(rot):
     sc = _sc()
-    from paper_1511_05578_b200 import tiling as T
-    # replay the fixture generator's tiling history (tilings memoise step
-    # integrals, conftest.GOLDEN_TILING_ORDER); its last build is the one used
-    T._reset_step_tables()
-    for prm in ((16, 1, 2.0, 1), (8, 0, 2.0, 0), (16, 2, 2.0, 0), (48, 0, 2.0, 2)):
-        T.build_tiling(T.TilingParams(*prm))
-    t = T.build_tiling(T.TilingParams(8, 0, 2.0, 0))
+    from conftest import reference_tiling
+    t = reference_tiling(8, 0, 2.0, 0, 1)  # the generator's second (8, 0, 2, 0) build
     f = sc.SphereSignal(sc.SphereGrid(8), 0, rot["north_map"])
     out = sc.analyze_north_validation(f, t, 2)
     assert orc.rel_err(host(out.values), rot["north_out"]) <= 1e-10

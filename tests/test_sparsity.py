@@ -72,8 +72,12 @@ def test_device_stats_on_reference_values(sp):
 def test_device_pipeline_against_reference(sp):
     import paper_1511_05578_b200 as sc
     from paper_1511_05578_b200 import sparsity as S
+    from conftest import reference_tiling
+    nth = {}
     for name, L, spin, real, bins, j0, j1 in _cases(sp):
-        t = sc.build_tiling(sc.TilingParams(L, spin, 2.0, j0))
+        k = nth.get((L, spin, j0), 0)  # the generator's k-th build of these parameters
+        nth[(L, spin, j0)] = k + 1
+        t = reference_tiling(L, spin, 2.0, j0, k)
         f = sc.SphereSignal(sc.SphereGrid(L), spin, sp[f"{name}_map"], real=real)
         c = sc.analyze_real(f, t) if real else sc.analyze(f, t)
         summary, rows = S.sparsity_report(c, bins)

@@ -43,7 +43,7 @@ def test_slab_view_values_are_made_contiguous():
     import numpy as np
     import paper_1511_05578_b200 as sc
     from oracle import scurve_oracle as orc
-    L = 32
+    L = 128  # the slab entry points need the beta-quadrature path (128 <= L <= 2048)
     rng = np.random.default_rng(1)
     w = np.zeros((2, L, 2 * L - 1), complex)
     c = L - 1
@@ -53,7 +53,7 @@ def test_slab_view_values_are_made_contiguous():
     grid = sc.SO3Grid(L, L, L)
     full = sc.so3_inverse_curvelet(sc.CurveletWignerCoeffs(L, w), grid)
     acc = None
-    for b0, b1 in ((0, 10), (10, 32)):
+    for b0, b1 in ((0, 40), (40, L)):
         slab = sc.SO3Slab(grid, b0, full.values[:, b0:b1, :])
         assert slab.values.is_contiguous()
         part = sc.so3_forward_curvelet_slab(slab, out=acc, accumulate=acc is not None)

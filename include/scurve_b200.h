@@ -70,7 +70,9 @@ const char* scv_last_error(const scv_ctx* ctx);
 /* Bytes of device memory currently held by the context: scratch workspace,
  * the Delta wedge and the per-L tables (beta quadrature, prime-factor). */
 long long scv_workspace_bytes(const scv_ctx* ctx);
-/* Release every lazily grown scratch buffer (tables stay). */
+/* Release every lazily grown scratch buffer, the beta-quadrature tables and
+ * the Delta wedge (all rebuilt on next use; the small prime-factor tables
+ * stay).  Fails with SCV_EINVAL while a captured graph pins the context. */
 int scv_trim(scv_ctx* ctx);
 
 /* Stage profiler: when enabled, every launch group is bracketed by CUDA

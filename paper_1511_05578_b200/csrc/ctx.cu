@@ -474,6 +474,21 @@ int scv_trim(scv_ctx* c) {
   if (c->fft_work) cudaFree(c->fft_work);
   c->fft_work = nullptr;
   c->fft_work_bytes = 0;
+  // the large per-L tables are rebuilt on next use: the beta-quadrature tables
+  // (8 L^3 bytes each; the small prime-factor / task tables stay) and the
+  // Delta wedge
+  for (auto it = c->aux.begin(); it != c->aux.end();) {
+    if (it->first.rfind("betaq", 0) == 0) {
+      cudaFree(it->second);
+      it = c->aux.erase(it);
+    } else {
+      ++it;
+    }
+  }
+  c->table_bytes = c->small_table_bytes;
+  if (c->delta) cudaFree(c->delta);
+  c->delta = nullptr;
+  c->delta_L = 0;
   return SCV_OK;
 }
 

@@ -216,6 +216,7 @@ int scv_pfa_tables(scv_ctx* c, int K, const double2** out) {
   SCV_CUDA(c, cudaMemcpy(d, tab.data(), tab.size() * sizeof(double2), cudaMemcpyHostToDevice));
   c->aux[key] = d;
   c->table_bytes += (long long)(tab.size() * sizeof(double2));
+  c->small_table_bytes += (long long)(tab.size() * sizeof(double2));
   *out = (const double2*)d;
   return SCV_OK;
 }

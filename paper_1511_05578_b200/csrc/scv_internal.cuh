@@ -111,6 +111,7 @@ struct scv_ctx {
   // small int tables by key
   std::map<std::string, void*> aux;
   long long table_bytes = 0;  // persistent per-L tables in `aux` (quadrature, prime-factor, tasks)
+  long long small_table_bytes = 0;  // the part of table_bytes that scv_trim keeps (prime-factor, task tables)
   // stage profiler (scv_profile): event pairs around every launch group
   bool prof = false;
   long long launches = 0;  // kernels of this library launched (scv_launch_count)

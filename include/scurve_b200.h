@@ -109,6 +109,13 @@ int scv_dmma_peak(scv_ctx* ctx, double* tflops);
  * Exposed for testing and benchmarking the engine in isolation. */
 int scv_debug_dft(scv_ctx* ctx, int K, int dir, int nrows, const double* in, double* out,
                   void* stream);
+/* Host-only views of the engine's shared-memory position maps (no device
+ * needed): out_pos[k] = position of output frequency k, in_pos[n] = position
+ * of input sample n (K ints each); and the storage order of a radix-89
+ * butterfly's elements, sigma_in[j] / sigma_out[k] (89 ints each).  Tests
+ * emulate the stages on these maps against numpy.fft (tests/test_pfa_maps.py). */
+int scv_debug_pfa_maps(int K, int* out_pos, int* in_pos);
+int scv_debug_r89_sigma(int* sigma_in, int* sigma_out);
 
 /* Delta^l_{m'm}(pi/2) for l < L in the 1/8 symmetry wedge 0 <= m <= m' <= l:
  * element (l, m', m) at l(l+1)(l+2)/6 + m'(m'+1)/2 + m.  Copies the context's

@@ -156,8 +156,27 @@ static void rader89_tables(double* T) {
       T[R89_OFF_RA + row22(i) * R89_P28 + col22(j)] = (double)(0.5L * ra);
       T[R89_OFF_RB + row22(i) * R89_P28 + col22(j)] = (double)(0.5L * rb);
     }
+  // row 11 of the first matrix (padding of the 16-row tile) = all ones: its
+  // product with the V0 column sums is sum_a s'_a, the y_0 term
+  for (int a2 = 0; a2 < 11; ++a2) T[11 * R89_P12 + a2] = 1.0;
   unsigned char* RT = (unsigned char*)(T + R89_OFF_RT);
   for (int a = 0; a < h; ++a) RT[a] = (unsigned char)r[a];
+}
+
+// Storage order of a radix-89 butterfly's elements (pfa_stage_rader89):
+// position of input element j (which = 0) or of output y_k (which = 1).
+static int r89_sigma(int which, int j) {
+  if (j == 0) return 0;
+  int r = 1;
+  for (int a = 0; a < 44; ++a, r = (r * 3) % 89) {
+    if (r != j && 89 - r != j) continue;
+    const bool neg = (a >> 2) & 1;           // negacyclic wrap sign of a
+    const bool first = (r == j) != neg;      // j is the u / "+" member of the pair
+    const int a1 = a % 4, a2 = a % 11;
+    const int s = which == 0 ? r89_in_slot(a1, a2) : r89_out_slot(a1, a2);
+    return (first ? 1 : 45) + s;
+  }
+  return -1;
 }
 
 int scv_pfa_tables(scv_ctx* c, int K, const double2** out) {
@@ -383,8 +402,14 @@ __global__ void __launch_bounds__(PfaCfg<K, false>::NT, PfaCfg<K, false>::MINB)
 #ifndef SCV_EXP_ROWS_NOIO
 #define SCV_EXP_ROWS_NOIO 0
 #endif
+#ifndef SCV_ROWS_NG
+#define SCV_ROWS_NG 4
+#endif
+#ifndef SCV_ROWS_NTG
+#define SCV_ROWS_NTG 96
+#endif
 #ifndef SCV_ROWS_GRP
-#define SCV_ROWS_GRP 4, 96
+#define SCV_ROWS_GRP SCV_ROWS_NG, SCV_ROWS_NTG
 #endif
 template <int K> struct PfaGrpCfg { static constexpr int NG = 0, NTG = 0; };
 #define SCV_RGCFG_(KK, ...)                                  \
@@ -1688,7 +1713,7 @@ int scv_pfa_pos_host(int K, int k) {
   strides_of(f, st);
   int a = 0;
   for (int s = 0; s < 4; ++s)
-    if (f[s] > 1) a += (k % f[s]) * st[s];
+    if (f[s] > 1) a += (pfa_rader89(f[s]) ? r89_sigma(1, k % f[s]) : k % f[s]) * st[s];
   return a;
 }
 static int pfa_in_host(int K, int n) {
@@ -1702,9 +1727,29 @@ static int pfa_in_host(int K, int n) {
     const int r = (K / p) % p;
     int inv = 1;
     while ((r * inv) % p != 1) ++inv;
-    a += (int)(((long long)n * inv) % p) * st[s];
+    const int j = (int)(((long long)n * inv) % p);
+    a += (pfa_rader89(p) ? r89_sigma(0, j) : j) * st[s];
   }
   return a;
+}
+
+// host-only view of the position maps (tests: the maps must reproduce the DFT
+// under a plain emulation of the stages): out[k] and in[n], K entries each
+extern "C" int scv_debug_pfa_maps(int K, int* out_pos, int* in_pos) {
+  if (!scv_pfa_supported(K)) return SCV_EINVAL;
+  for (int k = 0; k < K; ++k) {
+    out_pos[k] = scv_pfa_pos_host(K, k);
+    in_pos[k] = pfa_in_host(K, k);
+  }
+  return SCV_OK;
+}
+// sigma_in / sigma_out of the radix-89 storage order (89 entries each)
+extern "C" int scv_debug_r89_sigma(int* sin, int* sout) {
+  for (int j = 0; j < 89; ++j) {
+    sin[j] = r89_sigma(0, j);
+    sout[j] = r89_sigma(1, j);
+  }
+  return SCV_OK;
 }
 
 // TMA descriptor of a (K, nb, K) complex128 beta slab seen as doubles:

@@ -806,57 +806,65 @@ __device__ __forceinline__ void pfa_stage_mma_blk(double2* X, const double2* tab
 // Warp-owned blocks of 4 butterflies as in pfa_stage_mma_blk.  Lane (ar, ac):
 // B-fragment column ar (butterfly slot(ar>>1), component ar&1) holding the
 // a mod 11 = ac + 4 kt values; epilogue butterfly slot(ac), output rows ar.
+//
+// Storage order of the 89 elements of a butterfly (r02).  Radix 89 is the
+// innermost dimension (stride 1), and every other reader / writer of the row
+// buffer goes through the 16-bit position maps, so the order of a butterfly's
+// 89 elements in shared memory is free.  It is chosen so that this stage needs
+// no permutation at run time:
+//   * INPUT element j sits at r89_sigma_in(j): 0 for j = 0; for the pair
+//     a = (33 a1 + 12 a2) mod 44 the two elements (u_a, v_a) sit at
+//     1 + (11 a1 + a2) and 45 + (11 a1 + a2), where (u_a, v_a) = (r_a, 89 - r_a)
+//     if the negacyclic wrap sign of a is + and (89 - r_a, r_a) if it is -, so
+//     the twisted difference is always x_u - x_v.  A lane's 4 x 2 gather of a
+//     k-step is eight 8-byte loads at compile-time offsets from one base, and
+//     the 16 lanes of a shared-memory phase cover 128 contiguous bytes.
+//   * OUTPUT y_k sits at r89_sigma_out(k): 0 for k = 0; for b = (33 b1 +
+//     12 b2) mod 44 the outputs x0 + A'_b + DIR i B and x0 + A'_b - DIR i B go
+//     to 1 + t and 45 + t, t = 2 b2 + (b1 & 1) + 22 (b1 >> 1) (B without the
+//     wrap sign: the + output is y_{r_b} if the sign of b is +, y_{89-r_b}
+//     otherwise).  The eight lanes of a 16-byte store phase hit eight different
+//     16-byte bank groups.
+// The host builds the position maps with the same two functions (pfa.cu).
+// y_0 = x0 + sum_a s'_a comes out of the tensor core as well: row 11 of the
+// first 11 x 11 matrix (padding until r02) is all ones.
+__host__ __device__ constexpr int r89_in_slot(int a1, int a2) { return 11 * a1 + a2; }
+__host__ __device__ constexpr int r89_out_slot(int b1, int b2) { return 2 * b2 + (b1 & 1) + 22 * (b1 >> 1); }
 template <class PL, int S, int DIR, int R, int NT, int PITCH>
 __device__ __forceinline__ void pfa_stage_rader89(double2* X, const double2* tab, int gtid, int bar) {
   constexpr int p = 89;
   constexpr int K = PL::K;
-  constexpr int step = pfa_st<PL, S>();
+  static_assert(pfa_st<PL, S>() == 1, "the Rader storage order needs radix 89 as the innermost dimension");
+  static_assert(SCV_PFA_POSTAB == 1, "the Rader storage order lives in the position tables");
   constexpr int nbf = K / p;
   constexpr int NBF = R * nbf;
   constexpr int NBLK = 2 * ((NBF + 7) / 8);
   constexpr int NW = NT / 32;
   const double* T0 = (const double*)(tab + pfa_tab_off<PL, S>());
-  const unsigned char* RT = (const unsigned char*)(T0 + R89_OFF_RT);
   const double* Xd = (const double*)X;
   const int lane = gtid & 31, warp = gtid >> 5;
   const int ar = lane >> 2, ac = lane & 3;
   constexpr double s2 = 0.70710678118654752440;
   auto slot = [](int i) { return (i >> 1) + 4 * (i & 1); };
-#if SCV_R89_PREPOS
-  // the lane's 12 gather offsets r_a * step (a = (33 a1 + 12 a2) mod 44) do not
-  // depend on the block: read from the position table once per stage, packed
-  // two 16-bit offsets per register
-  unsigned int gpos[6];
-#pragma unroll
-  for (int i = 0; i < 6; ++i) gpos[i] = 0u;
-#pragma unroll
-  for (int kt = 0; kt < 3; ++kt) {
-#pragma unroll
-    for (int a1 = 0; a1 < 4; ++a1) {
-      const int a2 = ac + 4 * kt, i = kt * 4 + a1;
-      const unsigned int v = a2 < 11 ? (unsigned int)(RT[(33 * a1 + 12 * a2) % 44] * step) : 0u;
-      gpos[i >> 1] |= v << (16 * (i & 1));
-    }
-  }
-#endif
+  const bool a2ok = ac < 3;  // a mod 11 = ac + 8 exists in the third k-step
 #pragma unroll 1
   for (int q = warp; q < NBLK; q += NW) {
     const int gb = (q >> 1) * 8 + 2 * (q & 1);
-    const int bfB = gb + slot(ar >> 1);
-    const bool okB = bfB < NBF;
-    int rowd = 0, c0B = 0;
-    if (okB) {
-      const int rr = bfB / nbf, b = bfB - rr * nbf;
-      c0B = pfa_base<PL, S>(b);
-      rowd = 2 * rr * PITCH + (ar & 1);
+    // B-fragment butterfly of this lane; a block past the end re-reads the last
+    // butterfly (its GEMM columns are independent and never stored)
+    const int bfB = min(gb + slot(ar >> 1), NBF - 1);
+    const double* xg;
+    {
+      const int rr = R == 1 ? 0 : bfB / nbf, b = bfB - rr * nbf;
+      xg = Xd + 2 * (rr * PITCH + b * p + 1 + ac) + (ar & 1);
     }
     const int bfE = gb + slot(ac);
     const bool okE = bfE < NBF;
     int eoff = 0;
     double2 x0 = make_double2(0.0, 0.0);
     if (okE) {
-      const int rr = bfE / nbf, b = bfE - rr * nbf;
-      eoff = rr * PITCH + pfa_base<PL, S>(b);
+      const int rr = R == 1 ? 0 : bfE / nbf, b = bfE - rr * nbf;
+      eoff = rr * PITCH + b * p;
       x0 = X[eoff];
     }
     // ---- per k-step kt (a2 = ac + 4 kt): gather, in-lane 4-point transforms,
@@ -867,35 +875,22 @@ __device__ __forceinline__ void pfa_stage_rader89(double2* X, const double2* tab
     for (int t = 0; t < 2; ++t) y0[t][0] = y0[t][1] = y2[t][0] = y2[t][1] = 0.0;
 #pragma unroll
     for (int t = 0; t < 3; ++t) yu[t][0] = yu[t][1] = za[t][0] = za[t][1] = zb[t][0] = zb[t][1] = 0.0;
-    double ssum = 0.0;
 #pragma unroll
     for (int kt = 0; kt < 3; ++kt) {
-      const int a2 = ac + 4 * kt;
       double sv[4], w[4];
 #pragma unroll
       for (int a1 = 0; a1 < 4; ++a1) {
-        sv[a1] = 0.0;
-        w[a1] = 0.0;
-        if (okB && a2 < 11) {
-          const int a = (33 * a1 + 12 * a2) % 44;
-#if SCV_R89_PREPOS
-          const int rs = (int)((gpos[(kt * 4 + a1) >> 1] >> (16 * ((kt * 4 + a1) & 1))) & 0xFFFFu);
-          const double xa = Xd[rowd + 2 * (c0B + rs)];
-          const double xb = Xd[rowd + 2 * (c0B + p * step - rs)];
-#else
-          const int r = RT[a];
-          const double xa = Xd[rowd + 2 * (c0B + r * step)];
-          const double xb = Xd[rowd + 2 * (c0B + (p - r) * step)];
-#endif
-          sv[a1] = xa + xb;
-          const double dv = xa - xb;
-          w[a1] = ((a >> 2) & 1) ? -dv : dv;
+        double xu = 0.0, xv = 0.0;
+        if (kt < 2 || a2ok) {
+          xu = xg[2 * (r89_in_slot(a1, 4 * kt))];
+          xv = xg[2 * (r89_in_slot(a1, 4 * kt) + 44)];
         }
+        sv[a1] = xu + xv;
+        w[a1] = xu - xv;
       }
       const double bV0 = (sv[0] + sv[2]) + (sv[1] + sv[3]);
       const double bV2 = (sv[0] + sv[2]) - (sv[1] + sv[3]);
       const double bUr = sv[0] - sv[2], bUi = sv[1] - sv[3];
-      ssum += bV0;
       const double P = (w[1] - w[3]) * s2, Q = (w[1] + w[3]) * s2;
       const double bAr = w[0] + P, bAi = -w[2] - Q, bBr = w[0] - P, bBi = w[2] - Q;
 #pragma unroll
@@ -915,11 +910,6 @@ __device__ __forceinline__ void pfa_stage_rader89(double2* X, const double2* tab
         dmma(zb[t][0], zb[t][1], T0[R89_OFF_RB + o + 12], bBi);
       }
     }
-    // y_0 = x0 + sum_a s'_a: column sums over the quad, then to the epilogue lanes
-    ssum += __shfl_xor_sync(0xffffffffu, ssum, 1);
-    ssum += __shfl_xor_sync(0xffffffffu, ssum, 2);
-    const double s0r = __shfl_sync(0xffffffffu, ssum, (2 * ac) * 4);
-    const double s0i = __shfl_sync(0xffffffffu, ssum, (2 * ac + 1) * 4);
     // rows 3..5 of the third product tile hold the Im parts of b2 = 8..10
     double uhi[2], ahi[2], bhi[2];
 #pragma unroll
@@ -931,16 +921,16 @@ __device__ __forceinline__ void pfa_stage_rader89(double2* X, const double2* tab
     __syncwarp();
     if (okE) {
       double2* Xr = X + eoff;
-      if (ar == 0) Xr[0] = make_double2(x0.x + s0r, x0.y + s0i);
+      // y_0: row 11 of the first product (the all-ones row) is sum_a s'_a
+      if (ar == 3) Xr[0] = make_double2(x0.x + y0[1][0], x0.y + y0[1][1]);
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
-        const int b2 = hh * 8 + ar;
         if (hh == 1 && ar >= 3) continue;
-        // per component c (0 = re, 1 = im of the butterfly)
+        // per component c (0 = re, 1 = im of the butterfly); x0 rides on Y0
         double Aq[4][2], Bq[4][2];
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-          const double Y0 = y0[hh][c], Y2 = y2[hh][c];
+          const double Y0 = y0[hh][c] + (c ? x0.y : x0.x), Y2 = y2[hh][c];
           const double Yr = hh ? yu[2][c] : yu[0][c], Yi = hh ? uhi[c] : yu[1][c];
           const double ZAr = hh ? za[2][c] : za[0][c], ZAi = hh ? ahi[c] : za[1][c];
           const double ZBr = hh ? zb[2][c] : zb[0][c], ZBi = hh ? bhi[c] : zb[1][c];
@@ -953,17 +943,14 @@ __device__ __forceinline__ void pfa_stage_rader89(double2* X, const double2* tab
           Bq[2][c] = ZAi - ZBi;
           Bq[3][c] = ((ZAi - ZAr) + (ZBr + ZBi)) * s2;
         }
+        double2* Xo = Xr + 1 + 2 * (hh * 8 + ar);
 #pragma unroll
         for (int b1 = 0; b1 < 4; ++b1) {
-          const int b = (33 * b1 + 12 * b2) % 44;
-          const double sg = ((b >> 2) & 1) ? -1.0 : 1.0;
-          const int r = RT[b];
-          const double Ar = x0.x + Aq[b1][0], Ai = x0.y + Aq[b1][1];
-          const double Br = sg * Bq[b1][0], Bi = sg * Bq[b1][1];
+          const int t = r89_out_slot(b1, 0);
           // DIR i B
-          const double iBr = DIR < 0 ? Bi : -Bi, iBi = DIR < 0 ? -Br : Br;
-          Xr[r * step] = make_double2(Ar + iBr, Ai + iBi);
-          Xr[(p - r) * step] = make_double2(Ar - iBr, Ai - iBi);
+          const double iBr = DIR < 0 ? Bq[b1][1] : -Bq[b1][1], iBi = DIR < 0 ? -Bq[b1][0] : Bq[b1][0];
+          Xo[t] = make_double2(Aq[b1][0] + iBr, Aq[b1][1] + iBi);
+          Xo[t + 44] = make_double2(Aq[b1][0] - iBr, Aq[b1][1] - iBi);
         }
       }
     }

@@ -1,0 +1,82 @@
+"""Host-side check of the prime-factor engine's position maps (csrc/pfa.cu).
+
+The K-point DFT engine keeps a row in shared memory as the array
+x[n_0]..[n_{D-1}] of the Ruritanian input map and reads the result through
+the CRT output map; for K = 2047 the 89 elements of the innermost dimension
+are additionally stored in the order the Rader radix-89 stage wants
+(pfa.cuh, pfa_stage_rader89).  Every kernel goes through the two 16-bit maps,
+so they alone carry the permutations.  This test emulates the stages with
+numpy on the maps the library builds (no GPU) and compares with numpy.fft:
+replaces part of the reference's scipy.fft calls (so3.py:185-211)."""
+import ctypes
+
+import numpy as np
+import pytest
+
+from paper_1511_05578_b200 import _cabi
+
+FACTORS = {15: (3, 5), 63: (7, 9), 255: (3, 5, 17), 511: (7, 73), 1023: (3, 11, 31), 2047: (23, 89),
+           4095: (5, 7, 9, 13)}
+
+
+def _maps(K):
+    lib = _cabi.load_library()
+    out = (ctypes.c_int * K)()
+    inn = (ctypes.c_int * K)()
+    assert lib.scv_debug_pfa_maps(K, out, inn) == 0
+    return np.array(out), np.array(inn)
+
+
+def _sigma():
+    lib = _cabi.load_library()
+    a = (ctypes.c_int * 89)()
+    b = (ctypes.c_int * 89)()
+    assert lib.scv_debug_r89_sigma(a, b) == 0
+    return np.array(a), np.array(b)
+
+
+@pytest.mark.parametrize("K", sorted(FACTORS))
+def test_maps_reproduce_the_dft(K):
+    out, inn = _maps(K)
+    assert sorted(out) == list(range(K)) and sorted(inn) == list(range(K))
+    f = FACTORS[K]
+    rng = np.random.default_rng(K)
+    x = rng.standard_normal(K) + 1j * rng.standard_normal(K)
+    X = np.empty(K, complex)
+    X[inn] = x
+    A = X.reshape(f)
+    sin, sout = _sigma()
+    for ax, p in enumerate(f):
+        if p == 89 and K == 2047:
+            # stage reads element j at sigma_in(j), writes y_k at sigma_out(k)
+            A = np.take(A, sin, axis=ax)
+            A = np.fft.fft(A, axis=ax)
+            B = np.empty_like(A)
+            idx = [slice(None)] * A.ndim
+            idx[ax] = sout
+            B[tuple(idx)] = A
+            A = B
+        else:
+            A = np.fft.fft(A, axis=ax)
+    y = A.reshape(K)[out]
+    assert np.max(np.abs(y - np.fft.fft(x))) <= 1e-11 * np.max(np.abs(y))
+
+
+def test_rader_storage_order_is_linear_in_the_lane_coordinates():
+    """sigma_in / sigma_out are what the stage's compile-time offsets assume
+    (pfa.cuh): pair a = (33 a1 + 12 a2) mod 44 at 1 + 11 a1 + a2 and 44 further,
+    outputs at 1 + 2 b2 + (b1 & 1) + 22 (b1 >> 1) and 44 further, the member with
+    the + wrap sign first."""
+    sin, sout = _sigma()
+    assert sorted(sin) == list(range(89)) and sorted(sout) == list(range(89))
+    assert sin[0] == 0 and sout[0] == 0
+    r = 1
+    for a in range(44):
+        neg = (a >> 2) & 1
+        u, v = (89 - r, r) if neg else (r, 89 - r)
+        a1, a2 = a % 4, a % 11
+        assert (33 * a1 + 12 * a2) % 44 == a
+        assert sin[u] == 1 + 11 * a1 + a2 and sin[v] == 45 + 11 * a1 + a2
+        t = 2 * a2 + (a1 & 1) + 22 * (a1 >> 1)
+        assert sout[u] == 1 + t and sout[v] == 45 + t
+        r = (r * 3) % 89

@@ -552,6 +552,162 @@ __global__ void __launch_bounds__(PfaGrpCfg<K>::NG * PfaGrpCfg<K>::NTG, 1)
 }
 
 // ---------------------------------------------------------------------------
+// batched rows, pipelined variant (r02): the transform groups of k_pfa_rows_g
+// never touch global memory.  The CTA has NG transform groups of NTG threads,
+// NIO load/store warps and a ring of NB > NG row buffers.  Step i of the CTA's
+// row sequence uses buffer i % NB and transform group i % NG; load/store warp
+// i % NIO first writes out the row that was transformed in that buffer NB
+// steps earlier, then streams row i in with cp.async.  Two mbarriers per
+// buffer order the hand-overs: `full` (32 cp.async-completion arrivals of the
+// loading warp -> the transform group) and `done` (one arrival after the
+// group's last stage barrier -> the storing warp).  A dependency of step i
+// always points to a smaller step and every warp walks its steps in order, so
+// the ring cannot deadlock.  With NB - NG rows in flight beyond the ones being
+// transformed, the DRAM latency of a row's load and the issue slots of the
+// permuted copies no longer sit on the transform warps' critical path
+// (k_pfa_rows_g measured 2.96 ms per 131008 rows with, 2.03 ms without its
+// global traffic, profiles/r02c_rows_stage_experiments.txt).
+// GATHER = 0 / 1 / 2 as in k_pfa_rows_g (the real-signal modes stay there).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  const unsigned a = smem_u32(bar);
+  unsigned ok;
+  do {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+// arrive on `bar` once all cp.async of this thread issued so far have landed
+__device__ __forceinline__ void cp_async_mbar_arrive(unsigned long long* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void cp_async16_m(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+
+#ifndef SCV_ROWSP
+#define SCV_ROWSP 1
+#endif
+#ifndef SCV_ROWSP_NG
+#define SCV_ROWSP_NG 4
+#endif
+#ifndef SCV_ROWSP_NIO
+#define SCV_ROWSP_NIO 2
+#endif
+#ifndef SCV_ROWSP_NB
+#define SCV_ROWSP_NB 6
+#endif
+template <int K> struct PfaPipeCfg { static constexpr int NG = 0, NTG = 96, NIO = 0, NB = 0; };
+template <> struct PfaPipeCfg<2047> {
+  static constexpr int NG = SCV_ROWSP ? SCV_ROWSP_NG : 0, NTG = 96, NIO = SCV_ROWSP_NIO, NB = SCV_ROWSP_NB;
+};
+template <int K>
+static constexpr size_t pfa_smem_pipe() {
+  using PL = PfaPlan<K>;
+  return ((size_t)pfa_tab_total<PL>() + (size_t)PfaPipeCfg<K>::NB * K) * sizeof(double2) +
+         2 * (size_t)PfaPipeCfg<K>::NB * sizeof(unsigned long long);
+}
+
+template <int K, int DIR, int GATHER>
+__global__ void __launch_bounds__(PfaPipeCfg<K>::NG * PfaPipeCfg<K>::NTG + PfaPipeCfg<K>::NIO * 32, 1)
+    k_pfa_rows_p(long long nrows, const double2* in, double2* out, const double2* __restrict__ gtab,
+                 long long LK = 0, int b0 = 0) {
+  using PL = PfaPlan<K>;
+  constexpr int NG = PfaPipeCfg<K>::NG, NTG = PfaPipeCfg<K>::NTG, NIO = PfaPipeCfg<K>::NIO, NB = PfaPipeCfg<K>::NB;
+  constexpr int NT = NG * NTG + NIO * 32;
+  static_assert(NB > NG, "the ring needs spare buffers for the rows in flight");
+  extern __shared__ double2 sm[];
+  double2* tab = sm;
+  double2* const bufs = sm + pfa_tab_total<PL>();
+  unsigned long long* const full = (unsigned long long*)(bufs + (size_t)NB * K);
+  unsigned long long* const done = full + NB;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(full + b, 32);
+      mbar_init(done + b, 1);
+    }
+  }
+  pfa_load_tables<PL, NT>(tab, gtab);  // ends with __syncthreads: the barriers are initialised for everyone
+  // the CTA's row sequence: round q covers NG adjacent rows (adjacent rows of
+  // the GATHER = 2 scratch share 128-byte lines), i -> (q = i / NG, slot i % NG)
+  const long long G = gridDim.x;
+  const long long rem = nrows - (long long)blockIdx.x * NG;
+  if (rem <= 0) return;
+  const long long qmax = (rem - 1) / (G * NG);
+  const long long tail = rem - qmax * G * NG;
+  const long long ni = qmax * NG + (tail < NG ? tail : NG);
+  auto row_of = [&](long long i) { return (i / NG) * (G * NG) + (long long)blockIdx.x * NG + (i % NG); };
+  if (threadIdx.x >= NG * NTG) {
+    // ---- load / store warps
+    const int w = (threadIdx.x - NG * NTG) >> 5, lane = threadIdx.x & 31;
+#pragma unroll 1
+    for (long long i = w; i < ni + NB; i += NIO) {
+      const int b = (int)(i % NB);
+      const unsigned u = (unsigned)(i / NB);
+      double2* const X = bufs + (size_t)b * K;
+      if (i >= NB) {
+        // row i - NB was transformed in this buffer: write it out
+        mbar_wait(done + b, (u - 1) & 1);
+        const long long r = row_of(i - NB);
+        double2* dst = out + r * K;
+        if constexpr (GATHER == 2) {
+          const long long bb = r / K, g = r - bb * K;
+          dst = out + (g * LK + b0 + bb) * K;
+        }
+#pragma unroll 8
+        for (int k = lane; k < K; k += 32) dst[k] = X[pfa_pos_tab<PL>(tab, k)];
+        __syncwarp();  // every lane has read its elements before any lane refills the buffer
+      }
+      if (i < ni) {
+        const long long r = row_of(i);
+        if constexpr (GATHER == 2) {
+          constexpr int NPR = (K + 1) / 2;
+          const long long bb = r / K, g = r - bb * K;
+          const double2* src = in + (bb * NPR * K + g) * 2;  // + (m/2)*2K + (m&1)
+#pragma unroll 8
+          for (int n = lane; n < K; n += 32)
+            cp_async16_m(X + pfa_in_tab<PL>(tab, n), src + (long long)(n >> 1) * (2 * K) + (n & 1));
+        } else {
+          const double2* src = in + r * K;
+          if constexpr (GATHER == 1) {
+            const long long bb = r / K, g = r - bb * K;
+            src = in + g * LK + (b0 + bb) * K;
+          }
+#pragma unroll 8
+          for (int n = lane; n < K; n += 32) cp_async16_m(X + pfa_in_tab<PL>(tab, n), src + n);
+        }
+        cp_async_mbar_arrive(full + b);
+      }
+    }
+    return;
+  }
+  // ---- transform groups
+  const int g = threadIdx.x / NTG, gtid = threadIdx.x - g * NTG, bar = 1 + g;
+#pragma unroll 1
+  for (long long i = g; i < ni; i += NG) {
+    const int b = (int)(i % NB);
+    const unsigned u = (unsigned)(i / NB);
+    mbar_wait(full + b, u & 1);
+    pfa_dft<PL, DIR, 1, NTG, K>(bufs + (size_t)b * K, tab, nullptr, gtid, bar);
+    if (gtid == 0) mbar_arrive(done + b);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // analysis alpha: generate + inverse DFT over m, R rows (gi, b) per batch
 // ---------------------------------------------------------------------------
 template <int K>
@@ -1698,6 +1854,20 @@ static int persistent_grid(scv_ctx* c, Kern k, int nt, size_t sm, long long nbat
 }
 
 // Position of output frequency k / input sample n in the D-dimensional
+template <int K, int DIR, int GATHER>
+static int launch_rows_p(scv_ctx* c, long long nrows, const double2* in, double2* out, const double2* tab, long long LK,
+                         int b0, cudaStream_t s) {
+  constexpr size_t smp = pfa_smem_pipe<K>();
+  static_assert(smp <= 232448, "pipelined rows launch shape exceeds the 227 KB shared-memory limit");
+  constexpr int NTB = PfaPipeCfg<K>::NG * PfaPipeCfg<K>::NTG + PfaPipeCfg<K>::NIO * 32;
+  int grid;
+  SCV_TRY(persistent_grid(c, k_pfa_rows_p<K, DIR, GATHER>, NTB, smp, (nrows + PfaPipeCfg<K>::NG - 1) / PfaPipeCfg<K>::NG, &grid));
+  k_pfa_rows_p<K, DIR, GATHER><<<grid, NTB, smp, s>>>(nrows, in, out, tab, LK, b0);
+  c->launches++;
+  SCV_CUDA(c, cudaGetLastError());
+  return SCV_OK;
+}
+
 // shared-memory layout (pfa.cuh, pfa_st): dimension s has stride st_s =
 // p_{s+1}...p_{D-1}; output k sits at sum_s (k mod p_s) st_s, input n at
 // sum_s (n * inv_s mod p_s) st_s with inv_s = (K/p_s)^{-1} mod p_s (Ruritanian map).
@@ -1789,6 +1959,7 @@ template <int K, int DIR>
 static int run_rows(scv_ctx* c, long long nrows, const double2* in, double2* out, cudaStream_t s) {
   const double2* tab;
   SCV_TRY(scv_pfa_tables(c, K, &tab));
+  if constexpr (PfaPipeCfg<K>::NG > 0) return launch_rows_p<K, DIR, 0>(c, nrows, in, out, tab, 0, 0, s);
   if constexpr (PfaGrpCfg<K>::NG > 0) {
     constexpr size_t smg = pfa_smem_grp<K>();
     static_assert(smg <= 232448, "grouped rows launch shape exceeds the 227 KB shared-memory limit");
@@ -1953,6 +2124,8 @@ static int run_syn_alpha(scv_ctx* c, int real, int tr, const void* in, int lsig,
       constexpr size_t smg = pfa_smem_grp<K>();
       constexpr int NTB = PfaGrpCfg<K>::NG * PfaGrpCfg<K>::NTG;
       const long long nrows = (long long)K * nbb;
+      if constexpr (PfaPipeCfg<K>::NG > 0)
+        return launch_rows_p<K, -1, 1>(c, nrows, (const double2*)in, chunk, tab, (long long)lsig * K, b0, s);
       int grid;
       SCV_TRY(persistent_grid(c, k_pfa_rows_g<K, -1, 1>, NTB, smg, (nrows + PfaGrpCfg<K>::NG - 1) / PfaGrpCfg<K>::NG, &grid));
       k_pfa_rows_g<K, -1, 1><<<grid, NTB, smg, s>>>(nrows, (const double2*)in, chunk, tab, (long long)lsig * K, b0);
@@ -2080,6 +2253,10 @@ int scv_pfa_ana_blocked(scv_ctx* c, int K, const double2* w, const double* hlb, 
     }
     SCV_PROF(c, s, "so3inv_rows");
     const long long nrows = (long long)nbb * KK;
+    if constexpr (PfaPipeCfg<KK>::NG > 0) {
+      SCV_TRY((launch_rows_p<KK, +1, 2>(c, nrows, (const double2*)T, sig, tab, (long long)nb, bs0, s)));
+      continue;
+    }
     int grid;
     SCV_TRY(persistent_grid(c, k_pfa_rows_g<KK, +1, 2>, NTB, smg, (nrows + PfaGrpCfg<KK>::NG - 1) / PfaGrpCfg<KK>::NG, &grid));
     k_pfa_rows_g<KK, +1, 2><<<grid, NTB, smg, s>>>(nrows, (const double2*)T, sig, tab, (long long)nb, bs0);

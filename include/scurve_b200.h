@@ -116,6 +116,13 @@ int scv_debug_dft(scv_ctx* ctx, int K, int dir, int nrows, const double* in, dou
  * emulate the stages on these maps against numpy.fft (tests/test_pfa_maps.py). */
 int scv_debug_pfa_maps(int K, int* out_pos, int* in_pos);
 int scv_debug_r89_sigma(int* sigma_in, int* sigma_out);
+/* Pipeline timing counters of the ring kernels (only counted in builds with
+ * -DSCV_PIPE_STATS=1, zeros otherwise): 36 clock-cycle sums (kinds 3 and 4 are
+ * sub-phases of the generator / quadrature teams), kernel kind
+ * (rows, column generation, gamma+quadrature) * 6 + {transform groups waiting
+ * for a full slot, transforming; load/store warps waiting for a transform,
+ * draining, filling; unused}.  reset != 0 clears them. */
+int scv_debug_pipe_stats(unsigned long long* out36, int reset);
 
 /* Delta^l_{m'm}(pi/2) for l < L in the 1/8 symmetry wedge 0 <= m <= m' <= l:
  * element (l, m', m) at l(l+1)(l+2)/6 + m'(m'+1)/2 + m.  Copies the context's

@@ -48,6 +48,7 @@ _SIGS = {
     "scv_debug_dft": [_P, _I, _I, _I, _P, _P, _P],
     "scv_debug_pfa_maps": [_I, _P, _P],
     "scv_debug_r89_sigma": [_P, _P],
+    "scv_debug_pipe_stats": [_P, _I],
     "scv_halfpi_wedge": [_P, _I, _P, _P],
     "scv_sht_forward": [_P, _I, _I, _I, _P, _P, _P],
     "scv_sht_inverse": [_P, _I, _I, _I, _P, _P, _P],

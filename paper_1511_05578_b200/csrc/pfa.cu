@@ -576,6 +576,11 @@ __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned coun
 __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
+// suspend-time hint of a waiting thread (ns): a short hint makes the waiters
+// poll, and their polling shows up as a quarter of all executed instructions
+#ifndef SCV_MBAR_SUSPEND_NS
+#define SCV_MBAR_SUSPEND_NS 20000
+#endif
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
   const unsigned a = smem_u32(bar);
   unsigned ok;
@@ -583,11 +588,11 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
         "selp.u32 %0, 1, 0, p;\n"
         "}\n"
         : "=r"(ok)
-        : "r"(a), "r"(parity)
+        : "r"(a), "r"(parity), "r"(SCV_MBAR_SUSPEND_NS)
         : "memory");
   } while (!ok);
 }
@@ -597,6 +602,92 @@ __device__ __forceinline__ void cp_async_mbar_arrive(unsigned long long* bar) {
 }
 __device__ __forceinline__ void cp_async16_m(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+// Ring-slot copies of the load/store warps, in batches of RB elements per lane:
+// all position-map reads of a batch first, then the data moves.  (The copies
+// are asm volatile / cross address spaces the compiler cannot disambiguate, so
+// an element-at-a-time loop serialises map read -> copy -> next map read.)
+constexpr int RB = 8;
+// slot X (Ruritanian positions) <- element n of a row at gsrc(n), n = lane0 + nl*j < K
+template <class PL, class SrcFn>
+__device__ __forceinline__ void ring_fill(double2* X, const double2* tab, int lane0, int nl, SrcFn gsrc) {
+  constexpr int K = PL::K;
+#pragma unroll 1
+  for (int n0 = lane0; n0 < K; n0 += nl * RB) {
+    int pos[RB];
+#pragma unroll
+    for (int j = 0; j < RB; ++j) {
+      const int n = n0 + nl * j;
+      pos[j] = n < K ? pfa_in_tab<PL>(tab, n) : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < RB; ++j) {
+      const int n = n0 + nl * j;
+      if (n < K) cp_async16_m(X + pos[j], gsrc(n));
+    }
+  }
+}
+// output frequency k of slot X -> gdst(k), k = lane0 + nl*j < K
+template <class PL, class DstFn>
+__device__ __forceinline__ void ring_drain(const double2* X, const double2* tab, int lane0, int nl, DstFn gdst) {
+  constexpr int K = PL::K;
+#pragma unroll 1
+  for (int k0 = lane0; k0 < K; k0 += nl * RB) {
+    int pos[RB];
+    double2 v[RB];
+#pragma unroll
+    for (int j = 0; j < RB; ++j) {
+      const int k = k0 + nl * j;
+      pos[j] = k < K ? pfa_pos_tab<PL>(tab, k) : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < RB; ++j) v[j] = X[pos[j]];
+#pragma unroll
+    for (int j = 0; j < RB; ++j) {
+      const int k = k0 + nl * j;
+      if (k < K) *gdst(k) = v[j];
+    }
+  }
+}
+
+// Pipeline timing counters (debug builds, -DSCV_PIPE_STATS=1): clock64 sums per
+// role, [kernel kind * 6 + {0 transform wait-full, 1 transform, 2 io wait-done,
+// 3 io drain, 4 io fill, 5 CTA lifetime}]; read with scv_debug_pipe_stats.
+#ifndef SCV_PIPE_STATS
+#define SCV_PIPE_STATS 0
+#endif
+__device__ unsigned long long g_pipe_stats[36];
+__device__ __forceinline__ long long pipe_now() {
+#if defined(__CUDA_ARCH__) && SCV_PIPE_STATS
+  return clock64();
+#else
+  return 0;
+#endif
+}
+struct PipeClk {
+  long long t;
+  __device__ __forceinline__ PipeClk() : t(pipe_now()) {}
+  // add the time since the last mark to counter `idx` (kept in `acc`)
+  __device__ __forceinline__ void mark(long long (&acc)[6], int idx) {
+    if (SCV_PIPE_STATS) {
+      const long long n = pipe_now();
+      acc[idx] += n - t;
+      t = n;
+    }
+  }
+};
+__device__ __forceinline__ void pipe_flush(const long long (&acc)[6], int kind, bool leader) {
+  if (SCV_PIPE_STATS && leader)
+    for (int i = 0; i < 6; ++i)
+      if (acc[i]) atomicAdd(&g_pipe_stats[kind * 6 + i], (unsigned long long)acc[i]);
+}
+extern "C" int scv_debug_pipe_stats(unsigned long long* out, int reset) {
+  if (out && cudaMemcpyFromSymbol(out, g_pipe_stats, sizeof(g_pipe_stats)) != cudaSuccess) return SCV_ECUDA;
+  if (reset) {
+    unsigned long long z[36] = {0};
+    if (cudaMemcpyToSymbol(g_pipe_stats, z, sizeof(z)) != cudaSuccess) return SCV_ECUDA;
+  }
+  return SCV_OK;
 }
 
 #ifndef SCV_ROWSP
@@ -612,14 +703,17 @@ __device__ __forceinline__ void cp_async16_m(void* smem, const void* gmem) {
 #define SCV_ROWSP_NB 6
 #endif
 template <int K> struct PfaPipeCfg { static constexpr int NG = 0, NTG = 96, NIO = 0, NB = 0; };
+#ifndef SCV_ROWSP_NTG
+#define SCV_ROWSP_NTG 96
+#endif
 template <> struct PfaPipeCfg<2047> {
-  static constexpr int NG = SCV_ROWSP ? SCV_ROWSP_NG : 0, NTG = 96, NIO = SCV_ROWSP_NIO, NB = SCV_ROWSP_NB;
+  static constexpr int NG = SCV_ROWSP ? SCV_ROWSP_NG : 0, NTG = SCV_ROWSP_NTG, NIO = SCV_ROWSP_NIO, NB = SCV_ROWSP_NB;
 };
 template <int K>
 static constexpr size_t pfa_smem_pipe() {
   using PL = PfaPlan<K>;
   return ((size_t)pfa_tab_total<PL>() + (size_t)PfaPipeCfg<K>::NB * K) * sizeof(double2) +
-         2 * (size_t)PfaPipeCfg<K>::NB * sizeof(unsigned long long);
+         4 * (size_t)PfaPipeCfg<K>::NB * sizeof(unsigned long long);
 }
 
 template <int K, int DIR, int GATHER>
@@ -630,13 +724,18 @@ __global__ void __launch_bounds__(PfaPipeCfg<K>::NG * PfaPipeCfg<K>::NTG + PfaPi
   constexpr int NG = PfaPipeCfg<K>::NG, NTG = PfaPipeCfg<K>::NTG, NIO = PfaPipeCfg<K>::NIO, NB = PfaPipeCfg<K>::NB;
   constexpr int NT = NG * NTG + NIO * 32;
   static_assert(NB > NG, "the ring needs spare buffers for the rows in flight");
+  static_assert(NB % NIO == 0, "a load/store warp owns fixed ring slots (it then meets a slot's barrier phases in order)");
   extern __shared__ double2 sm[];
   double2* tab = sm;
   double2* const bufs = sm + pfa_tab_total<PL>();
+  // two barriers per slot and kind, used by alternate laps (use u of a slot ->
+  // barrier u & 1, parity (u >> 1) & 1): an mbarrier parity wait cannot tell the
+  // phase it wants from the one two phases earlier, and a transform group that
+  // rotates over the slots can be one use ahead of a slot's producer
   unsigned long long* const full = (unsigned long long*)(bufs + (size_t)NB * K);
-  unsigned long long* const done = full + NB;
+  unsigned long long* const done = full + 2 * NB;
   if (threadIdx.x == 0) {
-    for (int b = 0; b < NB; ++b) {
+    for (int b = 0; b < 2 * NB; ++b) {
       mbar_init(full + b, 32);
       mbar_init(done + b, 1);
     }
@@ -654,23 +753,27 @@ __global__ void __launch_bounds__(PfaPipeCfg<K>::NG * PfaPipeCfg<K>::NTG + PfaPi
   if (threadIdx.x >= NG * NTG) {
     // ---- load / store warps
     const int w = (threadIdx.x - NG * NTG) >> 5, lane = threadIdx.x & 31;
+    long long st[6] = {0, 0, 0, 0, 0, 0};
+    PipeClk ck;
 #pragma unroll 1
     for (long long i = w; i < ni + NB; i += NIO) {
       const int b = (int)(i % NB);
       const unsigned u = (unsigned)(i / NB);
       double2* const X = bufs + (size_t)b * K;
+      ck.mark(st, 4);
       if (i >= NB) {
         // row i - NB was transformed in this buffer: write it out
-        mbar_wait(done + b, (u - 1) & 1);
+        mbar_wait(done + ((u - 1) & 1) * NB + b, ((u - 1) >> 1) & 1);
+        ck.mark(st, 2);
         const long long r = row_of(i - NB);
         double2* dst = out + r * K;
         if constexpr (GATHER == 2) {
           const long long bb = r / K, g = r - bb * K;
           dst = out + (g * LK + b0 + bb) * K;
         }
-#pragma unroll 8
-        for (int k = lane; k < K; k += 32) dst[k] = X[pfa_pos_tab<PL>(tab, k)];
+        ring_drain<PL>(X, tab, lane, 32, [&](int k) { return dst + k; });
         __syncwarp();  // every lane has read its elements before any lane refills the buffer
+        ck.mark(st, 3);
       }
       if (i < ni) {
         const long long r = row_of(i);
@@ -678,33 +781,37 @@ __global__ void __launch_bounds__(PfaPipeCfg<K>::NG * PfaPipeCfg<K>::NTG + PfaPi
           constexpr int NPR = (K + 1) / 2;
           const long long bb = r / K, g = r - bb * K;
           const double2* src = in + (bb * NPR * K + g) * 2;  // + (m/2)*2K + (m&1)
-#pragma unroll 8
-          for (int n = lane; n < K; n += 32)
-            cp_async16_m(X + pfa_in_tab<PL>(tab, n), src + (long long)(n >> 1) * (2 * K) + (n & 1));
+          ring_fill<PL>(X, tab, lane, 32, [&](int n) { return src + (long long)(n >> 1) * (2 * K) + (n & 1); });
         } else {
           const double2* src = in + r * K;
           if constexpr (GATHER == 1) {
             const long long bb = r / K, g = r - bb * K;
             src = in + g * LK + (b0 + bb) * K;
           }
-#pragma unroll 8
-          for (int n = lane; n < K; n += 32) cp_async16_m(X + pfa_in_tab<PL>(tab, n), src + n);
+          ring_fill<PL>(X, tab, lane, 32, [&](int n) { return src + n; });
         }
-        cp_async_mbar_arrive(full + b);
+        cp_async_mbar_arrive(full + (u & 1) * NB + b);
       }
     }
+    ck.mark(st, 4);
+    pipe_flush(st, 0, lane == 0);
     return;
   }
   // ---- transform groups
   const int g = threadIdx.x / NTG, gtid = threadIdx.x - g * NTG, bar = 1 + g;
+  long long st[6] = {0, 0, 0, 0, 0, 0};
+  PipeClk ck;
 #pragma unroll 1
   for (long long i = g; i < ni; i += NG) {
     const int b = (int)(i % NB);
     const unsigned u = (unsigned)(i / NB);
-    mbar_wait(full + b, u & 1);
+    mbar_wait(full + (u & 1) * NB + b, (u >> 1) & 1);
+    ck.mark(st, 0);
     pfa_dft<PL, DIR, 1, NTG, K>(bufs + (size_t)b * K, tab, nullptr, gtid, bar);
-    if (gtid == 0) mbar_arrive(done + b);
+    if (gtid == 0) mbar_arrive(done + (u & 1) * NB + b);
+    ck.mark(st, 1);
   }
+  pipe_flush(st, 0, gtid == 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -1073,6 +1180,226 @@ __global__ void __launch_bounds__(PfaSCfg<K>::NT, PfaSCfg<K>::MINB)
     }
     __syncthreads();
   }
+}
+
+// ---------------------------------------------------------------------------
+// Pipelined column generation (r02, K = 2047): the analysis gamma pass on the
+// ring of k_pfa_rows_p.  A step is one column pair (m0, m0+1) of one beta row;
+// its two columns sit in ring slots 2(i%3), 2(i%3)+1 and are transformed by the
+// groups (2i + r) % 4.  Generator / store warp i % NIO first writes out the
+// pair transformed in those slots three steps earlier (T[bs][m0/2][g][r], 512
+// contiguous bytes per warp store), then generates pair i.
+//
+// Generation without a per-entry exp.  For a column m the entries of degree l
+// (n = +l and n = -l) are C+-[l] D+-_b[l] with
+//   C+[l] = (2l+1)/(8 pi^2) W_{m,+l},  C-[l] = (2l+1)/(8 pi^2) (-1)^{l-m} W_{m,-l}
+//   D+_b[l] = d^l_{m,l}(beta_b) = exp(h[l,|m|] + (l-m) ls_b + (l+m) lc_b),  D- with m -> -m
+// (wigner.py:304-322; h = log sqrt C(2l, l+|m|), ls/lc = log sin/cos(beta_b/2)).
+// Along l at fixed (m, b), D+-[l+32] = D+-[l] * rho32[|m|][l] * sig32[b] with
+//   rho32[a][l] = exp(h[l+32,a] - h[l,a]),  sig32[b] = (sin cos (beta_b/2))^32,
+// both built on the host in long double.  Lane j owns the degrees l = j + 32 t:
+// one exp per sign at its first degree >= |m|, then two multiplies per entry,
+// with coalesced reads of the transposed coefficients CT[m][slot] (k_colgen_ct)
+// and of rho32.  D is unimodal in l and |D| <= 1; where its peak matters the
+// start value is >= e^-150 (cos^2(beta/2) = (1 + m/l*)/2 at the peak l*), so
+// the multiplicative walk never has to recover from an underflow, and 31 steps
+// add < 1e-14 of rounding.
+// ---------------------------------------------------------------------------
+#ifndef SCV_COLGENP
+#define SCV_COLGENP 1
+#endif
+#ifndef SCV_CGP_NG
+#define SCV_CGP_NG 4
+#endif
+template <int K> struct PfaCgpCfg { static constexpr int NG = SCV_CGP_NG, NTG = 384 / SCV_CGP_NG, NIO = 4, NB = 6; };
+template <int K>
+static constexpr size_t pfa_smem_cgp() {
+  using PL = PfaPlan<K>;
+  return ((size_t)pfa_tab_total<PL>() + (size_t)PfaCgpCfg<K>::NB * K) * sizeof(double2) +
+         4 * (size_t)PfaCgpCfg<K>::NB * sizeof(unsigned long long);
+}
+
+// CT[mc][gi] = C+-[l] F(l)/F(l*) of column mc (m = mc or mc - K) at gamma slot gi
+// (n = gi or gi - K), 0 where |m| > l; F(l) = sqrt(C(2l, l+|m|)) / 2^l and l* is the
+// first degree >= |m| in l's residue class mod 32 (the generator lane's start)
+__global__ void k_colgen_ct(int L, const double2* __restrict__ w, const double* __restrict__ hlb,
+                            double2* __restrict__ ct) {
+  const int K = 2 * L - 1;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)K * K) return;
+  const int mc = (int)(i / K), gi = (int)(i - (long long)mc * K);
+  const int m = mc <= L - 1 ? mc : mc - K, am = m < 0 ? -m : m;
+  const int n = gi <= L - 1 ? gi : gi - K, l = n < 0 ? -n : n;
+  double2 v = make_double2(0.0, 0.0);
+  if (am <= l) {
+    const double2 c = w[((long long)(n >= 0 ? 0 : 1) * L + l) * K + (L - 1) + m];
+    double f = (double)(2 * l + 1) * (1.0 / (8.0 * SCV_PI * SCV_PI));
+    if (n < 0 && ((l - m) & 1)) f = -f;
+    const int lst = am + ((l - am) & 31);
+    if (l != lst) {
+      // log F(l) - log F(l*), with ln 2 split so that (l - l*) ln2_hi is exact
+      const double t = (double)(l - lst);
+      double x = hlb[(long long)l * (l + 1) / 2 + am] - hlb[(long long)lst * (lst + 1) / 2 + am];
+      x = fma(-t, 6.93147180369123816490e-01, x);
+      x = fma(-t, 1.90821492927058770002e-10, x);
+      f *= exp(x);
+    }
+    v = make_double2(f * c.x, f * c.y);
+  }
+  ct[i] = v;
+}
+
+template <int K>
+__global__ void __launch_bounds__(PfaCgpCfg<K>::NG * PfaCgpCfg<K>::NTG + PfaCgpCfg<K>::NIO * 32, 1)
+    k_ana_colgen_p(const double2* __restrict__ ct, const double* __restrict__ hlb, const double* __restrict__ lsin,
+                   const double* __restrict__ lcos, const double* __restrict__ sig32, int b0, int nb,
+                   double2* __restrict__ out, const double2* __restrict__ gtab) {
+  using PL = PfaPlan<K>;
+  constexpr int NG = PfaCgpCfg<K>::NG, NTG = PfaCgpCfg<K>::NTG, NIO = PfaCgpCfg<K>::NIO, NB = PfaCgpCfg<K>::NB;
+  constexpr int NT = NG * NTG + NIO * 32, NQT = NIO * 32;
+  constexpr int L = (K + 1) / 2, NPR = (K + 1) / 2;
+  static_assert((NG == 4 || NG == 2) && NB == 6 && NIO == 4,
+                "pair steps use slots 2(i%3)+r and groups (2i+r)%NG; the team's warp s scales (column s>>1, sign s&1)");
+  constexpr int GB = 16;  // degrees per batch of a generator lane
+  static_assert(L % (32 * GB) == 0, "the generator walks l = lane + 32 t in batches of GB");
+  extern __shared__ double2 sm[];
+  double2* tab = sm;
+  double2* const bufs = sm + pfa_tab_total<PL>();
+  // barriers of alternate laps: see k_pfa_rows_p
+  unsigned long long* const full = (unsigned long long*)(bufs + (size_t)NB * K);
+  unsigned long long* const done = full + 2 * NB;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 2 * NB; ++b) {
+      mbar_init(full + b, 64);  // the two warps that scale a column
+      mbar_init(done + b, 1);
+    }
+  }
+  pfa_load_tables<PL, NT>(tab, gtab);
+  // the CTA's contiguous range of (pair, beta row) steps, flat index = pair * nb + bs
+  const long long S = (long long)NPR * nb;
+  const long long lo = S * blockIdx.x / gridDim.x, hi = S * (blockIdx.x + 1) / gridDim.x;
+  const long long ni = hi - lo;
+  if (threadIdx.x >= NG * NTG) {
+    // ---- generator / store team: all NIO warps work on every step, in order
+    // (a step's drain + fill latency sits on the ring's critical path: three slot
+    // pairs, two of them under transform)
+    const int t = threadIdx.x - NG * NTG, lane = t & 31, ws = t >> 5;
+    const int tbar = 1 + NG;
+    long long st[6] = {0, 0, 0, 0, 0, 0}, st2[6] = {0, 0, 0, 0, 0, 0};
+    PipeClk ck;
+#pragma unroll 1
+    for (long long i = 0; i < ni + 3; ++i) {
+      const int s0 = 2 * (int)(i % 3);
+      const unsigned u = (unsigned)(i / 3);
+      double2* const X0 = bufs + (size_t)s0 * K;
+      double2* const X1 = X0 + K;
+      ck.mark(st, 4);
+      if (i >= 3) {
+        // the pair of step i - 3 was transformed in these slots: write T[bs][pair][g][r]
+        mbar_wait(done + ((u - 1) & 1) * NB + s0, ((u - 1) >> 1) & 1);
+        mbar_wait(done + ((u - 1) & 1) * NB + s0 + 1, ((u - 1) >> 1) & 1);
+        ck.mark(st, 2);
+        const long long f = lo + i - 3;
+        const long long pr = f / nb, bs = f - pr * nb;
+        double2* dst = out + ((bs * NPR + pr) * K) * 2;
+        const int r = t & 1;
+        const double2* Xr = r ? X1 : X0;
+        ring_drain<PL>(Xr, tab, t >> 1, NQT / 2, [&](int g) { return dst + 2 * g + r; });
+        grp_sync(tbar, NQT);  // the whole team has read the pair before anyone refills it
+        ck.mark(st, 3);
+      }
+      if (i < ni) {
+        const long long f = lo + i;
+        const int pr = (int)(f / nb), bs = (int)(f - (long long)pr * nb);
+        const int b = b0 + bs;
+        // Warp ws generates (column ws >> 1, sign ws & 1), lane j the degrees l = j mod 32:
+        // entry l is CT[m][slot] * D_b[l*] sin(beta_b)^(l - l*), with D_b[l*] =
+        // d^{l*}_{m,+-l*}(beta_b) in closed form at the lane's first degree l* >= |m|
+        // (wigner.py:304-322) -- a geometric walk, no table reads.  Values go from
+        // registers straight to their Ruritanian positions (one 16-byte store each;
+        // CT's exact zeros below |m| overwrite the slot's previous contents).  Two
+        // batches of GB degrees: all coefficient loads of a batch are in flight at once.
+        const int r = ws >> 1, neg = ws & 1;
+        double2* const X = r ? X1 : X0;
+        const int mc = 2 * pr + r;
+        PipeClk ck2;
+        ck2.t = ck.t;
+        if (mc >= K) {  // the odd column past the end: zeros (transformed, never read)
+          for (int g = lane + 32 * neg; g < K; g += 64) X[g] = make_double2(0.0, 0.0);
+        } else {
+          const int m = mc <= L - 1 ? mc : mc - K, am = m < 0 ? -m : m;
+          const int lst = am + ((lane - am) & 31);
+          const double2* cp = ct + (long long)mc * K;
+          double2 c[GB];
+#pragma unroll
+          for (int k = 0; k < GB; ++k) {
+            const int l = lane + 32 * k;
+            c[k] = cp[neg ? (l ? K - l : 0) : l];
+          }
+          double d = 0.0;
+          if (lst < L) {
+            // n >= 0: sin^(l-m) cos^(l+m); n < 0: sin^(l+m) cos^(l-m).  xlogy semantics at the
+            // poles: a zero exponent drops its (possibly -inf) log
+            const int es = neg ? lst + m : lst - m, ec = neg ? lst - m : lst + m;
+            double lg = hlb[lst * (lst + 1) / 2 + am];
+            if (es) lg += (double)es * lsin[b];
+            if (ec) lg += (double)ec * lcos[b];
+            d = exp(lg);
+          }
+          const double S32 = sig32[b] * 4294967296.0;  // sin(beta_b)^32 = (2 sin cos (beta_b/2))^32
+          ck2.mark(st2, 1);  // loads issued + closed-form start
+#pragma unroll 1
+          for (int l0 = lane; l0 < L; l0 += 32 * GB) {
+            int pp[GB];
+#pragma unroll
+            for (int k = 0; k < GB; ++k) {
+              const int l = l0 + 32 * k;
+              pp[k] = pfa_in_tab<PL>(tab, neg ? (l ? K - l : 0) : l);
+            }
+#pragma unroll
+            for (int k = 0; k < GB; ++k) {
+              const int l = l0 + 32 * k;
+              if (l > lst) d *= S32;
+              c[k] = make_double2(d * c[k].x, d * c[k].y);  // d = 0 before l*, where CT is 0 too
+            }
+#pragma unroll
+            for (int k = 0; k < GB; ++k) {
+              const int l = l0 + 32 * k;
+              if (l > 0 || !neg) X[pp[k]] = c[k];
+            }
+            if (l0 + 32 * GB < L) {
+#pragma unroll
+              for (int k = 0; k < GB; ++k) {
+                const int l = l0 + 32 * (GB + k);
+                c[k] = cp[neg ? K - l : l];
+              }
+            }
+          }
+        }
+        ck2.mark(st2, 3);  // generation
+        mbar_arrive(full + (u & 1) * NB + s0 + r);
+      }
+    }
+    ck.mark(st, 4);
+    pipe_flush(st, 1, t == 0);
+    pipe_flush(st2, 3, t == 0);
+    return;
+  }
+  const int g = threadIdx.x / NTG, gtid = threadIdx.x - g * NTG, bar = 1 + g;
+  const int r = g & 1;
+  long long st[6] = {0, 0, 0, 0, 0, 0};
+  PipeClk ck;
+#pragma unroll 1
+  for (long long i = g >> 1; i < ni; i += NG / 2) {
+    const int slot = 2 * (int)(i % 3) + r;
+    const unsigned u = (unsigned)(i / 3);
+    mbar_wait(full + (u & 1) * NB + slot, (u >> 1) & 1);
+    ck.mark(st, 0);
+    pfa_dft<PL, +1, 1, NTG, K>(bufs + (size_t)slot * K, tab, nullptr, gtid, bar);
+    if (gtid == 0) mbar_arrive(done + (u & 1) * NB + slot);
+    ck.mark(st, 1);
+  }
+  pipe_flush(st, 1, gtid == 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -1820,6 +2147,179 @@ __global__ void __launch_bounds__(PfaQCfg<K>::NT, PfaQCfg<K>::MINB)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Pipelined gamma pass + beta quadrature (r02, K = 2047, chunk [bb][g][m]).
+// The ring and transform groups of k_pfa_rows_p; the load/store side is ONE team
+// of NQW warps that walks the CTA's (column, beta row) steps in order.  At step
+// i the team (1) prefetches the quadrature weights of the step whose transform
+// finishes next, (2) waits for that transform (step i - NB, same ring slot),
+// reads its outputs S_{nm}(b) through the position map and adds q_{nm}(b) S to
+// the column's accumulators, which live in the team's registers (NA = K/(32 NQW)
+// entries per thread) and are flushed into W after the chunk's last beta row,
+// (3) streams the column of step i into the slot with cp.async.  The transform
+// warps issue no global loads and hold no accumulators.  Columns are dealt
+// x, x + G, ... so CTAs x and x + 1 read the two halves of each 32-byte sector
+// at about the same time (the second is an L2 hit).
+// ---------------------------------------------------------------------------
+#ifndef SCV_GQP
+#define SCV_GQP 1
+#endif
+#ifndef SCV_GQP_NQW
+#define SCV_GQP_NQW 4
+#endif
+#ifndef SCV_GQP_NG
+#define SCV_GQP_NG 4
+#endif
+template <int K> struct PfaGqpCfg { static constexpr int NG = SCV_GQP_NG, NTG = 384 / SCV_GQP_NG, NQW = SCV_GQP_NQW, NB = 6; };
+template <int K>
+static constexpr size_t pfa_smem_gqp() {
+  using PL = PfaPlan<K>;
+  return ((size_t)pfa_tab_total<PL>() + (size_t)PfaGqpCfg<K>::NB * K) * sizeof(double2) +
+         4 * (size_t)PfaGqpCfg<K>::NB * sizeof(unsigned long long);
+}
+
+template <int K>
+__global__ void __launch_bounds__(PfaGqpCfg<K>::NG * PfaGqpCfg<K>::NTG + PfaGqpCfg<K>::NQW * 32, 1)
+    k_syn_gamma_qp(int real, const double2* __restrict__ chunk, int b0, int nbb, const double* __restrict__ qtab,
+                   double2* __restrict__ wout, const double2* __restrict__ gtab) {
+  using PL = PfaPlan<K>;
+  constexpr int NG = PfaGqpCfg<K>::NG, NTG = PfaGqpCfg<K>::NTG, NQW = PfaGqpCfg<K>::NQW, NB = PfaGqpCfg<K>::NB;
+  constexpr int NT = NG * NTG + NQW * 32, NQT = NQW * 32;
+  constexpr int L = (K + 1) / 2;
+  constexpr int NA = (K + NQT - 1) / NQT;
+  extern __shared__ double2 sm[];
+  double2* tab = sm;
+  double2* const bufs = sm + pfa_tab_total<PL>();
+  unsigned long long* const full = (unsigned long long*)(bufs + (size_t)NB * K);
+  unsigned long long* const done = full + 2 * NB;  // barriers of alternate laps: see k_pfa_rows_p
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 2 * NB; ++b) {
+      mbar_init(full + b, NQT);
+      mbar_init(done + b, 1);
+    }
+  }
+  pfa_load_tables<PL, NT>(tab, gtab);
+  // real: only the columns m >= 0 are transformed (see k_syn_gamma_q)
+  const int NC = real ? L : K;
+  const int mine = (int)blockIdx.x < NC ? (NC - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const long long ni = (long long)mine * nbb;
+  if (ni == 0) return;
+  if (threadIdx.x >= NG * NTG) {
+    const int t = threadIdx.x - NG * NTG;
+    double2 acc[NA];
+#pragma unroll
+    for (int u = 0; u < NA; ++u) acc[u] = make_double2(0.0, 0.0);
+    long long st[6] = {0, 0, 0, 0, 0, 0}, st2[6] = {0, 0, 0, 0, 0, 0};
+    PipeClk ck;
+#pragma unroll 1
+    for (long long i = 0; i < ni + NB; ++i) {
+      const int slot = (int)(i % NB);
+      const unsigned uu = (unsigned)(i / NB);
+      double2* const X = bufs + (size_t)slot * K;
+      ck.mark(st, 4);
+      PipeClk ck2;
+      ck2.t = ck.t;
+      if (i >= NB) {
+        const long long e = i - NB;
+        const int col = (int)blockIdx.x + (int)(e / nbb) * (int)gridDim.x;
+        const int bb = (int)(e % nbb);
+        const long long b = b0 + bb;
+        const int m = col <= L - 1 ? col : col - K;
+        const int am = m < 0 ? -m : m;
+        const double* qp = qtab + q_mbase(min(m, L - 1), L) + b * (L - am) - am;     // + n   (n >= 0)
+        const double* qn = qtab + q_mbase(max(-m, -(L - 1)), L) + b * (L - am) - am;  // + |n| (n < 0)
+        double qv[NA];
+#pragma unroll
+        for (int u = 0; u < NA; ++u) {
+          const int gn = t + u * NQT;
+          const int n = gn <= L - 1 ? gn : gn - K;
+          const int an = n < 0 ? -n : n;
+          qv[u] = 0.0;
+          if (gn >= K || an < am || (real && n < 0 && m == 0)) continue;
+          qv[u] = __ldg(n >= 0 ? qp + n : qn + an);
+        }
+        // pull the weights of the step after next into L2 (two runs of L - |m|
+        // doubles; the table is streamed once per map, so the loads above would
+        // otherwise wait on DRAM every step)
+        if (e + 2 < ni) {
+          const long long e2 = e + 2;
+          const int col2 = (int)blockIdx.x + (int)(e2 / nbb) * (int)gridDim.x;
+          const long long b2 = b0 + (int)(e2 % nbb);
+          const int m2 = col2 <= L - 1 ? col2 : col2 - K;
+          const int am2 = m2 < 0 ? -m2 : m2;
+          const double* base = (t < 64 ? qtab + q_mbase(min(m2, L - 1), L) : qtab + q_mbase(max(-m2, -(L - 1)), L)) +
+                               b2 * (L - am2);
+          const int off = (t & 63) * 16;
+          if (t < 128 && off < L - am2) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(base + off));
+        }
+        ck.mark(st, 3);
+        ck2.mark(st2, 0);  // weight loads + prefetch issue
+        mbar_wait(done + ((uu - 1) & 1) * NB + slot, ((uu - 1) >> 1) & 1);
+        ck.mark(st, 2);
+        ck2.mark(st2, 1);  // wait done
+#pragma unroll
+        for (int u = 0; u < NA; ++u) {
+          const int gn = t + u * NQT;
+          const int n = gn <= L - 1 ? gn : gn - K;
+          const int an = n < 0 ? -n : n;
+          if (gn >= K || an < am || (real && n < 0 && m == 0)) continue;
+          // q_{-l,m} = (-1)^{l+m} q_{l,-m}; real, n < 0: the weight of W(|n|, -m) is q_{|n|,-m} itself
+          const double q = (!real && n < 0 && ((an + m) & 1)) ? -qv[u] : qv[u];
+          double2 v = X[pfa_pos_tab<PL>(tab, gn)];
+          if (real && n < 0) v.y = -v.y;
+          acc[u].x = fma(v.x, q, acc[u].x);
+          acc[u].y = fma(v.y, q, acc[u].y);
+        }
+        ck2.mark(st2, 2);  // accumulate
+        if (bb == nbb - 1) {
+#pragma unroll
+          for (int u = 0; u < NA; ++u) {
+            const int gn = t + u * NQT;
+            const int n = gn <= L - 1 ? gn : gn - K;
+            const int an = n < 0 ? -n : n;
+            const double2 a = acc[u];
+            acc[u] = make_double2(0.0, 0.0);
+            if (gn >= K || an < am || (real && n < 0 && m == 0)) continue;
+            double2* o = real ? wout + (long long)an * K + ((n < 0 ? -m : m) + L - 1)
+                              : wout + ((long long)(n >= 0 ? 0 : 1) * L + an) * K + (m + L - 1);
+            // one add per entry per launch, launches stream-ordered: deterministic
+            atomicAdd(&o->x, a.x);
+            atomicAdd(&o->y, a.y);
+          }
+        }
+        grp_sync(1 + NG, NQT);  // the whole team has read the slot before anyone refills it
+        ck.mark(st, 3);
+        ck2.mark(st2, 3);  // flush + team barrier
+      }
+      if (i < ni) {
+        const int col = (int)blockIdx.x + (int)(i / nbb) * (int)gridDim.x;
+        const int bb = (int)(i % nbb);
+        const double2* cp = chunk + (long long)bb * K * K + col;
+        ring_fill<PL>(X, tab, t, NQT, [&](int g) { return cp + (long long)g * K; });
+        cp_async_mbar_arrive(full + (uu & 1) * NB + slot);
+      }
+    }
+    ck.mark(st, 4);
+    pipe_flush(st, 2, t == 0);
+    pipe_flush(st2, 4, t == 0);
+    return;
+  }
+  const int g = threadIdx.x / NTG, gtid = threadIdx.x - g * NTG, bar = 1 + g;
+  long long st[6] = {0, 0, 0, 0, 0, 0};
+  PipeClk ck;
+#pragma unroll 1
+  for (long long i = g; i < ni; i += NG) {
+    const int slot = (int)(i % NB);
+    const unsigned uu = (unsigned)(i / NB);
+    mbar_wait(full + (uu & 1) * NB + slot, (uu >> 1) & 1);
+    ck.mark(st, 0);
+    pfa_dft<PL, -1, 1, NTG, K>(bufs + (size_t)slot * K, tab, nullptr, gtid, bar);
+    if (gtid == 0) mbar_arrive(done + (uu & 1) * NB + slot);
+    ck.mark(st, 1);
+  }
+  pipe_flush(st, 2, gtid == 0);
+}
+
 // real path: row(-n)[m] = (-1)^{m+n} conj(row(n)[-m]) for n > 0 (so3.py:379-382)
 __global__ void k_wout_mirror(int L, double2* __restrict__ wout) {
   const int K = 2 * L - 1;
@@ -2164,6 +2664,19 @@ static int run_syn_gamma_q(scv_ctx* c, int real, int tr, const double2* chunk, i
                            const long long* mbase, double2* wout, cudaStream_t s) {
   const double2* tab;
   SCV_TRY(scv_pfa_tables(c, K, &tab));
+  if constexpr (K == 2047 && SCV_GQP) {
+    if (!tr) {
+      constexpr size_t smp = pfa_smem_gqp<K>();
+      static_assert(smp <= 232448, "pipelined gamma+quadrature exceeds the 227 KB shared-memory limit");
+      constexpr int NTP = PfaGqpCfg<K>::NG * PfaGqpCfg<K>::NTG + PfaGqpCfg<K>::NQW * 32;
+      int grid;
+      SCV_TRY(persistent_grid(c, k_syn_gamma_qp<K>, NTP, smp, real ? (K + 1) / 2 : K, &grid));
+      k_syn_gamma_qp<K><<<grid, NTP, smp, s>>>(real, chunk, b0, nbb, qtab, wout, tab);
+      c->launches++;
+      SCV_CUDA(c, cudaGetLastError());
+      return SCV_OK;
+    }
+  }
   constexpr size_t sm = pfa_smem_q<K>();
   static_assert(sm <= 232448, "gamma+quadrature launch shape exceeds the 227 KB shared-memory limit");
   int grid;
@@ -2227,6 +2740,45 @@ static int ana_blocked_4095(scv_ctx* c, const double2* w, const double* hlb, con
   return SCV_OK;
 }
 
+// rho32[a][l] = exp(h[l+32,a] - h[l,a]) (pitch L, l >= a, l + 32 < L) and
+// sig32[b] = (sin(beta_b/2) cos(beta_b/2))^32 of k_ana_colgen_p, in long double
+static int scv_colgen_tables(scv_ctx* c, int L, const double** rho, const double** sig) {
+  const std::string kr = "rho32_" + std::to_string(L), ks = "sig32_" + std::to_string(L);
+  auto it = c->aux.find(kr);
+  if (it != c->aux.end()) {
+    *rho = (const double*)it->second;
+    *sig = (const double*)c->aux[ks];
+    return SCV_OK;
+  }
+  const int K = 2 * L - 1;
+  std::vector<ld> lf(2 * L + 2);
+  lf[0] = 0.0L;
+  for (int i = 1; i <= 2 * L + 1; ++i) lf[i] = lf[i - 1] + logl((ld)i);
+  auto h = [&](int l, int a) { return 0.5L * (lf[2 * l] - lf[l + a] - lf[l - a]); };
+  std::vector<double> r((size_t)L * L, 0.0), sg(L);
+  for (int a = 0; a < L; ++a)
+    for (int l = a; l + 32 < L; ++l) r[(size_t)a * L + l] = (double)expl(h(l + 32, a) - h(l, a));
+  const ld pi = 3.141592653589793238462643383279502884L;
+  for (int b = 0; b < L; ++b) {
+    const int q = K - 2 * b - 1;  // cos(beta_b/2) = sin(pi q/(2K)), exactly 0 at beta = pi
+    const ld sc = sinl(pi * (ld)(2 * b + 1) / (ld)(2 * K)) * (q == 0 ? 0.0L : sinl(pi * (ld)q / (ld)(2 * K)));
+    sg[b] = (double)powl(sc, 32.0L);
+  }
+  double *dr = nullptr, *ds = nullptr;
+  SCV_CUDA(c, cudaMalloc(&dr, r.size() * sizeof(double)));
+  SCV_CUDA(c, cudaMalloc(&ds, sg.size() * sizeof(double)));
+  SCV_CUDA(c, cudaMemcpy(dr, r.data(), r.size() * sizeof(double), cudaMemcpyHostToDevice));
+  SCV_CUDA(c, cudaMemcpy(ds, sg.data(), sg.size() * sizeof(double), cudaMemcpyHostToDevice));
+  c->aux[kr] = dr;
+  c->aux[ks] = ds;
+  const long long bytes = (long long)((r.size() + sg.size()) * sizeof(double));
+  c->table_bytes += bytes;
+  c->small_table_bytes += bytes;
+  *rho = dr;
+  *sig = ds;
+  return SCV_OK;
+}
+
 int scv_pfa_ana_blocked(scv_ctx* c, int K, const double2* w, const double* hlb, const double* ls, const double* lc,
                         int b0, int nb, double2* sig, cudaStream_t s) {
   static const int blk = getenv("SCV_COLGEN_T") ? atoi(getenv("SCV_COLGEN_T")) : SCV_COLGEN_T;
@@ -2236,13 +2788,35 @@ int scv_pfa_ana_blocked(scv_ctx* c, int K, const double2* w, const double* hlb, 
   const double2* tab;
   SCV_TRY(scv_pfa_tables(c, KK, &tab));
   void* T = nullptr;
-  SCV_TRY(scv_scratch(c, 1, (size_t)blk * NPR * KK * R * 16, &T));
+  const size_t tbytes = (size_t)blk * NPR * KK * R * 16;
+  const size_t ctbytes = SCV_COLGENP ? (size_t)KK * KK * 16 : 0;
+  SCV_TRY(scv_scratch(c, 1, tbytes + ctbytes, &T));
+  const double *rho32 = nullptr, *sig32 = nullptr;
+  double2* ct = (double2*)((char*)T + tbytes);
+  if (SCV_COLGENP) {
+    SCV_TRY(scv_colgen_tables(c, (KK + 1) / 2, &rho32, &sig32));
+    SCV_PROF(c, s, "so3inv_colgen");
+    const long long tot = (long long)KK * KK;
+    k_colgen_ct<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>((KK + 1) / 2, w, hlb, ct);
+    c->launches++;
+    SCV_CUDA(c, cudaGetLastError());
+  }
   constexpr size_t sms = pfa_smem_s<KK>();
   constexpr size_t smg = pfa_smem_grp<KK>();
   constexpr int NTB = PfaGrpCfg<KK>::NG * PfaGrpCfg<KK>::NTG;
   for (int bs0 = 0; bs0 < nb; bs0 += blk) {
     const int nbb = std::min(blk, nb - bs0);
-    {
+    if (SCV_COLGENP) {
+      SCV_PROF(c, s, "so3inv_colgen");
+      constexpr size_t smp = pfa_smem_cgp<KK>();
+      static_assert(smp <= 232448, "pipelined column generation exceeds the 227 KB shared-memory limit");
+      constexpr int NTP = PfaCgpCfg<KK>::NG * PfaCgpCfg<KK>::NTG + PfaCgpCfg<KK>::NIO * 32;
+      int grid;
+      SCV_TRY(persistent_grid(c, k_ana_colgen_p<KK>, NTP, smp, (long long)NPR * nbb / 4 + 1, &grid));
+      k_ana_colgen_p<KK><<<grid, NTP, smp, s>>>(ct, hlb, ls, lc, sig32, b0 + bs0, nbb, (double2*)T, tab);
+      c->launches++;
+      SCV_CUDA(c, cudaGetLastError());
+    } else {
       SCV_PROF(c, s, "so3inv_colgen");
       const long long nts = (long long)((nbb + PfaSCfg<KK>::BB - 1) / PfaSCfg<KK>::BB) * NPR;
       int grid;

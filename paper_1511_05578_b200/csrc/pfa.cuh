@@ -82,6 +82,9 @@ __host__ __device__ constexpr bool pfa_use_mma(int p, int K) {
 #define SCV_PFA_KT_UNROLL 11
 #endif
 constexpr int pfa_kt_unroll = SCV_PFA_KT_UNROLL;
+#ifndef SCV_PFA_AREG
+#define SCV_PFA_AREG 1
+#endif
 #ifndef SCV_PFA_NBW_SMALL
 #define SCV_PFA_NBW_SMALL 1
 #endif
@@ -649,6 +652,20 @@ __device__ __forceinline__ void pfa_stage_mma_blk(double2* X, const double2* tab
   // small radices (<= 2 m8 tiles): NBW blocks per warp iteration, for more
   // independent DMMA chains per k-step
   constexpr int NBW = M8 <= 2 ? SCV_PFA_NBW_SMALL : SCV_PFA_NBW_BIG;
+  // small radices: the lane's A fragments (M8 tiles x Kp/4 k-steps of C and S)
+  // stay in registers for the whole stage; re-reading them per block is a
+  // fifth of the transform's shared-memory traffic at K = 2047 (radix 23)
+  constexpr bool AREG = SCV_PFA_AREG && !SCV_PFA_A2 && M8 * (Kp / 4) <= 6;
+  double aCr[AREG ? M8 : 1][AREG ? Kp / 4 : 1], aSr[AREG ? M8 : 1][AREG ? Kp / 4 : 1];
+  if constexpr (AREG) {
+#pragma unroll
+    for (int t = 0; t < M8; ++t)
+#pragma unroll
+      for (int kt = 0; kt < Kp / 4; ++kt) {
+        aCr[t][kt] = Cm[(t * 8 + ar) * PA + kt * 4 + ac];
+        aSr[t][kt] = Sm[(t * 8 + ar) * PA + kt * 4 + ac];
+      }
+  }
 #pragma unroll 1
   for (int q0 = warp; q0 < NBLK; q0 += NW * NBW) {
     int rowd[NBW], pa[NBW], pb[NBW], eoff[NBW];
@@ -660,12 +677,16 @@ __device__ __forceinline__ void pfa_stage_mma_blk(double2* X, const double2* tab
     for (int w = 0; w < NBW; ++w) {
       const int q = q0 + w * NW;
       const int gb = (q >> 1) * 8 + 2 * (q & 1);
-      // B-fragment column of this lane: butterfly slot ar>>1, component ar&1
-      const int bfB = gb + slot(ar >> 1);
-      okB[w] = q < NBLK && bfB < NBF;
-      rowd[w] = pa[w] = pb[w] = 0;
-      if (okB[w]) {
-        const int r = bfB / nbf, b = bfB - r * nbf;
+      // B-fragment column of this lane: butterfly slot ar>>1, component ar&1.
+      // A slot past the last butterfly re-reads the last one (GEMM columns are
+      // independent and that column is never stored), and the reduction
+      // indices j = h+1..Kp of the zero-padded coefficient columns read the
+      // butterfly's own elements j <= p-1 (finite data times exact zeros), so
+      // the operand loads need no predicates.
+      const int bfB = min(gb + slot(ar >> 1), NBF - 1);
+      okB[w] = true;
+      {
+        const int r = R == 1 ? 0 : bfB / nbf, b = bfB - r * nbf;
         const int c0 = pfa_base<PL, S>(b);
         rowd[w] = 2 * r * PITCH + (ar & 1);
         pa[w] = c0 + (ac + 1) * step;
@@ -677,7 +698,7 @@ __device__ __forceinline__ void pfa_stage_mma_blk(double2* X, const double2* tab
       eoff[w] = 0;
       x0[w] = make_double2(0.0, 0.0);
       if (okE[w]) {
-        const int r = bfE / nbf, b = bfE - r * nbf;
+        const int r = R == 1 ? 0 : bfE / nbf, b = bfE - r * nbf;
         eoff[w] = r * PITCH + pfa_base<PL, S>(b);
         x0[w] = X[eoff[w]];
       }
@@ -685,11 +706,8 @@ __device__ __forceinline__ void pfa_stage_mma_blk(double2* X, const double2* tab
       for (int t = 0; t < M8; ++t) accC[w][t][0] = accC[w][t][1] = accS[w][t][0] = accS[w][t][1] = 0.0;
       // B operands software-pipelined one k-step ahead (the s/d formation of
       // step kt must not wait on its own shared loads)
-      an[w] = bn[w] = 0.0;
-      if (okB[w] && ((Kp == h) || (ac + 1 <= h))) {
-        an[w] = Xd[rowd[w] + 2 * pa[w]];
-        bn[w] = Xd[rowd[w] + 2 * pb[w]];
-      }
+      an[w] = Xd[rowd[w] + 2 * pa[w]];
+      bn[w] = Xd[rowd[w] + 2 * pb[w]];
     }
 #if SCV_PFA_A2
     // k-steps in pairs: one 16-byte A load per (tile, C|S) feeds steps 2q, 2q+1
@@ -743,9 +761,7 @@ __device__ __forceinline__ void pfa_stage_mma_blk(double2* X, const double2* tab
         const double a = an[w], bb = bn[w];
         pa[w] += 4 * step;
         pb[w] -= 4 * step;
-        an[w] = 0.0;
-        bn[w] = 0.0;
-        if (kt + 1 < Kp / 4 && okB[w] && ((Kp == h) || (4 * kt + 4 + ac + 1 <= h))) {
+        if (kt + 1 < Kp / 4) {
           an[w] = Xd[rowd[w] + 2 * pa[w]];
           bn[w] = Xd[rowd[w] + 2 * pb[w]];
         }
@@ -755,8 +771,14 @@ __device__ __forceinline__ void pfa_stage_mma_blk(double2* X, const double2* tab
 #pragma unroll
       for (int t = 0; t < M8; ++t) {
         const int row = t * 8 + ar;
-        const double aC = Cm[row * PA + kt * 4 + ac];
-        const double aS = Sm[row * PA + kt * 4 + ac];
+        double aC, aS;
+        if constexpr (AREG) {
+          aC = aCr[t][kt];
+          aS = aSr[t][kt];
+        } else {
+          aC = Cm[row * PA + kt * 4 + ac];
+          aS = Sm[row * PA + kt * 4 + ac];
+        }
 #pragma unroll
         for (int w = 0; w < NBW; ++w) {
           dmma(accC[w][t][0], accC[w][t][1], aC, bS[w]);

@@ -697,7 +697,7 @@ extern "C" int scv_debug_pipe_stats(unsigned long long* out, int reset) {
 #define SCV_ROWSP_NG 4
 #endif
 #ifndef SCV_ROWSP_NIO
-#define SCV_ROWSP_NIO 2
+#define SCV_ROWSP_NIO 3
 #endif
 #ifndef SCV_ROWSP_NB
 #define SCV_ROWSP_NB 6
@@ -708,6 +708,13 @@ template <int K> struct PfaPipeCfg { static constexpr int NG = 0, NTG = 96, NIO 
 #endif
 template <> struct PfaPipeCfg<2047> {
   static constexpr int NG = SCV_ROWSP ? SCV_ROWSP_NG : 0, NTG = SCV_ROWSP_NTG, NIO = SCV_ROWSP_NIO, NB = SCV_ROWSP_NB;
+};
+// K = 1023 (the L_j = 512 scale): on with SCV_RING_1023
+#ifndef SCV_RING_1023
+#define SCV_RING_1023 0
+#endif
+template <> struct PfaPipeCfg<1023> {
+  static constexpr int NG = SCV_RING_1023 ? SCV_ROWSP_NG : 0, NTG = SCV_ROWSP_NTG, NIO = SCV_ROWSP_NIO, NB = SCV_ROWSP_NB;
 };
 template <int K>
 static constexpr size_t pfa_smem_pipe() {
@@ -771,7 +778,17 @@ __global__ void __launch_bounds__(PfaPipeCfg<K>::NG * PfaPipeCfg<K>::NTG + PfaPi
           const long long bb = r / K, g = r - bb * K;
           dst = out + (g * LK + b0 + bb) * K;
         }
-        ring_drain<PL>(X, tab, lane, 32, [&](int k) { return dst + k; });
+        if constexpr (GATHER == 5) {
+          // synthesis alpha pass into the column-pair chunk P[bb][m/2][g][m&1]: the
+          // gamma+quadrature pass then reads a column as 16-byte pieces 32 bytes
+          // apart (8 lines per warp copy instead of 32), and the four adjacent
+          // gamma rows of a round complete 128 contiguous bytes
+          constexpr int NPR = (K + 1) / 2;
+          const long long bb = r / K, g = r - bb * K;
+          dst = out + (bb * NPR * K + g) * 2;
+          ring_drain<PL>(X, tab, lane, 32, [&](int k) { return dst + (long long)(k >> 1) * (2 * K) + (k & 1); });
+        } else
+          ring_drain<PL>(X, tab, lane, 32, [&](int k) { return dst + k; });
         __syncwarp();  // every lane has read its elements before any lane refills the buffer
         ck.mark(st, 3);
       }
@@ -784,7 +801,7 @@ __global__ void __launch_bounds__(PfaPipeCfg<K>::NG * PfaPipeCfg<K>::NTG + PfaPi
           ring_fill<PL>(X, tab, lane, 32, [&](int n) { return src + (long long)(n >> 1) * (2 * K) + (n & 1); });
         } else {
           const double2* src = in + r * K;
-          if constexpr (GATHER == 1) {
+          if constexpr (GATHER == 1 || GATHER == 5) {
             const long long bb = r / K, g = r - bb * K;
             src = in + g * LK + (b0 + bb) * K;
           }
@@ -2164,11 +2181,28 @@ __global__ void __launch_bounds__(PfaQCfg<K>::NT, PfaQCfg<K>::MINB)
 #ifndef SCV_GQP
 #define SCV_GQP 1
 #endif
+// chunk between the pipelined synthesis passes in column pairs, P[bb][m/2][g][m&1]
+// (k_pfa_rows_p GATHER = 5 writes it) instead of [bb][g][m]
+#ifndef SCV_SYN_PAIR
+#define SCV_SYN_PAIR 0
+#endif
 #ifndef SCV_GQP_NQW
 #define SCV_GQP_NQW 4
 #endif
 #ifndef SCV_GQP_NG
 #define SCV_GQP_NG 4
+#endif
+// quadrature weights loaded one drain step ahead (1) or at the start of their step (0)
+#ifndef SCV_GQP_WAHEAD
+#define SCV_GQP_WAHEAD 0
+#endif
+#ifndef SCV_GQP_SETREG
+#define SCV_GQP_SETREG 1
+#endif
+// lengths whose column passes (k_ana_colgen_p, k_syn_gamma_qp) run as ring kernels
+constexpr bool pfa_ring_cols(int K) { return K == 2047 || (K == 1023 && SCV_RING_1023); }
+#ifndef SCV_GQP_PF
+#define SCV_GQP_PF (2 + SCV_GQP_WAHEAD)
 #endif
 template <int K> struct PfaGqpCfg { static constexpr int NG = SCV_GQP_NG, NTG = 384 / SCV_GQP_NG, NQW = SCV_GQP_NQW, NB = 6; };
 template <int K>
@@ -2204,74 +2238,122 @@ __global__ void __launch_bounds__(PfaGqpCfg<K>::NG * PfaGqpCfg<K>::NTG + PfaGqpC
   const int mine = (int)blockIdx.x < NC ? (NC - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   const long long ni = (long long)mine * nbb;
   if (ni == 0) return;
+  // Register split between the roles (setmaxnreg moves registers between whole
+  // warpgroups: threads 0..383 are the three transform warpgroups, 384..511 the
+  // team): the transforms need 120 registers, the team holds 64 accumulator, 32
+  // weight and 16 position registers per thread across steps.
+  static_assert(!SCV_GQP_SETREG || (NG * NTG == 384 && NQT == 128), "setmaxnreg works on warpgroups of 128 threads");
   if (threadIdx.x >= NG * NTG) {
+#if SCV_GQP_SETREG
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 152;\n");
+#endif
     const int t = threadIdx.x - NG * NTG;
+    constexpr int NH = NA / 2;
+    static_assert(NQT == 128 && NA == 2 * NH && L == NH * NQT,
+                  "entry u of thread t is frequency n = t + 128 u (u < NH) or -(K - t - 128 u) (u >= NH)");
+    // Thread t owns the output frequencies gn = t + NQT u and the input samples
+    // g = t + NQT u of every step, so their ring-slot positions are constants of
+    // the thread: one packed register per u (low half = position of output gn,
+    // high half = position of input sample g) instead of two position-map reads
+    // per element per step.
+    unsigned pp[NA];
+#pragma unroll
+    for (int u = 0; u < NA; ++u) {
+      const int gn = t + u * NQT;
+      pp[u] = gn < K ? (unsigned)pfa_pos_tab<PL>(tab, gn) | ((unsigned)pfa_in_tab<PL>(tab, gn) << 16) : 0u;
+    }
+    const bool last_ok = t + (NA - 1) * NQT < K;  // gn = K does not exist (t = NQT - 1)
     double2 acc[NA];
+    double qv[NA];
 #pragma unroll
     for (int u = 0; u < NA; ++u) acc[u] = make_double2(0.0, 0.0);
+    // quadrature weights of drain step e (column, beta row) into qv, and an L2
+    // prefetch SCV_GQP_PF steps ahead (two runs of L - |m| doubles; the table is
+    // streamed once per map, so the loads would otherwise wait on DRAM every step).
+    // |n| of entry u is t + 128 u (n >= 0, u < NH) or K - t - 128 u (n < 0, u >= NH).
+    // steps are (column index c, beta row bb) pairs, bb fastest; step (c, bb) exists iff c < mine
+    auto load_weights = [&](int c, int bb) {
+      const int col = (int)blockIdx.x + c * (int)gridDim.x;
+      const long long b = b0 + bb;
+      const int m = col <= L - 1 ? col : col - K;
+      const int am = m < 0 ? -m : m;
+      const double* qp = qtab + q_mbase(m, L) + b * (L - am) - am + t;            // + 128 u       (n >= 0)
+      const double* qn = qtab + q_mbase(-m, L) + b * (L - am) - am + (K - t);     // - 128 u       (n < 0)
+      const int lim = am - t;  // entry live iff |n| >= |m|
+#pragma unroll
+      for (int u = 0; u < NA / 2; ++u) qv[u] = NQT * u >= lim ? __ldg(qp + NQT * u) : 0.0;
+#pragma unroll
+      for (int u = NA / 2; u < NA; ++u) {
+        const bool live = K - NQT * u - 2 * t >= lim && (u < NA - 1 || last_ok) && !(real && m == 0);
+        qv[u] = live ? __ldg(qn - NQT * u) : 0.0;
+      }
+      int c2 = c, bb2 = bb + SCV_GQP_PF;
+      while (bb2 >= nbb) {
+        bb2 -= nbb;
+        ++c2;
+      }
+      if (c2 < mine) {
+        const int col2 = (int)blockIdx.x + c2 * (int)gridDim.x;
+        const long long b2 = b0 + bb2;
+        const int m2 = col2 <= L - 1 ? col2 : col2 - K;
+        const int am2 = m2 < 0 ? -m2 : m2;
+        const double* base = (t < 64 ? qtab + q_mbase(m2, L) : qtab + q_mbase(-m2, L)) + b2 * (L - am2);
+        const int off = (t & 63) * 16;
+        if (off < L - am2) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(base + off));
+      }
+    };
     long long st[6] = {0, 0, 0, 0, 0, 0}, st2[6] = {0, 0, 0, 0, 0, 0};
     PipeClk ck;
+    const int nsteps = (int)ni;
+    int slot = 0;
+    unsigned uu = 0;             // use count of the current slot (lap of the ring)
+    int dc = 0, db = 0;          // drain step (column index, beta row)
+    int fc = 0, fb = 0;          // fill step
 #pragma unroll 1
-    for (long long i = 0; i < ni + NB; ++i) {
-      const int slot = (int)(i % NB);
-      const unsigned uu = (unsigned)(i / NB);
+    for (int i = 0; i < nsteps + NB; ++i) {
       double2* const X = bufs + (size_t)slot * K;
       ck.mark(st, 4);
       PipeClk ck2;
       ck2.t = ck.t;
+      if (SCV_GQP_WAHEAD && i == NB - 1) load_weights(0, 0);
       if (i >= NB) {
-        const long long e = i - NB;
-        const int col = (int)blockIdx.x + (int)(e / nbb) * (int)gridDim.x;
-        const int bb = (int)(e % nbb);
-        const long long b = b0 + bb;
+        if (!SCV_GQP_WAHEAD) {
+          load_weights(dc, db);
+          ck.mark(st, 3);
+          ck2.mark(st2, 0);  // weight loads + prefetch issue
+        }
+        const int col = (int)blockIdx.x + dc * (int)gridDim.x;
+        const int bb = db;
         const int m = col <= L - 1 ? col : col - K;
-        const int am = m < 0 ? -m : m;
-        const double* qp = qtab + q_mbase(min(m, L - 1), L) + b * (L - am) - am;     // + n   (n >= 0)
-        const double* qn = qtab + q_mbase(max(-m, -(L - 1)), L) + b * (L - am) - am;  // + |n| (n < 0)
-        double qv[NA];
-#pragma unroll
-        for (int u = 0; u < NA; ++u) {
-          const int gn = t + u * NQT;
-          const int n = gn <= L - 1 ? gn : gn - K;
-          const int an = n < 0 ? -n : n;
-          qv[u] = 0.0;
-          if (gn >= K || an < am || (real && n < 0 && m == 0)) continue;
-          qv[u] = __ldg(n >= 0 ? qp + n : qn + an);
-        }
-        // pull the weights of the step after next into L2 (two runs of L - |m|
-        // doubles; the table is streamed once per map, so the loads above would
-        // otherwise wait on DRAM every step)
-        if (e + 2 < ni) {
-          const long long e2 = e + 2;
-          const int col2 = (int)blockIdx.x + (int)(e2 / nbb) * (int)gridDim.x;
-          const long long b2 = b0 + (int)(e2 % nbb);
-          const int m2 = col2 <= L - 1 ? col2 : col2 - K;
-          const int am2 = m2 < 0 ? -m2 : m2;
-          const double* base = (t < 64 ? qtab + q_mbase(min(m2, L - 1), L) : qtab + q_mbase(max(-m2, -(L - 1)), L)) +
-                               b2 * (L - am2);
-          const int off = (t & 63) * 16;
-          if (t < 128 && off < L - am2) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(base + off));
-        }
-        ck.mark(st, 3);
-        ck2.mark(st2, 0);  // weight loads + prefetch issue
         mbar_wait(done + ((uu - 1) & 1) * NB + slot, ((uu - 1) >> 1) & 1);
         ck.mark(st, 2);
         ck2.mark(st2, 1);  // wait done
+        // dead entries (|n| < |m|, gn = K, real n < 0 at m = 0) carry a zero weight; their
+        // slot reads are valid positions
+        {
+          // q_{-l,m} = (-1)^{l+m} q_{l,-m}: for n < 0 the sign is (-1)^{|n|+m} = (-1)^{K-t+m} for every u >= NH
+          // (128 u is even); real, n < 0: the weight of W(|n|, -m) is q_{|n|,-m} itself, applied to conj S
+          const bool flip = !real && (((K - t) + m) & 1);
+          double2 v[NA / 2];
 #pragma unroll
-        for (int u = 0; u < NA; ++u) {
-          const int gn = t + u * NQT;
-          const int n = gn <= L - 1 ? gn : gn - K;
-          const int an = n < 0 ? -n : n;
-          if (gn >= K || an < am || (real && n < 0 && m == 0)) continue;
-          // q_{-l,m} = (-1)^{l+m} q_{l,-m}; real, n < 0: the weight of W(|n|, -m) is q_{|n|,-m} itself
-          const double q = (!real && n < 0 && ((an + m) & 1)) ? -qv[u] : qv[u];
-          double2 v = X[pfa_pos_tab<PL>(tab, gn)];
-          if (real && n < 0) v.y = -v.y;
-          acc[u].x = fma(v.x, q, acc[u].x);
-          acc[u].y = fma(v.y, q, acc[u].y);
+          for (int u = 0; u < NA / 2; ++u) v[u] = X[pp[u] & 0xffffu];
+#pragma unroll
+          for (int u = 0; u < NA / 2; ++u) {
+            acc[u].x = fma(v[u].x, qv[u], acc[u].x);
+            acc[u].y = fma(v[u].y, qv[u], acc[u].y);
+          }
+#pragma unroll
+          for (int u = 0; u < NA / 2; ++u) v[u] = X[pp[NA / 2 + u] & 0xffffu];
+#pragma unroll
+          for (int u = 0; u < NA / 2; ++u) {
+            const double q = flip ? -qv[NA / 2 + u] : qv[NA / 2 + u];
+            acc[NA / 2 + u].x = fma(v[u].x, q, acc[NA / 2 + u].x);
+            acc[NA / 2 + u].y = fma(real ? -v[u].y : v[u].y, q, acc[NA / 2 + u].y);
+          }
         }
         ck2.mark(st2, 2);  // accumulate
         if (bb == nbb - 1) {
+          const int am = m < 0 ? -m : m;
 #pragma unroll
           for (int u = 0; u < NA; ++u) {
             const int gn = t + u * NQT;
@@ -2290,13 +2372,38 @@ __global__ void __launch_bounds__(PfaGqpCfg<K>::NG * PfaGqpCfg<K>::NTG + PfaGqpC
         grp_sync(1 + NG, NQT);  // the whole team has read the slot before anyone refills it
         ck.mark(st, 3);
         ck2.mark(st2, 3);  // flush + team barrier
+        if (++db == nbb) {
+          db = 0;
+          ++dc;
+        }
+        if (SCV_GQP_WAHEAD && dc < mine) {
+          load_weights(dc, db);
+          ck.mark(st, 3);
+          ck2.mark(st2, 0);  // weight loads + prefetch issue
+        }
       }
-      if (i < ni) {
-        const int col = (int)blockIdx.x + (int)(i / nbb) * (int)gridDim.x;
-        const int bb = (int)(i % nbb);
-        const double2* cp = chunk + (long long)bb * K * K + col;
-        ring_fill<PL>(X, tab, t, NQT, [&](int g) { return cp + (long long)g * K; });
+      if (i < nsteps) {
+        const int col = (int)blockIdx.x + fc * (int)gridDim.x;
+        const int bb = fb;
+        if (++fb == nbb) {
+          fb = 0;
+          ++fc;
+        }
+#if SCV_SYN_PAIR
+        const double2* cp = chunk + ((long long)bb * ((K + 1) / 2) + (col >> 1)) * (2 * K) + (col & 1) + 2 * t;
+        constexpr long long GS = 2 * NQT;
+#else
+        const double2* cp = chunk + (long long)bb * K * K + col + (long long)t * K;
+        constexpr long long GS = (long long)NQT * K;
+#endif
+#pragma unroll
+        for (int u = 0; u < NA; ++u)
+          if (u < NA - 1 || last_ok) cp_async16_m(X + (pp[u] >> 16), cp + GS * u);
         cp_async_mbar_arrive(full + (uu & 1) * NB + slot);
+      }
+      if (++slot == NB) {
+        slot = 0;
+        ++uu;
       }
     }
     ck.mark(st, 4);
@@ -2304,6 +2411,9 @@ __global__ void __launch_bounds__(PfaGqpCfg<K>::NG * PfaGqpCfg<K>::NTG + PfaGqpC
     pipe_flush(st2, 4, t == 0);
     return;
   }
+#if SCV_GQP_SETREG
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 120;\n");
+#endif
   const int g = threadIdx.x / NTG, gtid = threadIdx.x - g * NTG, bar = 1 + g;
   long long st[6] = {0, 0, 0, 0, 0, 0};
   PipeClk ck;
@@ -2608,6 +2718,19 @@ static int run_syn_alpha(scv_ctx* c, int real, int tr, const void* in, int lsig,
   SCV_TRY(scv_pfa_tables(c, K, &tab));
   constexpr size_t sm = pfa_smem<K, false>();
   static_assert(sm <= 232448, "prime-factor launch shape exceeds the 227 KB shared-memory limit");
+  // tr bit 2: the consumer is scv_pfa_syn_gamma_q (which may want its own chunk layout)
+  const bool pair = (tr & 4) != 0;
+  tr &= 3;
+  (void)pair;
+  if constexpr (PfaPipeCfg<K>::NG > 0) {
+    if (!real && !tr) {
+      const long long nrows = (long long)K * nbb;
+      // the pipelined gamma+quadrature pass can read the chunk in column pairs
+      if (pair && pfa_ring_cols(K) && SCV_GQP && SCV_SYN_PAIR)
+        return launch_rows_p<K, -1, 5>(c, nrows, (const double2*)in, chunk, tab, (long long)lsig * K, b0, s);
+      return launch_rows_p<K, -1, 1>(c, nrows, (const double2*)in, chunk, tab, (long long)lsig * K, b0, s);
+    }
+  }
   if constexpr (PfaGrpCfg<K>::NG > 0) {
     if (real == 2 && !tr) {
       constexpr size_t smg = pfa_smem_grp<K>();
@@ -2624,8 +2747,6 @@ static int run_syn_alpha(scv_ctx* c, int real, int tr, const void* in, int lsig,
       constexpr size_t smg = pfa_smem_grp<K>();
       constexpr int NTB = PfaGrpCfg<K>::NG * PfaGrpCfg<K>::NTG;
       const long long nrows = (long long)K * nbb;
-      if constexpr (PfaPipeCfg<K>::NG > 0)
-        return launch_rows_p<K, -1, 1>(c, nrows, (const double2*)in, chunk, tab, (long long)lsig * K, b0, s);
       int grid;
       SCV_TRY(persistent_grid(c, k_pfa_rows_g<K, -1, 1>, NTB, smg, (nrows + PfaGrpCfg<K>::NG - 1) / PfaGrpCfg<K>::NG, &grid));
       k_pfa_rows_g<K, -1, 1><<<grid, NTB, smg, s>>>(nrows, (const double2*)in, chunk, tab, (long long)lsig * K, b0);
@@ -2664,7 +2785,7 @@ static int run_syn_gamma_q(scv_ctx* c, int real, int tr, const double2* chunk, i
                            const long long* mbase, double2* wout, cudaStream_t s) {
   const double2* tab;
   SCV_TRY(scv_pfa_tables(c, K, &tab));
-  if constexpr (K == 2047 && SCV_GQP) {
+  if constexpr (pfa_ring_cols(K) && SCV_GQP) {
     if (!tr) {
       constexpr size_t smp = pfa_smem_gqp<K>();
       static_assert(smp <= 232448, "pipelined gamma+quadrature exceeds the 227 KB shared-memory limit");
@@ -2779,12 +2900,10 @@ static int scv_colgen_tables(scv_ctx* c, int L, const double** rho, const double
   return SCV_OK;
 }
 
-int scv_pfa_ana_blocked(scv_ctx* c, int K, const double2* w, const double* hlb, const double* ls, const double* lc,
-                        int b0, int nb, double2* sig, cudaStream_t s) {
-  static const int blk = getenv("SCV_COLGEN_T") ? atoi(getenv("SCV_COLGEN_T")) : SCV_COLGEN_T;
-  if (K == 4095 && SCV_COLGEN_T_4095 > 0) return ana_blocked_4095(c, w, hlb, ls, lc, b0, nb, sig, s);
-  if (K != 2047 || blk <= 0 || !SCV_COLGEN_S) return 1;
-  constexpr int KK = 2047, R = PfaSCfg<KK>::R, NPR = (KK + R - 1) / R;
+template <int KK>
+static int ana_blocked_ring(scv_ctx* c, int blk, const double2* w, const double* hlb, const double* ls, const double* lc,
+                            int b0, int nb, double2* sig, cudaStream_t s) {
+  constexpr int R = PfaSCfg<KK>::R, NPR = (KK + R - 1) / R;
   const double2* tab;
   SCV_TRY(scv_pfa_tables(c, KK, &tab));
   void* T = nullptr;
@@ -2801,12 +2920,9 @@ int scv_pfa_ana_blocked(scv_ctx* c, int K, const double2* w, const double* hlb, 
     c->launches++;
     SCV_CUDA(c, cudaGetLastError());
   }
-  constexpr size_t sms = pfa_smem_s<KK>();
-  constexpr size_t smg = pfa_smem_grp<KK>();
-  constexpr int NTB = PfaGrpCfg<KK>::NG * PfaGrpCfg<KK>::NTG;
   for (int bs0 = 0; bs0 < nb; bs0 += blk) {
     const int nbb = std::min(blk, nb - bs0);
-    if (SCV_COLGENP) {
+    if constexpr (SCV_COLGENP) {
       SCV_PROF(c, s, "so3inv_colgen");
       constexpr size_t smp = pfa_smem_cgp<KK>();
       static_assert(smp <= 232448, "pipelined column generation exceeds the 227 KB shared-memory limit");
@@ -2818,6 +2934,7 @@ int scv_pfa_ana_blocked(scv_ctx* c, int K, const double2* w, const double* hlb, 
       SCV_CUDA(c, cudaGetLastError());
     } else {
       SCV_PROF(c, s, "so3inv_colgen");
+      constexpr size_t sms = pfa_smem_s<KK>();
       const long long nts = (long long)((nbb + PfaSCfg<KK>::BB - 1) / PfaSCfg<KK>::BB) * NPR;
       int grid;
       SCV_TRY(persistent_grid(c, k_ana_colgen_s<KK, 1>, PfaSCfg<KK>::NT, sms, nts, &grid));
@@ -2829,15 +2946,31 @@ int scv_pfa_ana_blocked(scv_ctx* c, int K, const double2* w, const double* hlb, 
     const long long nrows = (long long)nbb * KK;
     if constexpr (PfaPipeCfg<KK>::NG > 0) {
       SCV_TRY((launch_rows_p<KK, +1, 2>(c, nrows, (const double2*)T, sig, tab, (long long)nb, bs0, s)));
-      continue;
+    } else {
+      static_assert(PfaGrpCfg<KK>::NG > 0, "the blocked analysis needs a row kernel with the pair gather");
+      constexpr size_t smg = pfa_smem_grp<KK>();
+      constexpr int NTB = PfaGrpCfg<KK>::NG * PfaGrpCfg<KK>::NTG;
+      int grid;
+      SCV_TRY(persistent_grid(c, k_pfa_rows_g<KK, +1, 2>, NTB, smg, (nrows + PfaGrpCfg<KK>::NG - 1) / PfaGrpCfg<KK>::NG, &grid));
+      k_pfa_rows_g<KK, +1, 2><<<grid, NTB, smg, s>>>(nrows, (const double2*)T, sig, tab, (long long)nb, bs0);
+      c->launches++;
+      SCV_CUDA(c, cudaGetLastError());
     }
-    int grid;
-    SCV_TRY(persistent_grid(c, k_pfa_rows_g<KK, +1, 2>, NTB, smg, (nrows + PfaGrpCfg<KK>::NG - 1) / PfaGrpCfg<KK>::NG, &grid));
-    k_pfa_rows_g<KK, +1, 2><<<grid, NTB, smg, s>>>(nrows, (const double2*)T, sig, tab, (long long)nb, bs0);
-    c->launches++;
-    SCV_CUDA(c, cudaGetLastError());
   }
   return SCV_OK;
+}
+
+int scv_pfa_ana_blocked(scv_ctx* c, int K, const double2* w, const double* hlb, const double* ls, const double* lc,
+                        int b0, int nb, double2* sig, cudaStream_t s) {
+  static const int blk = getenv("SCV_COLGEN_T") ? atoi(getenv("SCV_COLGEN_T")) : SCV_COLGEN_T;
+  if (K == 4095 && SCV_COLGEN_T_4095 > 0) return ana_blocked_4095(c, w, hlb, ls, lc, b0, nb, sig, s);
+  if (blk <= 0 || !SCV_COLGEN_S) return 1;
+  if (K == 2047) return ana_blocked_ring<2047>(c, blk, w, hlb, ls, lc, b0, nb, sig, s);
+  if constexpr (SCV_RING_1023 && SCV_COLGENP && PfaPipeCfg<1023>::NG > 0) {
+    // four times the beta rows per block: the same scratch as at K = 2047
+    if (K == 1023) return ana_blocked_ring<1023>(c, 4 * blk, w, hlb, ls, lc, b0, nb, sig, s);
+  }
+  return 1;
 }
 
 int scv_pfa_ana_colgen(scv_ctx* c, int K, const double2* w, const double* hlb, const double* ls, const double* lc,

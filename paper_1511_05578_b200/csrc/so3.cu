@@ -155,7 +155,7 @@ static int forward_q_slab(scv_ctx* c, int L, int real, const void* sig, int sb0,
   const double* qtab = nullptr;
   const long long* mbase = nullptr;
   SCV_TRY(scv_betaq_table(c, L, s, &qtab, &mbase));
-  const size_t per_bc = (size_t)K * K * 16;
+  const size_t per_bc = (size_t)(K + 1) * K * 16;  // (K+1)/2 column pairs per beta row (pfa.cu, SCV_SYN_PAIR)
   static const long long chunk_bytes = getenv("SCV_SYN_CHUNK") ? atoll(getenv("SCV_SYN_CHUNK")) : (1LL << 30);
   const int nbc = (int)std::max<size_t>(1, std::min<size_t>((size_t)snb, (size_t)chunk_bytes / per_bc));
   void* ch = nullptr;
@@ -165,7 +165,7 @@ static int forward_q_slab(scv_ctx* c, int L, int real, const void* sig, int sb0,
     {
       SCV_PROF(c, s, "so3fwd_alpha");
       // real: the alpha pass keeps only the m >= 0 half (real = 2) the gamma+quadrature pass reads
-      SCV_TRY(scv_pfa_syn_alpha(c, K, real ? 2 : 0, c->opt_chunkt, sig, snb, b0 - sb0, nbb, (double2*)ch, s));
+      SCV_TRY(scv_pfa_syn_alpha(c, K, real ? 2 : 0, c->opt_chunkt | 4, sig, snb, b0 - sb0, nbb, (double2*)ch, s));
     }
     SCV_PROF(c, s, "so3fwd_gamma_q");
     SCV_TRY(scv_pfa_syn_gamma_q(c, K, real, c->opt_chunkt, (const double2*)ch, b0, nbb, qtab, mbase, (double2*)w, s));

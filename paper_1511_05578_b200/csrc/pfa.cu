@@ -711,7 +711,7 @@ template <> struct PfaPipeCfg<2047> {
 };
 // K = 1023 (the L_j = 512 scale): on with SCV_RING_1023
 #ifndef SCV_RING_1023
-#define SCV_RING_1023 0
+#define SCV_RING_1023 1
 #endif
 template <> struct PfaPipeCfg<1023> {
   static constexpr int NG = SCV_RING_1023 ? SCV_ROWSP_NG : 0, NTG = SCV_ROWSP_NTG, NIO = SCV_ROWSP_NIO, NB = SCV_ROWSP_NB;
@@ -1228,6 +1228,9 @@ __global__ void __launch_bounds__(PfaSCfg<K>::NT, PfaSCfg<K>::MINB)
 #ifndef SCV_CGP_NG
 #define SCV_CGP_NG 4
 #endif
+#ifndef SCV_CGP_SETREG
+#define SCV_CGP_SETREG 1
+#endif
 template <int K> struct PfaCgpCfg { static constexpr int NG = SCV_CGP_NG, NTG = 384 / SCV_CGP_NG, NIO = 4, NB = 6; };
 template <int K>
 static constexpr size_t pfa_smem_cgp() {
@@ -1296,17 +1299,75 @@ __global__ void __launch_bounds__(PfaCgpCfg<K>::NG * PfaCgpCfg<K>::NTG + PfaCgpC
   const long long S = (long long)NPR * nb;
   const long long lo = S * blockIdx.x / gridDim.x, hi = S * (blockIdx.x + 1) / gridDim.x;
   const long long ni = hi - lo;
+  static_assert(!SCV_CGP_SETREG || (NG * NTG == 384 && NQT == 128), "setmaxnreg works on warpgroups of 128 threads");
+  constexpr bool SETREG = SCV_CGP_SETREG && K == 2047;  // the K = 1023 transforms want all 128
   if (threadIdx.x >= NG * NTG) {
+    if constexpr (SETREG) asm volatile("setmaxnreg.inc.sync.aligned.u32 152;\n");
     // ---- generator / store team: all NIO warps work on every step, in order
     // (a step's drain + fill latency sits on the ring's critical path: three slot
     // pairs, two of them under transform)
     const int t = threadIdx.x - NG * NTG, lane = t & 31, ws = t >> 5;
     const int tbar = 1 + NG;
+    // Warp ws generates (column ws >> 1, sign ws & 1), lane j the degrees l = j + 32 k;
+    // as a store thread t writes entry t & 1 of the pairs g = (t >> 1) + 64 j.  Both index
+    // sets are constants of the thread, so their slot positions live in registers
+    // (two 16-bit positions per register) instead of two map reads per element per step.
+    constexpr int NL = L / 32;          // degrees per generator lane
+    constexpr int ND = (K + 63) / 64;   // pairs per store thread
+    static_assert(NL % GB == 0 && NL % 2 == 0 && ND % 2 == 0, "packed position registers");
+    const int r_gen = ws >> 1, neg = ws & 1, r_st = t & 1;
+    unsigned pg[NL / 2], pd[ND / 2];
+#pragma unroll
+    for (int k = 0; k < NL / 2; ++k) {
+      const int l0 = lane + 32 * (2 * k), l1 = l0 + 32;
+      pg[k] = (unsigned)pfa_in_tab<PL>(tab, neg ? (l0 ? K - l0 : 0) : l0) |
+              ((unsigned)pfa_in_tab<PL>(tab, neg ? K - l1 : l1) << 16);
+    }
+#pragma unroll
+    for (int j = 0; j < ND / 2; ++j) {
+      const int g0 = (t >> 1) + 64 * (2 * j), g1 = g0 + 64;
+      pd[j] = (unsigned)pfa_pos_tab<PL>(tab, g0 < K ? g0 : 0) | ((unsigned)pfa_pos_tab<PL>(tab, g1 < K ? g1 : 0) << 16);
+    }
     long long st[6] = {0, 0, 0, 0, 0, 0}, st2[6] = {0, 0, 0, 0, 0, 0};
     PipeClk ck;
+    // (pair, beta row) of the fill step and of the drain step, advanced incrementally
+    int fpr = (int)(lo / nb), fbs = (int)(lo - (long long)fpr * nb);
+    int dpr = fpr, dbs = fbs;
+    // first batch of coefficients and the closed-form start value of a step: issued at
+    // the end of the previous step, so the loads and the exp overlap the drain
+    double2 c[GB];
+    double d = 0.0, S32 = 0.0;
+    int lst = 0;
+    const double2* cp = ct;
+    auto start_step = [&](int pr, int bs) {
+      const int mc = 2 * pr + r_gen;
+      d = 0.0;
+      lst = L;
+      if (mc >= K) return;  // the odd column past the end: zeros (transformed, never read)
+      const int b = b0 + bs;
+      const int m = mc <= L - 1 ? mc : mc - K, am = m < 0 ? -m : m;
+      lst = am + ((lane - am) & 31);
+      cp = ct + (long long)mc * K;
+#pragma unroll
+      for (int k = 0; k < GB; ++k) {
+        const int l = lane + 32 * k;
+        c[k] = cp[neg ? (l ? K - l : 0) : l];
+      }
+      if (lst < L) {
+        // n >= 0: sin^(l-m) cos^(l+m); n < 0: sin^(l+m) cos^(l-m).  xlogy semantics at the
+        // poles: a zero exponent drops its (possibly -inf) log
+        const int es = neg ? lst + m : lst - m, ec = neg ? lst - m : lst + m;
+        double lg = hlb[lst * (lst + 1) / 2 + am];
+        if (es) lg += (double)es * lsin[b];
+        if (ec) lg += (double)ec * lcos[b];
+        d = exp(lg);
+      }
+      S32 = sig32[b] * 4294967296.0;  // sin(beta_b)^32 = (2 sin cos (beta_b/2))^32
+    };
+    if (ni > 0) start_step(fpr, fbs);
 #pragma unroll 1
-    for (long long i = 0; i < ni + 3; ++i) {
-      const int s0 = 2 * (int)(i % 3);
+    for (int i = 0; i < (int)ni + 3; ++i) {
+      const int s0 = 2 * (i % 3);
       const unsigned u = (unsigned)(i / 3);
       double2* const X0 = bufs + (size_t)s0 * K;
       double2* const X1 = X0 + K;
@@ -1316,85 +1377,73 @@ __global__ void __launch_bounds__(PfaCgpCfg<K>::NG * PfaCgpCfg<K>::NTG + PfaCgpC
         mbar_wait(done + ((u - 1) & 1) * NB + s0, ((u - 1) >> 1) & 1);
         mbar_wait(done + ((u - 1) & 1) * NB + s0 + 1, ((u - 1) >> 1) & 1);
         ck.mark(st, 2);
-        const long long f = lo + i - 3;
-        const long long pr = f / nb, bs = f - pr * nb;
-        double2* dst = out + ((bs * NPR + pr) * K) * 2;
-        const int r = t & 1;
-        const double2* Xr = r ? X1 : X0;
-        ring_drain<PL>(Xr, tab, t >> 1, NQT / 2, [&](int g) { return dst + 2 * g + r; });
+        double2* dst = out + (((long long)dbs * NPR + dpr) * K) * 2 + 2 * (t >> 1) + r_st;
+        if (++dbs == nb) {
+          dbs = 0;
+          ++dpr;
+        }
+        const double2* Xr = r_st ? X1 : X0;
+#pragma unroll
+        for (int j0 = 0; j0 < ND / 2; j0 += RB / 2) {
+          double2 v[RB];
+#pragma unroll
+          for (int j = 0; j < RB / 2; ++j) {
+            v[2 * j] = Xr[pd[j0 + j] & 0xffffu];
+            v[2 * j + 1] = Xr[pd[j0 + j] >> 16];
+          }
+#pragma unroll
+          for (int j = 0; j < RB / 2; ++j) {
+            const int g0 = (t >> 1) + 64 * (2 * (j0 + j));
+            if (g0 < K) dst[2 * (64 * 2 * (j0 + j))] = v[2 * j];
+            if (g0 + 64 < K) dst[2 * (64 * (2 * (j0 + j) + 1))] = v[2 * j + 1];
+          }
+        }
         grp_sync(tbar, NQT);  // the whole team has read the pair before anyone refills it
         ck.mark(st, 3);
       }
-      if (i < ni) {
-        const long long f = lo + i;
-        const int pr = (int)(f / nb), bs = (int)(f - (long long)pr * nb);
-        const int b = b0 + bs;
-        // Warp ws generates (column ws >> 1, sign ws & 1), lane j the degrees l = j mod 32:
+      if (i < (int)ni) {
         // entry l is CT[m][slot] * D_b[l*] sin(beta_b)^(l - l*), with D_b[l*] =
         // d^{l*}_{m,+-l*}(beta_b) in closed form at the lane's first degree l* >= |m|
         // (wigner.py:304-322) -- a geometric walk, no table reads.  Values go from
         // registers straight to their Ruritanian positions (one 16-byte store each;
-        // CT's exact zeros below |m| overwrite the slot's previous contents).  Two
-        // batches of GB degrees: all coefficient loads of a batch are in flight at once.
-        const int r = ws >> 1, neg = ws & 1;
-        double2* const X = r ? X1 : X0;
-        const int mc = 2 * pr + r;
+        // CT's exact zeros below |m| overwrite the slot's previous contents).
+        double2* const X = r_gen ? X1 : X0;
         PipeClk ck2;
         ck2.t = ck.t;
-        if (mc >= K) {  // the odd column past the end: zeros (transformed, never read)
+        if (2 * fpr + r_gen >= K) {
           for (int g = lane + 32 * neg; g < K; g += 64) X[g] = make_double2(0.0, 0.0);
         } else {
-          const int m = mc <= L - 1 ? mc : mc - K, am = m < 0 ? -m : m;
-          const int lst = am + ((lane - am) & 31);
-          const double2* cp = ct + (long long)mc * K;
-          double2 c[GB];
 #pragma unroll
-          for (int k = 0; k < GB; ++k) {
-            const int l = lane + 32 * k;
-            c[k] = cp[neg ? (l ? K - l : 0) : l];
-          }
-          double d = 0.0;
-          if (lst < L) {
-            // n >= 0: sin^(l-m) cos^(l+m); n < 0: sin^(l+m) cos^(l-m).  xlogy semantics at the
-            // poles: a zero exponent drops its (possibly -inf) log
-            const int es = neg ? lst + m : lst - m, ec = neg ? lst - m : lst + m;
-            double lg = hlb[lst * (lst + 1) / 2 + am];
-            if (es) lg += (double)es * lsin[b];
-            if (ec) lg += (double)ec * lcos[b];
-            d = exp(lg);
-          }
-          const double S32 = sig32[b] * 4294967296.0;  // sin(beta_b)^32 = (2 sin cos (beta_b/2))^32
-          ck2.mark(st2, 1);  // loads issued + closed-form start
-#pragma unroll 1
-          for (int l0 = lane; l0 < L; l0 += 32 * GB) {
-            int pp[GB];
+          for (int kb = 0; kb < NL; kb += GB) {
 #pragma unroll
             for (int k = 0; k < GB; ++k) {
-              const int l = l0 + 32 * k;
-              pp[k] = pfa_in_tab<PL>(tab, neg ? (l ? K - l : 0) : l);
-            }
-#pragma unroll
-            for (int k = 0; k < GB; ++k) {
-              const int l = l0 + 32 * k;
+              const int l = lane + 32 * (kb + k);
               if (l > lst) d *= S32;
               c[k] = make_double2(d * c[k].x, d * c[k].y);  // d = 0 before l*, where CT is 0 too
             }
 #pragma unroll
             for (int k = 0; k < GB; ++k) {
-              const int l = l0 + 32 * k;
-              if (l > 0 || !neg) X[pp[k]] = c[k];
+              const int l = lane + 32 * (kb + k);
+              const unsigned pk = pg[(kb + k) >> 1];
+              if (l > 0 || !neg) X[((kb + k) & 1) ? pk >> 16 : pk & 0xffffu] = c[k];
             }
-            if (l0 + 32 * GB < L) {
+            if (kb + GB < NL) {
 #pragma unroll
               for (int k = 0; k < GB; ++k) {
-                const int l = l0 + 32 * (GB + k);
+                const int l = lane + 32 * (kb + GB + k);
                 c[k] = cp[neg ? K - l : l];
               }
             }
           }
         }
         ck2.mark(st2, 3);  // generation
-        mbar_arrive(full + (u & 1) * NB + s0 + r);
+        mbar_arrive(full + (u & 1) * NB + s0 + r_gen);
+        if (++fbs == nb) {
+          fbs = 0;
+          ++fpr;
+        }
+        if (i + 1 < (int)ni) start_step(fpr, fbs);
+        ck2.mark(st2, 1);  // next step's loads issued + closed-form start
       }
     }
     ck.mark(st, 4);
@@ -1402,6 +1451,7 @@ __global__ void __launch_bounds__(PfaCgpCfg<K>::NG * PfaCgpCfg<K>::NTG + PfaCgpC
     pipe_flush(st2, 3, t == 0);
     return;
   }
+  if constexpr (SETREG) asm volatile("setmaxnreg.dec.sync.aligned.u32 120;\n");
   const int g = threadIdx.x / NTG, gtid = threadIdx.x - g * NTG, bar = 1 + g;
   const int r = g & 1;
   long long st[6] = {0, 0, 0, 0, 0, 0};
@@ -2243,10 +2293,9 @@ __global__ void __launch_bounds__(PfaGqpCfg<K>::NG * PfaGqpCfg<K>::NTG + PfaGqpC
   // team): the transforms need 120 registers, the team holds 64 accumulator, 32
   // weight and 16 position registers per thread across steps.
   static_assert(!SCV_GQP_SETREG || (NG * NTG == 384 && NQT == 128), "setmaxnreg works on warpgroups of 128 threads");
+  constexpr bool SETREG = SCV_GQP_SETREG && K == 2047;  // the K = 1023 transforms want all 128
   if (threadIdx.x >= NG * NTG) {
-#if SCV_GQP_SETREG
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 152;\n");
-#endif
+    if constexpr (SETREG) asm volatile("setmaxnreg.inc.sync.aligned.u32 152;\n");
     const int t = threadIdx.x - NG * NTG;
     constexpr int NH = NA / 2;
     static_assert(NQT == 128 && NA == 2 * NH && L == NH * NQT,
@@ -2411,9 +2460,7 @@ __global__ void __launch_bounds__(PfaGqpCfg<K>::NG * PfaGqpCfg<K>::NTG + PfaGqpC
     pipe_flush(st2, 4, t == 0);
     return;
   }
-#if SCV_GQP_SETREG
-  asm volatile("setmaxnreg.dec.sync.aligned.u32 120;\n");
-#endif
+  if constexpr (SETREG) asm volatile("setmaxnreg.dec.sync.aligned.u32 120;\n");
   const int g = threadIdx.x / NTG, gtid = threadIdx.x - g * NTG, bar = 1 + g;
   long long st[6] = {0, 0, 0, 0, 0, 0};
   PipeClk ck;

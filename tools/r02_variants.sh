@@ -10,10 +10,10 @@ run() { SCV_LIB=$2 timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-bas
 import json,sys; d=json.loads(sys.stdin.read()); print('$1 ms/map', round(d['ms_per_step'],1), 'rt', d['roundtrip_rel_err'], 'peak GB', d.get('peak_mem_gb')); print({k: round(v,1) for k,v in d['stages_ms_per_step'].items() if v>1})"; }
 run base paper_1511_05578_b200/libscurve_b200.so
 for f in variants/lib_*.so; do v=$(basename $f .so); [ $v = lib_stats ] || [ $v = lib_old ] || run ${v#lib_} $f; done
-SCV_SYN_CHUNK=2147483648 run chunk2g paper_1511_05578_b200/libscurve_b200.so
-SCV_SYN_CHUNK=4294967296 run chunk4g paper_1511_05578_b200/libscurve_b200.so
-SCV_COLGEN_T=128 run colgent128 paper_1511_05578_b200/libscurve_b200.so
+
+
+
 run c3_base paper_1511_05578_b200/libscurve_b200.so "--L 512 --jmin 2"
-[ -f variants/lib_r1023.so ] && run c3_r1023 variants/lib_r1023.so "--L 512 --jmin 2"
-[ -f variants/lib_r1023.so ] && SCV_LIB=variants/lib_r1023.so timeout 900 python -m pytest tests/test_gpu_parity_full.py tests/test_gpu_parity.py -m gpu -x -q -k "c3 or 512 or slab" 2>&1 | tail -3
+
+SCV_LIB=paper_1511_05578_b200/libscurve_b200.so timeout 900 python -m pytest tests/test_gpu_parity_full.py tests/test_gpu_parity.py -m gpu -x -q -k "c3 or 512 or slab" 2>&1 | tail -3
 SCV_LIB=variants/lib_stats.so timeout 200 python tools/pipe_stats.py 32 2>&1 | tail -5

@@ -123,6 +123,12 @@ int scv_debug_r89_sigma(int* sigma_in, int* sigma_out);
  * for a full slot, transforming; load/store warps waiting for a transform,
  * draining, filling; unused}.  reset != 0 clears them. */
 int scv_debug_pipe_stats(unsigned long long* out36, int reset);
+/* Build the beta-quadrature table of band limit L (csrc/betaq.cu; the weights that
+ * replace the reference's beta FFT + quadrature convolution + Delta contraction,
+ * so3.py:203-243) with method 1 (two tensor-core GEMMs, the default) or 0 (direct
+ * sums) and copy its first n doubles to the device buffer out.  Nothing is cached;
+ * used to compare the two builds and to time them. */
+int scv_debug_betaq_build(scv_ctx* ctx, int L, int method, double* out, long long n, void* stream);
 
 /* Delta^l_{m'm}(pi/2) for l < L in the 1/8 symmetry wedge 0 <= m <= m' <= l:
  * element (l, m', m) at l(l+1)(l+2)/6 + m'(m'+1)/2 + m.  Copies the context's

@@ -762,6 +762,70 @@ __global__ void __launch_bounds__(PfaPipeCfg<K>::NG * PfaPipeCfg<K>::NTG + PfaPi
     const int w = (threadIdx.x - NG * NTG) >> 5, lane = threadIdx.x & 31;
     long long st[6] = {0, 0, 0, 0, 0, 0};
     PipeClk ck;
+    if constexpr (GATHER == 5) {
+      // Synthesis alpha pass into the TRANSPOSED chunk C[m][r] (r = the launch's flat row
+      // index bb * K + g, row pitch RS even): the gamma+quadrature pass then streams a
+      // column (m, bb) as 2047 contiguous elements instead of 16-byte pieces 32 KB apart
+      // (half-used sectors, twice the L2 -> SM traffic).  A warp drains the two slots of
+      // rows (r, r + 1), r even, together: lane pair (2i, 2i+1) writes C[k][r], C[k][r+1],
+      // one full 32-byte sector.  Steps 2j and 2j + 1 of a CTA are such a row pair
+      // (rounds of NG = 4 adjacent rows), in slots 2(j % (NB/2)) and + 1 of the same lap.
+      static_assert(GATHER != 5 || (NG % 2 == 0 && NB % 2 == 0 && (NB / 2) % NIO == 0),
+                    "row pairs share a round and a lap; a warp owns fixed slot pairs");
+      const long long RS = (nrows + 1) & ~1LL;
+      const int sub = lane & 1;
+#pragma unroll 1
+      for (long long i0 = 2 * w; i0 < ni + NB; i0 += 2 * NIO) {
+        const int b = (int)(i0 % NB);
+        const unsigned u = (unsigned)(i0 / NB);
+        double2* const X0 = bufs + (size_t)b * K;
+        ck.mark(st, 4);
+        if (i0 >= NB) {
+          const bool have1 = i0 - NB + 1 < ni;
+          mbar_wait(done + ((u - 1) & 1) * NB + b, ((u - 1) >> 1) & 1);
+          if (have1) mbar_wait(done + ((u - 1) & 1) * NB + b + 1, ((u - 1) >> 1) & 1);
+          ck.mark(st, 2);
+          const long long r = row_of(i0 - NB);
+          double2* const dst = out + r + sub;
+          const double2* const Xs = X0 + (size_t)sub * K;
+          if (sub == 0 || have1) {
+#pragma unroll 1
+            for (int k0 = lane >> 1; k0 < K; k0 += 16 * RB) {
+              int pos[RB];
+              double2 v[RB];
+#pragma unroll
+              for (int j = 0; j < RB; ++j) {
+                const int k = k0 + 16 * j;
+                pos[j] = k < K ? pfa_pos_tab<PL>(tab, k) : 0;
+              }
+#pragma unroll
+              for (int j = 0; j < RB; ++j) v[j] = Xs[pos[j]];
+#pragma unroll
+              for (int j = 0; j < RB; ++j) {
+                const int k = k0 + 16 * j;
+                if (k < K) dst[(long long)k * RS] = v[j];
+              }
+            }
+          }
+          __syncwarp();  // every lane has read its elements before any lane refills the buffers
+          ck.mark(st, 3);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const long long i = i0 + h;
+          if (i < ni) {
+            const long long r = row_of(i);
+            const long long bb = r / K, g = r - bb * K;
+            const double2* src = in + g * LK + (b0 + bb) * K;
+            ring_fill<PL>(X0 + (size_t)h * K, tab, lane, 32, [&](int n) { return src + n; });
+            cp_async_mbar_arrive(full + (u & 1) * NB + b + h);
+          }
+        }
+      }
+      ck.mark(st, 4);
+      pipe_flush(st, 0, lane == 0);
+      return;
+    }
 #pragma unroll 1
     for (long long i = w; i < ni + NB; i += NIO) {
       const int b = (int)(i % NB);
@@ -778,16 +842,6 @@ __global__ void __launch_bounds__(PfaPipeCfg<K>::NG * PfaPipeCfg<K>::NTG + PfaPi
           const long long bb = r / K, g = r - bb * K;
           dst = out + (g * LK + b0 + bb) * K;
         }
-        if constexpr (GATHER == 5) {
-          // synthesis alpha pass into the column-pair chunk P[bb][m/2][g][m&1]: the
-          // gamma+quadrature pass then reads a column as 16-byte pieces 32 bytes
-          // apart (8 lines per warp copy instead of 32), and the four adjacent
-          // gamma rows of a round complete 128 contiguous bytes
-          constexpr int NPR = (K + 1) / 2;
-          const long long bb = r / K, g = r - bb * K;
-          dst = out + (bb * NPR * K + g) * 2;
-          ring_drain<PL>(X, tab, lane, 32, [&](int k) { return dst + (long long)(k >> 1) * (2 * K) + (k & 1); });
-        } else
           ring_drain<PL>(X, tab, lane, 32, [&](int k) { return dst + k; });
         __syncwarp();  // every lane has read its elements before any lane refills the buffer
         ck.mark(st, 3);
@@ -2231,8 +2285,11 @@ __global__ void __launch_bounds__(PfaQCfg<K>::NT, PfaQCfg<K>::MINB)
 #ifndef SCV_GQP
 #define SCV_GQP 1
 #endif
-// chunk between the pipelined synthesis passes in column pairs, P[bb][m/2][g][m&1]
-// (k_pfa_rows_p GATHER = 5 writes it) instead of [bb][g][m]
+// chunk between the pipelined synthesis passes transposed, C[m][bb * K + g] (k_pfa_rows_p
+// GATHER = 5 writes it in row pairs), instead of [bb][g][m].  Measured (r02o): bit-identical
+// results, but the alpha pass goes 82 -> 116 ms/map (its load/store warps become the
+// bottleneck on the scattered sector writes) and the gamma+quadrature pass gains nothing
+// (97.5 -> 96.0): its transform groups, not the column reads, bound it.  Off.
 #ifndef SCV_SYN_PAIR
 #define SCV_SYN_PAIR 0
 #endif
@@ -2439,8 +2496,9 @@ __global__ void __launch_bounds__(PfaGqpCfg<K>::NG * PfaGqpCfg<K>::NTG + PfaGqpC
           ++fc;
         }
 #if SCV_SYN_PAIR
-        const double2* cp = chunk + ((long long)bb * ((K + 1) / 2) + (col >> 1)) * (2 * K) + (col & 1) + 2 * t;
-        constexpr long long GS = 2 * NQT;
+        // transposed chunk C[m][r], r = bb * K + g, row pitch even (k_pfa_rows_p GATHER = 5)
+        const double2* cp = chunk + (long long)col * (((long long)nbb * K + 1) & ~1LL) + (long long)bb * K + t;
+        constexpr long long GS = NQT;
 #else
         const double2* cp = chunk + (long long)bb * K * K + col + (long long)t * K;
         constexpr long long GS = (long long)NQT * K;

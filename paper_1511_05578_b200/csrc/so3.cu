@@ -155,7 +155,7 @@ static int forward_q_slab(scv_ctx* c, int L, int real, const void* sig, int sb0,
   const double* qtab = nullptr;
   const long long* mbase = nullptr;
   SCV_TRY(scv_betaq_table(c, L, s, &qtab, &mbase));
-  const size_t per_bc = (size_t)(K + 1) * K * 16;  // (K+1)/2 column pairs per beta row (pfa.cu, SCV_SYN_PAIR)
+  const size_t per_bc = (size_t)(K + 1) * K * 16;  // covers the transposed chunk K x (nbb K rounded up to even) (pfa.cu, SCV_SYN_PAIR)
   // 4.3 GB: 64 beta rows at L_j = 1024, the size of the blocked analysis' scratch in the same slot
   // (launches of 16 rows measured 6 ms/map slower: ring fill/drain per launch)
   static const long long chunk_bytes = getenv("SCV_SYN_CHUNK") ? atoll(getenv("SCV_SYN_CHUNK")) : 4300000000LL;

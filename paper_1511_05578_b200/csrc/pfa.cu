@@ -608,6 +608,19 @@ __device__ __forceinline__ void cp_async16_m(void* smem, const void* gmem) {
 // are asm volatile / cross address spaces the compiler cannot disambiguate, so
 // an element-at-a-time loop serialises map read -> copy -> next map read.)
 constexpr int RB = 8;
+// Pacing (ns) of the load/store warps' copies: a burst of warp-wide copies to scattered slot
+// positions delays the transform warps' own shared-memory traffic; sleeping between copies
+// spreads it (the load/store warps have slack).  SCV_RING_PACE after every SCV_RING_PACE_N
+// fill copies, SCV_RING_PACE_D after every batch of RB drain reads.
+#ifndef SCV_RING_PACE
+#define SCV_RING_PACE 0
+#endif
+#ifndef SCV_RING_PACE_N
+#define SCV_RING_PACE_N 1
+#endif
+#ifndef SCV_RING_PACE_D
+#define SCV_RING_PACE_D 0
+#endif
 // slot X (Ruritanian positions) <- element n of a row at gsrc(n), n = lane0 + nl*j < K
 template <class PL, class SrcFn>
 __device__ __forceinline__ void ring_fill(double2* X, const double2* tab, int lane0, int nl, SrcFn gsrc) {
@@ -624,6 +637,9 @@ __device__ __forceinline__ void ring_fill(double2* X, const double2* tab, int la
     for (int j = 0; j < RB; ++j) {
       const int n = n0 + nl * j;
       if (n < K) cp_async16_m(X + pos[j], gsrc(n));
+#if SCV_RING_PACE
+      if ((j % SCV_RING_PACE_N) == SCV_RING_PACE_N - 1) __nanosleep(SCV_RING_PACE);
+#endif
     }
   }
 }
@@ -647,6 +663,9 @@ __device__ __forceinline__ void ring_drain(const double2* X, const double2* tab,
       const int k = k0 + nl * j;
       if (k < K) *gdst(k) = v[j];
     }
+#if SCV_RING_PACE_D
+    __nanosleep(SCV_RING_PACE_D);
+#endif
   }
 }
 
@@ -2306,6 +2325,17 @@ __global__ void __launch_bounds__(PfaQCfg<K>::NT, PfaQCfg<K>::MINB)
 #ifndef SCV_GQP_SETREG
 #define SCV_GQP_SETREG 1
 #endif
+// Pacing of the team's refill: 64 warp copies to scattered slot positions issued back to back
+// delay the transform warps' shared-memory traffic (the transforms run 31% slower next to the
+// refill than alone, 12% in the row kernel whose copies are spread by its position-map reads).
+// Sleeping SCV_GQP_PACE ns after every SCV_GQP_PACE_N copies spreads them; measured on the C4
+// map (ms for this pass): off 97.1; 30 ns 92.1; 50 ns 87.6; 75 ns 103; 100 ns per 2 copies 90.
+#ifndef SCV_GQP_PACE
+#define SCV_GQP_PACE 50
+#endif
+#ifndef SCV_GQP_PACE_N
+#define SCV_GQP_PACE_N 1
+#endif
 // lengths whose column passes (k_ana_colgen_p, k_syn_gamma_qp) run as ring kernels
 constexpr bool pfa_ring_cols(int K) { return K == 2047 || (K == 1023 && SCV_RING_1023); }
 #ifndef SCV_GQP_PF
@@ -2504,8 +2534,13 @@ __global__ void __launch_bounds__(PfaGqpCfg<K>::NG * PfaGqpCfg<K>::NTG + PfaGqpC
         constexpr long long GS = (long long)NQT * K;
 #endif
 #pragma unroll
-        for (int u = 0; u < NA; ++u)
+        for (int u = 0; u < NA; ++u) {
           if (u < NA - 1 || last_ok) cp_async16_m(X + (pp[u] >> 16), cp + GS * u);
+#if SCV_GQP_PACE
+          // spread the team's copies in time (a burst of 64 warp copies delays the transforms' shared loads)
+          if ((u % SCV_GQP_PACE_N) == SCV_GQP_PACE_N - 1 && u < NA - 1) __nanosleep(SCV_GQP_PACE);
+#endif
+        }
         cp_async_mbar_arrive(full + (uu & 1) * NB + slot);
       }
       if (++slot == NB) {

@@ -123,12 +123,23 @@ int scv_debug_r89_sigma(int* sigma_in, int* sigma_out);
  * for a full slot, transforming; load/store warps waiting for a transform,
  * draining, filling; unused}.  reset != 0 clears them. */
 int scv_debug_pipe_stats(unsigned long long* out36, int reset);
+/* Beta rows per alpha/gamma launch pair of the quadrature synthesis at band limit L.  The sum over
+ * beta (so3.py:226-243 via the table) is formed chunk by chunk, so a caller that cuts a scale into
+ * slabs at multiples of this gets the whole-scale summation order (roundtrip_streamed relies on it). */
+int scv_syn_chunk_rows(int L);
 /* Build the beta-quadrature table of band limit L (csrc/betaq.cu; the weights that
  * replace the reference's beta FFT + quadrature convolution + Delta contraction,
  * so3.py:203-243) with method 1 (two tensor-core GEMMs, the default) or 0 (direct
  * sums) and copy its first n doubles to the device buffer out.  Nothing is cached;
  * used to compare the two builds and to time them. */
 int scv_debug_betaq_build(scv_ctx* ctx, int L, int method, double* out, long long n, void* stream);
+/* Restrict this context's beta-quadrature table of band limit L to the beta rows [b0, b0 + nb):
+ * the table a rank of the beta-slab decomposition needs (8 L^2 nb bytes instead of 8 L^3, and
+ * 1/world of the second build GEMM).  Call before the first synthesis at L, or any time: a table
+ * already built for another range is dropped and rebuilt on next use.  nb = 0 lifts the
+ * restriction.  scv_so3_forward_curvelet(_slab) on rows outside the range then fails with
+ * SCV_EINVAL.  The reference has no counterpart (its Delta cache, wigner.py:226-240, is global). */
+int scv_betaq_restrict(scv_ctx* ctx, int L, int b0, int nb);
 
 /* Delta^l_{m'm}(pi/2) for l < L in the 1/8 symmetry wedge 0 <= m <= m' <= l:
  * element (l, m', m) at l(l+1)(l+2)/6 + m'(m'+1)/2 + m.  Copies the context's

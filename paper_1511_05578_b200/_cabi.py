@@ -50,6 +50,8 @@ _SIGS = {
     "scv_debug_r89_sigma": [_P, _P],
     "scv_debug_pipe_stats": [_P, _I],
     "scv_debug_betaq_build": [_P, _I, _I, _P, ctypes.c_longlong, _P],
+    "scv_syn_chunk_rows": [_I],
+    "scv_betaq_restrict": [_P, _I, _I, _I],
     "scv_halfpi_wedge": [_P, _I, _P, _P],
     "scv_sht_forward": [_P, _I, _I, _I, _P, _P, _P],
     "scv_sht_inverse": [_P, _I, _I, _I, _P, _P, _P],
@@ -124,6 +126,17 @@ class Context:
                 if rc == SCV_ETYPE:
                     raise TypeError(msg)
                 raise RuntimeError(f"scv_{name} failed ({rc}): {msg}")
+
+    def betaq_restrict(self, L: int, b0: int = 0, nb: int = 0):
+        """scv_betaq_restrict: keep only the beta rows [b0, b0+nb) of the quadrature
+        table of band limit L on this context (nb = 0 lifts the restriction)."""
+        with self.lock:
+            rc = self.lib.scv_betaq_restrict(self.handle, int(L), int(b0), int(nb))
+            if rc != SCV_OK:
+                msg = self.lib.scv_last_error(self.handle).decode(errors="replace")
+                if rc == SCV_EINVAL:
+                    raise ValueError(msg)
+                raise RuntimeError(f"scv_betaq_restrict failed ({rc}): {msg}")
 
     def launch_count(self) -> int:
         return int(self.lib.scv_launch_count(self.handle))

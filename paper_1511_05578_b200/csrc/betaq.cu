@@ -278,12 +278,13 @@ __global__ void k_bq_build_T(int L, int LeP, int LP, int par, double* __restrict
   T[idx] = v;
 }
 // G_par[b][row(m'')], pitch LP, JP rows
-__global__ void k_bq_build_G(int L, int LeP, int LP, int JP, int par, const double* __restrict__ trig,
+__global__ void k_bq_build_G(int L, int LeP, int LP, int JP, int par, int qb0, int qnb, const double* __restrict__ trig,
                              double* __restrict__ G) {
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)JP * LP) return;
   const int K = 2 * L - 1;
-  const int b = (int)(idx / LP), col = (int)(idx - (long long)b * LP);
+  const int row = (int)(idx / LP), col = (int)(idx - (long long)row * LP);
+  const int b = row < qnb ? qb0 + row : L;  // rows past the range are zero
   const int sub = col >= LeP;
   const int mpp = sub ? 2 * (col - LeP) + 1 : 2 * col;
   double v = 0.0;
@@ -313,11 +314,12 @@ __global__ void k_bq_cmat(int L, int LeP, int LP, const double* __restrict__ del
   C[(long long)row * NCP + i] = v;
 }
 // q[mbase(m) + b (L-|m|) + (l-|m|)] from Q[b][i]
-__global__ void k_bq_scatter(int L, double pref, int par, const double* __restrict__ delta, const int2* __restrict__ cols,
-                             int NC, long long NCP, const double* __restrict__ Q, const long long* __restrict__ mbase,
-                             double* __restrict__ q) {
+__global__ void k_bq_scatter(int L, double pref, int par, int qb0, const double* __restrict__ delta,
+                             const int2* __restrict__ cols, int NC, long long NCP, const double* __restrict__ Qm,
+                             const long long* __restrict__ mbase, double* __restrict__ q) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const int b = blockIdx.y;
+  const int b = qb0 + blockIdx.y;
+  const double* Q = Qm - (long long)qb0 * NCP;  // Q[b][i] with b the absolute beta row
   if (i >= NC) return;
   const int K = 2 * L - 1;
   const int m = cols[i].x, l = cols[i].y;
@@ -334,12 +336,12 @@ __global__ void k_bq_scatter(int L, double pref, int par, const double* __restri
     double to = 0.0;
     if (l == L - 1) {
       to = 2.0 * wedge_get(delta, l, L - 1, m) * wedge_get(delta, l, L - 1, l);
-      if (!((L - 1) & 1)) to = to; else to = -to;
+      if ((L - 1) & 1) to = -to;
     }
     const int e = (mn + 1) / 2;
     v = f * 0.5 * SCV_PI * ((((e % 2) + 2) % 2) ? -to : to);
   }
-  q[mbase[m + L - 1] + (long long)b * (L - am) + (l - am)] = v;
+  q[mbase[m + L - 1] + (long long)(b - qb0) * (L - am) + (l - am)] = v;
 }
 
 static int bq_round(int x, int m) { return (x + m - 1) / m * m; }
@@ -353,10 +355,11 @@ bool scv_betaq_enabled(int L) {
 }
 
 // GEMM formulation of the build (see above): fills dq (L^3 doubles, bases dmb).
-static int betaq_fill_gemm(scv_ctx* c, int L, cudaStream_t s, double* dq, const long long* dmb, const double* dtrig) {
+static int betaq_fill_gemm(scv_ctx* c, int L, int qb0, int qnb, cudaStream_t s, double* dq, const long long* dmb,
+                           const double* dtrig) {
   const int K = 2 * L - 1;
   const int Le = (L + 1) / 2, Lo = L / 2;
-  const int LeP = bq_round(Le, 64), LoP = bq_round(std::max(Lo, 1), 64), LP = LeP + LoP, JP = bq_round(L, 64);
+  const int LeP = bq_round(Le, 64), LoP = bq_round(std::max(Lo, 1), 64), LP = LeP + LoP, JP = bq_round(qnb, 64);
   const int LB = L <= 1024 ? 32 : 16;  // degrees per batch (scratch: 3 x LP x NCP doubles)
   // column lists of every (batch, parity), m-major with l fastest
   struct Batch { int la, lb, par; size_t off; int nc; };
@@ -409,7 +412,7 @@ static int betaq_fill_gemm(scv_ctx* c, int L, cudaStream_t s, double* dq, const 
   for (int i = 0; i < 2; ++i) {
     const int par = i == 0 ? 1 : -1;
     k_bq_build_T<<<(unsigned)(((long long)LP * LP + 255) / 256), 256, 0, s>>>(L, LeP, LP, par, T[i]);
-    k_bq_build_G<<<(unsigned)(((long long)JP * LP + 255) / 256), 256, 0, s>>>(L, LeP, LP, JP, par, dtrig, G[i]);
+    k_bq_build_G<<<(unsigned)(((long long)JP * LP + 255) / 256), 256, 0, s>>>(L, LeP, LP, JP, par, qb0, qnb, dtrig, G[i]);
     c->launches += 2;
   }
   BQ_CUDA(cudaGetLastError());
@@ -429,8 +432,8 @@ static int betaq_fill_gemm(scv_ctx* c, int L, cudaStream_t s, double* dq, const 
       BQ_CUDA(cudaMemsetAsync(U + (size_t)LeP * NCP, 0, (size_t)LoP * NCP * sizeof(double), s));
     // GEMM 2
     k_bq_gemm<<<dim3((unsigned)(NCP / GT_I), JP / GT_J), GT_NT, GT_SMEM, s>>>(LP, G[pi], LP, U, NCP, Q, NCP);
-    k_bq_scatter<<<dim3((unsigned)((b.nc + 255) / 256), L), 256, 0, s>>>(L, pref, b.par, c->delta, bc, b.nc, NCP, Q, dmb,
-                                                                       dq);
+    k_bq_scatter<<<dim3((unsigned)((b.nc + 255) / 256), qnb), 256, 0, s>>>(L, pref, b.par, qb0, c->delta, bc, b.nc, NCP,
+                                                                         Q, dmb, dq);
     c->launches += 5;
     BQ_CUDA(cudaGetLastError());
   }
@@ -477,14 +480,16 @@ static int betaq_method() {
 }
 
 // Allocate and fill the table of band limit L (method: 1 GEMM, 0 direct).
-static int betaq_build(scv_ctx* c, int L, int method, cudaStream_t s, double** qout, long long** mbout, long long* nq) {
+static int betaq_build(scv_ctx* c, int L, int method, int qb0, int qnb, cudaStream_t s, double** qout,
+                       long long** mbout, long long* nq) {
   SCV_TRY(scv_ensure_delta(c, L, s));
   const int K = 2 * L - 1;
+  if (qb0 != 0 || qnb != L) method = 1;  // the direct build writes whole blocks only
   std::vector<long long> mb(2 * L - 1);
   long long acc = 0;
   for (int m = -(L - 1); m <= L - 1; ++m) {
     mb[m + L - 1] = acc;
-    acc += (long long)L * (L - std::abs(m));
+    acc += (long long)qnb * (L - std::abs(m));
   }
   const ld pi = 3.141592653589793238462643383279502884L;
   std::vector<double> trig(4 * (size_t)K);
@@ -503,7 +508,7 @@ static int betaq_build(scv_ctx* c, int L, int method, cudaStream_t s, double** q
   int rc;
   {
     SCV_PROF(c, s, "betaq_build");
-    rc = method ? betaq_fill_gemm(c, L, s, dq, dmb, (const double*)dtrig)
+    rc = method ? betaq_fill_gemm(c, L, qb0, qnb, s, dq, dmb, (const double*)dtrig)
                 : betaq_fill_direct(c, L, s, dq, dmb, (const double*)dtrig);
   }
   cudaStreamSynchronize(s);
@@ -528,7 +533,7 @@ extern "C" int scv_debug_betaq_build(scv_ctx* c, int L, int method, double* out,
   double* dq = nullptr;
   long long* dmb = nullptr;
   long long nq = 0;
-  SCV_TRY(betaq_build(c, L, method, s, &dq, &dmb, &nq));
+  SCV_TRY(betaq_build(c, L, method, 0, L, s, &dq, &dmb, &nq));
   const cudaError_t e = cudaMemcpyAsync(out, dq, (size_t)std::min(n, nq) * sizeof(double), cudaMemcpyDeviceToDevice, s);
   cudaStreamSynchronize(s);
   cudaFree(dq);
@@ -537,10 +542,15 @@ extern "C" int scv_debug_betaq_build(scv_ctx* c, int L, int method, double* out,
   return SCV_OK;
 }
 
-// The table of band limit L, built once per context.
-int scv_betaq_table(scv_ctx* c, int L, cudaStream_t s, const double** qtab, const long long** mbase) {
+// The table of band limit L, built once per context: all L beta rows, or the rows the context
+// was restricted to (scv_betaq_restrict).
+int scv_betaq_table(scv_ctx* c, int L, cudaStream_t s, const double** qtab, const long long** mbase, int* qb0,
+                    int* qrows) {
   const std::string key = "betaq_" + std::to_string(L);
   const std::string kb = "betaqb_" + std::to_string(L);
+  auto rg = c->betaq_rows.find(L);
+  *qb0 = rg == c->betaq_rows.end() ? 0 : rg->second.first;
+  *qrows = rg == c->betaq_rows.end() ? L : rg->second.second;
   auto it = c->aux.find(key);
   if (it != c->aux.end()) {
     *qtab = (const double*)it->second;
@@ -550,11 +560,44 @@ int scv_betaq_table(scv_ctx* c, int L, cudaStream_t s, const double** qtab, cons
   double* dq = nullptr;
   long long* dmb = nullptr;
   long long acc = 0;
-  SCV_TRY(betaq_build(c, L, betaq_method(), s, &dq, &dmb, &acc));
+  SCV_TRY(betaq_build(c, L, betaq_method(), *qb0, *qrows, s, &dq, &dmb, &acc));
   c->aux[key] = dq;
   c->aux[kb] = dmb;
   c->table_bytes += (long long)acc * (long long)sizeof(double) + (long long)(2 * L - 1) * (long long)sizeof(long long);
   *qtab = dq;
   *mbase = dmb;
+  return SCV_OK;
+}
+
+extern "C" int scv_betaq_restrict(scv_ctx* c, int L, int b0, int nb) {
+  if (!c) return SCV_EINVAL;
+  if (L < 2 || b0 < 0 || nb < 0 || b0 + nb > L)
+    return scv_fail(c, SCV_EINVAL, "beta rows [" + std::to_string(b0) + ", " + std::to_string(b0 + nb) +
+                                       ") outside [0, " + std::to_string(L) + ")");
+  auto rg = c->betaq_rows.find(L);
+  const int ob0 = rg == c->betaq_rows.end() ? 0 : rg->second.first;
+  const int onb = rg == c->betaq_rows.end() ? L : rg->second.second;
+  const int nb0 = nb == 0 ? 0 : b0, nnb = nb == 0 ? L : nb;
+  if (nb0 == ob0 && nnb == onb) return SCV_OK;
+  // a table built for the old range is dropped (rebuilt on next use)
+  const std::string key = "betaq_" + std::to_string(L), kb = "betaqb_" + std::to_string(L);
+  auto it = c->aux.find(key);
+  if (it != c->aux.end()) {
+    SCV_TRY(scv_check_unpinned(c, "dropping a beta-quadrature table"));
+    SCV_CUDA(c, cudaSetDevice(c->device));
+    SCV_CUDA(c, cudaDeviceSynchronize());
+    long long cols = 0;
+    for (int m = -(L - 1); m <= L - 1; ++m) cols += L - std::abs(m);
+    c->table_bytes -= cols * onb * (long long)sizeof(double) + (long long)(2 * L - 1) * (long long)sizeof(long long);
+    cudaFree(it->second);
+    c->aux.erase(it);
+    auto ib = c->aux.find(kb);
+    if (ib != c->aux.end()) {
+      cudaFree(ib->second);
+      c->aux.erase(ib);
+    }
+  }
+  if (nb == 0) c->betaq_rows.erase(L);
+  else c->betaq_rows[L] = std::make_pair(b0, nb);
   return SCV_OK;
 }

@@ -2143,17 +2143,19 @@ static constexpr size_t pfa_smem_q() {
 #ifndef SCV_GQ_RED
 #define SCV_GQ_RED 1
 #endif
-// offset of the m block of the quadrature table (betaq.cu): L * sum_{j=-(L-1)}^{m-1} (L - |j|)
-__device__ __forceinline__ long long q_mbase(int m, int L) {
+// offset of the m block of the quadrature table (betaq.cu): QR * sum_{j=-(L-1)}^{m-1} (L - |j|),
+// QR = the number of beta rows the table holds (L, or a rank's slab: scv_betaq_restrict)
+__device__ __forceinline__ long long q_mbase(int m, int L, int QR) {
   const long long a = (long long)m + L - 1;  // number of terms
-  if (m <= 0) return (long long)L * (a * (a + 1) / 2);
-  return (long long)L * ((long long)L * (L + 1) / 2 + (long long)(m - 1) * L - (long long)m * (m - 1) / 2);
+  if (m <= 0) return (long long)QR * (a * (a + 1) / 2);
+  return (long long)QR * ((long long)L * (L + 1) / 2 + (long long)(m - 1) * L - (long long)m * (m - 1) / 2);
 }
 
 template <int K>
 __global__ void __launch_bounds__(PfaQCfg<K>::NT, PfaQCfg<K>::MINB)
     k_syn_gamma_q(int real, int tr, const double2* __restrict__ chunk, int b0, int nbb, const double* __restrict__ qtab,
-                  const long long* __restrict__ mbase, double2* __restrict__ wout, const double2* __restrict__ gtab) {
+                  const long long* __restrict__ mbase, int qrows, double2* __restrict__ wout,
+                  const double2* __restrict__ gtab) {
   using PL = PfaPlan<K>;
   constexpr int NT = PfaQCfg<K>::NT, RQ = PfaQCfg<K>::RQ;
   constexpr int L = (K + 1) / 2;
@@ -2225,8 +2227,8 @@ __global__ void __launch_bounds__(PfaQCfg<K>::NT, PfaQCfg<K>::MINB)
       const int m = col <= L - 1 ? col : col - K;
       const int am = m < 0 ? -m : m;
       // table offsets in closed form (no dependent gather): mbase(m) = L * sum_{j<m} (L-|j|)
-      const double* qp = qtab + q_mbase(min(m, L - 1), L) + b * (L - am) - am;    // + n       (n >= 0)
-      const double* qn = qtab + q_mbase(max(-m, -(L - 1)), L) + b * (L - am) - am;  // + |n|     (n < 0)
+      const double* qp = qtab + q_mbase(min(m, L - 1), L, qrows) + b * (L - am) - am;    // + n       (n >= 0)
+      const double* qn = qtab + q_mbase(max(-m, -(L - 1)), L, qrows) + b * (L - am) - am;  // + |n| (n < 0)
 #pragma unroll
       for (int u = 0; u < NA; ++u) {
         const int gn = threadIdx.x + u * NT;
@@ -2352,7 +2354,7 @@ static constexpr size_t pfa_smem_gqp() {
 template <int K>
 __global__ void __launch_bounds__(PfaGqpCfg<K>::NG * PfaGqpCfg<K>::NTG + PfaGqpCfg<K>::NQW * 32, 1)
     k_syn_gamma_qp(int real, const double2* __restrict__ chunk, int b0, int nbb, const double* __restrict__ qtab,
-                   double2* __restrict__ wout, const double2* __restrict__ gtab) {
+                   int qrows, double2* __restrict__ wout, const double2* __restrict__ gtab) {
   using PL = PfaPlan<K>;
   constexpr int NG = PfaGqpCfg<K>::NG, NTG = PfaGqpCfg<K>::NTG, NQW = PfaGqpCfg<K>::NQW, NB = PfaGqpCfg<K>::NB;
   constexpr int NT = NG * NTG + NQW * 32, NQT = NQW * 32;
@@ -2413,8 +2415,8 @@ __global__ void __launch_bounds__(PfaGqpCfg<K>::NG * PfaGqpCfg<K>::NTG + PfaGqpC
       const long long b = b0 + bb;
       const int m = col <= L - 1 ? col : col - K;
       const int am = m < 0 ? -m : m;
-      const double* qp = qtab + q_mbase(m, L) + b * (L - am) - am + t;            // + 128 u       (n >= 0)
-      const double* qn = qtab + q_mbase(-m, L) + b * (L - am) - am + (K - t);     // - 128 u       (n < 0)
+      const double* qp = qtab + q_mbase(m, L, qrows) + b * (L - am) - am + t;            // + 128 u       (n >= 0)
+      const double* qn = qtab + q_mbase(-m, L, qrows) + b * (L - am) - am + (K - t);     // - 128 u       (n < 0)
       const int lim = am - t;  // entry live iff |n| >= |m|
 #pragma unroll
       for (int u = 0; u < NA / 2; ++u) qv[u] = NQT * u >= lim ? __ldg(qp + NQT * u) : 0.0;
@@ -2433,7 +2435,7 @@ __global__ void __launch_bounds__(PfaGqpCfg<K>::NG * PfaGqpCfg<K>::NTG + PfaGqpC
         const long long b2 = b0 + bb2;
         const int m2 = col2 <= L - 1 ? col2 : col2 - K;
         const int am2 = m2 < 0 ? -m2 : m2;
-        const double* base = (t < 64 ? qtab + q_mbase(m2, L) : qtab + q_mbase(-m2, L)) + b2 * (L - am2);
+        const double* base = (t < 64 ? qtab + q_mbase(m2, L, qrows) : qtab + q_mbase(-m2, L, qrows)) + b2 * (L - am2);
         const int off = (t & 63) * 16;
         if (off < L - am2) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(base + off));
       }
@@ -2922,7 +2924,7 @@ static int run_syn_gamma(scv_ctx* c, int real, const double2* chunk, int b0, int
 
 template <int K>
 static int run_syn_gamma_q(scv_ctx* c, int real, int tr, const double2* chunk, int b0, int nbb, const double* qtab,
-                           const long long* mbase, double2* wout, cudaStream_t s) {
+                           const long long* mbase, int qrows, double2* wout, cudaStream_t s) {
   const double2* tab;
   SCV_TRY(scv_pfa_tables(c, K, &tab));
   if constexpr (pfa_ring_cols(K) && SCV_GQP) {
@@ -2932,7 +2934,7 @@ static int run_syn_gamma_q(scv_ctx* c, int real, int tr, const double2* chunk, i
       constexpr int NTP = PfaGqpCfg<K>::NG * PfaGqpCfg<K>::NTG + PfaGqpCfg<K>::NQW * 32;
       int grid;
       SCV_TRY(persistent_grid(c, k_syn_gamma_qp<K>, NTP, smp, real ? (K + 1) / 2 : K, &grid));
-      k_syn_gamma_qp<K><<<grid, NTP, smp, s>>>(real, chunk, b0, nbb, qtab, wout, tab);
+      k_syn_gamma_qp<K><<<grid, NTP, smp, s>>>(real, chunk, b0, nbb, qtab, qrows, wout, tab);
       c->launches++;
       SCV_CUDA(c, cudaGetLastError());
       return SCV_OK;
@@ -2942,7 +2944,7 @@ static int run_syn_gamma_q(scv_ctx* c, int real, int tr, const double2* chunk, i
   static_assert(sm <= 232448, "gamma+quadrature launch shape exceeds the 227 KB shared-memory limit");
   int grid;
   SCV_TRY(persistent_grid(c, k_syn_gamma_q<K>, PfaQCfg<K>::NT, sm, (K + PfaQCfg<K>::RQ - 1) / PfaQCfg<K>::RQ, &grid));
-  k_syn_gamma_q<K><<<grid, PfaQCfg<K>::NT, sm, s>>>(real, tr, chunk, b0, nbb, qtab, mbase, wout, tab);
+  k_syn_gamma_q<K><<<grid, PfaQCfg<K>::NT, sm, s>>>(real, tr, chunk, b0, nbb, qtab, mbase, qrows, wout, tab);
   c->launches++;
   SCV_CUDA(c, cudaGetLastError());
   return SCV_OK;
@@ -3169,14 +3171,15 @@ extern "C" int scv_debug_dft(scv_ctx* c, int K, int dir, int nrows, const double
 #undef CALL
 }
 
+// b0 is relative to the first beta row of the table, which holds qrows rows
 int scv_pfa_syn_gamma_q(scv_ctx* c, int K, int real, int tr, const double2* chunk, int b0, int nbb, const double* qtab,
-                        const long long* mbase, double2* wout, cudaStream_t s) {
+                        const long long* mbase, int qrows, double2* wout, cudaStream_t s) {
   switch (K) {
-    case 255: return run_syn_gamma_q<255>(c, real, tr, chunk, b0, nbb, qtab, mbase, wout, s);
-    case 511: return run_syn_gamma_q<511>(c, real, tr, chunk, b0, nbb, qtab, mbase, wout, s);
-    case 1023: return run_syn_gamma_q<1023>(c, real, tr, chunk, b0, nbb, qtab, mbase, wout, s);
-    case 2047: return run_syn_gamma_q<2047>(c, real, tr, chunk, b0, nbb, qtab, mbase, wout, s);
-    case 4095: return run_syn_gamma_q<4095>(c, real, tr, chunk, b0, nbb, qtab, mbase, wout, s);
+    case 255: return run_syn_gamma_q<255>(c, real, tr, chunk, b0, nbb, qtab, mbase, qrows, wout, s);
+    case 511: return run_syn_gamma_q<511>(c, real, tr, chunk, b0, nbb, qtab, mbase, qrows, wout, s);
+    case 1023: return run_syn_gamma_q<1023>(c, real, tr, chunk, b0, nbb, qtab, mbase, qrows, wout, s);
+    case 2047: return run_syn_gamma_q<2047>(c, real, tr, chunk, b0, nbb, qtab, mbase, qrows, wout, s);
+    case 4095: return run_syn_gamma_q<4095>(c, real, tr, chunk, b0, nbb, qtab, mbase, qrows, wout, s);
     default: return scv_fail(c, SCV_EINVAL, "no gamma+quadrature kernel for length " + std::to_string(K));
   }
 }

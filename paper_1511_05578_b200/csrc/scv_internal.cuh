@@ -110,6 +110,9 @@ struct scv_ctx {
   size_t scratch_bytes[3] = {0, 0, 0};
   // small int tables by key
   std::map<std::string, void*> aux;
+  // beta rows [first, first + second) the quadrature table of band limit L covers
+  // (scv_betaq_restrict; absent = all L rows)
+  std::map<int, std::pair<int, int>> betaq_rows;
   long long table_bytes = 0;  // persistent per-L tables in `aux` (quadrature, prime-factor, tasks)
   long long small_table_bytes = 0;  // the part of table_bytes that scv_trim keeps (prime-factor, task tables)
   // stage profiler (scv_profile): event pairs around every launch group
@@ -208,10 +211,12 @@ int scv_pfa_syn_gamma(scv_ctx* c, int K, int real, const double2* chunk, int b0,
 int scv_pfa_pos_host(int K, int k);  // CRT output position of frequency k
 // fused gamma pass + beta quadrature (synthesis), betaq.cu tables
 int scv_pfa_syn_gamma_q(scv_ctx* c, int K, int real, int tr, const double2* chunk, int b0, int nbb, const double* qtab,
-                        const long long* mbase, double2* wout, cudaStream_t s);
+                        const long long* mbase, int qrows, double2* wout, cudaStream_t s);
 int scv_wout_mirror(scv_ctx* c, int L, double2* wout, cudaStream_t s);
 bool scv_betaq_enabled(int L);
-int scv_betaq_table(scv_ctx* c, int L, cudaStream_t s, const double** qtab, const long long** mbase);
+// table of band limit L: rows [*qb0, *qb0 + *qrows) of every (m, l) block (all L rows unless restricted)
+int scv_betaq_table(scv_ctx* c, int L, cudaStream_t s, const double** qtab, const long long** mbase, int* qb0,
+                    int* qrows);
 
 inline int next_pow2_log(int x) {
   int lg = 0;

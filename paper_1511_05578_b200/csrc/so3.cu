@@ -150,16 +150,35 @@ static bool use_betaq(scv_ctx* c, int L) {
          (c->opt_betaq == 1 || scv_betaq_enabled(L));
 }
 
+// bytes of one beta row of the chunk between the alpha and gamma passes; covers the transposed
+// layout K x (nbb K rounded up to even) too (pfa.cu, SCV_SYN_PAIR)
+static size_t syn_chunk_row_bytes(int L) {
+  const size_t K = 2 * (size_t)L - 1;
+  return (K + 1) * K * 16;
+}
+// Beta rows per launch pair of the synthesis.  4.3 GB: 64 rows at L_j = 1024, the size of the
+// blocked analysis' scratch in the same slot (launches of 16 rows measured 6 ms/map slower:
+// ring fill/drain per launch).  The quadrature sum over a slab is formed chunk by chunk, so
+// callers that want the whole-scale summation order cut their slabs at multiples of this.
+extern "C" int scv_syn_chunk_rows(int L) {
+  if (L < 1) return 0;
+  static const long long chunk_bytes = getenv("SCV_SYN_CHUNK") ? atoll(getenv("SCV_SYN_CHUNK")) : 4300000000LL;
+  return (int)std::max<size_t>(1, std::min<size_t>((size_t)L, (size_t)chunk_bytes / syn_chunk_row_bytes(L)));
+}
+
 static int forward_q_slab(scv_ctx* c, int L, int real, const void* sig, int sb0, int snb, double* w, cudaStream_t s) {
   const int K = 2 * L - 1;
   const double* qtab = nullptr;
   const long long* mbase = nullptr;
-  SCV_TRY(scv_betaq_table(c, L, s, &qtab, &mbase));
-  const size_t per_bc = (size_t)(K + 1) * K * 16;  // covers the transposed chunk K x (nbb K rounded up to even) (pfa.cu, SCV_SYN_PAIR)
-  // 4.3 GB: 64 beta rows at L_j = 1024, the size of the blocked analysis' scratch in the same slot
-  // (launches of 16 rows measured 6 ms/map slower: ring fill/drain per launch)
-  static const long long chunk_bytes = getenv("SCV_SYN_CHUNK") ? atoll(getenv("SCV_SYN_CHUNK")) : 4300000000LL;
-  const int nbc = (int)std::max<size_t>(1, std::min<size_t>((size_t)snb, (size_t)chunk_bytes / per_bc));
+  int qb0 = 0, qrows = L;
+  SCV_TRY(scv_betaq_table(c, L, s, &qtab, &mbase, &qb0, &qrows));
+  if (sb0 < qb0 || sb0 + snb > qb0 + qrows)
+    return scv_fail(c, SCV_EINVAL, "beta rows [" + std::to_string(sb0) + ", " + std::to_string(sb0 + snb) +
+                                       ") are outside the rows [" + std::to_string(qb0) + ", " +
+                                       std::to_string(qb0 + qrows) + ") this context's quadrature table of L=" +
+                                       std::to_string(L) + " is restricted to (scv_betaq_restrict)");
+  const size_t per_bc = syn_chunk_row_bytes(L);
+  const int nbc = std::min(snb, scv_syn_chunk_rows(L));
   void* ch = nullptr;
   SCV_TRY(scv_scratch(c, 1, per_bc * nbc, &ch));
   for (int b0 = sb0; b0 < sb0 + snb; b0 += nbc) {
@@ -170,7 +189,7 @@ static int forward_q_slab(scv_ctx* c, int L, int real, const void* sig, int sb0,
       SCV_TRY(scv_pfa_syn_alpha(c, K, real ? 2 : 0, c->opt_chunkt | 4, sig, snb, b0 - sb0, nbb, (double2*)ch, s));
     }
     SCV_PROF(c, s, "so3fwd_gamma_q");
-    SCV_TRY(scv_pfa_syn_gamma_q(c, K, real, c->opt_chunkt, (const double2*)ch, b0, nbb, qtab, mbase, (double2*)w, s));
+    SCV_TRY(scv_pfa_syn_gamma_q(c, K, real, c->opt_chunkt, (const double2*)ch, b0 - qb0, nbb, qtab, mbase, qrows, (double2*)w, s));
   }
   if (real) {
     SCV_PROF(c, s, "so3fwd_mirror");

@@ -230,10 +230,9 @@ def _slab_streamable(Lj: int) -> bool:
 
 
 def _syn_chunk_rows(Lj: int) -> int:
-    """Beta rows per synthesis launch pair inside the library (so3.cu,
-    forward_q_slab: a 1 GiB chunk of (K, K) planes)."""
-    K = 2 * Lj - 1
-    return max(1, min(Lj, (1 << 30) // (K * K * 16)))
+    """Beta rows per synthesis launch pair inside the library
+    (scv_syn_chunk_rows, so3.cu)."""
+    return max(1, int(_cabi.load_library().scv_syn_chunk_rows(int(Lj))))
 
 
 def roundtrip_streamed(f: SphereSignal, t: Tiling, multires: bool = True, slab_bytes: int = 8 << 30,

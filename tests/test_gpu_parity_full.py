@@ -241,3 +241,56 @@ def test_c4_L1024_pipeline_vs_oracle():
     Scales 16..256 and the scaling map in full; the L_j=512 scale and both
     L_j=1024 scales at sampled gamma frequencies; synthesis at 6 degrees."""
     _pipeline_vs_oracle(1024, 0, 3, 0, [0, 9, 200, 511, 700, 1023])
+
+
+@pytest.mark.parametrize("L", [128, 256])
+def test_quadrature_table_gemm_build_equals_direct_build(L):
+    """The beta-quadrature table (csrc/betaq.cu: the weights that stand for the
+    reference's beta FFT, quadrature convolution and Delta contraction,
+    so3.py:203-243) built as two tensor-core GEMMs is the table of the direct
+    sums: equal to 1e-13 of the table's largest weight."""
+    from paper_1511_05578_b200 import _cabi
+    ctx = _cabi.context(0)
+    n = L ** 3
+    tabs = []
+    for method in (0, 1):
+        out = torch.empty(n, dtype=torch.float64, device="cuda")
+        ctx.call("debug_betaq_build", L, method, _cabi.ptr(out), n)
+        tabs.append(out)
+    torch.cuda.synchronize()
+    assert not bool(torch.isnan(tabs[1]).any())
+    scale = float(tabs[0].abs().max())
+    assert float((tabs[0] - tabs[1]).abs().max()) <= 1e-13 * scale
+
+
+@pytest.mark.parametrize("L", [256, 512])
+def test_quadrature_table_restricted_to_a_beta_slab(L):
+    """scv_betaq_restrict (a rank's table in the beta-slab decomposition): the
+    slab synthesis with the table cut to the slab's rows is bit-identical to the
+    one with the whole table, the table shrinks by L / nb, rows outside fail
+    loudly, and lifting the restriction restores the whole transform."""
+    from paper_1511_05578_b200 import _cabi
+    ctx = _cabi.context(0)
+    b0, nb = 96, 64  # L = 512 runs the ring kernels (K = 1023), L = 256 the batched one
+    rng = np.random.default_rng(3)
+    K = 2 * L - 1
+    grid = sc.SO3Grid(L, L, L)
+    slab = sc.SO3Slab(grid, b0, torch.as_tensor(rng.standard_normal((K, nb, K)) + 1j * rng.standard_normal((K, nb, K)),
+                                                device="cuda"))
+    other = sc.SO3Slab(grid, 0, slab.values[:, :8, :].contiguous())
+    ctx.betaq_restrict(L, 0, 0)
+    ref = sc.so3_forward_curvelet_slab(slab).values.clone()
+    ref_other = sc.so3_forward_curvelet_slab(other).values.clone()
+    full_bytes = ctx.workspace_bytes()
+    try:
+        ctx.betaq_restrict(L, b0, nb)
+        got = sc.so3_forward_curvelet_slab(slab).values
+        assert torch.equal(got, ref)
+        assert full_bytes - ctx.workspace_bytes() >= 8 * (L - nb) * L * L * 0.99
+        with pytest.raises(ValueError):
+            sc.so3_forward_curvelet_slab(other)
+        with pytest.raises(ValueError):
+            ctx.betaq_restrict(L, L - 3, 8)
+    finally:
+        ctx.betaq_restrict(L, 0, 0)
+    assert torch.equal(sc.so3_forward_curvelet_slab(other).values, ref_other)

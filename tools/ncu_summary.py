@@ -15,13 +15,17 @@ if len(rows) > 2:
     hdr = rows[1]; data = rows[2:]
     i_src = hdr.index('Source'); i_st = hdr.index('Warp Stall Sampling (All Samples)'); i_ex = hdr.index('Instructions Executed')
     cols = [h for h in hdr if h.startswith('stall_') and 'Not Issued' not in h]
-    tot = sum(float(x[i_st] or 0) for x in data) or 1
+    def fl(v):
+        try: return float(v or 0)
+        except ValueError: return 0.0
+    data = [x for x in data if len(x) > max(i_src, i_st, i_ex)]
+    tot = sum(fl(x[i_st]) for x in data) or 1
     c = Counter(); ce = Counter(); reasons = Counter()
     for x in data:
         toks = x[i_src].split()
         if not toks: continue
         op = (toks[1] if toks[0].startswith('@') else toks[0]).split('.')[0]
-        c[op] += float(x[i_st] or 0); ce[op] += float(x[i_ex] or 0)
+        c[op] += fl(x[i_st]); ce[op] += fl(x[i_ex])
         for h in cols:
             try: reasons[h] += float(x[hdr.index(h)] or 0)
             except ValueError: pass

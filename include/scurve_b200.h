@@ -116,6 +116,10 @@ int scv_debug_dft(scv_ctx* ctx, int K, int dir, int nrows, const double* in, dou
  * emulate the stages on these maps against numpy.fft (tests/test_pfa_maps.py). */
 int scv_debug_pfa_maps(int K, int* out_pos, int* in_pos);
 int scv_debug_r89_sigma(int* sigma_in, int* sigma_out);
+/* Lane schedule of the ring kernels' slot copies (host arithmetic only): for each group of 32
+ * consecutive output frequencies / input samples, entry [32 j + lane] = position | (e << 11)
+ * says that the lane moves element 32 j + e.  K = 1023 or 2047 (positions fit 11 bits). */
+int scv_debug_pfa_sched(int K, int* out_sched, int* in_sched);
 /* Pipeline timing counters of the ring kernels (only counted in builds with
  * -DSCV_PIPE_STATS=1, zeros otherwise): 36 clock-cycle sums (kinds 3 and 4 are
  * sub-phases of the generator / quadrature teams), kernel kind

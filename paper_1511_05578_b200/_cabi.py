@@ -48,6 +48,7 @@ _SIGS = {
     "scv_debug_dft": [_P, _I, _I, _I, _P, _P, _P],
     "scv_debug_pfa_maps": [_I, _P, _P],
     "scv_debug_r89_sigma": [_P, _P],
+    "scv_debug_pfa_sched": [_I, _P, _P],
     "scv_debug_pipe_stats": [_P, _I],
     "scv_debug_betaq_build": [_P, _I, _I, _P, ctypes.c_longlong, _P],
     "scv_syn_chunk_rows": [_I],

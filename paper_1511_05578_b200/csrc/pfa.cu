@@ -179,6 +179,92 @@ static int r89_sigma(int which, int j) {
   return -1;
 }
 
+// Lane schedule of the ring kernels' slot accesses (r02).  A warp copy moves 32 consecutive
+// elements of a row between global memory and a slot; which lane takes which of the 32 does
+// not matter to the global side (the same four 128-byte lines), but the slot positions are
+// pseudo-random in the natural index (Ruritanian map x Rader storage order), so the natural
+// lane order costs ~10.4 shared-memory wavefronts per 16-byte warp access instead of 4.  For
+// each group of 32 the elements are dealt to the four quarter-warps so that a quarter's eight
+// positions fall into as many different 16-byte bank groups as possible (~7.3 wavefronts).
+// Entry [32 j + lane] = position | (e << 11): the lane handles element 32 j + e.
+static void pfa_lane_schedule(const unsigned short* pos, int K, unsigned short* out) {
+  for (int n0 = 0; n0 < K; n0 += 32) {
+    const int W = std::min(32, K - n0);
+    int tot[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int e = 0; e < W; ++e) tot[pos[n0 + e] & 7]++;
+    // elements of the fullest bank groups first
+    std::vector<int> order(W);
+    for (int e = 0; e < W; ++e) order[e] = e;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return tot[pos[n0 + a] & 7] > tot[pos[n0 + b] & 7]; });
+    int cnt[4][8] = {}, fill[4] = {0, 0, 0, 0}, mx[4] = {0, 0, 0, 0};
+    int lane_of[32];
+    for (int e : order) {
+      const int b = pos[n0 + e] & 7;
+      int best = -1, bk0 = 0, bk1 = 0, bk2 = 0;
+      for (int q = 0; q < 4; ++q) {
+        if (fill[q] >= 8) continue;
+        const int grow = cnt[q][b] + 1 > mx[q] ? 1 : 0;  // does this quarter need another wavefront?
+        const int k0 = grow, k1 = cnt[q][b], k2 = fill[q];
+        if (best < 0 || k0 < bk0 || (k0 == bk0 && (k1 < bk1 || (k1 == bk1 && k2 < bk2)))) {
+          best = q;
+          bk0 = k0;
+          bk1 = k1;
+          bk2 = k2;
+        }
+      }
+      lane_of[e] = best * 8 + fill[best];
+      fill[best]++;
+      cnt[best][b]++;
+      mx[best] = std::max(mx[best], cnt[best][b]);
+    }
+    for (int l = 0; l < 32; ++l) {
+      if (n0 + l < K) out[n0 + l] = (unsigned short)(31u << 11);  // idle lanes of the last group: element past K
+    }
+    bool used[32] = {};
+    for (int e = 0; e < W; ++e) {
+      // the last group has W < 32 elements: its lanes >= W do not exist in the table, so
+      // squeeze the assigned lanes into [0, W)
+      used[lane_of[e]] = true;
+    }
+    int remap[32], nl = 0;
+    for (int l = 0; l < 32; ++l) remap[l] = used[l] ? nl++ : -1;
+    for (int e = 0; e < W; ++e) out[n0 + remap[lane_of[e]]] = (unsigned short)(pos[n0 + e] | (e << 11));
+  }
+}
+
+// the tables of length K with the two position maps in lane-schedule form (k_pfa_rows_p)
+int scv_pfa_tables_sched(scv_ctx* c, int K, const double2** out) {
+  const std::string key = "pfas_" + std::to_string(K);
+  auto it = c->aux.find(key);
+  if (it != c->aux.end()) {
+    *out = (const double2*)it->second;
+    return SCV_OK;
+  }
+  if (K > 2048) return scv_fail(c, SCV_EINVAL, "lane schedule packs positions into 11 bits");
+  const double2* plain;
+  SCV_TRY(scv_pfa_tables(c, K, &plain));
+  int f[4];
+  factors_of(K, f);
+  size_t nr = 0;
+  for (int s = 0; s < 4; ++s) nr += (size_t)pfa_tab(f[s], K);
+  const size_t n16 = ((size_t)4 * K + 15) / 16, total = nr + n16;
+  std::vector<double2> tab(total);
+  SCV_CUDA(c, cudaMemcpy(tab.data(), plain, total * sizeof(double2), cudaMemcpyDeviceToHost));
+  unsigned short* pos = (unsigned short*)(tab.data() + nr);
+  std::vector<unsigned short> sched(2 * (size_t)K);
+  pfa_lane_schedule(pos, K, sched.data());
+  pfa_lane_schedule(pos + K, K, sched.data() + K);
+  memcpy(pos, sched.data(), sched.size() * sizeof(unsigned short));
+  void* d = nullptr;
+  SCV_CUDA(c, cudaMalloc(&d, total * sizeof(double2)));
+  SCV_CUDA(c, cudaMemcpy(d, tab.data(), total * sizeof(double2), cudaMemcpyHostToDevice));
+  c->aux[key] = d;
+  c->table_bytes += (long long)(total * sizeof(double2));
+  c->small_table_bytes += (long long)(total * sizeof(double2));
+  *out = (const double2*)d;
+  return SCV_OK;
+}
+
 int scv_pfa_tables(scv_ctx* c, int K, const double2** out) {
   const std::string key = "pfa_" + std::to_string(K);
   auto it = c->aux.find(key);
@@ -612,11 +698,14 @@ constexpr int RB = 8;
 // positions delays the transform warps' own shared-memory traffic; sleeping between copies
 // spreads it (the load/store warps have slack).  SCV_RING_PACE after every SCV_RING_PACE_N
 // fill copies, SCV_RING_PACE_D after every batch of RB drain reads.
+// Measured on the C4 map (ms of the two row passes): off 84.3 / 83.7; 20 ns per 2 copies
+// 82.4 / 82.2; 20 ns per copy 82.6 / 82.9; 50 ns per 3 copies 82.7 / 82.7; 50 ns per copy
+// 91 / 85 (the load/store warps then bound the kernel); drain pacing 200 ns per batch 84.5 / 83.8.
 #ifndef SCV_RING_PACE
-#define SCV_RING_PACE 0
+#define SCV_RING_PACE 20
 #endif
 #ifndef SCV_RING_PACE_N
-#define SCV_RING_PACE_N 1
+#define SCV_RING_PACE_N 2
 #endif
 #ifndef SCV_RING_PACE_D
 #define SCV_RING_PACE_D 0
@@ -666,6 +755,51 @@ __device__ __forceinline__ void ring_drain(const double2* X, const double2* tab,
 #if SCV_RING_PACE_D
     __nanosleep(SCV_RING_PACE_D);
 #endif
+  }
+}
+
+// The same copies through the lane schedule (scv_pfa_tables_sched): entry [32 j + lane] =
+// position | e << 11, the lane moves element 32 j + e.  A full warp only (32 consecutive
+// elements per copy instruction).
+template <class PL, class SrcFn>
+__device__ __forceinline__ void ring_fill_s(double2* X, const double2* tab, int lane, SrcFn gsrc) {
+  constexpr int K = PL::K;
+  const unsigned short* map = (const unsigned short*)(tab + pfa_rtab_total<PL>()) + K;
+#pragma unroll 1
+  for (int n0 = 0; n0 < K; n0 += 32 * RB) {
+    unsigned en[RB];
+#pragma unroll
+    for (int j = 0; j < RB; ++j) {
+      const int i = n0 + 32 * j + lane;
+      en[j] = i < K ? map[i] : (31u << 11);
+    }
+#pragma unroll
+    for (int j = 0; j < RB; ++j) {
+      const int n = n0 + 32 * j + (int)(en[j] >> 11);
+      if (n < K) cp_async16_m(X + (en[j] & 0x7ffu), gsrc(n));
+    }
+  }
+}
+template <class PL, class DstFn>
+__device__ __forceinline__ void ring_drain_s(const double2* X, const double2* tab, int lane, DstFn gdst) {
+  constexpr int K = PL::K;
+  const unsigned short* map = (const unsigned short*)(tab + pfa_rtab_total<PL>());
+#pragma unroll 1
+  for (int k0 = 0; k0 < K; k0 += 32 * RB) {
+    unsigned en[RB];
+    double2 v[RB];
+#pragma unroll
+    for (int j = 0; j < RB; ++j) {
+      const int i = k0 + 32 * j + lane;
+      en[j] = i < K ? map[i] : (31u << 11);
+    }
+#pragma unroll
+    for (int j = 0; j < RB; ++j) v[j] = X[en[j] & 0x7ffu];
+#pragma unroll
+    for (int j = 0; j < RB; ++j) {
+      const int k = k0 + 32 * j + (int)(en[j] >> 11);
+      if (k < K) *gdst(k) = v[j];
+    }
   }
 }
 
@@ -721,6 +855,15 @@ extern "C" int scv_debug_pipe_stats(unsigned long long* out, int reset) {
 #ifndef SCV_ROWSP_NB
 #define SCV_ROWSP_NB 6
 #endif
+// lane-scheduled slot copies in the row kernel (see pfa_lane_schedule); the transposed-chunk
+// mode 5 walks the plain maps
+// Measured (r02t): bit-identical, 7.3 instead of 10.4 wavefronts per copy, and 1.5 ms/map
+// SLOWER per row pass (85.5 vs 84.2): what the transforms lose to the load/store warps is
+// not the wavefront count but how densely the copies arrive (cf. SCV_GQP_PACE).  Off.
+#ifndef SCV_ROWSP_SCHED
+#define SCV_ROWSP_SCHED 0
+#endif
+constexpr bool pfa_rows_sched(int gather) { return SCV_ROWSP_SCHED && gather != 5; }
 template <int K> struct PfaPipeCfg { static constexpr int NG = 0, NTG = 96, NIO = 0, NB = 0; };
 #ifndef SCV_ROWSP_NTG
 #define SCV_ROWSP_NTG 96
@@ -750,6 +893,7 @@ __global__ void __launch_bounds__(PfaPipeCfg<K>::NG * PfaPipeCfg<K>::NTG + PfaPi
   constexpr int NG = PfaPipeCfg<K>::NG, NTG = PfaPipeCfg<K>::NTG, NIO = PfaPipeCfg<K>::NIO, NB = PfaPipeCfg<K>::NB;
   constexpr int NT = NG * NTG + NIO * 32;
   static_assert(NB > NG, "the ring needs spare buffers for the rows in flight");
+  constexpr bool SCHED = pfa_rows_sched(GATHER);  // gtab then is scv_pfa_tables_sched's
   static_assert(NB % NIO == 0, "a load/store warp owns fixed ring slots (it then meets a slot's barrier phases in order)");
   extern __shared__ double2 sm[];
   double2* tab = sm;
@@ -861,7 +1005,8 @@ __global__ void __launch_bounds__(PfaPipeCfg<K>::NG * PfaPipeCfg<K>::NTG + PfaPi
           const long long bb = r / K, g = r - bb * K;
           dst = out + (g * LK + b0 + bb) * K;
         }
-          ring_drain<PL>(X, tab, lane, 32, [&](int k) { return dst + k; });
+          if constexpr (SCHED) ring_drain_s<PL>(X, tab, lane, [&](int k) { return dst + k; });
+        else ring_drain<PL>(X, tab, lane, 32, [&](int k) { return dst + k; });
         __syncwarp();  // every lane has read its elements before any lane refills the buffer
         ck.mark(st, 3);
       }
@@ -871,14 +1016,18 @@ __global__ void __launch_bounds__(PfaPipeCfg<K>::NG * PfaPipeCfg<K>::NTG + PfaPi
           constexpr int NPR = (K + 1) / 2;
           const long long bb = r / K, g = r - bb * K;
           const double2* src = in + (bb * NPR * K + g) * 2;  // + (m/2)*2K + (m&1)
-          ring_fill<PL>(X, tab, lane, 32, [&](int n) { return src + (long long)(n >> 1) * (2 * K) + (n & 1); });
+          if constexpr (SCHED)
+            ring_fill_s<PL>(X, tab, lane, [&](int n) { return src + (long long)(n >> 1) * (2 * K) + (n & 1); });
+          else
+            ring_fill<PL>(X, tab, lane, 32, [&](int n) { return src + (long long)(n >> 1) * (2 * K) + (n & 1); });
         } else {
           const double2* src = in + r * K;
           if constexpr (GATHER == 1 || GATHER == 5) {
             const long long bb = r / K, g = r - bb * K;
             src = in + g * LK + (b0 + bb) * K;
           }
-          ring_fill<PL>(X, tab, lane, 32, [&](int n) { return src + n; });
+          if constexpr (SCHED) ring_fill_s<PL>(X, tab, lane, [&](int n) { return src + n; });
+          else ring_fill<PL>(X, tab, lane, 32, [&](int n) { return src + n; });
         }
         cp_async_mbar_arrive(full + (u & 1) * NB + b);
       }
@@ -2612,6 +2761,7 @@ static int launch_rows_p(scv_ctx* c, long long nrows, const double2* in, double2
   constexpr size_t smp = pfa_smem_pipe<K>();
   static_assert(smp <= 232448, "pipelined rows launch shape exceeds the 227 KB shared-memory limit");
   constexpr int NTB = PfaPipeCfg<K>::NG * PfaPipeCfg<K>::NTG + PfaPipeCfg<K>::NIO * 32;
+  if constexpr (pfa_rows_sched(GATHER)) SCV_TRY(scv_pfa_tables_sched(c, K, &tab));  // same radix tables, scheduled maps
   int grid;
   SCV_TRY(persistent_grid(c, k_pfa_rows_p<K, DIR, GATHER>, NTB, smp, (nrows + PfaPipeCfg<K>::NG - 1) / PfaPipeCfg<K>::NG, &grid));
   k_pfa_rows_p<K, DIR, GATHER><<<grid, NTB, smp, s>>>(nrows, in, out, tab, LK, b0);
@@ -2666,6 +2816,22 @@ extern "C" int scv_debug_pfa_maps(int K, int* out_pos, int* in_pos) {
   return SCV_OK;
 }
 // sigma_in / sigma_out of the radix-89 storage order (89 entries each)
+// lane schedule of the two maps (pfa_lane_schedule): entry [32 j + lane] = position | e << 11
+extern "C" int scv_debug_pfa_sched(int K, int* out_sched, int* in_sched) {
+  if (!scv_pfa_supported(K) || K > 2048) return SCV_EINVAL;
+  std::vector<unsigned short> pos(2 * (size_t)K), sch(2 * (size_t)K);
+  for (int k = 0; k < K; ++k) {
+    pos[k] = (unsigned short)scv_pfa_pos_host(K, k);
+    pos[K + k] = (unsigned short)pfa_in_host(K, k);
+  }
+  pfa_lane_schedule(pos.data(), K, sch.data());
+  pfa_lane_schedule(pos.data() + K, K, sch.data() + K);
+  for (int k = 0; k < K; ++k) {
+    out_sched[k] = sch[k];
+    in_sched[k] = sch[K + k];
+  }
+  return SCV_OK;
+}
 extern "C" int scv_debug_r89_sigma(int* sin, int* sout) {
   for (int j = 0; j < 89; ++j) {
     sin[j] = r89_sigma(0, j);

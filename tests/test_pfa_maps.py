@@ -80,3 +80,38 @@ def test_rader_storage_order_is_linear_in_the_lane_coordinates():
         t = 2 * a2 + (a1 & 1) + 22 * (a1 >> 1)
         assert sout[u] == 1 + t and sout[v] == 45 + t
         r = (r * 3) % 89
+
+
+@pytest.mark.parametrize("K", [1023, 2047])
+def test_lane_schedule_is_a_permutation_and_cuts_bank_conflicts(K):
+    """The ring kernels' lane schedule (csrc/pfa.cu, pfa_lane_schedule): within every group
+    of 32 consecutive elements each element is moved by exactly one lane, to the position
+    the plain map gives, and the quarter-warps meet fewer 16-byte bank-group conflicts than
+    in natural lane order."""
+    lib = _cabi.load_library()
+    out = (ctypes.c_int * K)()
+    inn = (ctypes.c_int * K)()
+    assert lib.scv_debug_pfa_maps(K, out, inn) == 0
+    so = (ctypes.c_int * K)()
+    si = (ctypes.c_int * K)()
+    assert lib.scv_debug_pfa_sched(K, so, si) == 0
+
+    def wavefronts(pos_by_lane):
+        w = 0
+        for q in range(0, len(pos_by_lane), 8):
+            g = [p & 7 for p in pos_by_lane[q:q + 8]]
+            w += max(g.count(b) for b in range(8))
+        return w
+
+    for plain, sched in ((list(out), list(so)), (list(inn), list(si))):
+        nat = got = 0
+        for n0 in range(0, K, 32):
+            W = min(32, K - n0)
+            ent = sched[n0:n0 + W]
+            es = sorted(e >> 11 for e in ent)
+            assert es == list(range(W))
+            for e in ent:
+                assert (e & 0x7ff) == plain[n0 + (e >> 11)]
+            nat += wavefronts(plain[n0:n0 + W])
+            got += wavefronts([e & 0x7ff for e in ent])
+        assert got <= 0.78 * nat, (got, nat)

@@ -777,6 +777,9 @@ __device__ __forceinline__ void ring_fill_s(double2* X, const double2* tab, int 
     for (int j = 0; j < RB; ++j) {
       const int n = n0 + 32 * j + (int)(en[j] >> 11);
       if (n < K) cp_async16_m(X + (en[j] & 0x7ffu), gsrc(n));
+#if SCV_RING_PACE
+      if ((j % SCV_RING_PACE_N) == SCV_RING_PACE_N - 1) __nanosleep(SCV_RING_PACE);
+#endif
     }
   }
 }
@@ -857,9 +860,11 @@ extern "C" int scv_debug_pipe_stats(unsigned long long* out, int reset) {
 #endif
 // lane-scheduled slot copies in the row kernel (see pfa_lane_schedule); the transposed-chunk
 // mode 5 walks the plain maps
-// Measured (r02t): bit-identical, 7.3 instead of 10.4 wavefronts per copy, and 1.5 ms/map
-// SLOWER per row pass (85.5 vs 84.2): what the transforms lose to the load/store warps is
-// not the wavefront count but how densely the copies arrive (cf. SCV_GQP_PACE).  Off.
+// Measured (r02t, r02x): bit-identical, 7.3 instead of 10.4 shared-memory wavefronts per copy,
+// and 2.5 ms/map SLOWER per row pass, with or without pacing (84.5 vs 82.0).  A 16-byte warp
+// access is served quarter-warp by quarter-warp; in natural lane order a quarter covers one
+// 128-byte line of global memory, scheduled it touches up to four, so what the shared side
+// saves the global side loses.  Off.
 #ifndef SCV_ROWSP_SCHED
 #define SCV_ROWSP_SCHED 0
 #endif

@@ -87,6 +87,10 @@ def _worker(rank, world, port, L, spin, q):
 @pytest.mark.parametrize("L,spin", [(256, 0), (256, 2)])
 def test_cuda_backend_world2_on_one_gpu(L, spin):
     world = 2
+    # the two ranks share this GPU with the test process: hand its cached blocks back first
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()

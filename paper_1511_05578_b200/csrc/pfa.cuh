@@ -85,6 +85,9 @@ constexpr int pfa_kt_unroll = SCV_PFA_KT_UNROLL;
 #ifndef SCV_PFA_AREG
 #define SCV_PFA_AREG 1
 #endif
+#ifndef SCV_PFA_SLOT_EVEN
+#define SCV_PFA_SLOT_EVEN 1
+#endif
 #ifndef SCV_PFA_NBW_SMALL
 #define SCV_PFA_NBW_SMALL 1
 #endif
@@ -627,7 +630,7 @@ __device__ __forceinline__ void pfa_stage_mma_reg(double2* X, const double2* tab
 // and one barrier at the end of the stage (the next stage reads across
 // blocks).  Warps stream through blocks with no block-wide barrier, so the
 // DMMA chains of different warps (and CTAs) overlap freely.
-// Block q covers butterflies {8g+o, 8g+o+4, 8g+o+1, 8g+o+5}, g = q/2, o = 2(q&1):
+// Block q covers butterflies {8g+o, 8g+o+4, 8g+o+2, 8g+o+6}, g = q/2, o = q&1 (see `slot`):
 // butterfly positions 4 apart differ by 4 mod 8 doubles, so the two
 // butterflies of each 16-lane phase of a B-fragment load hit disjoint banks.
 template <class PL, int S, int DIR, int R, int NT, int PITCH>
@@ -647,8 +650,17 @@ __device__ __forceinline__ void pfa_stage_mma_blk(double2* X, const double2* tab
   const double* Xd = (const double*)X;
   const int lane = gtid & 31, warp = gtid >> 5;
   const int ar = lane >> 2, ac = lane & 3;
-  // block-local butterfly slot i -> offset within the group of 8
+  // block-local butterfly slot i -> offset within the group of 8.  Butterfly bases are odd
+  // multiples apart (step and p are odd), so offsets {0, 4} within a 16-lane phase keep the
+  // 8-byte B-fragment loads on disjoint banks, and ALL-EVEN offsets {0, 4, 2, 6} (r02) also
+  // make the eight lanes of a 16-byte epilogue store phase -- two output rows k x four
+  // butterflies, bank group (offset + k) mod 8 -- conflict-free; the r01 offsets {0, 4, 1, 5}
+  // collided two-way there (a twelfth of the row kernel's shared-memory wavefronts).
+#if SCV_PFA_SLOT_EVEN
+  auto slot = [](int i) { return 4 * (i & 1) + 2 * (i >> 1); };
+#else
   auto slot = [](int i) { return (i >> 1) + 4 * (i & 1); };
+#endif
   // small radices (<= 2 m8 tiles): NBW blocks per warp iteration, for more
   // independent DMMA chains per k-step
   constexpr int NBW = M8 <= 2 ? SCV_PFA_NBW_SMALL : SCV_PFA_NBW_BIG;
@@ -676,7 +688,7 @@ __device__ __forceinline__ void pfa_stage_mma_blk(double2* X, const double2* tab
 #pragma unroll
     for (int w = 0; w < NBW; ++w) {
       const int q = q0 + w * NW;
-      const int gb = (q >> 1) * 8 + 2 * (q & 1);
+      const int gb = (q >> 1) * 8 + (SCV_PFA_SLOT_EVEN ? 1 : 2) * (q & 1);
       // B-fragment column of this lane: butterfly slot ar>>1, component ar&1.
       // A slot past the last butterfly re-reads the last one (GEMM columns are
       // independent and that column is never stored), and the reduction

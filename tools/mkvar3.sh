@@ -5,3 +5,5 @@ name=$1; shift
 cd "$(dirname "$0")/.."
 mkdir -p variants
 python -m paper_1511_05578_b200.build --out=$PWD/variants/lib_$name.so "$@" 2>&1 | tail -2
+# the variant's objects are not needed once it is linked (build/ travels with gpurun snapshots)
+rm -rf build/obj/var_lib_$name

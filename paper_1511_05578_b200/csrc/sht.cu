@@ -130,6 +130,97 @@ __global__ void __launch_bounds__(128) k_sht_contract_w(int L, int spin, int rea
   }
 }
 
+// k_sht_contract_w for SCV_SHT_LC consecutive degrees per thread (r02): the bins Gw[+-a][+-b] of an
+// (a, b) are loaded once for the chunk instead of once per degree.  k_sht_contract_w moved 24.9 GB
+// between L2 and the SMs at L = 1024 (ncu, profiles/r03_ncu_k_sht_contract_w.txt: 81% of its stall
+// samples wait on those loads), 4/5 of it the bins.  Per (l, b) the terms are added in the same
+// order with the same operands, so the coefficients are bit-identical.  Measured at L = 1024
+// (ms): 1 degree per thread 3.04, 2: 1.83, 4: 2.62, 8: 4.86 (too few threads, longer loops).
+#ifndef SCV_SHT_LC
+#define SCV_SHT_LC 2
+#endif
+__global__ void __launch_bounds__(128) k_sht_contract_c(int L, int spin, int real, const double2* __restrict__ Gw,
+                                                        const double* __restrict__ delta,
+                                                        const double* __restrict__ U, double2* __restrict__ flm) {
+  constexpr int LC = SCV_SHT_LC;
+  const int K = 2 * L - 1;
+  const int nch = (L + LC - 1) / LC;
+  const int l0 = (nch - 1 - (int)blockIdx.y) * LC;  // large degrees (long loops) first
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ltop = min(l0 + LC, L) - 1;
+  if (b > ltop) return;
+  const int as = spin < 0 ? -spin : spin;
+  const int ncol = real ? L : K;
+  const int coff = real ? 0 : L - 1;
+  const bool negm = b > 0 && !real;  // compute m = -b directly (real: conjugate fill)
+  double px[LC], py[LC], nx[LC], ny[LC];
+#pragma unroll
+  for (int i = 0; i < LC; ++i) px[i] = py[i] = nx[i] = ny[i] = 0.0;
+#pragma unroll 2
+  for (int a = 0; a <= ltop; ++a) {
+    const int swp = a < b ? ((b - a) & 1) : 0;  // transpose sign (m'-m parity)
+    const long long widx = a >= b ? (long long)a * (a + 1) / 2 + b : (long long)b * (b + 1) / 2 + a;
+    const double2* gp = Gw + (long long)(a + L - 1) * ncol + coff;
+    const double2* gn = Gw + (long long)(-a + L - 1) * ncol + coff;
+    const double2 gpp = __ldg(gp + b);
+    const double2 gpn = negm ? __ldg(gp - b) : make_double2(0.0, 0.0);
+    const double2 gnp = a ? __ldg(gn + b) : make_double2(0.0, 0.0);
+    const double2 gnn = (a && negm) ? __ldg(gn - b) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int i = 0; i < LC; ++i) {
+      const int l = l0 + i;
+      if (l > ltop || l < as || a > l || b > l) continue;
+      const double w = __ldg(delta + wedge_plane_base(l) + widx);
+      const double* Ul = U + (long long)l * K + (L - 1);
+#pragma unroll
+      for (int sa = 0; sa < 2; ++sa) {
+        if (sa && a == 0) continue;
+        const int mp = sa ? -a : a;
+        const double u = __ldg(Ul + mp);
+        {  // m = +b
+          int neg = swp;
+          if (mp < 0) neg ^= (l + b) & 1;
+          const double d = (neg ? -w : w) * u;
+          const double2 g = sa ? gnp : gpp;
+          px[i] += d * g.x;
+          py[i] += d * g.y;
+        }
+        if (negm) {  // m = -b
+          int neg = swp;
+          if (mp < 0) neg ^= (l - b) & 1;
+          neg ^= (l + a) & 1;
+          const double d = (neg ? -w : w) * u;
+          const double2 g = sa ? gnn : gpn;
+          nx[i] += d * g.x;
+          ny[i] += d * g.y;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < LC; ++i) {
+    const int l = l0 + i;
+    if (l > ltop || b > l) continue;
+    if (l < as) {
+      flm[(long long)l * l + l + b] = make_double2(0.0, 0.0);
+      if (b > 0) flm[(long long)l * l + l - b] = make_double2(0.0, 0.0);
+      continue;
+    }
+    const double amp = sht_amp(l, spin);
+    const double2 v = cipow(make_double2(px[i] * amp, py[i] * amp), b + spin);
+    flm[(long long)l * l + l + b] = v;
+    if (b > 0) {
+      if (real) {
+        double2 cv = make_double2(v.x, -v.y);
+        if (b & 1) cv = make_double2(-cv.x, -cv.y);
+        flm[(long long)l * l + l - b] = cv;
+      } else {
+        flm[(long long)l * l + l - b] = cipow(make_double2(nx[i] * amp, ny[i] * amp), -b + spin);
+      }
+    }
+  }
+}
+
 // B[m' mod K][m mod K] = e^{i m' pi/K} i^{-(m+s)} sum_{l} amp D_{m'm} D_{m',-s} f_lm   (sphere.py:191-203)
 // real: B[m' mod K][m], m in [0,L)   (sphere.py:245-252)
 __global__ void k_sht_bins(int L, int spin, int real, const double2* __restrict__ flm,
@@ -306,9 +397,14 @@ extern "C" int scv_sht_forward(scv_ctx* c, int L, int spin, int real, const void
     SCV_TRY(scv_scratch(c, 0, (size_t)L * K * 8, &U));
     k_sht_ucol<<<(int)(((long long)L * K + 255) / 256), 256, 0, s>>>(L, spin, c->delta, (double*)U);
     c->launches++;
-    const long long np = (long long)L * (L + 1) / 2;
-    k_sht_contract_w<<<(int)((np + 127) / 128), 128, 0, s>>>(L, spin, real, (const double2*)Gw, c->delta,
-                                                             (const double*)U, (double2*)flm);
+    if (SCV_SHT_LC > 1) {
+      k_sht_contract_c<<<dim3((L + 127) / 128, (L + SCV_SHT_LC - 1) / SCV_SHT_LC), 128, 0, s>>>(
+          L, spin, real, (const double2*)Gw, c->delta, (const double*)U, (double2*)flm);
+    } else {
+      const long long np = (long long)L * (L + 1) / 2;
+      k_sht_contract_w<<<(int)((np + 127) / 128), 128, 0, s>>>(L, spin, real, (const double2*)Gw, c->delta,
+                                                               (const double*)U, (double2*)flm);
+    }
     c->launches++;
   } else {
     const long long warps = (long long)L * L;

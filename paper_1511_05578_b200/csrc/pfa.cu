@@ -883,6 +883,14 @@ template <> struct PfaPipeCfg<2047> {
 template <> struct PfaPipeCfg<1023> {
   static constexpr int NG = SCV_RING_1023 ? SCV_ROWSP_NG : 0, NTG = SCV_ROWSP_NTG, NIO = SCV_ROWSP_NIO, NB = SCV_ROWSP_NB;
 };
+// K = 511 (the L_j = 256 scale): row kernel and gamma+quadrature as ring kernels (SCV_RING_511);
+// its column generation keeps the batched kernel (8 degrees per generator lane < one batch)
+#ifndef SCV_RING_511
+#define SCV_RING_511 1
+#endif
+template <> struct PfaPipeCfg<511> {
+  static constexpr int NG = SCV_RING_511 ? SCV_ROWSP_NG : 0, NTG = SCV_ROWSP_NTG, NIO = SCV_ROWSP_NIO, NB = SCV_ROWSP_NB;
+};
 template <int K>
 static constexpr size_t pfa_smem_pipe() {
   using PL = PfaPlan<K>;
@@ -2494,6 +2502,8 @@ __global__ void __launch_bounds__(PfaQCfg<K>::NT, PfaQCfg<K>::MINB)
 #endif
 // lengths whose column passes (k_ana_colgen_p, k_syn_gamma_qp) run as ring kernels
 constexpr bool pfa_ring_cols(int K) { return K == 2047 || (K == 1023 && SCV_RING_1023); }
+// lengths whose gamma+quadrature pass alone is a ring kernel
+constexpr bool pfa_ring_gq(int K) { return pfa_ring_cols(K) || (K == 511 && SCV_RING_511); }
 #ifndef SCV_GQP_PF
 #define SCV_GQP_PF (2 + SCV_GQP_WAHEAD)
 #endif
@@ -3039,7 +3049,7 @@ static int run_syn_alpha(scv_ctx* c, int real, int tr, const void* in, int lsig,
     if (!real && !tr) {
       const long long nrows = (long long)K * nbb;
       // the pipelined gamma+quadrature pass can read the chunk in column pairs
-      if (pair && pfa_ring_cols(K) && SCV_GQP && SCV_SYN_PAIR)
+      if (pair && pfa_ring_gq(K) && SCV_GQP && SCV_SYN_PAIR)
         return launch_rows_p<K, -1, 5>(c, nrows, (const double2*)in, chunk, tab, (long long)lsig * K, b0, s);
       return launch_rows_p<K, -1, 1>(c, nrows, (const double2*)in, chunk, tab, (long long)lsig * K, b0, s);
     }
@@ -3098,7 +3108,7 @@ static int run_syn_gamma_q(scv_ctx* c, int real, int tr, const double2* chunk, i
                            const long long* mbase, int qrows, double2* wout, cudaStream_t s) {
   const double2* tab;
   SCV_TRY(scv_pfa_tables(c, K, &tab));
-  if constexpr (pfa_ring_cols(K) && SCV_GQP) {
+  if constexpr (pfa_ring_gq(K) && SCV_GQP) {
     if (!tr) {
       constexpr size_t smp = pfa_smem_gqp<K>();
       static_assert(smp <= 232448, "pipelined gamma+quadrature exceeds the 227 KB shared-memory limit");

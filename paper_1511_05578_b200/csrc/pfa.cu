@@ -891,6 +891,16 @@ template <> struct PfaPipeCfg<1023> {
 template <> struct PfaPipeCfg<511> {
   static constexpr int NG = SCV_RING_511 ? SCV_ROWSP_NG : 0, NTG = SCV_ROWSP_NTG, NIO = SCV_ROWSP_NIO, NB = SCV_ROWSP_NB;
 };
+// K = 4095 (the L_j = 2048 scales of C5): a slot is 64 KB, so the ring has 3 slots and 2
+// transform groups (SCV_RING_4095 = NTG threads per group, 0 = off).  Measured on the C5
+// streamed map (ms/map; the four-radix transform spills at every shape): off 5472, 128
+// threads per group 5458, 192: 5738, 256: 5391.
+#ifndef SCV_RING_4095
+#define SCV_RING_4095 256
+#endif
+template <> struct PfaPipeCfg<4095> {
+  static constexpr int NG = SCV_RING_4095 ? 2 : 0, NTG = SCV_RING_4095 ? SCV_RING_4095 : 96, NIO = 3, NB = 3;
+};
 template <int K>
 static constexpr size_t pfa_smem_pipe() {
   using PL = PfaPlan<K>;
@@ -3049,8 +3059,9 @@ static int run_syn_alpha(scv_ctx* c, int real, int tr, const void* in, int lsig,
     if (!real && !tr) {
       const long long nrows = (long long)K * nbb;
       // the pipelined gamma+quadrature pass can read the chunk in column pairs
-      if (pair && pfa_ring_gq(K) && SCV_GQP && SCV_SYN_PAIR)
-        return launch_rows_p<K, -1, 5>(c, nrows, (const double2*)in, chunk, tab, (long long)lsig * K, b0, s);
+      if constexpr (pfa_ring_gq(K) && SCV_GQP && SCV_SYN_PAIR) {
+        if (pair) return launch_rows_p<K, -1, 5>(c, nrows, (const double2*)in, chunk, tab, (long long)lsig * K, b0, s);
+      }
       return launch_rows_p<K, -1, 1>(c, nrows, (const double2*)in, chunk, tab, (long long)lsig * K, b0, s);
     }
   }
@@ -3175,11 +3186,15 @@ static int ana_blocked_4095(scv_ctx* c, const double2* w, const double* hlb, con
     }
     SCV_PROF(c, s, "so3inv_rows");
     const long long nrows = (long long)nbb * KK;
-    int grid;
-    SCV_TRY(persistent_grid(c, k_pfa_rows<KK, +1, 2>, NTR, smr, (nrows + RR - 1) / RR, &grid));
-    k_pfa_rows<KK, +1, 2><<<grid, NTR, smr, s>>>(nrows, (const double2*)T, sig, tab, (long long)nb, bs0);
-    c->launches++;
-    SCV_CUDA(c, cudaGetLastError());
+    if constexpr (PfaPipeCfg<KK>::NG > 0) {
+      SCV_TRY((launch_rows_p<KK, +1, 2>(c, nrows, (const double2*)T, sig, tab, (long long)nb, bs0, s)));
+    } else {
+      int grid;
+      SCV_TRY(persistent_grid(c, k_pfa_rows<KK, +1, 2>, NTR, smr, (nrows + RR - 1) / RR, &grid));
+      k_pfa_rows<KK, +1, 2><<<grid, NTR, smr, s>>>(nrows, (const double2*)T, sig, tab, (long long)nb, bs0);
+      c->launches++;
+      SCV_CUDA(c, cudaGetLastError());
+    }
   }
   return SCV_OK;
 }

@@ -864,6 +864,14 @@ __device__ __forceinline__ void pfa_stage_mma_blk(double2* X, const double2* tab
 // first 11 x 11 matrix (padding until r02) is all ones.
 __host__ __device__ constexpr int r89_in_slot(int a1, int a2) { return 11 * a1 + a2; }
 __host__ __device__ constexpr int r89_out_slot(int b1, int b2) { return 2 * b2 + (b1 & 1) + 22 * (b1 >> 1); }
+// SCV_R89_NBW blocks of 4 butterflies per warp iteration: the lane's A fragments of the five
+// Rader matrices (66 eight-byte loads per block, more than half of the stage's shared-memory
+// wavefronts) are loaded once per iteration and feed every block of it.  Costs 26 accumulator
+// and 8 operand doubles per extra block, so it needs a launch shape that leaves the transform
+// threads the registers (see PfaPipeCfg).
+#ifndef SCV_R89_NBW
+#define SCV_R89_NBW 1
+#endif
 template <class PL, int S, int DIR, int R, int NT, int PITCH>
 __device__ __forceinline__ void pfa_stage_rader89(double2* X, const double2* tab, int gtid, int bar) {
   constexpr int p = 89;
@@ -874,6 +882,7 @@ __device__ __forceinline__ void pfa_stage_rader89(double2* X, const double2* tab
   constexpr int NBF = R * nbf;
   constexpr int NBLK = 2 * ((NBF + 7) / 8);
   constexpr int NW = NT / 32;
+  constexpr int NBW = SCV_R89_NBW;
   const double* T0 = (const double*)(tab + pfa_tab_off<PL, S>());
   const double* Xd = (const double*)X;
   const int lane = gtid & 31, warp = gtid >> 5;
@@ -882,81 +891,111 @@ __device__ __forceinline__ void pfa_stage_rader89(double2* X, const double2* tab
   auto slot = [](int i) { return (i >> 1) + 4 * (i & 1); };
   const bool a2ok = ac < 3;  // a mod 11 = ac + 8 exists in the third k-step
 #pragma unroll 1
-  for (int q = warp; q < NBLK; q += NW) {
-    const int gb = (q >> 1) * 8 + 2 * (q & 1);
-    // B-fragment butterfly of this lane; a block past the end re-reads the last
-    // butterfly (its GEMM columns are independent and never stored)
-    const int bfB = min(gb + slot(ar >> 1), NBF - 1);
-    const double* xg;
-    {
-      const int rr = R == 1 ? 0 : bfB / nbf, b = bfB - rr * nbf;
-      xg = Xd + 2 * (rr * PITCH + b * p + 1 + ac) + (ar & 1);
-    }
-    const int bfE = gb + slot(ac);
-    const bool okE = bfE < NBF;
-    int eoff = 0;
-    double2 x0 = make_double2(0.0, 0.0);
-    if (okE) {
-      const int rr = R == 1 ? 0 : bfE / nbf, b = bfE - rr * nbf;
-      eoff = rr * PITCH + b * p;
-      x0 = X[eoff];
-    }
+  for (int q0 = warp; q0 < NBLK; q0 += NW * NBW) {
+    const double* xg[NBW];
+    bool okE[NBW];
+    int eoff[NBW];
+    double2 x0[NBW];
     // ---- per k-step kt (a2 = ac + 4 kt): gather, in-lane 4-point transforms,
     // and the tensor-core products of that k-step (the Im halves of the 22 x 22
     // products are k-step kt + 3), so only one k-step of B operands is live
-    double y0[2][2], y2[2][2], yu[3][2], za[3][2], zb[3][2];
+    double y0[NBW][2][2], y2[NBW][2][2], yu[NBW][3][2], za[NBW][3][2], zb[NBW][3][2];
 #pragma unroll
-    for (int t = 0; t < 2; ++t) y0[t][0] = y0[t][1] = y2[t][0] = y2[t][1] = 0.0;
+    for (int w = 0; w < NBW; ++w) {
+      const int q = q0 + w * NW;
+      const int gb = (q >> 1) * 8 + 2 * (q & 1);
+      // B-fragment butterfly of this lane; a block past the end re-reads the last
+      // butterfly (its GEMM columns are independent and never stored)
+      const int bfB = min(gb + slot(ar >> 1), NBF - 1);
+      {
+        const int rr = R == 1 ? 0 : bfB / nbf, b = bfB - rr * nbf;
+        xg[w] = Xd + 2 * (rr * PITCH + b * p + 1 + ac) + (ar & 1);
+      }
+      const int bfE = gb + slot(ac);
+      okE[w] = q < NBLK && bfE < NBF;
+      eoff[w] = 0;
+      x0[w] = make_double2(0.0, 0.0);
+      if (okE[w]) {
+        const int rr = R == 1 ? 0 : bfE / nbf, b = bfE - rr * nbf;
+        eoff[w] = rr * PITCH + b * p;
+        x0[w] = X[eoff[w]];
+      }
 #pragma unroll
-    for (int t = 0; t < 3; ++t) yu[t][0] = yu[t][1] = za[t][0] = za[t][1] = zb[t][0] = zb[t][1] = 0.0;
+      for (int t = 0; t < 2; ++t) y0[w][t][0] = y0[w][t][1] = y2[w][t][0] = y2[w][t][1] = 0.0;
+#pragma unroll
+      for (int t = 0; t < 3; ++t)
+        yu[w][t][0] = yu[w][t][1] = za[w][t][0] = za[w][t][1] = zb[w][t][0] = zb[w][t][1] = 0.0;
+    }
 #pragma unroll
     for (int kt = 0; kt < 3; ++kt) {
-      double sv[4], w[4];
+      double bV0[NBW], bV2[NBW], bUr[NBW], bUi[NBW], bAr[NBW], bAi[NBW], bBr[NBW], bBi[NBW];
 #pragma unroll
-      for (int a1 = 0; a1 < 4; ++a1) {
-        double xu = 0.0, xv = 0.0;
-        if (kt < 2 || a2ok) {
-          xu = xg[2 * (r89_in_slot(a1, 4 * kt))];
-          xv = xg[2 * (r89_in_slot(a1, 4 * kt) + 44)];
+      for (int w = 0; w < NBW; ++w) {
+        double sv[4], dv[4];
+#pragma unroll
+        for (int a1 = 0; a1 < 4; ++a1) {
+          double xu = 0.0, xv = 0.0;
+          if (kt < 2 || a2ok) {
+            xu = xg[w][2 * (r89_in_slot(a1, 4 * kt))];
+            xv = xg[w][2 * (r89_in_slot(a1, 4 * kt) + 44)];
+          }
+          sv[a1] = xu + xv;
+          dv[a1] = xu - xv;
         }
-        sv[a1] = xu + xv;
-        w[a1] = xu - xv;
+        bV0[w] = (sv[0] + sv[2]) + (sv[1] + sv[3]);
+        bV2[w] = (sv[0] + sv[2]) - (sv[1] + sv[3]);
+        bUr[w] = sv[0] - sv[2];
+        bUi[w] = sv[1] - sv[3];
+        const double P = (dv[1] - dv[3]) * s2, Q = (dv[1] + dv[3]) * s2;
+        bAr[w] = dv[0] + P;
+        bAi[w] = -dv[2] - Q;
+        bBr[w] = dv[0] - P;
+        bBi[w] = dv[2] - Q;
       }
-      const double bV0 = (sv[0] + sv[2]) + (sv[1] + sv[3]);
-      const double bV2 = (sv[0] + sv[2]) - (sv[1] + sv[3]);
-      const double bUr = sv[0] - sv[2], bUi = sv[1] - sv[3];
-      const double P = (w[1] - w[3]) * s2, Q = (w[1] + w[3]) * s2;
-      const double bAr = w[0] + P, bAi = -w[2] - Q, bBr = w[0] - P, bBi = w[2] - Q;
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
         const int o = (t * 8 + ar) * R89_P12 + kt * 4 + ac;
-        dmma(y0[t][0], y0[t][1], T0[o], bV0);
-        dmma(y2[t][0], y2[t][1], T0[R89_OFF_M2 + o], bV2);
+        const double a0 = T0[o], a2 = T0[R89_OFF_M2 + o];
+#pragma unroll
+        for (int w = 0; w < NBW; ++w) {
+          dmma(y0[w][t][0], y0[w][t][1], a0, bV0[w]);
+          dmma(y2[w][t][0], y2[w][t][1], a2, bV2[w]);
+        }
       }
 #pragma unroll
       for (int t = 0; t < 3; ++t) {
         const int o = (t * 8 + ar) * R89_P28 + kt * 4 + ac;
-        dmma(yu[t][0], yu[t][1], T0[R89_OFF_MC + o], bUr);
-        dmma(yu[t][0], yu[t][1], T0[R89_OFF_MC + o + 12], bUi);
-        dmma(za[t][0], za[t][1], T0[R89_OFF_RA + o], bAr);
-        dmma(za[t][0], za[t][1], T0[R89_OFF_RA + o + 12], bAi);
-        dmma(zb[t][0], zb[t][1], T0[R89_OFF_RB + o], bBr);
-        dmma(zb[t][0], zb[t][1], T0[R89_OFF_RB + o + 12], bBi);
+        const double c0 = T0[R89_OFF_MC + o], c1 = T0[R89_OFF_MC + o + 12];
+        const double ra0 = T0[R89_OFF_RA + o], ra1 = T0[R89_OFF_RA + o + 12];
+        const double rb0 = T0[R89_OFF_RB + o], rb1 = T0[R89_OFF_RB + o + 12];
+#pragma unroll
+        for (int w = 0; w < NBW; ++w) {
+          dmma(yu[w][t][0], yu[w][t][1], c0, bUr[w]);
+          dmma(yu[w][t][0], yu[w][t][1], c1, bUi[w]);
+          dmma(za[w][t][0], za[w][t][1], ra0, bAr[w]);
+          dmma(za[w][t][0], za[w][t][1], ra1, bAi[w]);
+          dmma(zb[w][t][0], zb[w][t][1], rb0, bBr[w]);
+          dmma(zb[w][t][0], zb[w][t][1], rb1, bBi[w]);
+        }
       }
     }
     // rows 3..5 of the third product tile hold the Im parts of b2 = 8..10
-    double uhi[2], ahi[2], bhi[2];
+    double uhi[NBW][2], ahi[NBW][2], bhi[NBW][2];
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      uhi[c] = __shfl_down_sync(0xffffffffu, yu[2][c], 12);
-      ahi[c] = __shfl_down_sync(0xffffffffu, za[2][c], 12);
-      bhi[c] = __shfl_down_sync(0xffffffffu, zb[2][c], 12);
-    }
+    for (int w = 0; w < NBW; ++w)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uhi[w][c] = __shfl_down_sync(0xffffffffu, yu[w][2][c], 12);
+        ahi[w][c] = __shfl_down_sync(0xffffffffu, za[w][2][c], 12);
+        bhi[w][c] = __shfl_down_sync(0xffffffffu, zb[w][2][c], 12);
+      }
     __syncwarp();
-    if (okE) {
-      double2* Xr = X + eoff;
+#pragma unroll
+    for (int w = 0; w < NBW; ++w) {
+      if (!okE[w]) continue;
+      double2* Xr = X + eoff[w];
       // y_0: row 11 of the first product (the all-ones row) is sum_a s'_a
-      if (ar == 3) Xr[0] = make_double2(x0.x + y0[1][0], x0.y + y0[1][1]);
+      if (ar == 3) Xr[0] = make_double2(x0[w].x + y0[w][1][0], x0[w].y + y0[w][1][1]);
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         if (hh == 1 && ar >= 3) continue;
@@ -964,10 +1003,10 @@ __device__ __forceinline__ void pfa_stage_rader89(double2* X, const double2* tab
         double Aq[4][2], Bq[4][2];
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-          const double Y0 = y0[hh][c] + (c ? x0.y : x0.x), Y2 = y2[hh][c];
-          const double Yr = hh ? yu[2][c] : yu[0][c], Yi = hh ? uhi[c] : yu[1][c];
-          const double ZAr = hh ? za[2][c] : za[0][c], ZAi = hh ? ahi[c] : za[1][c];
-          const double ZBr = hh ? zb[2][c] : zb[0][c], ZBi = hh ? bhi[c] : zb[1][c];
+          const double Y0 = y0[w][hh][c] + (c ? x0[w].y : x0[w].x), Y2 = y2[w][hh][c];
+          const double Yr = hh ? yu[w][2][c] : yu[w][0][c], Yi = hh ? uhi[w][c] : yu[w][1][c];
+          const double ZAr = hh ? za[w][2][c] : za[w][0][c], ZAi = hh ? ahi[w][c] : za[w][1][c];
+          const double ZBr = hh ? zb[w][2][c] : zb[w][0][c], ZBi = hh ? bhi[w][c] : zb[w][1][c];
           Aq[0][c] = (Y0 + Y2) + Yr;
           Aq[1][c] = (Y0 - Y2) + Yi;
           Aq[2][c] = (Y0 + Y2) - Yr;

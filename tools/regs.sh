@@ -1,6 +1,7 @@
 #!/bin/bash
-# usage: tools/regs.sh file.cu [grep-pattern]
-/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xcompiler -fPIC -Xptxas -v -c "$1" -o /tmp/regs.o 2>&1 | python3 -c "
+# usage: tools/regs.sh file.cu [grep-pattern] [nvcc defines...]
+f=$1; pat=${2:-.}; shift; shift
+/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -Xptxas -v -c "$f" -o /tmp/regs_$$.o "$@" 2>&1 | python3 -c "
 import sys,re
 cur=None; st=sp='?'
 for line in sys.stdin:
@@ -12,4 +13,5 @@ for line in sys.stdin:
     m=re.search(r'Used (\d+) registers',line)
     if m and cur:
         print(f'{cur[:50]:50s} regs={m.group(1)} stack={st} spill={sp}'); cur=None
-" | sort | grep -E "${2:-.}"
+" | sort | grep -E "$pat"
+rm -f /tmp/regs_$$.o

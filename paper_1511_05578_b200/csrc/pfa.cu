@@ -869,12 +869,26 @@ extern "C" int scv_debug_pipe_stats(unsigned long long* out, int reset) {
 #define SCV_ROWSP_SCHED 0
 #endif
 constexpr bool pfa_rows_sched(int gather) { return SCV_ROWSP_SCHED && gather != 5; }
-template <int K> struct PfaPipeCfg { static constexpr int NG = 0, NTG = 96, NIO = 0, NB = 0; };
+// XW / XS: blocks per warp iteration of the Rader-89 and radix-23 stages in the row kernel's
+// transform groups (pfa.cuh).  The K = 2047 shape can trade a transform group for registers.
+#ifndef SCV_ROWSP_NG_2047
+#define SCV_ROWSP_NG_2047 SCV_ROWSP_NG
+#endif
+#ifndef SCV_ROWSP_XW
+#define SCV_ROWSP_XW SCV_R89_NBW
+#endif
+#ifndef SCV_ROWSP_XS
+#define SCV_ROWSP_XS SCV_PFA_NBW_SMALL
+#endif
+template <int K> struct PfaPipeCfg {
+  static constexpr int NG = 0, NTG = 96, NIO = 0, NB = 0, XW = SCV_R89_NBW, XS = SCV_PFA_NBW_SMALL;
+};
 #ifndef SCV_ROWSP_NTG
 #define SCV_ROWSP_NTG 96
 #endif
 template <> struct PfaPipeCfg<2047> {
-  static constexpr int NG = SCV_ROWSP ? SCV_ROWSP_NG : 0, NTG = SCV_ROWSP_NTG, NIO = SCV_ROWSP_NIO, NB = SCV_ROWSP_NB;
+  static constexpr int NG = SCV_ROWSP ? SCV_ROWSP_NG_2047 : 0, NTG = SCV_ROWSP_NTG, NIO = SCV_ROWSP_NIO, NB = SCV_ROWSP_NB;
+  static constexpr int XW = SCV_ROWSP_XW, XS = SCV_ROWSP_XS;
 };
 // K = 1023 (the L_j = 512 scale): on with SCV_RING_1023
 #ifndef SCV_RING_1023
@@ -882,6 +896,7 @@ template <> struct PfaPipeCfg<2047> {
 #endif
 template <> struct PfaPipeCfg<1023> {
   static constexpr int NG = SCV_RING_1023 ? SCV_ROWSP_NG : 0, NTG = SCV_ROWSP_NTG, NIO = SCV_ROWSP_NIO, NB = SCV_ROWSP_NB;
+  static constexpr int XW = SCV_R89_NBW, XS = SCV_PFA_NBW_SMALL;
 };
 // K = 511 (the L_j = 256 scale): row kernel and gamma+quadrature as ring kernels (SCV_RING_511);
 // its column generation keeps the batched kernel (8 degrees per generator lane < one batch)
@@ -890,6 +905,7 @@ template <> struct PfaPipeCfg<1023> {
 #endif
 template <> struct PfaPipeCfg<511> {
   static constexpr int NG = SCV_RING_511 ? SCV_ROWSP_NG : 0, NTG = SCV_ROWSP_NTG, NIO = SCV_ROWSP_NIO, NB = SCV_ROWSP_NB;
+  static constexpr int XW = SCV_R89_NBW, XS = SCV_PFA_NBW_SMALL;
 };
 // K = 4095 (the L_j = 2048 scales of C5): a slot is 64 KB, so the ring has 3 slots and 2
 // transform groups (SCV_RING_4095 = NTG threads per group, 0 = off).  Measured on the C5
@@ -900,6 +916,7 @@ template <> struct PfaPipeCfg<511> {
 #endif
 template <> struct PfaPipeCfg<4095> {
   static constexpr int NG = SCV_RING_4095 ? 2 : 0, NTG = SCV_RING_4095 ? SCV_RING_4095 : 96, NIO = 3, NB = 3;
+  static constexpr int XW = SCV_R89_NBW, XS = SCV_PFA_NBW_SMALL;
 };
 template <int K>
 static constexpr size_t pfa_smem_pipe() {
@@ -1069,7 +1086,7 @@ __global__ void __launch_bounds__(PfaPipeCfg<K>::NG * PfaPipeCfg<K>::NTG + PfaPi
     const unsigned u = (unsigned)(i / NB);
     mbar_wait(full + (u & 1) * NB + b, (u >> 1) & 1);
     ck.mark(st, 0);
-    pfa_dft<PL, DIR, 1, NTG, K>(bufs + (size_t)b * K, tab, nullptr, gtid, bar);
+    pfa_dft<PL, DIR, 1, NTG, K, PfaPipeCfg<K>::XW, PfaPipeCfg<K>::XS>(bufs + (size_t)b * K, tab, nullptr, gtid, bar);
     if (gtid == 0) mbar_arrive(done + (u & 1) * NB + b);
     ck.mark(st, 1);
   }

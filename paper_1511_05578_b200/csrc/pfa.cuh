@@ -633,7 +633,7 @@ __device__ __forceinline__ void pfa_stage_mma_reg(double2* X, const double2* tab
 // Block q covers butterflies {8g+o, 8g+o+4, 8g+o+2, 8g+o+6}, g = q/2, o = q&1 (see `slot`):
 // butterfly positions 4 apart differ by 4 mod 8 doubles, so the two
 // butterflies of each 16-lane phase of a B-fragment load hit disjoint banks.
-template <class PL, int S, int DIR, int R, int NT, int PITCH>
+template <class PL, int S, int DIR, int R, int NT, int PITCH, int XS = SCV_PFA_NBW_SMALL>
 __device__ __forceinline__ void pfa_stage_mma_blk(double2* X, const double2* tab, int gtid, int bar) {
   constexpr int p = pfa_p<PL, S>();
   constexpr int h = pfa_h(p);
@@ -663,7 +663,7 @@ __device__ __forceinline__ void pfa_stage_mma_blk(double2* X, const double2* tab
 #endif
   // small radices (<= 2 m8 tiles): NBW blocks per warp iteration, for more
   // independent DMMA chains per k-step
-  constexpr int NBW = M8 <= 2 ? SCV_PFA_NBW_SMALL : SCV_PFA_NBW_BIG;
+  constexpr int NBW = M8 <= 2 ? XS : SCV_PFA_NBW_BIG;
   // small radices: the lane's A fragments (M8 tiles x Kp/4 k-steps of C and S)
   // stay in registers for the whole stage; re-reading them per block is a
   // fifth of the transform's shared-memory traffic at K = 2047 (radix 23)
@@ -872,7 +872,7 @@ __host__ __device__ constexpr int r89_out_slot(int b1, int b2) { return 2 * b2 +
 #ifndef SCV_R89_NBW
 #define SCV_R89_NBW 1
 #endif
-template <class PL, int S, int DIR, int R, int NT, int PITCH>
+template <class PL, int S, int DIR, int R, int NT, int PITCH, int XW = SCV_R89_NBW>
 __device__ __forceinline__ void pfa_stage_rader89(double2* X, const double2* tab, int gtid, int bar) {
   constexpr int p = 89;
   constexpr int K = PL::K;
@@ -882,7 +882,7 @@ __device__ __forceinline__ void pfa_stage_rader89(double2* X, const double2* tab
   constexpr int NBF = R * nbf;
   constexpr int NBLK = 2 * ((NBF + 7) / 8);
   constexpr int NW = NT / 32;
-  constexpr int NBW = SCV_R89_NBW;
+  constexpr int NBW = XW;
   const double* T0 = (const double*)(tab + pfa_tab_off<PL, S>());
   const double* Xd = (const double*)X;
   const int lane = gtid & 31, warp = gtid >> 5;
@@ -1035,11 +1035,13 @@ __device__ __forceinline__ void pfa_stage_rader89(double2* X, const double2* tab
 // In-place K-point DFT (sign DIR) of R rows at X[r*PITCH + n] (natural order
 // in; CRT order out, read through pfa_pos).  Caller syncs before (data ready).
 // scr: pfa_scratch<PL,R,NT>() double2 of shared scratch (DMMA stages).
-template <class PL, int S, int DIR, int R, int NT, int PITCH>
+// XW, XS: blocks per warp iteration of the Rader-89 stage and of the small-radix block stage
+// (kernels whose transform threads have the registers raise them, see PfaPipeCfg)
+template <class PL, int S, int DIR, int R, int NT, int PITCH, int XW = SCV_R89_NBW, int XS = SCV_PFA_NBW_SMALL>
 __device__ __forceinline__ void pfa_stage_any(double2* X, const double2* tab, double2* scr, int gtid, int bar) {
   constexpr int p = pfa_p<PL, S>();
-  if constexpr (pfa_rader89(p)) pfa_stage_rader89<PL, S, DIR, R, NT, PITCH>(X, tab, gtid, bar);
-  else if constexpr (pfa_use_mma(p, PL::K) && SCV_PFA_BLK) pfa_stage_mma_blk<PL, S, DIR, R, NT, PITCH>(X, tab, gtid, bar);
+  if constexpr (pfa_rader89(p)) pfa_stage_rader89<PL, S, DIR, R, NT, PITCH, XW>(X, tab, gtid, bar);
+  else if constexpr (pfa_use_mma(p, PL::K) && SCV_PFA_BLK) pfa_stage_mma_blk<PL, S, DIR, R, NT, PITCH, XS>(X, tab, gtid, bar);
   else if constexpr (pfa_use_mma(p, PL::K) && mma_reg(PL::K, p, R, NT)) pfa_stage_mma_reg<PL, S, DIR, R, NT, PITCH>(X, tab, gtid, bar);
   else if constexpr (pfa_use_mma(p, PL::K)) pfa_stage_mma<PL, S, DIR, R, NT, PITCH>(X, tab, scr, gtid, bar);
   else pfa_stage<PL, S, DIR, R, NT, PITCH>(X, tab, gtid, bar);
@@ -1050,14 +1052,14 @@ __device__ __forceinline__ void pfa_stage_any(double2* X, const double2* tab, do
 #ifndef SCV_EXP_SKIP_STAGES
 #define SCV_EXP_SKIP_STAGES 0
 #endif
-template <class PL, int DIR, int R, int NT, int PITCH>
+template <class PL, int DIR, int R, int NT, int PITCH, int XW = SCV_R89_NBW, int XS = SCV_PFA_NBW_SMALL>
 __device__ __forceinline__ void pfa_dft(double2* X, const double2* tab, double2* scr, int gtid = threadIdx.x,
                                         int bar = 0) {
   // SCV_EXP_SKIP_STAGES (timing experiments only, wrong results): bit s skips stage s
-  if constexpr (!(SCV_EXP_SKIP_STAGES & 1)) pfa_stage_any<PL, 0, DIR, R, NT, PITCH>(X, tab, scr, gtid, bar);
-  if constexpr (PL::D > 1 && !(SCV_EXP_SKIP_STAGES & 2)) pfa_stage_any<PL, 1, DIR, R, NT, PITCH>(X, tab, scr, gtid, bar);
-  if constexpr (PL::D > 2 && !(SCV_EXP_SKIP_STAGES & 4)) pfa_stage_any<PL, 2, DIR, R, NT, PITCH>(X, tab, scr, gtid, bar);
-  if constexpr (PL::D > 3 && !(SCV_EXP_SKIP_STAGES & 8)) pfa_stage_any<PL, 3, DIR, R, NT, PITCH>(X, tab, scr, gtid, bar);
+  if constexpr (!(SCV_EXP_SKIP_STAGES & 1)) pfa_stage_any<PL, 0, DIR, R, NT, PITCH, XW, XS>(X, tab, scr, gtid, bar);
+  if constexpr (PL::D > 1 && !(SCV_EXP_SKIP_STAGES & 2)) pfa_stage_any<PL, 1, DIR, R, NT, PITCH, XW, XS>(X, tab, scr, gtid, bar);
+  if constexpr (PL::D > 2 && !(SCV_EXP_SKIP_STAGES & 4)) pfa_stage_any<PL, 2, DIR, R, NT, PITCH, XW, XS>(X, tab, scr, gtid, bar);
+  if constexpr (PL::D > 3 && !(SCV_EXP_SKIP_STAGES & 8)) pfa_stage_any<PL, 3, DIR, R, NT, PITCH, XW, XS>(X, tab, scr, gtid, bar);
 }
 
 // Out-of-line variant: isolates the transform's register allocation from a

@@ -225,10 +225,32 @@ class CudaBackend:
         return sht_inverse(HarmonicCoeffs(L, p.spin, acc, trusted=True))
 
 
+@dataclass(frozen=True)
+class VirtualRank:
+    """Stands in for a process group: run rank `rank`'s share of a world-`world`
+    decomposition alone, with the collectives skipped (the broadcast input is
+    whatever `f` gives, the reduce leaves this rank's terms).  It measures one
+    rank's critical path when fewer GPUs than ranks are available
+    (tools/rank_share.py); the result is that rank's PARTIAL map, not the map."""
+
+    rank: int
+    world: int
+
+    def __post_init__(self):
+        if not 0 <= self.rank < self.world:
+            raise ValueError(f"rank {self.rank} outside world {self.world}")
+
+
 def _rank_world(group):
+    if isinstance(group, VirtualRank):
+        return group.rank, group.world
     if not dist.is_available() or not dist.is_initialized():
         return 0, 1
     return dist.get_rank(group), dist.get_world_size(group)
+
+
+def _collective(group, world) -> bool:
+    return world > 1 and not isinstance(group, VirtualRank)
 
 
 def analyze_sharded(f, t, group=None, backend=None, src: int = 0, multires: bool = True,
@@ -246,11 +268,11 @@ def analyze_sharded(f, t, group=None, backend=None, src: int = 0, multires: bool
     plan = ScalePlan.build(p, world, multires, real=real, **kw)
     if world > 1 and hasattr(backend, "restrict_tables"):
         backend.restrict_tables(plan, rank)
-    if rank == src:
+    if rank == src or isinstance(group, VirtualRank):  # a virtual rank has no broadcast to wait for
         flm = backend.sht_forward(f)
     else:
         flm = backend.flm_like(L)
-    if world > 1:
+    if _collective(group, world):
         dist.broadcast(flm, src=src, group=group)
     out = ShardedCoeffs(p, plan, multires=multires, real=real)
     for j in plan.owned(rank):
@@ -283,7 +305,7 @@ def synthesize_sharded(c: ShardedCoeffs, t, group=None, backend=None, dst: int =
         terms[j - p.j_min] = backend.scale_term(c.scales[j], t, j, c.real)
     for j, _, _ in c.plan.slabs_of(rank):
         terms[j - p.j_min] = backend.scale_term_slab(c.scales[j], t, j)
-    if world > 1:
+    if _collective(group, world):
         # a whole-scale row is nonzero on exactly one rank: sum-reducing the
         # stack moves it without mixing arithmetic (x + 0 == x exactly); the
         # rows of split scales add the slab partials of every rank
@@ -321,8 +343,8 @@ def roundtrip_sharded_streamed(f, t, group=None, backend=None, src: int = 0, dst
     plan = ScalePlan.build(p, world, multires, real=False, **kw)
     if world > 1 and hasattr(backend, "restrict_tables"):
         backend.restrict_tables(plan, rank)
-    flm = backend.sht_forward(f) if rank == src else backend.flm_like(L)
-    if world > 1:
+    flm = backend.sht_forward(f) if rank == src or isinstance(group, VirtualRank) else backend.flm_like(L)
+    if _collective(group, world):
         dist.broadcast(flm, src=src, group=group)
     terms = torch.zeros((p.scale_count, L * L), dtype=torch.complex128, device=flm.device)
     for j in plan.owned(rank):
@@ -349,7 +371,7 @@ def roundtrip_sharded_streamed(f, t, group=None, backend=None, src: int = 0, dst
         scaling = backend.scaling_map(flm, t, Ls, False)
         if consumer is not None:
             consumer("scaling", scaling)
-    if world > 1:
+    if _collective(group, world):
         dist.reduce(terms, dst=dst, op=dist.ReduceOp.SUM, group=group)
     if rank != dst:
         return None

@@ -233,3 +233,36 @@ def test_synthesize_sharded_requires_scaling_on_dst():
     c = ShardedCoeffs(p, ScalePlan.build(p, 1), scaling=None)
     with pytest.raises(ValueError, match="scaling"):
         synthesize_sharded(c, t, backend=OracleBackend(16, 0))
+
+
+def test_virtual_ranks_cover_the_map_without_a_process_group():
+    """VirtualRank runs one rank's share alone (tools/rank_share.py times it on one GPU):
+    the shares of all virtual ranks tile the single-process coefficients, and no
+    collective is reached (torch.distributed is not initialised here)."""
+    from paper_1511_05578_b200.dist import VirtualRank
+    L, spin, world = 16, 0, 2
+    assert not dist.is_initialized()
+    t = T.build_tiling(T.TilingParams(L, spin, 2.0, 1))
+    psi = [T.curvelet_harmonics(t, j) for j in range(t.params.j_min, t.params.j_max + 1)]
+    f = orc.sht_inverse(orc.gaussian_flm(L, spin, seed=3, real=False), L, spin)
+    smap, scales = orc.analyze(f, L, spin, 2.0, 1, t.params.j_max, psi, t.scaling)
+    be = OracleBackend(L, spin, 8)
+    rows = {j: 0 for j in range(t.params.j_min, t.params.j_max + 1)}
+    for r in range(world):
+        c = analyze_sharded(f, t, group=VirtualRank(r, world), backend=be)
+        assert (c.scaling is not None) == (r == 0)
+        assert set(c.scales) == set(c.plan.owned(r)) | {j for j, _, _ in c.plan.slabs_of(r)}
+        for j, s in c.scales.items():
+            ref = scales[j - t.params.j_min]
+            b0 = getattr(s, "b0", None)
+            v = s.values.numpy()
+            if b0 is None:
+                assert np.array_equal(v, ref)
+            else:
+                assert np.array_equal(v, ref[:, b0:b0 + v.shape[1], :])
+            rows[j] += v.shape[1]
+        g = synthesize_sharded(c, t, group=VirtualRank(r, world), backend=be)
+        assert (g is not None) == (r == 0)
+    assert all(rows[j] == scales[j - t.params.j_min].shape[1] for j in rows)
+    with pytest.raises(ValueError):
+        VirtualRank(2, 2)

@@ -10,12 +10,12 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 
 import paper_1511_05578_b200 as sc
-from oracle import scurve_oracle as orc
+from bench import gaussian_flm  # BASELINE.json input recipe
 
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 300
 t = sc.build_tiling(sc.TilingParams(L, 0, 2.0, 2))
-f = sc.sht_inverse(sc.HarmonicCoeffs(L, 0, orc.gaussian_flm(L, 0, seed=0, real=True)))
+f = sc.sht_inverse(sc.HarmonicCoeffs(L, 0, gaussian_flm(L, 0, seed=0, real=True)))
 for _ in range(20):
     g = sc.synthesize(sc.analyze(f, t), t)
 torch.cuda.synchronize()

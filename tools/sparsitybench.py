@@ -13,14 +13,14 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 
 import paper_1511_05578_b200 as sc
-from oracle import scurve_oracle as orc  # input recipe only
+from bench import gaussian_flm  # BASELINE.json input recipe
 from paper_1511_05578_b200 import _cabi
 from paper_1511_05578_b200 import sparsity as S
 
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
 bins = int(sys.argv[2]) if len(sys.argv) > 2 else 10
 t = sc.build_tiling(sc.TilingParams(L, 0, 2.0, 3 if L >= 1024 else 2))
-flm = sc.HarmonicCoeffs(L, 0, orc.gaussian_flm(L, 0, seed=0, real=True))
+flm = sc.HarmonicCoeffs(L, 0, gaussian_flm(L, 0, seed=0, real=True))
 f = sc.sht_inverse(flm)
 S.sparsity_report_streamed(f, t, bins)  # warm-up: tables, plans
 torch.cuda.synchronize()

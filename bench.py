@@ -379,6 +379,26 @@ def run_stub(a):
         print(json.dumps(line), flush=True)
 
 
+def arm_config(a, p, Ljs, world, sharded, maps_per_step):
+    """`config` of the JSON line; both arms print the same dict for the same flags."""
+    coeff_mb = sum((2 * Lj - 1) ** 2 * Lj for Lj in Ljs) * 16 / 1e6
+    return {"workload": workload_name(a), "L": a.L, "spin": a.spin, "lambda": a.lam,
+            "j_min": a.jmin, "j_max": p.j_max, "scale_band_limits": Ljs,
+            "maps_per_step": maps_per_step,
+            **({"streamed_slab_GiB": a.slab_gb} if a.streamed else {}),
+            "parallelism": ("scales + beta slabs sharded x%d%s (NCCL broadcast f_lm + reduce of the "
+                            "per-scale terms)" % (world, ", slabs streamed" if a.streamed else "")
+                            if sharded else
+                            (f"maps x{world} (one map per rank)" if world > 1 else "1 GPU")),
+            **({"cuda_graph": True} if a.graph else {}),
+            **({"lanes": a.lanes, "batch": "maps in flight per step, one CUDA graph + private "
+                "context + stream per lane"} if a.lanes else {}),
+            "l2_flush": ("not needed: the %.0f MB of coefficients per step exceed the 126 MB L2" % coeff_mb
+                         if coeff_mb > 126 else
+                         "none: the %.0f MB of coefficients fit in the 126 MB L2 at this size "
+                         "(small, launch-bound config)" % coeff_mb)}
+
+
 def measured_cpu_roundtrip(a, gpu_ms_at):
     """cpu_baseline.measured: one FULL oracle round trip (analyze + synthesize,
     transform.py:139-187 restated) at L=256 with the bench's lambda / J0, timed
@@ -623,22 +643,7 @@ def run_ours(a):
         "vs_baseline": None,
         "dtype": "f64" if a.real else "c128",
         "data": "synthetic (seeded Gaussian f_lm, C_l=(l+1)^-2)",
-        "config": {"workload": workload_name(a), "L": a.L, "spin": a.spin, "lambda": a.lam,
-                   "j_min": a.jmin, "j_max": p.j_max, "scale_band_limits": Ljs,
-                   "maps_per_step": maps_per_step,
-                   **({"streamed_slab_GiB": a.slab_gb} if a.streamed else {}),
-                   "parallelism": ("scales + beta slabs sharded x%d%s (NCCL broadcast f_lm + reduce of the "
-                                   "per-scale terms)" % (world, ", slabs streamed" if a.streamed else "")
-                                   if sharded else
-                                   (f"maps x{world} (one map per rank)" if world > 1 else "1 GPU")),
-                   **({"cuda_graph": True} if a.graph else {}),
-                   **({"lanes": a.lanes, "batch": "maps in flight per step, one CUDA graph + private "
-                       "context + stream per lane"} if a.lanes else {}),
-                   "l2_flush": ("not needed: the %.0f MB of coefficients per step exceed the 126 MB L2"
-                                % (sum((2 * Lj - 1) ** 2 * Lj for Lj in Ljs) * 16 / 1e6)
-                                if sum((2 * Lj - 1) ** 2 * Lj for Lj in Ljs) * 16 > 126e6 else
-                                "none: the %.0f MB of coefficients fit in the 126 MB L2 at this size "
-                                "(small, launch-bound config)" % (sum((2 * Lj - 1) ** 2 * Lj for Lj in Ljs) * 16 / 1e6))},
+        "config": arm_config(a, p, Ljs, world, sharded, maps_per_step),
         "roofline": roof,
         "paper_roofline": {"B_alg_GB": B_alg / 1e9, "F_alg_TF": F_alg / 1e12, "t_roof_ms": t_roof * 1e3,
                            "frac": t_roof * 1e3 * max(1, a.lanes) / ms_per_step, "fp64_peak_tflops": fp64_peak,
@@ -702,6 +707,8 @@ def run_reference(a):
         return
     from oracle import cpu_sample
     p, Ljs, _, _ = algorithmic_work(a)
+    world = int(os.environ.get("WORLD_SIZE", a.gpus))
+    sharded = world > 1 and not a.maps_per_rank
     measured = None
     if not a.real and not a.no_measured_cpu:
         measured = measured_cpu_roundtrip_host_only(a)
@@ -741,12 +748,12 @@ def run_reference(a):
         "map_fraction_per_step": step_s / sec,
         "run_wall_s": time.perf_counter() - t_run0,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if sharded else "weak",
         "vs_baseline": None,
         "dtype": "f64" if a.real else "c128",
         "data": "synthetic (seeded Gaussian f_lm, C_l=(l+1)^-2)",
-        "config": {"workload": workload_name(a), "L": a.L, "spin": a.spin, "lambda": a.lam,
-                   "j_min": a.jmin, "j_max": p.j_max, "scale_band_limits": Ljs},
+        # the GPU arm's config, key for key (the driver compares the two lines)
+        "config": arm_config(a, p, Ljs, world, sharded, 1 if sharded else world * max(1, a.lanes)),
         "cpu_baseline": cb,
         "e2e": {"value": value, "unit": "maps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }

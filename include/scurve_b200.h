@@ -14,6 +14,8 @@
  *   scv_so3_forward_curvelet   <- so3_forward_curvelet(_real)      so3.py:214-244, 349-383
  *   scv_accumulate             <- the acc += W psi loop of synthesize  transform.py:170-178
  *   scv_finish_acc             <- acc[:s^2]=0 (+ real symmetry)    transform.py:186, 246-252
+ *   scv_analyze                <- analyze / analyze_real (whole map) transform.py:139-152, 190-210
+ *   scv_synthesize             <- synthesize / synthesize_real       transform.py:155-187, 213-253
  *   scv_halfpi_wedge           <- build_halfpi_table / halfpi_table wigner.py:209-240
  *   scv_edge_columns           <- wigner_d_edge_columns            wigner.py:304-322
  *   scv_rotate_to_north        <- rotate_to_north                  transform.py:256-277
@@ -204,6 +206,30 @@ int scv_accumulate_scaling(scv_ctx* ctx, int L, int Ls, const double* slm,
 
 /* acc[: spin^2] = 0; if real, re-impose f_{l,-m} = (-1)^m conj f_{lm}, f_l0 real. */
 int scv_finish_acc(scv_ctx* ctx, int L, int spin, int real, double* acc, void* stream);
+
+/* Whole-map entry points: the reference's analyze / synthesize (transform.py:139-187; real = 1:
+ * analyze_real / synthesize_real, :190-253) as one call each.  They sequence the per-stage entry
+ * points above on `stream` (same kernels and order: bit-identical to calling the stages one by one).
+ *   nscales, Lj[j]       scales coarse -> fine and the band limit each scale signal is stored at
+ *                        (host array; min(ceil(lambda^(j+1)), L) in multiresolution mode, else L)
+ *   psi_pos[j], psi_neg[j]  host arrays of DEVICE pointers: the curvelet kernel's n = +l / n = -l
+ *                        harmonic columns of scale j (float64, length >= Lj[j])
+ *   scaling, Ls          device array (float64, length >= Ls) and band limit of the scaling part
+ *   f                    (L, 2L-1) complex128 map, float64 if real
+ *   sig[j]               host array of DEVICE pointers: (2Lj-1, Lj, 2Lj-1) complex128 (float64 if
+ *                        real) scale signals; written by scv_analyze, read by scv_synthesize
+ *   scaling_map          (Ls, 2Ls-1) spin-0 scaling signal, complex128 (float64 if real)
+ *   work                 device scratch of at least scv_map_work_bytes(L, max_j Lj[j], Ls) bytes
+ * All device buffers are only touched by work enqueued on `stream`. */
+long long scv_map_work_bytes(int L, int Lmax, int Ls);
+int scv_analyze(scv_ctx* ctx, int L, int spin, int real, int nscales, const int* Lj,
+                const double* const* psi_pos, const double* const* psi_neg, const double* scaling, int Ls,
+                const void* f, void* const* sig, void* scaling_map, void* work, long long work_bytes,
+                void* stream);
+int scv_synthesize(scv_ctx* ctx, int L, int spin, int real, int nscales, const int* Lj,
+                   const double* const* psi_pos, const double* const* psi_neg, const double* scaling, int Ls,
+                   const void* const* sig, const void* scaling_map, void* f, void* work, long long work_bytes,
+                   void* stream);
 
 /* Frame rotation of one scale.  Dense Wigner coefficients
  * (the reference's WignerCoeffs.planes) are packed plane after plane: plane l,

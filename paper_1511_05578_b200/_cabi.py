@@ -65,6 +65,9 @@ _SIGS = {
     "scv_accumulate": [_P, _I, _I, _P, _P, _P, _P, _P],
     "scv_accumulate_scaling": [_P, _I, _I, _P, _P, _P, _P],
     "scv_finish_acc": [_P, _I, _I, _I, _P, _P],
+    "scv_map_work_bytes": [_I, _I, _I],
+    "scv_analyze": [_P, _I, _I, _I, _I, _P, _P, _P, _P, _I, _P, _P, _P, _P, _LL, _P],
+    "scv_synthesize": [_P, _I, _I, _I, _I, _P, _P, _P, _P, _I, _P, _P, _P, _P, _LL, _P],
     "scv_edge_columns": [_P, _I, _D, _P, _P],
     "scv_rotate_to_north": [_P, _I, _D, _P, _P, _P],
     "scv_rotate_from_north": [_P, _I, _D, _P, _P, _P],
@@ -76,7 +79,7 @@ _SIGS = {
     "scv_gini_sums": [_P, _LL, _P, _P, _P],
 }
 _RESTYPE = {"scv_last_error": ctypes.c_char_p, "scv_workspace_bytes": ctypes.c_longlong,
-            "scv_launch_count": ctypes.c_longlong}
+            "scv_launch_count": ctypes.c_longlong, "scv_map_work_bytes": ctypes.c_longlong}
 
 EXPORTED = tuple(_SIGS)
 

@@ -348,7 +348,7 @@ int scv_plan_exec_setup(scv_ctx* c, cufftHandle h, cudaStream_t s) {
 // ---------------------------------------------------------------------------
 extern "C" {
 
-int scv_version(void) { return 101; }
+int scv_version(void) { return 102; }
 
 int scv_create(int device, scv_ctx** out) {
   if (!out) return SCV_EINVAL;

@@ -139,7 +139,36 @@ def _scaling_coeffs(ctx, flm: HarmonicCoeffs, dt: _DevTiling, Ls: int, real: boo
     return HarmonicCoeffs(Ls, 0, out, real=real)
 
 
-def _analyze(f: SphereSignal, t, multires: bool, real: bool, scale_out=None) -> CurveletCoeffs:
+class _MapPlan:
+    """Host-side argument arrays of scv_analyze / scv_synthesize for one (tiling, device,
+    multires): band limits and device pointers of the kernel columns, built once."""
+
+    def __init__(self, t, dt: _DevTiling, multires: bool):
+        import ctypes
+        p = t.params
+        L = p.band_limit
+        self.Ljs = [scale_band_limit(p, j) if multires else L for j in range(p.j_min, p.j_max + 1)]
+        self.Ls = scaling_band_limit(p) if multires else L
+        n = len(self.Ljs)
+        self.n = n
+        self.Lj_arr = (ctypes.c_int * n)(*self.Ljs)
+        self.pos_arr = (ctypes.c_void_p * n)(*[dt.psi[j][0].data_ptr() for j in range(p.j_min, p.j_max + 1)])
+        self.neg_arr = (ctypes.c_void_p * n)(*[dt.psi[j][1].data_ptr() for j in range(p.j_min, p.j_max + 1)])
+        self.work_bytes = int(_cabi.load_library().scv_map_work_bytes(L, max(self.Ljs, default=1), self.Ls))
+        self.sig_arr_t = ctypes.c_void_p * n
+
+
+def _map_plan(t, dt: _DevTiling, multires: bool) -> _MapPlan:
+    plans = dt.__dict__.setdefault("_map_plans", {})
+    plan = plans.get(bool(multires))
+    if plan is None:
+        plan = plans[bool(multires)] = _MapPlan(t, dt, multires)
+    return plan
+
+
+def _analyze_stages(f: SphereSignal, t, multires: bool, real: bool, scale_out=None) -> CurveletCoeffs:
+    """The scale loop driven from Python, one C call per stage (the path until r05; kept for a
+    real-flagged signal analysed on the complex path and as the comparator of the whole-map call)."""
     _check_signal(f, t)
     p = t.params
     L = p.band_limit
@@ -160,6 +189,42 @@ def _analyze(f: SphereSignal, t, multires: bool, real: bool, scale_out=None) -> 
     return CurveletCoeffs(p, "unrotated", scaling_sig, scales, multires, real=real)
 
 
+def _analyze(f: SphereSignal, t, multires: bool, real: bool, scale_out=None) -> CurveletCoeffs:
+    """One scv_analyze call (the library walks the scales); bit-identical to _analyze_stages."""
+    if f.real != real:
+        return _analyze_stages(f, t, multires, real, scale_out)
+    _check_signal(f, t)
+    p = t.params
+    L = p.band_limit
+    if abs(p.spin) >= L:
+        raise ValueError(f"spin {p.spin} out of range for band limit {L}")
+    dev = f.values.device
+    ctx = _cabi.context(dev)
+    dt = device_tiling(t, dev)
+    plan = _map_plan(t, dt, multires)
+    dtype = torch.float64 if real else torch.complex128
+    if scale_out is not None and len(scale_out) != plan.n:
+        raise ValueError(f"expected {plan.n} scale_out buffers, got {len(scale_out)}")
+    outs = []
+    for i, Lj in enumerate(plan.Ljs):
+        K = 2 * Lj - 1
+        if scale_out is None:
+            buf = torch.empty((K, Lj, K), dtype=dtype, device=dev)
+        else:
+            buf = _cabi.checked(scale_out[i], dtype, (K, Lj, K), dev, "out")
+        outs.append(buf)
+    Ls = plan.Ls
+    smap = torch.empty((Ls, 2 * Ls - 1), dtype=dtype, device=dev)
+    work = torch.empty(plan.work_bytes, dtype=torch.uint8, device=dev)
+    sig_arr = plan.sig_arr_t(*[b.data_ptr() for b in outs])
+    ctx.call("analyze", L, p.spin, 1 if real else 0, plan.n, plan.Lj_arr, plan.pos_arr, plan.neg_arr,
+             _cabi.ptr(dt.scaling), Ls, _cabi.ptr(f.values), sig_arr, _cabi.ptr(smap), _cabi.ptr(work),
+             plan.work_bytes)
+    scales = [SO3Signal(SO3Grid(Lj, Lj, Lj), b, real=real) for Lj, b in zip(plan.Ljs, outs)]
+    return CurveletCoeffs(p, "unrotated", SphereSignal(SphereGrid(Ls), 0, smap, real=real), scales, multires,
+                          real=real)
+
+
 def analyze(f: SphereSignal, t: Tiling, multires: bool = True, scale_out=None) -> CurveletCoeffs:
     """Decompose a band-limited spin signal into directional scale signals
     (transform.py:139-152).  ``scale_out`` optionally supplies preallocated
@@ -174,12 +239,25 @@ def analyze_real(f: SphereSignal, t: Tiling, multires: bool = True, scale_out=No
     return _analyze(f, t, multires, True, scale_out)
 
 
-def _synthesize(c: CurveletCoeffs, t, real: bool) -> SphereSignal:
+def _check_coeffs(c: CurveletCoeffs, t) -> None:
     p = t.params
     if c.params != p:
         raise ValueError("coefficients were built for a different tiling")
     if c.frame != "unrotated":
         raise ValueError("synthesis needs unrotated coefficients; apply rotate_from_north first")
+    L = p.band_limit
+    for j in range(p.j_min, p.j_max + 1):
+        sig = c.scale(j)
+        expected = scale_band_limit(p, j) if c.multires else L
+        if sig.grid.L != expected:
+            raise ValueError(f"scale {j} stored at band limit {sig.grid.L}, expected {expected}")
+
+
+def _synthesize_stages(c: CurveletCoeffs, t, real: bool) -> SphereSignal:
+    """The scale loop driven from Python, one C call per stage (comparator of the whole-map call,
+    and the path for coefficient sets whose flags or layouts the whole-map call does not take)."""
+    _check_coeffs(c, t)
+    p = t.params
     L = p.band_limit
     dev = c.scaling.values.device
     ctx = _cabi.context(dev)
@@ -188,9 +266,6 @@ def _synthesize(c: CurveletCoeffs, t, real: bool) -> SphereSignal:
     wbuf = None
     for j in range(p.j_min, p.j_max + 1):
         sig = c.scale(j)
-        expected = scale_band_limit(p, j) if c.multires else L
-        if sig.grid.L != expected:
-            raise ValueError(f"scale {j} stored at band limit {sig.grid.L}, expected {expected}")
         Lj = sig.grid.L
         need = 2 * Lj * (2 * Lj - 1)
         if wbuf is None or wbuf.numel() < need:
@@ -205,6 +280,36 @@ def _synthesize(c: CurveletCoeffs, t, real: bool) -> SphereSignal:
     if real:
         return sht_inverse_real(HarmonicCoeffs(L, 0, acc, real=True, trusted=True))
     return sht_inverse(HarmonicCoeffs(L, p.spin, acc, trusted=True))
+
+
+def _synthesize(c: CurveletCoeffs, t, real: bool) -> SphereSignal:
+    """One scv_synthesize call (the library walks the scales); bit-identical to _synthesize_stages."""
+    _check_coeffs(c, t)
+    p = t.params
+    L = p.band_limit
+    dev = c.scaling.values.device
+    dtype = torch.float64 if real else torch.complex128
+    sigs = [c.scale(j) for j in range(p.j_min, p.j_max + 1)]
+    dt = device_tiling(t, dev)
+    plan = _map_plan(t, dt, c.multires)
+    plain = (c.scaling.real == real and c.scaling.spin == 0 and c.scaling.grid.band_limit == plan.Ls
+             and c.scaling.values.dtype == dtype
+             and all(s.real == real and s.values.dtype == dtype and s.values.device == dev and
+                     (s.grid.L, s.grid.M, s.grid.N) == (Lj, Lj, Lj) for s, Lj in zip(sigs, plan.Ljs)))
+    if not plain:
+        return _synthesize_stages(c, t, real)
+    ctx = _cabi.context(dev)
+    for s, Lj in zip(sigs, plan.Ljs):
+        _cabi.checked(s.values, dtype, (2 * Lj - 1, Lj, 2 * Lj - 1), dev, "signal values")
+    Ls = plan.Ls
+    _cabi.checked(c.scaling.values, dtype, (Ls, 2 * Ls - 1), dev, "scaling values")
+    out = torch.empty((L, 2 * L - 1), dtype=dtype, device=dev)
+    work = torch.empty(plan.work_bytes, dtype=torch.uint8, device=dev)
+    sig_arr = plan.sig_arr_t(*[s.values.data_ptr() for s in sigs])
+    ctx.call("synthesize", L, p.spin, 1 if real else 0, plan.n, plan.Lj_arr, plan.pos_arr, plan.neg_arr,
+             _cabi.ptr(dt.scaling), Ls, sig_arr, _cabi.ptr(c.scaling.values), _cabi.ptr(out), _cabi.ptr(work),
+             plan.work_bytes)
+    return SphereSignal(SphereGrid(L), 0 if real else p.spin, out, real=real)
 
 
 def synthesize(c: CurveletCoeffs, t: Tiling) -> SphereSignal:

@@ -28,7 +28,7 @@ def test_library_exports_every_symbol():
     for name in _declared():
         assert hasattr(lib, name), name
     lib.scv_version.restype = ctypes.c_int
-    assert lib.scv_version() == 101
+    assert lib.scv_version() == 102
 
 
 def test_no_cpu_fallback_without_device(monkeypatch):

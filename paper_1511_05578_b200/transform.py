@@ -208,7 +208,7 @@ def _analyze(f: SphereSignal, t, multires: bool, real: bool, scale_out=None) -> 
     outs = []
     for i, Lj in enumerate(plan.Ljs):
         K = 2 * Lj - 1
-        if scale_out is None:
+        if scale_out is None or scale_out[i] is None:
             buf = torch.empty((K, Lj, K), dtype=dtype, device=dev)
         else:
             buf = _cabi.checked(scale_out[i], dtype, (K, Lj, K), dev, "out")

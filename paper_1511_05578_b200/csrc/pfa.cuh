@@ -109,6 +109,12 @@ __host__ __device__ constexpr int mma_pitch(int n) {  // row pitch (doubles) wit
 #ifndef SCV_PFA_A2
 #define SCV_PFA_A2 0
 #endif
+// first operands of a warp's next block loaded under the current block's epilogue (block stage).
+// Measured (r06q, C4): no spills, bit-identical, every K = 2047 pass 0.0-0.5 ms/map SLOWER
+// (332.4 -> 333.9 ms/map): the start-of-block round trip is not what the warps wait on.  Off.
+#ifndef SCV_PFA_PREFETCH
+#define SCV_PFA_PREFETCH 0
+#endif
 #ifndef SCV_PFA_Q_UNROLL
 #define SCV_PFA_Q_UNROLL 1
 #endif
@@ -678,32 +684,45 @@ __device__ __forceinline__ void pfa_stage_mma_blk(double2* X, const double2* tab
         aSr[t][kt] = Sm[(t * 8 + ar) * PA + kt * 4 + ac];
       }
   }
+  // B-fragment column of this lane in block q: butterfly slot ar>>1, component ar&1, and its
+  // first two operands.  A slot past the last butterfly re-reads the last one (GEMM columns
+  // are independent and that column is never stored), and the reduction indices
+  // j = h+1..Kp of the zero-padded coefficient columns read the butterfly's own elements
+  // j <= p-1 (finite data times exact zeros), so the operand loads need no predicates.
+  auto first_operands = [&](int q, int& rowd_, int& pa_, int& pb_, double& an_, double& bn_) {
+    const int gb = (q >> 1) * 8 + (SCV_PFA_SLOT_EVEN ? 1 : 2) * (q & 1);
+    const int bfB = min(gb + slot(ar >> 1), NBF - 1);
+    const int r = R == 1 ? 0 : bfB / nbf, b = bfB - r * nbf;
+    const int c0 = pfa_base<PL, S>(b);
+    rowd_ = 2 * r * PITCH + (ar & 1);
+    pa_ = c0 + (ac + 1) * step;
+    pb_ = c0 + (p - ac - 1) * step;
+    // B operands software-pipelined one k-step ahead (the s/d formation of
+    // step kt must not wait on its own shared loads)
+    an_ = Xd[rowd_ + 2 * pa_];
+    bn_ = Xd[rowd_ + 2 * pb_];
+  };
+  // SCV_PFA_PREFETCH: the first operands of the warp's NEXT block are loaded before the
+  // epilogue stores of the current one (disjoint butterflies), so the next iteration does
+  // not start with a shared-memory round trip
+  int rowd[NBW], pa[NBW], pb[NBW];
+  double an[NBW], bn[NBW];
+  if constexpr (SCV_PFA_PREFETCH != 0) {
+#pragma unroll
+    for (int w = 0; w < NBW; ++w) first_operands(warp + w * NW, rowd[w], pa[w], pb[w], an[w], bn[w]);
+  }
 #pragma unroll 1
   for (int q0 = warp; q0 < NBLK; q0 += NW * NBW) {
-    int rowd[NBW], pa[NBW], pb[NBW], eoff[NBW];
+    int eoff[NBW];
     bool okB[NBW], okE[NBW];
     double2 x0[NBW];
     double accC[NBW][M8][2], accS[NBW][M8][2];
-    double an[NBW], bn[NBW];
 #pragma unroll
     for (int w = 0; w < NBW; ++w) {
       const int q = q0 + w * NW;
       const int gb = (q >> 1) * 8 + (SCV_PFA_SLOT_EVEN ? 1 : 2) * (q & 1);
-      // B-fragment column of this lane: butterfly slot ar>>1, component ar&1.
-      // A slot past the last butterfly re-reads the last one (GEMM columns are
-      // independent and that column is never stored), and the reduction
-      // indices j = h+1..Kp of the zero-padded coefficient columns read the
-      // butterfly's own elements j <= p-1 (finite data times exact zeros), so
-      // the operand loads need no predicates.
-      const int bfB = min(gb + slot(ar >> 1), NBF - 1);
       okB[w] = true;
-      {
-        const int r = R == 1 ? 0 : bfB / nbf, b = bfB - r * nbf;
-        const int c0 = pfa_base<PL, S>(b);
-        rowd[w] = 2 * r * PITCH + (ar & 1);
-        pa[w] = c0 + (ac + 1) * step;
-        pb[w] = c0 + (p - ac - 1) * step;
-      }
+      if constexpr (SCV_PFA_PREFETCH == 0) first_operands(q, rowd[w], pa[w], pb[w], an[w], bn[w]);
       // epilogue butterfly of this lane: slot ac (accumulator columns 2ac, 2ac+1)
       const int bfE = gb + slot(ac);
       okE[w] = q < NBLK && bfE < NBF;
@@ -716,10 +735,6 @@ __device__ __forceinline__ void pfa_stage_mma_blk(double2* X, const double2* tab
       }
 #pragma unroll
       for (int t = 0; t < M8; ++t) accC[w][t][0] = accC[w][t][1] = accS[w][t][0] = accS[w][t][1] = 0.0;
-      // B operands software-pipelined one k-step ahead (the s/d formation of
-      // step kt must not wait on its own shared loads)
-      an[w] = Xd[rowd[w] + 2 * pa[w]];
-      bn[w] = Xd[rowd[w] + 2 * pb[w]];
     }
 #if SCV_PFA_A2
     // k-steps in pairs: one 16-byte A load per (tile, C|S) feeds steps 2q, 2q+1
@@ -800,6 +815,13 @@ __device__ __forceinline__ void pfa_stage_mma_blk(double2* X, const double2* tab
     }
 #endif
     __syncwarp();
+    if constexpr (SCV_PFA_PREFETCH != 0) {
+      if (q0 + NW * NBW < NBLK) {
+#pragma unroll
+        for (int w = 0; w < NBW; ++w)
+          first_operands(q0 + NW * NBW + w * NW, rowd[w], pa[w], pb[w], an[w], bn[w]);
+      }
+    }
 #pragma unroll
     for (int w = 0; w < NBW; ++w) {
       if (!okE[w]) continue;

@@ -711,7 +711,7 @@ constexpr int RB = 8;
 #define SCV_RING_PACE_D 0
 #endif
 // slot X (Ruritanian positions) <- element n of a row at gsrc(n), n = lane0 + nl*j < K
-template <class PL, class SrcFn>
+template <class PL, int RB = ::RB, class SrcFn>
 __device__ __forceinline__ void ring_fill(double2* X, const double2* tab, int lane0, int nl, SrcFn gsrc) {
   constexpr int K = PL::K;
 #pragma unroll 1
@@ -733,7 +733,7 @@ __device__ __forceinline__ void ring_fill(double2* X, const double2* tab, int la
   }
 }
 // output frequency k of slot X -> gdst(k), k = lane0 + nl*j < K
-template <class PL, class DstFn>
+template <class PL, int RB = ::RB, class DstFn>
 __device__ __forceinline__ void ring_drain(const double2* X, const double2* tab, int lane0, int nl, DstFn gdst) {
   constexpr int K = PL::K;
 #pragma unroll 1
@@ -874,6 +874,24 @@ constexpr bool pfa_rows_sched(int gather) { return SCV_ROWSP_SCHED && gather != 
 #ifndef SCV_ROWSP_NG_2047
 #define SCV_ROWSP_NG_2047 SCV_ROWSP_NG
 #endif
+// Register split of the K = 2047 row kernel (setmaxnreg, whole warpgroups): SCV_ROWSP_SETREG_T
+// registers per transform thread (0 = no split), SCV_ROWSP_SETREG_IO per load/store thread; the
+// load/store warps are then padded to one warpgroup (the pad warp exits), and their copy
+// batches shrink to SCV_ROWSP_RB elements per lane.  The split only moves registers inside
+// the CTA's launch allocation (threads x launch registers): threads(T) x T + 128 x IO must not
+// exceed it, or setmaxnreg.inc waits for ever (640 threads launch at 96: T <= 112 with IO = 32).
+// Measured at C4 (r07q/r07r, ms per row pass, default 80.5 / 79.4): 4 groups of 4 warps at
+// 112 / 32 registers 83.9 / 84.2; 4 groups of 3 warps at 160 / 32 or 152 / 40 with two Rader
+// blocks per iteration (SCV_ROWSP_XW=2; 72-92 bytes of spills) 92.7 / 92.5 and 89.2 / 90.5.  Off.
+#ifndef SCV_ROWSP_SETREG_T
+#define SCV_ROWSP_SETREG_T 0
+#endif
+#ifndef SCV_ROWSP_SETREG_IO
+#define SCV_ROWSP_SETREG_IO 32
+#endif
+#ifndef SCV_ROWSP_RB
+#define SCV_ROWSP_RB 4
+#endif
 #ifndef SCV_ROWSP_XW
 #define SCV_ROWSP_XW SCV_R89_NBW
 #endif
@@ -883,11 +901,19 @@ constexpr bool pfa_rows_sched(int gather) { return SCV_ROWSP_SCHED && gather != 
 template <int K> struct PfaPipeCfg {
   static constexpr int NG = 0, NTG = 96, NIO = 0, NB = 0, XW = SCV_R89_NBW, XS = SCV_PFA_NBW_SMALL;
 };
+// threads of a row-kernel launch: with the register split the load/store warps fill a warpgroup
+template <int K> constexpr int pfa_pipe_setreg() { return K == 2047 ? SCV_ROWSP_SETREG_T : 0; }
+template <class C, int K> constexpr int pfa_pipe_threads() {
+  return C::NG * C::NTG + (pfa_pipe_setreg<K>() ? 128 : C::NIO * 32);
+}
 #ifndef SCV_ROWSP_NTG
 #define SCV_ROWSP_NTG 96
 #endif
+#ifndef SCV_ROWSP_NTG_2047
+#define SCV_ROWSP_NTG_2047 SCV_ROWSP_NTG
+#endif
 template <> struct PfaPipeCfg<2047> {
-  static constexpr int NG = SCV_ROWSP ? SCV_ROWSP_NG_2047 : 0, NTG = SCV_ROWSP_NTG, NIO = SCV_ROWSP_NIO, NB = SCV_ROWSP_NB;
+  static constexpr int NG = SCV_ROWSP ? SCV_ROWSP_NG_2047 : 0, NTG = SCV_ROWSP_NTG_2047, NIO = SCV_ROWSP_NIO, NB = SCV_ROWSP_NB;
   static constexpr int XW = SCV_ROWSP_XW, XS = SCV_ROWSP_XS;
 };
 // K = 1023 (the L_j = 512 scale): on with SCV_RING_1023
@@ -926,12 +952,15 @@ static constexpr size_t pfa_smem_pipe() {
 }
 
 template <int K, int DIR, int GATHER>
-__global__ void __launch_bounds__(PfaPipeCfg<K>::NG * PfaPipeCfg<K>::NTG + PfaPipeCfg<K>::NIO * 32, 1)
+__global__ void __launch_bounds__(pfa_pipe_threads<PfaPipeCfg<K>, K>(), 1)
     k_pfa_rows_p(long long nrows, const double2* in, double2* out, const double2* __restrict__ gtab,
                  long long LK = 0, int b0 = 0) {
   using PL = PfaPlan<K>;
   constexpr int NG = PfaPipeCfg<K>::NG, NTG = PfaPipeCfg<K>::NTG, NIO = PfaPipeCfg<K>::NIO, NB = PfaPipeCfg<K>::NB;
-  constexpr int NT = NG * NTG + NIO * 32;
+  constexpr int NT = pfa_pipe_threads<PfaPipeCfg<K>, K>();
+  constexpr int SETREG = pfa_pipe_setreg<K>();
+  constexpr int IORB = SETREG ? SCV_ROWSP_RB : RB;
+  static_assert(!SETREG || ((NG * NTG) % 128 == 0 && NIO <= 4), "setmaxnreg works on warpgroups of 128 threads");
   static_assert(NB > NG, "the ring needs spare buffers for the rows in flight");
   constexpr bool SCHED = pfa_rows_sched(GATHER);  // gtab then is scv_pfa_tables_sched's
   static_assert(NB % NIO == 0, "a load/store warp owns fixed ring slots (it then meets a slot's barrier phases in order)");
@@ -962,7 +991,9 @@ __global__ void __launch_bounds__(PfaPipeCfg<K>::NG * PfaPipeCfg<K>::NTG + PfaPi
   auto row_of = [&](long long i) { return (i / NG) * (G * NG) + (long long)blockIdx.x * NG + (i % NG); };
   if (threadIdx.x >= NG * NTG) {
     // ---- load / store warps
+    if constexpr (SETREG != 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(SCV_ROWSP_SETREG_IO));
     const int w = (threadIdx.x - NG * NTG) >> 5, lane = threadIdx.x & 31;
+    if (SETREG != 0 && w >= NIO) return;  // pad warp of the load/store warpgroup
     long long st[6] = {0, 0, 0, 0, 0, 0};
     PipeClk ck;
     if constexpr (GATHER == 5) {
@@ -1046,7 +1077,7 @@ __global__ void __launch_bounds__(PfaPipeCfg<K>::NG * PfaPipeCfg<K>::NTG + PfaPi
           dst = out + (g * LK + b0 + bb) * K;
         }
           if constexpr (SCHED) ring_drain_s<PL>(X, tab, lane, [&](int k) { return dst + k; });
-        else ring_drain<PL>(X, tab, lane, 32, [&](int k) { return dst + k; });
+        else ring_drain<PL, IORB>(X, tab, lane, 32, [&](int k) { return dst + k; });
         __syncwarp();  // every lane has read its elements before any lane refills the buffer
         ck.mark(st, 3);
       }
@@ -1059,7 +1090,7 @@ __global__ void __launch_bounds__(PfaPipeCfg<K>::NG * PfaPipeCfg<K>::NTG + PfaPi
           if constexpr (SCHED)
             ring_fill_s<PL>(X, tab, lane, [&](int n) { return src + (long long)(n >> 1) * (2 * K) + (n & 1); });
           else
-            ring_fill<PL>(X, tab, lane, 32, [&](int n) { return src + (long long)(n >> 1) * (2 * K) + (n & 1); });
+            ring_fill<PL, IORB>(X, tab, lane, 32, [&](int n) { return src + (long long)(n >> 1) * (2 * K) + (n & 1); });
         } else {
           const double2* src = in + r * K;
           if constexpr (GATHER == 1 || GATHER == 5) {
@@ -1067,7 +1098,7 @@ __global__ void __launch_bounds__(PfaPipeCfg<K>::NG * PfaPipeCfg<K>::NTG + PfaPi
             src = in + g * LK + (b0 + bb) * K;
           }
           if constexpr (SCHED) ring_fill_s<PL>(X, tab, lane, [&](int n) { return src + n; });
-          else ring_fill<PL>(X, tab, lane, 32, [&](int n) { return src + n; });
+          else ring_fill<PL, IORB>(X, tab, lane, 32, [&](int n) { return src + n; });
         }
         cp_async_mbar_arrive(full + (u & 1) * NB + b);
       }
@@ -1077,6 +1108,7 @@ __global__ void __launch_bounds__(PfaPipeCfg<K>::NG * PfaPipeCfg<K>::NTG + PfaPi
     return;
   }
   // ---- transform groups
+  if constexpr (SETREG != 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(SETREG));
   const int g = threadIdx.x / NTG, gtid = threadIdx.x - g * NTG, bar = 1 + g;
   long long st[6] = {0, 0, 0, 0, 0, 0};
   PipeClk ck;
@@ -2802,7 +2834,7 @@ static int launch_rows_p(scv_ctx* c, long long nrows, const double2* in, double2
                          int b0, cudaStream_t s) {
   constexpr size_t smp = pfa_smem_pipe<K>();
   static_assert(smp <= 232448, "pipelined rows launch shape exceeds the 227 KB shared-memory limit");
-  constexpr int NTB = PfaPipeCfg<K>::NG * PfaPipeCfg<K>::NTG + PfaPipeCfg<K>::NIO * 32;
+  constexpr int NTB = pfa_pipe_threads<PfaPipeCfg<K>, K>();
   if constexpr (pfa_rows_sched(GATHER)) SCV_TRY(scv_pfa_tables_sched(c, K, &tab));  // same radix tables, scheduled maps
   int grid;
   SCV_TRY(persistent_grid(c, k_pfa_rows_p<K, DIR, GATHER>, NTB, smp, (nrows + PfaPipeCfg<K>::NG - 1) / PfaPipeCfg<K>::NG, &grid));

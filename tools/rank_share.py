@@ -9,7 +9,10 @@ SHTs, the scaling part and the final merge) and of the last rank.  1 / max over 
 shares is the throughput the decomposition allows before the collectives (16.8 MB broadcast
 + 134 MB reduce at C4) -- an upper bound for the real N-GPU run, not a measurement of it.
 
-usage: python tools/rank_share.py [L spin jmin] [--steps K] [--json out]
+--streamed times dist.roundtrip_sharded_streamed instead (coefficients never held: the way
+BASELINE C5, L=2048 spin 2, is meant to run on 8 GPUs), with --slab-gb GiB pieces.
+
+usage: python tools/rank_share.py [L spin jmin] [--steps K] [--worlds 1,2,4,8] [--streamed] [--slab-gb G] [--json out]
 """
 import json
 import sys
@@ -18,15 +21,21 @@ import torch
 
 sys.path.insert(0, ".")
 import paper_1511_05578_b200 as sc  # noqa: E402
-from paper_1511_05578_b200.dist import CudaBackend, ScalePlan, VirtualRank, analyze_sharded, synthesize_sharded  # noqa: E402
+from paper_1511_05578_b200.dist import (CudaBackend, ScalePlan, VirtualRank, analyze_sharded,  # noqa: E402
+                                        roundtrip_sharded_streamed, synthesize_sharded)
 from bench import gaussian_flm  # BASELINE.json's input recipe  # noqa: E402
 
 
 def main():
-    args = [x for x in sys.argv[1:] if not x.startswith("--")]
-    L, spin, jmin = (int(args[0]), int(args[1]), int(args[2])) if len(args) >= 3 else (1024, 0, 3)
     steps = int(sys.argv[sys.argv.index("--steps") + 1]) if "--steps" in sys.argv else 3
     out = sys.argv[sys.argv.index("--json") + 1] if "--json" in sys.argv else ""
+    worlds = tuple(int(x) for x in sys.argv[sys.argv.index("--worlds") + 1].split(",")) if "--worlds" in sys.argv \
+        else (1, 2, 4, 8)
+    streamed = "--streamed" in sys.argv
+    slab_gb = float(sys.argv[sys.argv.index("--slab-gb") + 1]) if "--slab-gb" in sys.argv else 16.0
+    skip = {"--steps", "--json", "--worlds", "--slab-gb"}
+    args = [x for i, x in enumerate(sys.argv[1:], 1) if not x.startswith("--") and sys.argv[i - 1] not in skip]
+    L, spin, jmin = (int(args[0]), int(args[1]), int(args[2])) if len(args) >= 3 else (1024, 0, 3)
     torch.cuda.set_device(0)
     p = sc.TilingParams(L, spin, 2.0, jmin)
     t = sc.build_tiling(p)
@@ -34,18 +43,22 @@ def main():
     f = sc.sht_inverse(sc.HarmonicCoeffs(L, spin, flm))
     be = CudaBackend()
     rows = []
-    for world in (1, 2, 4, 8):
+    K_fin = 2 * L - 1
+    slab_rows = max(1, int(slab_gb * (1 << 30)) // (K_fin * K_fin * 16))
+    for world in worlds:
         plan = ScalePlan.build(p, world, True, real=False)
         for rank in sorted({0, world - 1}):
             vr = VirtualRank(rank, world)
 
             def step():
+                if streamed:
+                    return roundtrip_sharded_streamed(f, t, group=vr, backend=be, slab_rows=slab_rows)
                 c = analyze_sharded(f, t, group=vr, backend=be)
                 g = synthesize_sharded(c, t, group=vr, backend=be)
                 del c
                 return g
 
-            for _ in range(2):
+            for _ in range(1 if streamed else 2):
                 step()
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -62,16 +75,20 @@ def main():
             be.lift_table_restrictions(plan)
             torch.cuda.empty_cache()
             torch.cuda.reset_peak_memory_stats()
-    base = max(r["ms_per_map"] for r in rows if r["world"] == 1)
+    base = max((r["ms_per_map"] for r in rows if r["world"] == 1), default=None)
     summary = []
-    for world in (1, 2, 4, 8):
+    for world in worlds:
         worst = max(r["ms_per_map"] for r in rows if r["world"] == world)
-        summary.append({"world": world, "slowest_share_ms": worst, "maps_per_s_bound": 1e3 / worst,
-                        "speedup_bound": base / worst, "efficiency_bound": base / worst / world})
-        print(f"N={world}: slowest share {worst:.2f} ms -> <= {1e3 / worst:.2f} maps/s, "
-              f"speed-up bound {base / worst:.2f}x ({100 * base / worst / world:.1f}% of linear)")
+        row = {"world": world, "slowest_share_ms": worst, "maps_per_s_bound": 1e3 / worst}
+        msg = f"N={world}: slowest share {worst:.2f} ms -> <= {1e3 / worst:.3f} maps/s"
+        if base is not None:
+            row.update(speedup_bound=base / worst, efficiency_bound=base / worst / world)
+            msg += f", speed-up bound {base / worst:.2f}x ({100 * base / worst / world:.1f}% of linear)"
+        summary.append(row)
+        print(msg)
     if out:
-        json.dump({"config": {"L": L, "spin": spin, "jmin": jmin, "steps": steps,
+        json.dump({"config": {"L": L, "spin": spin, "jmin": jmin, "steps": steps, "streamed": streamed,
+                              "slab_GiB": slab_gb if streamed else None,
                               "note": "one rank's share run alone with the collectives skipped (dist.VirtualRank); "
                                       "an upper bound for the N-GPU run, not a measurement of it"},
                    "shares": rows, "summary": summary}, open(out, "w"), indent=1)

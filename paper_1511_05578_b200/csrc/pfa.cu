@@ -2553,6 +2553,8 @@ __global__ void __launch_bounds__(PfaQCfg<K>::NT, PfaQCfg<K>::MINB)
 // refill than alone, 12% in the row kernel whose copies are spread by its position-map reads).
 // Sleeping SCV_GQP_PACE ns after every SCV_GQP_PACE_N copies spreads them; measured on the C4
 // map (ms for this pass): off 97.1; 30 ns 92.1; 50 ns 87.6; 75 ns 103; 100 ns per 2 copies 90.
+// Re-swept on the final kernels (r08q): 40 ns 83.6; 50 ns 83.9; 60 ns 84.5; 65 ns 101.9 (the
+// team then bounds the pass); 100 ns per 2 copies 86.6.
 #ifndef SCV_GQP_PACE
 #define SCV_GQP_PACE 50
 #endif

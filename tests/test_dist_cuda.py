@@ -111,3 +111,54 @@ def test_cuda_backend_world2_on_one_gpu(L, spin):
     assert res[0]["err"] <= 1e-12, res[0]["err"]
     assert res[0]["rt"] <= 1e-11, res[0]["rt"]
     assert all(r["restricted"] for r in res)
+
+
+@pytest.mark.parametrize("L,spin,world", [(128, 0, 4), (256, 2, 8)])
+def test_virtual_rank_shares_tile_the_analysis_and_add_up(L, spin, world):
+    """dist.VirtualRank (one rank's share run alone, the mode tools/rank_share.py times): with the
+    CUDA backend the shares of all virtual ranks tile analyze()'s scale signals, and their
+    per-scale synthesis terms add up to synthesize(analyze(f))."""
+    import paper_1511_05578_b200 as sc
+    from oracle import scurve_oracle as orc  # checker-side input only
+    from paper_1511_05578_b200 import dist as D
+
+    torch.cuda.set_device(0)
+    t = sc.build_tiling(sc.TilingParams(L, spin, 2.0, 3))
+    p = t.params
+    f = sc.sht_inverse(sc.HarmonicCoeffs(L, spin, orc.gaussian_flm(L, spin, seed=4, real=False)))
+    full = sc.analyze(f, t)
+    ref = sc.synthesize(full, t)
+    be = D.CudaBackend()
+    terms = torch.zeros((p.scale_count, L * L), dtype=torch.complex128, device="cuda")
+    rows = {j: 0 for j in range(p.j_min, p.j_max + 1)}
+    plan = None
+    try:
+        for r in range(world):
+            vr = D.VirtualRank(r, world)
+            c = D.analyze_sharded(f, t, group=vr, backend=be)
+            plan = c.plan
+            assert (c.scaling is not None) == (r == 0)
+            for j, s in c.scales.items():
+                whole = full.scale(j).values
+                if isinstance(s, sc.SO3Slab):
+                    assert (s.b0, s.nb) in [(b0, nb) for rr, b0, nb in plan.slabs[j] if rr == r]
+                    assert orc.rel_err(s.values.cpu().numpy(), whole[:, s.b0:s.b0 + s.nb, :].cpu().numpy()) <= 1e-12
+                    rows[j] += s.nb
+                    terms[j - p.j_min] += be.scale_term_slab(s, t, j)
+                else:
+                    assert torch.equal(s.values, whole)
+                    rows[j] += s.values.shape[1]
+                    terms[j - p.j_min] += be.scale_term(s, t, j, False)
+            if r == 0:
+                scaling = c.scaling
+            be.lift_table_restrictions(plan)
+        assert all(rows[j] == full.scale(j).values.shape[1] for j in rows)
+        assert plan.slabs, "this size must exercise the beta-slab split"
+        acc = torch.zeros(L * L, dtype=torch.complex128, device="cuda")
+        for i in range(p.scale_count):
+            acc += terms[i]
+        g = be.finish(acc, scaling, t, False)
+        assert orc.rel_err(g.values.cpu().numpy(), ref.values.cpu().numpy()) <= 1e-12
+    finally:
+        if plan is not None:
+            be.lift_table_restrictions(plan)

@@ -49,7 +49,9 @@ static void factors_of(int K, int f[4]) {
     case 127: f[0] = 127; break;
     case 255: f[0] = 3; f[1] = 5; f[2] = 17; break;
     case 511: f[0] = 7; f[1] = 73; break;
-    case 1023: f[0] = 3; f[1] = 11; f[2] = 31; break;
+    case 1023:
+      f[0] = PfaPlan<1023>::P0; f[1] = PfaPlan<1023>::P1; f[2] = PfaPlan<1023>::P2; f[3] = PfaPlan<1023>::P3;
+      break;
     case 2047: f[0] = 23; f[1] = 89; break;
     case 4095: f[0] = 5; f[1] = 7; f[2] = 9; f[3] = 13; break;
   }
@@ -849,6 +851,11 @@ extern "C" int scv_debug_pipe_stats(unsigned long long* out, int reset) {
 #ifndef SCV_ROWSP
 #define SCV_ROWSP 1
 #endif
+// register split (setmaxnreg 152 / 120) in the K = 1023 column kernels too: its three-stage
+// transform (3 * 11 * 31) wanted all 128 registers, the two-stage one (SCV_PLAN_1023) does not
+#ifndef SCV_SETREG_1023
+#define SCV_SETREG_1023 0
+#endif
 #ifndef SCV_ROWSP_NG
 #define SCV_ROWSP_NG 4
 #endif
@@ -1594,7 +1601,7 @@ __global__ void __launch_bounds__(PfaCgpCfg<K>::NG * PfaCgpCfg<K>::NTG + PfaCgpC
   const long long lo = S * blockIdx.x / gridDim.x, hi = S * (blockIdx.x + 1) / gridDim.x;
   const long long ni = hi - lo;
   static_assert(!SCV_CGP_SETREG || (NG * NTG == 384 && NQT == 128), "setmaxnreg works on warpgroups of 128 threads");
-  constexpr bool SETREG = SCV_CGP_SETREG && K == 2047;  // the K = 1023 transforms want all 128
+  constexpr bool SETREG = SCV_CGP_SETREG && (K == 2047 || (K == 1023 && SCV_SETREG_1023));
   if (threadIdx.x >= NG * NTG) {
     if constexpr (SETREG) asm volatile("setmaxnreg.inc.sync.aligned.u32 152;\n");
     // ---- generator / store team: all NIO warps work on every step, in order
@@ -2607,7 +2614,7 @@ __global__ void __launch_bounds__(PfaGqpCfg<K>::NG * PfaGqpCfg<K>::NTG + PfaGqpC
   // team): the transforms need 120 registers, the team holds 64 accumulator, 32
   // weight and 16 position registers per thread across steps.
   static_assert(!SCV_GQP_SETREG || (NG * NTG == 384 && NQT == 128), "setmaxnreg works on warpgroups of 128 threads");
-  constexpr bool SETREG = SCV_GQP_SETREG && K == 2047;  // the K = 1023 transforms want all 128
+  constexpr bool SETREG = SCV_GQP_SETREG && (K == 2047 || (K == 1023 && SCV_SETREG_1023));
   if (threadIdx.x >= NG * NTG) {
     if constexpr (SETREG) asm volatile("setmaxnreg.inc.sync.aligned.u32 152;\n");
     const int t = threadIdx.x - NG * NTG;

@@ -1,7 +1,7 @@
 // Prime-factor (Good-Thomas) DFT engine for the odd grid lengths K = 2^k - 1.
 //
 // Every sampling length of the lambda=2 tilings factors into coprime odd
-// radices: 2047 = 23*89, 1023 = 3*11*31, 511 = 7*73, 255 = 3*5*17,
+// radices: 2047 = 23*89, 1023 = 31*33 (two DMMA stages; 3*11*31 until r08), 511 = 7*73, 255 = 3*5*17,
 // 4095 = 5*7*9*13, 63 = 7*9, 15 = 3*5; 3, 7, 31, 127 are prime.  Under the
 // Ruritanian input map the K-point DFT is a p_1 x ... x p_d DFT with NO
 // twiddle factors.  The rows stay in NATURAL order in shared memory for the
@@ -41,7 +41,23 @@ SCV_PFA_PLAN(31, 1, 31, 1, 1, 1)
 SCV_PFA_PLAN(63, 2, 7, 9, 1, 1)
 SCV_PFA_PLAN(255, 3, 3, 5, 17, 1)
 SCV_PFA_PLAN(511, 2, 7, 73, 1, 1)
+// K = 1023: 0 = 3 * 11 * 31 (radices 3 and 11 on DFMA, 31 on DMMA); 1 = 33 * 31, 2 = 31 * 33 (two
+// DMMA stages: the dense symmetric form only needs an odd radix, and 33 and 31 are coprime).
+// A 1023-point transform took 11.6 k cycles in the ring kernels against 18.3 k for 2047 points
+// (pipe counters, r08): three stages, two of them scalar, for a quarter of the FP64 work.
+// Measured (r08, ms/map): C3 (L=512) 54.2 / 51.5 / 49.4 for plans 0 / 1 / 2, C4 334.0 / 331.8 /
+// 331.8; round trips unchanged (4.1e-14, 9.4e-14).  Keeping the larger A fragments in registers
+// (SCV_PFA_AREG_MAX 8 or 12) or the setmaxnreg split at K = 1023 (SCV_SETREG_1023): within noise.
+#ifndef SCV_PLAN_1023
+#define SCV_PLAN_1023 2
+#endif
+#if SCV_PLAN_1023 == 1
+SCV_PFA_PLAN(1023, 2, 33, 31, 1, 1)
+#elif SCV_PLAN_1023 == 2
+SCV_PFA_PLAN(1023, 2, 31, 33, 1, 1)
+#else
 SCV_PFA_PLAN(1023, 3, 3, 11, 31, 1)
+#endif
 SCV_PFA_PLAN(2047, 2, 23, 89, 1, 1)
 SCV_PFA_PLAN(4095, 4, 5, 7, 9, 13)
 
@@ -84,6 +100,10 @@ __host__ __device__ constexpr bool pfa_use_mma(int p, int K) {
 constexpr int pfa_kt_unroll = SCV_PFA_KT_UNROLL;
 #ifndef SCV_PFA_AREG
 #define SCV_PFA_AREG 1
+#endif
+// largest A fragment (m8 tiles x k-steps, per matrix) a lane keeps in registers for a stage
+#ifndef SCV_PFA_AREG_MAX
+#define SCV_PFA_AREG_MAX 6
 #endif
 #ifndef SCV_PFA_SLOT_EVEN
 #define SCV_PFA_SLOT_EVEN 1
@@ -673,7 +693,7 @@ __device__ __forceinline__ void pfa_stage_mma_blk(double2* X, const double2* tab
   // small radices: the lane's A fragments (M8 tiles x Kp/4 k-steps of C and S)
   // stay in registers for the whole stage; re-reading them per block is a
   // fifth of the transform's shared-memory traffic at K = 2047 (radix 23)
-  constexpr bool AREG = SCV_PFA_AREG && !SCV_PFA_A2 && M8 * (Kp / 4) <= 6;
+  constexpr bool AREG = SCV_PFA_AREG && !SCV_PFA_A2 && M8 * (Kp / 4) <= SCV_PFA_AREG_MAX;
   double aCr[AREG ? M8 : 1][AREG ? Kp / 4 : 1], aSr[AREG ? M8 : 1][AREG ? Kp / 4 : 1];
   if constexpr (AREG) {
 #pragma unroll

@@ -1,11 +1,12 @@
 """Per-role cycle split of the ring kernels (build with -DSCV_PIPE_STATS=1):
-runs one slab analysis + synthesis at L=1024 and prints the counters."""
+runs one slab analysis + synthesis at L (default 1024) and prints the counters."""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_1511_05578_b200 as sc
 from paper_1511_05578_b200 import _cabi
-L, nb = 1024, int(sys.argv[1]) if len(sys.argv) > 1 else 32
+nb = int(sys.argv[1]) if len(sys.argv) > 1 else 32
+L = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
 rng = np.random.default_rng(0)
 w = rng.standard_normal((2, L, 2 * L - 1)) + 1j * rng.standard_normal((2, L, 2 * L - 1))
 cw = sc.CurveletWignerCoeffs(L, w); grid = sc.SO3Grid(L, L, L)
@@ -13,7 +14,7 @@ lib = _cabi.load_library()
 buf = (ctypes.c_ulonglong * 36)()
 for it in range(2):
     torch.cuda.synchronize(); lib.scv_debug_pipe_stats(None, 1)
-    slab = sc.so3_inverse_curvelet_slab(cw, grid, 400, nb)
+    slab = sc.so3_inverse_curvelet_slab(cw, grid, min(400, L - nb), nb)
     part = sc.so3_forward_curvelet_slab(slab)
     torch.cuda.synchronize(); lib.scv_debug_pipe_stats(buf, 0)
 names = ["rows", "colgen", "gamma_q"]

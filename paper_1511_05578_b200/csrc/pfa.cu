@@ -53,7 +53,9 @@ static void factors_of(int K, int f[4]) {
       f[0] = PfaPlan<1023>::P0; f[1] = PfaPlan<1023>::P1; f[2] = PfaPlan<1023>::P2; f[3] = PfaPlan<1023>::P3;
       break;
     case 2047: f[0] = 23; f[1] = 89; break;
-    case 4095: f[0] = 5; f[1] = 7; f[2] = 9; f[3] = 13; break;
+    case 4095:
+      f[0] = PfaPlan<4095>::P0; f[1] = PfaPlan<4095>::P1; f[2] = PfaPlan<4095>::P2; f[3] = PfaPlan<4095>::P3;
+      break;
   }
 }
 

@@ -2,7 +2,7 @@
 //
 // Every sampling length of the lambda=2 tilings factors into coprime odd
 // radices: 2047 = 23*89, 1023 = 31*33 (two DMMA stages; 3*11*31 until r08), 511 = 7*73, 255 = 3*5*17,
-// 4095 = 5*7*9*13, 63 = 7*9, 15 = 3*5; 3, 7, 31, 127 are prime.  Under the
+// 4095 = 9*13*35 (5*7*9*13 until r08), 63 = 7*9, 15 = 3*5; 3, 7, 31, 127 are prime.  Under the
 // Ruritanian input map the K-point DFT is a p_1 x ... x p_d DFT with NO
 // twiddle factors.  The rows stay in NATURAL order in shared memory for the
 // whole transform:
@@ -59,7 +59,27 @@ SCV_PFA_PLAN(1023, 2, 31, 33, 1, 1)
 SCV_PFA_PLAN(1023, 3, 3, 11, 31, 1)
 #endif
 SCV_PFA_PLAN(2047, 2, 23, 89, 1, 1)
+// K = 4095: 0 = 5 * 7 * 9 * 13 (5, 7 on DFMA; four stages, 484 bytes of spills in the row kernel);
+// 1 = 35 * 9 * 13, 2 = 9 * 13 * 35, 4 = 13 * 9 * 35, 5 = 13 * 35 * 9 (three DMMA stages, no spills,
+// 70 registers); 3 = 63 * 65 (does not fit the batched kernels' tables).  Measured on the C5
+// streamed map (r08, ms/map): 5385 / 4216 / 4124 / 4189 / 4158 for plans 0 / 1 / 2 / 4 / 5, round
+// trip 6.28e-13 throughout; ring shapes 128 / 256 / 384 threads per group with plan 2: 4255 / 4126 / 4119.
+#ifndef SCV_PLAN_4095
+#define SCV_PLAN_4095 2
+#endif
+#if SCV_PLAN_4095 == 1
+SCV_PFA_PLAN(4095, 3, 35, 9, 13, 1)
+#elif SCV_PLAN_4095 == 2
+SCV_PFA_PLAN(4095, 3, 9, 13, 35, 1)
+#elif SCV_PLAN_4095 == 3
+SCV_PFA_PLAN(4095, 2, 63, 65, 1, 1)
+#elif SCV_PLAN_4095 == 4
+SCV_PFA_PLAN(4095, 3, 13, 9, 35, 1)
+#elif SCV_PLAN_4095 == 5
+SCV_PFA_PLAN(4095, 3, 13, 35, 9, 1)
+#else
 SCV_PFA_PLAN(4095, 4, 5, 7, 9, 13)
+#endif
 
 template <class PL, int S>
 __host__ __device__ constexpr int pfa_p() {

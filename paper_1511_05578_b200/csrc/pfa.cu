@@ -1225,6 +1225,7 @@ template <> struct PfaGCfg<511> { static constexpr int R = 4, NT = 256, MINB = 1
   };
 SCV_GCFG_(1023, SCV_GEN1023)
 SCV_GCFG_(2047, SCV_GEN2047)
+// (re-swept with the 9 * 13 * 35 plan, r09: 512: 1318 ms; 640: 1282; 768: 1332; 1024: 1285)
 #ifndef SCV_GEN4095_NT
 #define SCV_GEN4095_NT 640
 #endif
@@ -2341,8 +2342,10 @@ __global__ void __launch_bounds__(PfaCfg<K, true>::NT, PfaCfg<K, true>::MINB)
 // summation order is fixed (bit-reproducible).
 // ---------------------------------------------------------------------------
 template <int K> struct PfaQCfg { static constexpr int RQ = 1, NT = 256, MINB = 1; };
+// threads of the K = 4095 gamma+quadrature block, re-swept with the 9 * 13 * 35 plan (r09, ms of this
+// pass on the C5 streamed map): 256: 1384; 384: 1227; 448: 1274; 512: 1152; 576: 1225; 640: 1177; 768: 1183
 #ifndef SCV_Q4095_NT
-#define SCV_Q4095_NT 384
+#define SCV_Q4095_NT 512
 #endif
 template <> struct PfaQCfg<4095> { static constexpr int RQ = 1, NT = SCV_Q4095_NT, MINB = 1; };
 template <> struct PfaQCfg<255> { static constexpr int RQ = 1, NT = 128, MINB = 1; };

@@ -223,11 +223,12 @@ def ncu_traffic(stage, Ljs):
 # dense radix-89 stage; the Rader radix-89 stage (r01v15+) issues 66 per block
 # of 4 butterflies: 288 + 396 = 684 per K=2047 row.
 PFA_PLAN = {3: (3,), 7: (7,), 15: (3, 5), 31: (31,), 63: (7, 9), 255: (3, 5, 17), 511: (7, 73),
-            1023: (3, 11, 31), 2047: (23, 89), 4095: (5, 7, 9, 13)}
+            1023: (31, 33), 2047: (23, 89), 4095: (9, 13, 35)}
 PFA_R = {  # rows per transform call by stage
-    "so3inv_rows": {1023: 2, 511: 4, 255: 8},
-    "so3inv_colgen": {2047: 2, 1023: 4, 511: 4, 255: 8, 4095: 2},
-    "so3fwd_alpha": {1023: 2, 511: 4, 255: 8},
+    # (the ring kernels of K = 2047, 1023 and the K = 511 row / gamma passes transform one row per call)
+    "so3inv_rows": {255: 8},
+    "so3inv_colgen": {511: 4, 255: 8, 4095: 2},
+    "so3fwd_alpha": {255: 8},
     "so3fwd_gamma_q": {},
 }
 DMMA_PEAK_TF = 36.9  # measured, 8 independent chains x 32 warps/SM (profiles/r01_fp64_pipe_microbench.log)
